@@ -1,0 +1,457 @@
+/*
+ * duhl_oracle.c -- plain, slow, single-threaded CPU oracle for the DuHL hot path
+ * (arXiv 1708.05357, "Efficient Use of Limited-Memory Accelerators for Linear
+ * Learning on Heterogeneous Systems").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  It
+ * shares no code, header, table or helper with the CUDA path
+ * (paper_1708_05357_b200/csrc); neither side includes the other.
+ *
+ * Conventions (citations: P:n = PAPER.md line n, with section/equation):
+ *   A is d x n, column-major float32: column a_i starts at A + i*ld (Eq. 1).
+ *   Every accumulation is in double; a float32 value converts to double exactly.
+ *   model 0 = Lasso  (App. C eq. lassoobj):  (1/2d)||A a - b||^2 + lambda ||a||_1
+ *   model 1 = SVM dual (App. C eq. dualsvm): (1/n) sum(-y_i a_i) + (1/(2 lambda n^2)) ||A a||^2,
+ *             y_i a_i in [0,1].
+ *   Primal-dual map (App. E): Lasso w = A a - b; SVM w = A a / (lambda n).
+ *   Lasso Lipschitzing bound B = ||b||^2 / (2 lambda d)  (reading R1).
+ *
+ * Every function below is the plain definition or the paper's algorithm written
+ * out step by step: no blocking, fusion or reordering.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef int64_t i64;
+typedef uint64_t u64;
+
+#define OR_LASSO 0
+#define OR_SVM 1
+
+#define OR_OK 0
+#define OR_E_INVALID 2
+#define OR_E_NUMERIC 4
+#define OR_E_NOT_CONVERGED 9
+
+/* ------------------------------------------------------------------------- */
+/* Counter-based generator for permutations and uniform blocks (DESIGN.md
+ * "Randomness").  splitmix64 finaliser; key(seed, round, pass, j).  The CUDA
+ * side implements the same documented generator independently. */
+u64 or_mix64(u64 x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+u64 or_perm_key(u64 seed, i64 round, i64 pass, i64 j) {
+    u64 h = or_mix64(seed);
+    h = or_mix64(h ^ (u64)round);
+    h = or_mix64(h ^ (u64)pass);
+    return or_mix64(h ^ (u64)j);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Precompute: ||a_i||^2 for every column. */
+void or_col_norms(const float* A, i64 d, i64 n, i64 ld, double* norms) {
+    for (i64 i = 0; i < n; ++i) {
+        const float* a = A + i * ld;
+        double acc = 0.0;
+        for (i64 k = 0; k < d; ++k) acc += (double)a[k] * (double)a[k];
+        norms[i] = acc;
+    }
+}
+
+/* B = ||b||^2 / (2 lambda d)   (App. E "Lasso"). */
+double or_lasso_B(const double* b, i64 d, double lambda) {
+    double bb = 0.0;
+    for (i64 k = 0; k < d; ++k) bb += b[k] * b[k];
+    return bb / (2.0 * lambda * (double)d);
+}
+
+/* v = A alpha  ("current shared state v := A alpha"). */
+void or_matvec(const float* A, i64 d, i64 n, i64 ld, const double* alpha, double* v) {
+    for (i64 k = 0; k < d; ++k) v[k] = 0.0;
+    for (i64 i = 0; i < n; ++i) {
+        if (alpha[i] == 0.0) continue;
+        const float* a = A + i * ld;
+        for (i64 k = 0; k < d; ++k) v[k] += (double)a[k] * alpha[i];
+    }
+}
+
+/* Primal-dual map w(alpha) from v = A alpha  (App. E: P:855 Lasso, P:870 SVM). */
+void or_primal_dual_w(int model, const double* v, const double* b, i64 d, i64 n, double lambda,
+                      double* w) {
+    for (i64 k = 0; k < d; ++k)
+        w[k] = (model == OR_LASSO) ? (v[k] - b[k]) : (v[k] / (lambda * (double)n));
+}
+
+/* Per-coordinate duality gap, Eq. 4 in the closed forms of App. E:
+ *   Lasso: gap_i = (1/d) [ a_i s_i + B [|s_i| - lambda d]_+ + lambda d |a_i| ]
+ *   SVM: gap_i = (1/n) [ a_i s_i + max(0, 1 - y_i s_i) - y_i a_i ]
+ * with s_i = a_i^T w.  gap_out[i] = max(gap, +0.0) (reading R17); returns
+ * OR_E_NUMERIC if a gap is below -1e-12 * (scale of its terms) or not finite.
+ * idx == NULL means all columns (k must equal n).  s_out may be NULL. */
+int or_coord_gaps(int model, const float* A, i64 d, i64 n, i64 ld, const double* alpha,
+                  const double* y, const double* w, double lambda, double B, const i64* idx,
+                  i64 k, double* s_out, double* gap_out) {
+    int status = OR_OK;
+    for (i64 t = 0; t < k; ++t) {
+        i64 i = idx ? idx[t] : t;
+        const float* a = A + i * ld;
+        double s = 0.0;
+        for (i64 r = 0; r < d; ++r) s += (double)a[r] * w[r];
+        double g, scale;
+        if (model == OR_LASSO) {
+            double lam_d = lambda * (double)d;
+            double thr = fabs(s) - lam_d;
+            double t1 = alpha[i] * s, t2 = B * (thr > 0.0 ? thr : 0.0), t3 = lam_d * fabs(alpha[i]);
+            g = (t1 + t2 + t3) / (double)d;
+            scale = (fabs(t1) + t2 + t3) / (double)d;
+        } else {
+            double h = 1.0 - y[i] * s;
+            double t1 = alpha[i] * s, t2 = (h > 0.0 ? h : 0.0), t3 = y[i] * alpha[i];
+            g = (t1 + t2 - t3) / (double)n;
+            scale = (fabs(t1) + t2 + fabs(t3)) / (double)n;
+        }
+        if (!isfinite(g) || g < -1e-12 * (scale > 1.0 ? scale : 1.0)) status = OR_E_NUMERIC;
+        if (s_out) s_out[t] = s;
+        gap_out[t] = (g > 0.0) ? g : 0.0; /* clamp, also maps -0.0 to +0.0 */
+    }
+    return status;
+}
+
+/* Top-m selection, Eq. 9 / Eq. 11:
+ * P := argmax_{|P|=m} sum_{j in P} z_j  == the m largest z, ties to the lowest
+ * index (reading R7).  Output: the m indices in (-z, i) order.
+ * Plain stable insertion into a sorted list is O(n m); a library sort would do,
+ * this is written out so the order rule is visible. */
+static int or_before(const double* z, i64 a, i64 b) { /* a ranks before b */
+    if (z[a] != z[b]) return z[a] > z[b];
+    return a < b;
+}
+static void or_sort_idx(const double* z, i64* idx, i64 len) { /* merge sort by (-z, i) */
+    if (len < 2) return;
+    i64 h = len / 2;
+    or_sort_idx(z, idx, h);
+    or_sort_idx(z, idx + h, len - h);
+    i64* tmp = (i64*)malloc(sizeof(i64) * (size_t)len);
+    i64 p = 0, q = h, o = 0;
+    while (p < h && q < len) tmp[o++] = or_before(z, idx[q], idx[p]) ? idx[q++] : idx[p++];
+    while (p < h) tmp[o++] = idx[p++];
+    while (q < len) tmp[o++] = idx[q++];
+    memcpy(idx, tmp, sizeof(i64) * (size_t)len);
+    free(tmp);
+}
+void or_select_topm(const double* z, i64 n, i64 m, i64* P_out) {
+    i64* idx = (i64*)malloc(sizeof(i64) * (size_t)n);
+    for (i64 i = 0; i < n; ++i) idx[i] = i;
+    or_sort_idx(z, idx, n);
+    for (i64 t = 0; t < m; ++t) P_out[t] = idx[t];
+    free(idx);
+}
+
+/* Baseline selection policies (P:401 sequential blocks [Yu 2012]; P:434 uniform):
+ *   sequential: block k = round mod ceil(n/m), indices [k m, min((k+1) m, n))
+ *   uniform   : the m indices with the smallest (key(seed, round, -1, j), j)
+ * Returns the number of indices written (sequential's last block may be short). */
+static void or_sort_by_key(u64* key, i64* idx, i64 len) { /* insertion-free merge sort */
+    if (len < 2) return;
+    i64 h = len / 2;
+    or_sort_by_key(key, idx, h);
+    or_sort_by_key(key + h, idx + h, len - h);
+    u64* tk = (u64*)malloc(sizeof(u64) * (size_t)len);
+    i64* ti = (i64*)malloc(sizeof(i64) * (size_t)len);
+    i64 p = 0, q = h, o = 0;
+    while (p < h && q < len) {
+        int take_q = (key[q] < key[p]) || (key[q] == key[p] && idx[q] < idx[p]);
+        if (take_q) { tk[o] = key[q]; ti[o++] = idx[q++]; }
+        else { tk[o] = key[p]; ti[o++] = idx[p++]; }
+    }
+    while (p < h) { tk[o] = key[p]; ti[o++] = idx[p++]; }
+    while (q < len) { tk[o] = key[q]; ti[o++] = idx[q++]; }
+    memcpy(key, tk, sizeof(u64) * (size_t)len);
+    memcpy(idx, ti, sizeof(i64) * (size_t)len);
+    free(tk);
+    free(ti);
+}
+i64 or_select_policy(int policy, i64 n, i64 m, i64 round, u64 seed, const double* z, i64* P_out) {
+    if (policy == 0) { or_select_topm(z, n, m, P_out); return m; }
+    if (policy == 1) {
+        i64 nblk = (n + m - 1) / m, k = round % nblk, lo = k * m, hi = lo + m < n ? lo + m : n;
+        for (i64 i = lo; i < hi; ++i) P_out[i - lo] = i;
+        return hi - lo;
+    }
+    u64* key = (u64*)malloc(sizeof(u64) * (size_t)n);
+    i64* idx = (i64*)malloc(sizeof(i64) * (size_t)n);
+    for (i64 j = 0; j < n; ++j) { key[j] = or_perm_key(seed, round, -1, j); idx[j] = j; }
+    or_sort_by_key(key, idx, n);
+    for (i64 t = 0; t < m; ++t) P_out[t] = idx[t];
+    free(key);
+    free(idx);
+    return m;
+}
+
+/* Permutation of the working set for one randomized pass ("randomized
+ * passes"; reading R10): P sorted by (key(seed, round, pass, j), j). */
+void or_make_perm(const i64* P, i64 m, u64 seed, i64 round, i64 pass, i64* out) {
+    u64* key = (u64*)malloc(sizeof(u64) * (size_t)(m > 0 ? m : 1));
+    for (i64 t = 0; t < m; ++t) { out[t] = P[t]; key[t] = or_perm_key(seed, round, pass, P[t]); }
+    or_sort_by_key(key, out, m);
+    free(key);
+}
+
+/* One exact coordinate step (App. D, eta = 0 for Lasso):
+ *   Lasso: gamma = (alpha_j ||a_j||^2 - a_j^T v~) / ||a_j||^2,
+ *                      tau = lambda d / ||a_j||^2,  alpha' = sign(gamma) [|gamma| - tau]_+
+ *   SVM: Delta = (y_j - a_j^T v^ /(lambda n)) / (||a_j||^2 /(lambda n)),
+ *                      alpha' = y_j max(0, min(1, y_j (alpha_j + Delta)))
+ * s = a_j^T v~ (Lasso, v~ = A alpha - b) or a_j^T v^ (SVM, v^ = A alpha).
+ * Zero column (reading R5): the exact 1-D minimiser, Lasso 0, SVM y_j. */
+double or_coord_update(int model, double alpha_j, double s, double norm, double y_j,
+                       double lambda, i64 d, i64 n) {
+    if (model == OR_LASSO) {
+        if (norm == 0.0) return 0.0;
+        double gamma = (alpha_j * norm - s) / norm;
+        double tau = lambda * (double)d / norm;
+        double mag = fabs(gamma) - tau;
+        if (mag <= 0.0) return 0.0;
+        return gamma > 0.0 ? mag : -mag;
+    } else {
+        if (norm == 0.0) return y_j;
+        double ln = lambda * (double)n;
+        double delta = (y_j - s / ln) / (norm / ln);
+        double u = y_j * (alpha_j + delta);
+        if (u < 0.0) u = 0.0;
+        if (u > 1.0) u = 1.0;
+        return y_j * u;
+    }
+}
+
+/* Sequential SCD over `order` (one randomized pass; App. D, TPA-SCD run with
+ * one coordinate at a time): s = a_j^T vt; alpha' by the closed form;
+ * vt += (alpha' - alpha_j) a_j; alpha_j = alpha'.   vt is v~ (Lasso) or v^ (SVM). */
+void or_scd_pass(int model, const float* A, i64 d, i64 n, i64 ld, const double* norms,
+                 const double* y, double lambda, double* alpha, double* vt, const i64* order,
+                 i64 len) {
+    for (i64 t = 0; t < len; ++t) {
+        i64 j = order[t];
+        const float* a = A + j * ld;
+        double s = 0.0;
+        for (i64 r = 0; r < d; ++r) s += (double)a[r] * vt[r];
+        double yj = (model == OR_SVM) ? y[j] : 0.0;
+        double an = or_coord_update(model, alpha[j], s, norms[j], yj, lambda, d, n);
+        double delta = an - alpha[j];
+        if (delta != 0.0)
+            for (i64 r = 0; r < d; ++r) vt[r] += delta * (double)a[r];
+        alpha[j] = an;
+    }
+}
+
+/* Certificate (Eq. 2 / Eq. 4, App. E) plus the independent O - D cross-check.
+ * Recomputes v = A alpha from scratch.  Returns gap = sum_i gap_i and
+ *   Lasso: primal O = (1/2d)||w||^2 + lambda ||alpha||_1 (w = v - b),
+ *          dual  D = -(u^T b + (d/2)||u||^2) - sum_i B [|a_i^T u| - lambda]_+,  u = w/d
+ *   SVM:   primal O = -(1/n) sum y_i alpha_i + ||v||^2/(2 lambda n^2)
+ *          dual  D = -P(w) = -[(1/n) sum_i max(0, 1 - y_i a_i^T w) + (lambda/2)||w||^2]
+ * so that gap == O - D in exact arithmetic.  b_or_y = b (Lasso) / y (SVM). */
+int or_duality_gap(int model, const float* A, i64 d, i64 n, i64 ld, const double* alpha,
+                   const double* b_or_y, double lambda, double B, double* gap, double* primal,
+                   double* dual) {
+    double* v = (double*)malloc(sizeof(double) * (size_t)d);
+    double* w = (double*)malloc(sizeof(double) * (size_t)d);
+    double* s = (double*)malloc(sizeof(double) * (size_t)n);
+    double* g = (double*)malloc(sizeof(double) * (size_t)n);
+    or_matvec(A, d, n, ld, alpha, v);
+    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    const double* y = (model == OR_SVM) ? b_or_y : NULL;
+    or_primal_dual_w(model, v, b, d, n, lambda, w);
+    int st = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, s, g);
+    double G = 0.0;
+    for (i64 i = 0; i < n; ++i) G += g[i];
+    double O = 0.0, D = 0.0;
+    if (model == OR_LASSO) {
+        double ww = 0.0, l1 = 0.0, ub = 0.0, uu = 0.0, conj = 0.0;
+        for (i64 k = 0; k < d; ++k) ww += w[k] * w[k];
+        for (i64 i = 0; i < n; ++i) l1 += fabs(alpha[i]);
+        O = ww / (2.0 * (double)d) + lambda * l1;
+        for (i64 k = 0; k < d; ++k) {
+            double u = w[k] / (double)d;
+            ub += u * b[k];
+            uu += u * u;
+        }
+        for (i64 i = 0; i < n; ++i) {
+            double x = fabs(s[i] / (double)d) - lambda;
+            conj += B * (x > 0.0 ? x : 0.0);
+        }
+        D = -(ub + 0.5 * (double)d * uu) - conj;
+    } else {
+        double vv = 0.0, ya = 0.0, hinge = 0.0, ww = 0.0;
+        for (i64 k = 0; k < d; ++k) vv += v[k] * v[k];
+        for (i64 i = 0; i < n; ++i) ya += y[i] * alpha[i];
+        O = -ya / (double)n + vv / (2.0 * lambda * (double)n * (double)n);
+        for (i64 i = 0; i < n; ++i) {
+            double h = 1.0 - y[i] * s[i];
+            hinge += (h > 0.0 ? h : 0.0);
+        }
+        for (i64 k = 0; k < d; ++k) ww += w[k] * w[k];
+        D = -(hinge / (double)n + 0.5 * lambda * ww);
+    }
+    *gap = G;
+    if (primal) *primal = O;
+    if (dual) *dual = D;
+    free(v);
+    free(w);
+    free(s);
+    free(g);
+    return st;
+}
+
+/* Plain SCD over all n coordinates: the paper's single-threaded CPU baseline
+ * (P:406).  One permutation of [n] per epoch (key(seed, epoch, 0, j)),
+ * certificate after every epoch; stop at gap <= eps.  alpha (in/out) starts as
+ * given.  Returns OR_OK, or OR_E_NOT_CONVERGED after max_epochs. */
+int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* b_or_y,
+                 double lambda, double eps, i64 max_epochs, u64 seed, double* alpha,
+                 double* gap_out, i64* epochs_out) {
+    double* norms = (double*)malloc(sizeof(double) * (size_t)n);
+    double* vt = (double*)malloc(sizeof(double) * (size_t)d);
+    i64* all = (i64*)malloc(sizeof(i64) * (size_t)n);
+    i64* perm = (i64*)malloc(sizeof(i64) * (size_t)n);
+    or_col_norms(A, d, n, ld, norms);
+    double B = (model == OR_LASSO) ? or_lasso_B(b_or_y, d, lambda) : 0.0;
+    const double* y = (model == OR_SVM) ? b_or_y : NULL;
+    or_matvec(A, d, n, ld, alpha, vt);
+    if (model == OR_LASSO)
+        for (i64 k = 0; k < d; ++k) vt[k] -= b_or_y[k];
+    for (i64 i = 0; i < n; ++i) all[i] = i;
+    int st = OR_E_NOT_CONVERGED;
+    double gap = INFINITY;
+    i64 e = 0;
+    for (e = 0; e < max_epochs; ++e) {
+        or_make_perm(all, n, seed, e, 0, perm);
+        or_scd_pass(model, A, d, n, ld, norms, y, lambda, alpha, vt, perm, n);
+        int s2 = or_duality_gap(model, A, d, n, ld, alpha, b_or_y, lambda, B, &gap, NULL, NULL);
+        if (s2 != OR_OK) { st = s2; ++e; break; }
+        if (gap <= eps) { st = OR_OK; ++e; break; }
+    }
+    *gap_out = gap;
+    if (epochs_out) *epochs_out = e;
+    free(norms);
+    free(vt);
+    free(all);
+    free(perm);
+    return st;
+}
+
+/* DuHL, Algorithm 2, deterministic semantics (DESIGN.md readings
+ * R6, R8, R9, R10):
+ *   init  alpha = 0 (given alpha is used as is), z_i = gap_i(alpha) for all i      (R6)
+ *   round t:
+ *     1. P = select(z)   -- Eq. 11 top-m for policy 0; baselines 1/2          (l.3)
+ *     2. swaps = |P \ P_prev|                                                   (l.4)
+ *     3. unit A: z_j := gap_j(alpha^(t)) for the k = refresh_count columns of
+ *        the rotating cursor (refresh_count = n: o-DuHL)  at the round-start
+ *        state                                                            (l.7-10, R8)
+ *     4. unit B: `passes` randomized SCD passes over P, permutation
+ *        key(seed, t, pass, j); alpha and v~ updated in place (gamma = 1)    (l.6, l.11)
+ *     5. z_P := gap_P(alpha^(t+1))                                              (R9)
+ *     6. every cert_every rounds: certificate; stop at gap <= eps
+ * Trace arrays (length >= max_rounds, may be NULL): swaps, certified gap (-1 if
+ * not computed that round). */
+/* w from the shared vector: Lasso w = v~ (P:855 with v~ = A alpha - b),
+ * SVM w = v^/(lambda n). */
+static void or_shadow_w(int model, const double* vt, i64 d, i64 n, double lambda, double* w) {
+    for (i64 k = 0; k < d; ++k) w[k] = (model == OR_LASSO) ? vt[k] : vt[k] / (lambda * (double)n);
+}
+
+typedef struct {
+    int model;
+    int policy;           /* 0 gap top-m, 1 sequential, 2 uniform */
+    i64 m;
+    int passes;
+    i64 refresh_count;    /* unit-A refreshes per round (rotating cursor) */
+    double eps;
+    i64 max_rounds;
+    i64 cert_every;
+    u64 seed;
+} or_duhl_cfg;
+
+int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
+                  const double* b_or_y, double lambda, double* alpha, double* z,
+                  i64* rounds_out, double* gap_out, i64* trace_swaps, double* trace_gap) {
+    int model = cfg->model;
+    i64 m = cfg->m;
+    if (m < 1 || m > n) return OR_E_INVALID;
+    double* norms = (double*)malloc(sizeof(double) * (size_t)n);
+    double* v = (double*)malloc(sizeof(double) * (size_t)d);
+    double* vt = (double*)malloc(sizeof(double) * (size_t)d);
+    double* w = (double*)malloc(sizeof(double) * (size_t)d);
+    i64* P = (i64*)malloc(sizeof(i64) * (size_t)m);
+    i64* perm = (i64*)malloc(sizeof(i64) * (size_t)m);
+    i64* idx = (i64*)malloc(sizeof(i64) * (size_t)n);
+    double* gtmp = (double*)malloc(sizeof(double) * (size_t)n);
+    char* in_prev = (char*)calloc((size_t)n, 1);
+    char* in_cur = (char*)calloc((size_t)n, 1);
+    const double* y = (model == OR_SVM) ? b_or_y : NULL;
+    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    or_col_norms(A, d, n, ld, norms);
+    double B = (model == OR_LASSO) ? or_lasso_B(b, d, lambda) : 0.0;
+    int st = OR_E_NOT_CONVERGED;
+    double gap = INFINITY;
+
+    /* state: the shared vector of App. D, v~ = A alpha - b (Lasso) or
+     * v^ = A alpha (SVM); w follows from it (App. E). */
+    or_matvec(A, d, n, ld, alpha, v);
+    for (i64 r = 0; r < d; ++r) vt[r] = (model == OR_LASSO) ? v[r] - b[r] : v[r];
+    or_shadow_w(model, vt, d, n, lambda, w);
+    int s0 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
+    if (s0 != OR_OK) st = s0;
+    i64 cursor = 0, t = 0;
+    for (t = 0; t < cfg->max_rounds && s0 == OR_OK; ++t) {
+        /* 1. selection */
+        i64 mt = or_select_policy(cfg->policy, n, m, t, cfg->seed, z, P);
+        /* 2. swap accounting */
+        i64 swaps = 0;
+        memset(in_cur, 0, (size_t)n);
+        for (i64 q = 0; q < mt; ++q) { in_cur[P[q]] = 1; if (!in_prev[P[q]]) ++swaps; }
+        memcpy(in_prev, in_cur, (size_t)n);
+        if (trace_swaps) trace_swaps[t] = swaps;
+        /* 3. unit A refresh at the round-start state (w from alpha^(t)) */
+        or_shadow_w(model, vt, d, n, lambda, w);
+        i64 k = cfg->refresh_count < n ? cfg->refresh_count : n;
+        for (i64 q = 0; q < k; ++q) idx[q] = (cursor + q) % n;
+        cursor = (cursor + k) % n;
+        if (k > 0) {
+            int s1 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, idx, k, NULL, gtmp);
+            if (s1 != OR_OK) { st = s1; break; }
+            for (i64 q = 0; q < k; ++q) z[idx[q]] = gtmp[q];
+        }
+        /* 4. unit B: randomized SCD passes on P, updating alpha and the shared vector */
+        for (int p = 0; p < cfg->passes; ++p) {
+            or_make_perm(P, mt, cfg->seed, t, p, perm);
+            or_scd_pass(model, A, d, n, ld, norms, y, lambda, alpha, vt, perm, mt);
+        }
+        /* 5. refresh z on P at the new state */
+        or_shadow_w(model, vt, d, n, lambda, w);
+        int s5 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, P, mt, NULL, gtmp);
+        if (s5 != OR_OK) { st = s5; break; }
+        for (i64 q = 0; q < mt; ++q) z[P[q]] = gtmp[q];
+        /* 6. certificate */
+        if (trace_gap) trace_gap[t] = -1.0;
+        if (cfg->cert_every > 0 && ((t + 1) % cfg->cert_every == 0)) {
+            int s6 = or_duality_gap(model, A, d, n, ld, alpha, b_or_y, lambda, B, &gap, NULL, NULL);
+            if (trace_gap) trace_gap[t] = gap;
+            if (s6 != OR_OK) { st = s6; break; }
+            if (gap <= cfg->eps) { st = OR_OK; ++t; break; }
+        }
+    }
+    *rounds_out = t;
+    *gap_out = gap;
+    free(norms); free(v); free(vt); free(w); free(P); free(perm); free(idx); free(gtmp);
+    free(in_prev); free(in_cur);
+    return st;
+}

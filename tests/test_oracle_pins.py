@@ -1,0 +1,364 @@
+"""Pins that tie the CPU oracle to what the paper and mathematics fix.
+
+None of these re-types an oracle formula: each compares the oracle against a
+hand-evaluated worked example (tests/golden), a closed form, an invariant, a
+textbook generator, brute force on tiny inputs, or a library solver with the
+paper's exact objective (scikit-learn, scipy).
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(name):
+    return np.loadtxt(os.path.join(GOLD, name), comments="#")
+
+
+# ----------------------------------------------------------------------------- P1 / P2
+def test_P1_lasso_worked_example():
+    """P:758 objective, P:852 gap, P:848 B on A = I2, b = (1,1), lambda = 0.25."""
+    A = np.eye(2, dtype=np.float32)
+    b = np.ones(2)
+    lam = 0.25
+    B = O.lasso_B(b, lam)
+    assert B == 2.0
+    for a1, a2, g1, g2, tot, obj in _load("lasso_identity_2x2.txt"):
+        alpha = np.array([a1, a2])
+        v = O.matvec(A, alpha)
+        w = O.primal_dual_w(O.LASSO, v, b, 2, lam)
+        st, s, g = O.coord_gaps(O.LASSO, A, alpha, None, w, lam, B)
+        assert st == O.OK
+        np.testing.assert_allclose(g, [g1, g2], atol=1e-15)
+        st, G, Ob, D = O.duality_gap(O.LASSO, A, alpha, b, lam, B)
+        assert st == O.OK and abs(G - tot) < 1e-15 and abs(Ob - obj) < 1e-15
+        assert abs((Ob - D) - tot) < 1e-14
+
+
+def test_P2_svm_worked_example():
+    """P:773 dual, P:862 primal, P:867 gap on A = I2, y = (+1,-1)."""
+    A = np.eye(2, dtype=np.float32)
+    y = np.array([1.0, -1.0])
+    for lam, a1, a2, g1, g2, tot, dual_obj, primal in _load("svm_identity_2x2.txt"):
+        alpha = np.array([a1, a2])
+        v = O.matvec(A, alpha)
+        w = O.primal_dual_w(O.SVM, v, None, 2, lam)
+        st, s, g = O.coord_gaps(O.SVM, A, alpha, y, w, lam)
+        assert st == O.OK
+        np.testing.assert_allclose(g, [g1, g2], atol=1e-15)
+        st, G, Ob, D = O.duality_gap(O.SVM, A, alpha, y, lam)
+        assert abs(G - tot) < 1e-15 and abs(Ob - dual_obj) < 1e-15 and abs(-D - primal) < 1e-15
+
+
+def test_P2_svm_zero_state_gap_is_one():
+    """alpha = 0 => gap_i = 1/n exactly, total 1."""
+    A, y = synth.svm_dense(37, 301, seed=5)
+    n = A.shape[0]
+    w = O.primal_dual_w(O.SVM, np.zeros(37), None, n, 0.01)
+    st, s, g = O.coord_gaps(O.SVM, A, np.zeros(n), y, w, 0.01)
+    assert np.all(g == 1.0 / n)
+    st, G, Ob, D = O.duality_gap(O.SVM, A, np.zeros(n), y, 0.01)
+    assert abs(G - 1.0) < 1e-13 and Ob == 0.0
+
+
+# ----------------------------------------------------------------------------- P3 / P4
+def _numpy_objectives(model, A, alpha, b_or_y, lam):
+    """O and D from the paper's objective and conjugate definitions, in numpy.
+
+    Lasso: f(v) = ||v - b||^2/(2d), g_i = lam |.| on |alpha_i| <= B;
+      f*(u) = u^T b + (d/2)||u||^2, g_i*(x) = B [|x| - lam]_+,  u = grad f(A alpha).
+    SVM: dual objective P:773 and primal P:862."""
+    A64 = A.astype(np.float64)
+    n, d = A64.shape
+    v = A64.T @ alpha
+    if model == O.LASSO:
+        b = b_or_y
+        B = (b @ b) / (2 * lam * d)
+        Ob = ((v - b) @ (v - b)) / (2 * d) + lam * np.abs(alpha).sum()
+        u = (v - b) / d
+        D = -(u @ b + 0.5 * d * (u @ u)) - B * np.maximum(np.abs(A64 @ u) - lam, 0).sum()
+        return Ob, D
+    y = b_or_y
+    Ob = -(y @ alpha) / n + (v @ v) / (2 * lam * n * n)
+    w = v / (lam * n)
+    P = np.maximum(0, 1 - y * (A64 @ w)).sum() / n + 0.5 * lam * (w @ w)
+    return Ob, -P
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_P3_gap_identity_and_nonnegativity(model):
+    """sum_i gap_i = O(alpha) - D(w) (Eq. 2 / Eq. 4), gap_i >= 0."""
+    rng = np.random.default_rng(3)
+    if model == O.LASSO:
+        A, b = synth.lasso_dense(60, 90, seed=11)
+        lab, lam = b, 0.05
+    else:
+        A, y = synth.svm_dense(40, 120, seed=12)
+        lab, lam = y, 0.02
+    n = A.shape[0]
+    for trial in range(5):
+        if model == O.LASSO:
+            alpha = rng.standard_normal(n) * (rng.random(n) < 0.3) * 0.1
+        else:
+            alpha = y * rng.random(n) * (rng.random(n) < 0.5)
+        B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+        st, G, Ob, D = O.duality_gap(model, A, alpha, lab, lam, B)
+        On, Dn = _numpy_objectives(model, A, alpha, lab, lam)
+        assert abs(Ob - On) <= 1e-12 * max(1, abs(On))
+        assert abs(D - Dn) <= 1e-11 * max(1, abs(Dn))
+        assert abs(G - (On - Dn)) <= 1e-11 * max(1, abs(On) + abs(Dn))
+        v = O.matvec(A, alpha)
+        w = O.primal_dual_w(model, v, lab if model == O.LASSO else None, n, lam)
+        st, s, g = O.coord_gaps(model, A, alpha, None if model == O.LASSO else lab, w, lam, B)
+        assert st == O.OK and np.all(g >= 0)
+        np.testing.assert_allclose(s, A.astype(np.float64) @ w, rtol=1e-12, atol=1e-12)
+
+
+def test_P4_gap_vanishes_at_lasso_kkt_point():
+    """Lasso KKT: |a_i^T w| <= lam d, with equality where alpha_i != 0 => gap_i = 0."""
+    A, b = synth.lasso_dense(80, 40, seed=21)
+    lam = 0.05
+    st, alpha, gap, ep = O.solve_scd(O.LASSO, A, b, lam, 1e-13, 5000, seed=1)
+    assert st == O.OK and gap <= 1e-13
+    w = A.astype(np.float64).T @ alpha - b
+    s = A.astype(np.float64) @ w
+    d = A.shape[1]
+    assert np.all(np.abs(s) <= lam * d * (1 + 1e-6))
+    on = alpha != 0
+    np.testing.assert_allclose(s[on], -np.sign(alpha[on]) * lam * d, rtol=1e-6)
+
+
+# ----------------------------------------------------------------------------- P5 / P6
+def test_P5_lasso_step_hand_examples():
+    """SPEC S:221-222 (App. D.1, eta=0): tau=0.5, gamma=1 => 0.5; lambda=0.5 => 0."""
+    # a_j = (1,0), ||a_j||^2 = 1, alpha_j = 0, v~ = (-1, 0) => s = -1, d = 2
+    assert O.coord_update(O.LASSO, 0.0, -1.0, 1.0, 0.0, 0.25, 2, 2) == 0.5
+    assert O.coord_update(O.LASSO, 0.0, -1.0, 1.0, 0.0, 0.5, 2, 2) == 0.0
+
+
+def test_P6_svm_step_hand_examples():
+    """SPEC S:231-232 (App. D.2): alpha=0, ||a||^2=1, lambda=1, n=1 => +-1."""
+    assert O.coord_update(O.SVM, 0.0, 0.0, 1.0, 1.0, 1.0, 1, 1) == 1.0
+    assert O.coord_update(O.SVM, 0.0, 0.0, 1.0, -1.0, 1.0, 1, 1) == -1.0
+
+
+def test_P5_P6_steps_minimise_1d_objective():
+    """Each closed-form step is the exact 1-D minimiser of the true objective (scipy bounded)."""
+    from scipy.optimize import minimize_scalar
+    rng = np.random.default_rng(7)
+    for _ in range(100):
+        d, n = int(rng.integers(2, 50)), int(rng.integers(2, 50))
+        nrm = float(rng.uniform(0.1, 5))
+        aj = float(rng.normal())
+        s = float(rng.normal() * 3)
+        lam = float(rng.uniform(0.001, 0.5))
+        # Lasso: phi(x) = (1/2d)||v~ + (x - a_j) a||^2 + lam|x| = (1/2d)[2 s (x-aj) + nrm (x-aj)^2] + lam|x|
+        phi = lambda x: (2 * s * (x - aj) + nrm * (x - aj) ** 2) / (2 * d) + lam * abs(x)
+        x = O.coord_update(O.LASSO, aj, s, nrm, 0.0, lam, d, n)
+        r = minimize_scalar(phi, bounds=(-50, 50), method="bounded", options={"xatol": 1e-10})
+        assert phi(x) <= r.fun + 1e-12
+        assert abs(x - r.x) < 1e-6
+        # SVM dual: psi(x) = -y x / n + (1/(2 lam n^2))[2 s (x - aj) + nrm (x - aj)^2], y x in [0, 1]
+        y = float(rng.choice([-1.0, 1.0]))
+        ajs = y * float(rng.uniform(0, 1))
+        psi = lambda x: -y * x / n + (2 * s * (x - ajs) + nrm * (x - ajs) ** 2) / (2 * lam * n * n)
+        x = O.coord_update(O.SVM, ajs, s, nrm, y, lam, d, n)
+        lo, hi = (0.0, 1.0) if y > 0 else (-1.0, 0.0)
+        r = minimize_scalar(psi, bounds=(lo, hi), method="bounded", options={"xatol": 1e-12})
+        cand = min([r.x, lo, hi], key=psi)
+        assert lo - 1e-15 <= x <= hi + 1e-15
+        assert psi(x) <= psi(cand) + 1e-12 * max(1, abs(psi(cand)))
+
+
+# ----------------------------------------------------------------------------- P7 / P8
+def test_P7_hadamard_lasso_closed_form_one_epoch():
+    """Orthogonal design A^T A = d I: alpha* = soft(A^T b, lam d)/d (north_star pin).
+    One sequential epoch in any order reaches it; the gap then vanishes."""
+    d, n = 256, 128
+    A = synth.hadamard_columns(d, n)
+    rng = np.random.default_rng(0)
+    b = rng.integers(-3, 4, size=d).astype(np.float64)
+    lam = 0.1
+    c = A.astype(np.float64) @ b
+    astar = np.sign(c) * np.maximum(np.abs(c) - lam * d, 0) / d
+    assert np.count_nonzero(astar) > 5
+    norms = O.col_norms(A)
+    assert np.all(norms == d)
+    alpha = np.zeros(n)
+    vt = -b.copy()
+    O.scd_pass(O.LASSO, A, norms, None, lam, alpha, vt, synth.permutation(np.arange(n), 3))
+    np.testing.assert_allclose(alpha, astar, atol=1e-14)
+    st, G, Ob, D = O.duality_gap(O.LASSO, A, alpha, b, lam, O.lasso_B(b, lam))
+    assert G < 1e-12
+
+
+def test_P8_orthogonal_sample_svm_closed_form():
+    """Orthogonal samples: y_i alpha_i* = clip(lam n/||a_i||^2, 0, 1), one epoch from 0."""
+    d, n = 64, 32
+    rng = np.random.default_rng(1)
+    scales = rng.uniform(0.5, 2.0, n)
+    A = synth.hadamard_columns(d, n, scales)
+    y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    for lam in (0.01, 1.0):
+        norms = O.col_norms(A)
+        beta = np.clip(lam * n / norms, 0, 1)
+        alpha = np.zeros(n)
+        vt = np.zeros(d)
+        O.scd_pass(O.SVM, A, norms, y, lam, alpha, vt, synth.permutation(np.arange(n), 4))
+        np.testing.assert_allclose(y * alpha, beta, atol=1e-14)
+        st, G, Ob, D = O.duality_gap(O.SVM, A, alpha, y, lam)
+        assert G < 1e-13
+
+
+# ----------------------------------------------------------------------------- P9 / P10
+def _svm_bruteforce(A64, y, lam):
+    """Enumerate beta_i = y_i alpha_i in {0, 1, free}; solve free block stationarity."""
+    n = A64.shape[0]
+    K = (A64 @ A64.T) * np.outer(y, y)
+    best = None
+    for pat in itertools.product((0, 1, 2), repeat=n):
+        beta = np.array([0.0 if p == 0 else 1.0 for p in pat])
+        F = [i for i in range(n) if pat[i] == 2]
+        if F:
+            NF = [i for i in range(n) if pat[i] != 2]
+            rhs = lam * n * np.ones(len(F)) - K[np.ix_(F, NF)] @ beta[NF]
+            sol, *_ = np.linalg.lstsq(K[np.ix_(F, F)], rhs, rcond=None)
+            if np.linalg.norm(K[np.ix_(F, F)] @ sol - rhs) > 1e-9:
+                continue
+            if np.any(sol < -1e-12) or np.any(sol > 1 + 1e-12):
+                continue
+            beta[F] = np.clip(sol, 0, 1)
+        alpha = y * beta
+        v = A64.T @ alpha
+        obj = -(y @ alpha) / n + (v @ v) / (2 * lam * n * n)
+        if best is None or obj < best[0]:
+            best = (obj, v / (lam * n))
+    return best
+
+
+def test_P9_tiny_svm_bruteforce_optimum():
+    rng = np.random.default_rng(9)
+    for trial in range(8):
+        d, n = int(rng.integers(2, 5)), int(rng.integers(3, 7))
+        A = rng.standard_normal((n, d)).astype(np.float32)
+        y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        lam = float(rng.uniform(0.05, 1.0))
+        obj_bf, w_bf = _svm_bruteforce(A.astype(np.float64), y, lam)
+        st, alpha, gap, ep = O.solve_scd(O.SVM, A, y, lam, 1e-12, 200000, seed=trial)
+        assert st == O.OK
+        st, G, Ob, D = O.duality_gap(O.SVM, A, alpha, y, lam)
+        assert Ob - obj_bf <= 1e-11 and obj_bf - Ob <= G + 1e-12
+        w = A.astype(np.float64).T @ alpha / (lam * n)
+        np.testing.assert_allclose(w, w_bf, atol=1e-5)
+
+
+def test_P10_lasso_matches_sklearn_objective():
+    """sklearn Lasso(alpha=lam, fit_intercept=False) minimises exactly P:758."""
+    from sklearn.linear_model import Lasso
+    A, b = synth.lasso_dense(300, 150, seed=31)
+    lam = 0.05
+    st, alpha, gap, ep = O.solve_scd(O.LASSO, A, b, lam, 1e-10, 5000, seed=2)
+    assert st == O.OK
+    X = A.astype(np.float64).T
+    sk = Lasso(alpha=lam, fit_intercept=False, tol=1e-14, max_iter=200000).fit(X, b)
+    obj = lambda a: ((X @ a - b) @ (X @ a - b)) / (2 * len(b)) + lam * np.abs(a).sum()
+    assert abs(obj(alpha) - obj(sk.coef_)) <= 1e-9 * obj(sk.coef_)
+    # certificate dominates suboptimality: gap >= O(alpha) - O*
+    assert gap >= obj(alpha) - obj(sk.coef_) - 1e-12
+
+
+def test_P10_lambda_max_gives_zero_solution():
+    """lam >= ||A^T b||_inf / d => alpha* = 0 and gap(0) = 0."""
+    A, b = synth.lasso_dense(50, 30, seed=32)
+    lam = np.abs(A.astype(np.float64) @ b).max() / 50 * 1.0001
+    st, G, Ob, D = O.duality_gap(O.LASSO, A, np.zeros(30), b, lam, O.lasso_B(b, lam))
+    assert G <= 1e-15
+
+
+# ----------------------------------------------------------------------------- P11
+def test_P11_topm_exhaustive_and_ties():
+    rng = np.random.default_rng(4)
+    for _ in range(60):
+        n = int(rng.integers(1, 9))
+        m = int(rng.integers(1, n + 1))
+        z = rng.integers(0, 4, n).astype(np.float64) * 0.25  # many ties
+        P = O.select_topm(z, m)
+        best = max(sum(z[list(c)]) for c in itertools.combinations(range(n), m))
+        assert abs(z[P].sum() - best) < 1e-15 and len(set(P)) == m
+        # tie rule: among optimal sets, the lexicographically lowest indices
+        thr = np.sort(z)[::-1][m - 1]
+        expect = [i for i in range(n) if z[i] > thr]
+        expect += [i for i in range(n) if z[i] == thr][: m - len(expect)]
+        assert sorted(P.tolist()) == sorted(expect)
+    assert O.select_topm(np.array([3.0, 1, 1, 1]), 2).tolist() == [0, 1]
+    # rho >= 1
+    g = rng.random(1000)
+    P = O.select_topm(g, 100)
+    assert g[P].mean() / g.mean() >= 1
+
+
+def test_baseline_policies():
+    """Sequential blocks (P:401, S:318 example) and uniform sampling without replacement."""
+    seq = [O.select_policy(O.SEL_SEQUENTIAL, 10, 4, r, 0).tolist() for r in range(4)]
+    assert seq == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9], [0, 1, 2, 3]]
+    u = O.select_policy(O.SEL_UNIFORM, 1000, 100, 3, 5)
+    assert len(set(u.tolist())) == 100 and u.min() >= 0 and u.max() < 1000
+    counts = np.zeros(50)
+    for r in range(2000):
+        counts[O.select_policy(O.SEL_UNIFORM, 50, 5, r, 9)] += 1
+    assert abs(counts.mean() - 200) < 1e-9 and counts.std() < 3 * math.sqrt(200)
+
+
+# ----------------------------------------------------------------------------- generator
+def test_counter_generator_is_splitmix64():
+    """or_mix64(x) is one splitmix64 step from state x; splitmix64(seed=0) first output."""
+    assert O.lib().or_mix64(0) == 0xE220A8397B1DCDAF
+    # second output of the splitmix64 stream from 0 = mix(0x9E37..) step
+    assert O.lib().or_mix64(0x9E3779B97F4A7C15) == 0x6E789E6AA1B965F4
+    P = np.arange(10, 60)
+    p1 = O.make_perm(P, 1, 2, 3)
+    assert sorted(p1.tolist()) == P.tolist()
+    keys = [O.perm_key(1, 2, 3, int(j)) for j in p1]
+    assert keys == sorted(keys)
+
+
+# ----------------------------------------------------------------------------- DuHL loop
+def test_duhl_full_block_equals_plain_scd():
+    """m = n: every round selects [n]; the permutation key matches the plain-SCD epoch."""
+    A, b = synth.lasso_dense(100, 60, seed=41)
+    lam = 0.05
+    r = O.duhl_solve(O.LASSO, A, b, lam, m=60, passes=1, eps=1e-9, max_rounds=200, seed=4)
+    st, alpha, gap, ep = O.solve_scd(O.LASSO, A, b, lam, 1e-9, 200, seed=4)
+    assert r["status"] == O.OK and st == O.OK and r["rounds"] == ep
+    assert np.array_equal(r["alpha"], alpha)
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_duhl_converges_to_certified_optimum(model):
+    if model == O.LASSO:
+        A, lab = synth.lasso_dense(200, 400, seed=51)
+        lam = 0.05
+    else:
+        A, lab = synth.svm_dense(30, 400, seed=52)
+        lam = 1.0 / 400
+    n = A.shape[0]
+    res = {}
+    for pol in (O.SEL_GAP, O.SEL_SEQUENTIAL, O.SEL_UNIFORM):
+        r = O.duhl_solve(model, A, lab, lam, m=n // 4, passes=2, policy=pol,
+                         refresh_count=n // 10, eps=1e-6, max_rounds=5000, seed=1)
+        assert r["status"] == O.OK and r["gap"] <= 1e-6, (pol, r["gap"])
+        st, G, Ob, D = O.duality_gap(model, A, r["alpha"], lab, lam,
+                                     O.lasso_B(lab, lam) if model == O.LASSO else 0.0)
+        res[pol] = (r["rounds"], Ob, r["swaps"])
+        assert r["swaps"][0] == n // 4
+    obs = [v[1] for v in res.values()]
+    assert max(obs) - min(obs) <= 2e-6
+    # gap-based selection needs fewer rounds than the sequential scheme (P:433-435 shape)
+    assert res[O.SEL_GAP][0] < res[O.SEL_SEQUENTIAL][0]
