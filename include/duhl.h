@@ -1,0 +1,172 @@
+/*
+ * duhl.h -- C ABI of the B200-native DuHL hot path (arXiv 1708.05357).
+ *
+ * DuHL ("Duality-gap based Heterogeneous Learning", Alg. 2)
+ * trains a generalized linear model  min_alpha  f(A alpha) + sum_i g_i(alpha_i)
+ * (Eq. 1) when A (d x n, columns a_i) is larger than accelerator memory:
+ *   - unit A = pinned host DRAM holding all of A,
+ *   - unit B = B200 HBM holding the working set A_[P] (|P| = m) under a budget.
+ * Each round selects the m coordinates with the largest (time-delayed) duality
+ * gaps z (Eq. 11), swaps their columns into HBM, runs randomized
+ * coordinate-descent passes on them (App. D) and refreshes z
+ * (Alg. 2 l.7-10).  Models:
+ *   DUHL_LASSO    (App. C eq. lassoobj):  (1/2d)||A alpha - b||^2 + lambda ||alpha||_1
+ *   DUHL_SVM_DUAL (App. C eq. dualsvm,  P:773):  (1/n) sum(-y_i alpha_i)
+ *                                                + (1/(2 lambda n^2)) ||A alpha||^2,  y_i alpha_i in [0,1]
+ *
+ * Conventions (all entry points):
+ *   - Every function returns a duhl_status; 0 = DUHL_OK.  Nothing throws across
+ *     the ABI.  On error, duhl_last_error(ctx) holds a message (owned by ctx,
+ *     valid until the next call on that ctx).
+ *   - Pointers named *_host / marked "host" are host memory owned by the caller;
+ *     the library never keeps them past the call unless cfg.borrow_host = 1.
+ *   - A duhl_ctx is not thread-safe; distinct contexts are independent.
+ *   - Matrices are dense, column-major float32: column a_i starts at
+ *     values + i*ld, ld >= d (Eq. 1: A = [a_1 ... a_n]).
+ *   - Vectors alpha, z, gaps are float64 of length n; v, b are float64 of length d.
+ *   - "shared vector" v~ = A alpha - b (Lasso) or v^ = A alpha (SVM)
+ *     is the state unit B updates; w (App. E) = v~ (Lasso) or v^/(lambda n) (SVM).
+ *   - All work runs in the library's CUDA kernels for sm_100a on cfg.device;
+ *     there is no CPU fallback: without a usable B200 every call that computes
+ *     returns DUHL_E_CUDA.
+ */
+#ifndef DUHL_H
+#define DUHL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct duhl_ctx duhl_ctx; /* opaque; one per problem instance */
+
+typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1 } duhl_model;
+
+/* Block selection policies: Eq. 11 gap memory, and the paper's
+ * reference schemes: sequential blocks [Yu 2012], uniform. */
+typedef enum { DUHL_SEL_GAP = 0, DUHL_SEL_SEQUENTIAL = 1, DUHL_SEL_UNIFORM = 2 } duhl_policy;
+
+typedef enum {
+    DUHL_OK = 0,
+    DUHL_E_INVALID = 2,       /* bad argument: d,n < 1, non-finite data, y not +-1, lambda <= 0, m > n, budget too small */
+    DUHL_E_IO = 3,
+    DUHL_E_NUMERIC = 4,       /* non-finite state, or a gap below -1e-12 x its scale (reading R17) */
+    DUHL_E_BOUND = 5,         /* Lasso |alpha_i| > B: the Lipschitzing bound was violated */
+    DUHL_E_NOMEM = 6,
+    DUHL_E_CUDA = 7,          /* CUDA runtime failure or no sm_100 device */
+    DUHL_E_NCCL = 8,
+    DUHL_E_NOT_CONVERGED = 9  /* max_rounds reached; outputs are still valid */
+} duhl_status;
+
+typedef struct {
+    int64_t d;            /* rows (Lasso: samples; SVM: features) */
+    int64_t n;            /* columns = coordinates of alpha (Lasso: features; SVM: samples) */
+    const float* values;  /* host, column-major: a_i at values + i*ld */
+    int64_t ld;           /* leading dimension, ld >= d */
+} duhl_matrix;
+
+typedef struct {
+    size_t hbm_budget_bytes;  /* HBM for the working-set slot pool; 0 = all n columns resident */
+    int64_t m;                /* working-set size |P|; 0 = as many columns as the budget holds (n if budget 0) */
+    int device;               /* CUDA device ordinal */
+    int scd_block;            /* W: coordinates per Gram block of the exact SCD kernel; 0 = auto */
+    int scd_ctas;             /* CTAs of the SCD epoch (row partition); 0 = auto */
+    double refresh_fraction;  /* unit-A refresh per round, fraction of n (rotating cursor, reading R8); 1 = o-DuHL */
+    int64_t cert_every;       /* certificate (full duality gap) every R rounds in duhl_solve; >= 1 */
+    uint64_t seed;            /* seeds the counter-based permutation generator */
+    int borrow_host;          /* 1: pin the caller's matrix in place (it must outlive the ctx); 0: copy */
+} duhl_config;
+
+/* One entry per round of duhl_solve (SPEC RoundTrace columns). */
+typedef struct {
+    int64_t round;
+    int64_t swaps;            /* |P_t \ P_{t-1}|: columns copied host -> HBM (Fig. 4b) */
+    int64_t refreshed;        /* unit-A gap refreshes this round */
+    double cert_gap;          /* certified duality gap after the round; -1 if not computed */
+    double time_s;            /* wall seconds since duhl_solve entry, after the round */
+} duhl_round_record;
+
+/* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,
+ * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0. */
+void duhl_default_config(duhl_config* cfg);
+
+/* Creates a problem instance.
+ *   A       host dense matrix (copied into library-owned pinned memory unless borrow_host)
+ *   b_or_y  host float64: Lasso b[d] (labels); SVM y[n] in {-1,+1}
+ *   lambda  > 0: Lasso L1 weight; SVM L2 weight
+ * Precomputes ||a_i||^2 and B = ||b||^2/(2 lambda d), sets alpha = 0 and
+ * the gap memory z to the exact gaps at alpha = 0 (reading R6).
+ * Errors: DUHL_E_INVALID, DUHL_E_NOMEM, DUHL_E_CUDA.  *out = NULL on error. */
+duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambda,
+                        duhl_model model, const duhl_config* cfg, duhl_ctx** out);
+
+duhl_status duhl_destroy(duhl_ctx* ctx);
+
+/* Duality-gap pass (Eq. 4; App. E closed forms P:852 / P:867) at the
+ * current state for the k columns idx[0..k) (host int64; idx = NULL: all n
+ * columns, k ignored).  Writes z_i = max(gap_i, 0) into the gap memory and, if
+ * non-NULL, gap_i to z_out[k] and s_i = a_i^T w to s_out[k] (host float64).
+ * Resident columns are read from HBM, the others from pinned host memory.
+ * Errors: DUHL_E_INVALID (index out of range), DUHL_E_NUMERIC, DUHL_E_CUDA. */
+duhl_status duhl_gaps(duhl_ctx* ctx, const int64_t* idx, int64_t k, double* z_out, double* s_out);
+
+/* Working-set selection (Eq. 11 for DUHL_SEL_GAP: the m largest z, ties to the
+ * lowest index, reading R7) for round `round`, then stages A_[P] into the HBM
+ * slot pool (Alg. 2 l.4).  m = 0 uses cfg.m.  P_out (host int64[m], may be NULL)
+ * receives P in ascending index order; *n_swaps_out (may be NULL) the number of
+ * columns copied host -> HBM.  Errors: DUHL_E_INVALID (m > n or > pool), DUHL_E_CUDA. */
+duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t round,
+                        int64_t* P_out, int64_t* n_swaps_out);
+
+/* `passes` randomized coordinate-descent passes over the working set (App. D:
+ * Lasso soft-threshold step P:804-815 with eta = 0, SVM box step P:824-827),
+ * updating alpha_P and the shared vector.  The pass-p order is P sorted by
+ * key(seed, round, p, j).  If perm (host int64) is
+ * given, exactly one pass is run in the order perm[0..perm_len), whose entries
+ * must be distinct, resident members of P.  The kernel executes the sequential
+ * SCD semantics exactly (Gram-block reformulation).
+ * Errors: DUHL_E_INVALID, DUHL_E_CUDA. */
+duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round,
+                           const int64_t* perm, int64_t perm_len);
+
+/* Certificate (Eq. 2 = sum of Eq. 4 terms) at the current state over all n
+ * columns, plus the primal objective O(alpha) and the dual value D so that
+ * gap = O - D (D per App. E conjugates).  Any output may be NULL.
+ * Errors: DUHL_E_NUMERIC, DUHL_E_BOUND (Lasso max|alpha_i| > B), DUHL_E_CUDA. */
+duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double* dual);
+
+/* DuHL rounds (Alg. 2): select -> swap -> [unit-A refresh of
+ * ceil(refresh_fraction n) gaps at the round-start state] -> `passes` SCD
+ * passes -> refresh z_P at the new state; certificate every cfg.cert_every
+ * rounds; stops when the certified gap <= eps.  trace (host, may be NULL)
+ * receives up to trace_cap records.  Returns DUHL_OK when certified,
+ * DUHL_E_NOT_CONVERGED after max_rounds (outputs valid). */
+duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes,
+                       duhl_policy policy, duhl_round_record* trace, int64_t trace_cap,
+                       int64_t* rounds_out, double* gap_out);
+
+/* Copies the state to host buffers (any may be NULL): alpha[n], shared vector
+ * v[d] (v~ or v^ as above), gap memory z[n]. */
+duhl_status duhl_get_state(duhl_ctx* ctx, double* alpha_out, double* v_out, double* z_out);
+
+/* Sets alpha (host float64[n]; SVM entries must satisfy y_i alpha_i in [0,1]),
+ * recomputes the shared vector exactly from A and resets z to the exact gaps. */
+duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha);
+
+/* Device-side view for callers that time kernels on their own stream:
+ * returns the CUDA stream (cudaStream_t) all compute of ctx is issued on. */
+duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out);
+
+/* Counters since creation: kernel launches issued, bytes copied host->device,
+ * SCD coordinate updates.  Any may be NULL. */
+duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes,
+                              int64_t* updates);
+
+const char* duhl_last_error(const duhl_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DUHL_H */

@@ -1,0 +1,164 @@
+// device.cuh -- sm_100a device helpers for the DuHL kernels (no host code).
+//
+// PTX wrappers for the Blackwell async-copy path (mbarrier + cp.async.bulk,
+// SASS UBLKCP / SYNCS), acquire/release global accesses for the grid barrier,
+// warp reductions in fp64, and the closed-form coordinate/gap arithmetic of the
+// paper (App. D, App. E).  Independent of oracle/ (shares nothing with it).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace duhl {
+
+constexpr int kLasso = 0;
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+constexpr int kSvm = 1;
+
+// ---------------------------------------------------------------- counter RNG
+// splitmix64 finaliser; permutation key(seed, round, pass, j) (DESIGN.md
+// "Randomness").  Written independently of the oracle's copy of the same
+// documented generator.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t perm_key(uint64_t seed, int64_t round, int64_t pass,
+                                                      int64_t j) {
+    uint64_t h = mix64(seed);
+    h = mix64(h ^ (uint64_t)round);
+    h = mix64(h ^ (uint64_t)pass);
+    return mix64(h ^ (uint64_t)j);
+}
+
+// ---------------------------------------------------------------- closed forms
+// Exact coordinate step (App. D).  s = a_j^T v~ (Lasso, v~ = A alpha - b) or
+// a_j^T v^ (SVM, v^ = A alpha); nrm = ||a_j||^2.
+//   Lasso, eta = 0: gamma = (alpha nrm - s)/nrm, tau = lambda d/nrm,
+//                               alpha' = sign(gamma) max(|gamma| - tau, 0)
+//   SVM: Delta = (y - s/(lambda n)) / (nrm/(lambda n)),
+//                    alpha' = y clip(y (alpha + Delta), 0, 1)
+// Zero column: the exact 1-D minimiser (Lasso 0, SVM y) -- reading R5.
+__device__ __forceinline__ double coord_step(int model, double alpha, double s, double nrm,
+                                             double y, double lambda, double dd, double nn) {
+    if (model == kLasso) {
+        if (nrm == 0.0) return 0.0;
+        double gamma = (alpha * nrm - s) / nrm;
+        double tau = lambda * dd / nrm;
+        double mag = fabs(gamma) - tau;
+        if (mag <= 0.0) return 0.0;
+        return gamma > 0.0 ? mag : -mag;
+    }
+    if (nrm == 0.0) return y;
+    double ln = lambda * nn;
+    double delta = (y - s / ln) / (nrm / ln);
+    double u = y * (alpha + delta);
+    u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
+    return y * u;
+}
+
+// Per-coordinate gap, Eq. 4 with the App. E closed forms; s = a_i^T w.
+//   Lasso: (1/d)[alpha s + B max(|s| - lambda d, 0) + lambda d |alpha|]
+//   SVM: (1/n)[alpha s + max(0, 1 - y s) - y alpha]
+// Returns the raw gap; *scale receives the magnitude of its terms (for the
+// negative-gap check, reading R17); *aux receives the conjugate / loss term
+// used by the certificate: Lasso B max(|s|/d - lambda, 0), SVM max(0, 1 - y s).
+__device__ __forceinline__ double coord_gap(int model, double alpha, double s, double y,
+                                            double lambda, double B, double dd, double nn,
+                                            double* scale, double* aux) {
+    if (model == kLasso) {
+        double lam_d = lambda * dd;
+        double thr = fabs(s) - lam_d;
+        double t1 = alpha * s, t2 = B * (thr > 0.0 ? thr : 0.0), t3 = lam_d * fabs(alpha);
+        *scale = (fabs(t1) + t2 + t3) / dd;
+        double x = fabs(s / dd) - lambda;
+        *aux = B * (x > 0.0 ? x : 0.0);
+        return (t1 + t2 + t3) / dd;
+    }
+    double h = 1.0 - y * s;
+    double t1 = alpha * s, t2 = (h > 0.0 ? h : 0.0), t3 = y * alpha;
+    *scale = (fabs(t1) + t2 + fabs(t3)) / nn;
+    *aux = t2;
+    return (t1 + t2 - t3) / nn;
+}
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- memory model
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_cg_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {  // streamed once: no L1 allocate
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).  `bar` is
+// a monotone counter zeroed before the launch; generation g waits for
+// (g+1)*nblocks arrivals.  __syncthreads + gpu-scope fence make every prior
+// write of the CTA visible before the arrival (fence cumulativity).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_u32(bar) < target) { __nanosleep(32); }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA engine), completion on mbarrier.
+// bytes % 16 == 0, both addresses 16-B aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+}  // namespace duhl

@@ -1,0 +1,729 @@
+// duhl.cu -- host runtime and C ABI of the B200-native DuHL hot path.
+//
+// Unit A (PAPER.md Assumption 1) = pinned host DRAM holding all of A,
+// mapped into the device address space; unit B = HBM holding the working set
+// A_[P] in a slot pool sized by cfg.hbm_budget_bytes.  Selected columns are
+// staged with cudaMemcpyAsync on a copy stream (Alg. 2 l.4); the compute stream
+// waits on an event before the SCD epoch.  See include/duhl.h for the contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/duhl.h"
+#include "kernels.h"
+
+using namespace duhl;
+
+namespace {
+constexpr int kGapTileRows = 4096;
+inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
+}  // namespace
+
+struct duhl_ctx {
+    // ---- problem
+    int model = 0;
+    int64_t d = 0, d4 = 0, n = 0;
+    double lambda = 0, B = 0;
+    duhl_config cfg{};
+    std::string err;
+    int dev = 0, nsm = 0;
+    cudaStream_t st = nullptr, cst = nullptr;
+    cudaEvent_t ev_copy = nullptr;
+    // ---- unit A: pinned host store
+    float* h_store = nullptr;
+    bool own_store = false, registered = false;
+    int64_t ld_host = 0;
+    const float* h_alias = nullptr;  // device address of h_store
+    // ---- unit B: HBM slot pool
+    float* pool = nullptr;
+    int64_t S = 0, ld_dev = 0, m_cfg = 0;
+    std::vector<int> col_slot, slot_col;
+    int* d_col_slot = nullptr;
+    // ---- state
+    double *d_alpha = nullptr, *d_vt = nullptr, *d_b = nullptr, *d_y = nullptr;
+    double *d_norms = nullptr, *d_z = nullptr;
+    // ---- working set
+    std::vector<int64_t> P;      // current working set, ascending
+    std::vector<char> inP;       // [n]
+    int64_t *d_P = nullptr, *d_order_j = nullptr, *d_cols = nullptr, *d_chg_cols = nullptr;
+    int *d_P_slot = nullptr, *d_order_slot = nullptr, *d_chg_slots = nullptr;
+    uint64_t *d_keys = nullptr, *d_keys2 = nullptr;
+    int *d_idx = nullptr, *d_idx2 = nullptr;
+    void* d_sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    // ---- gap scratch
+    double *d_s_acc = nullptr, *d_gap_out = nullptr, *d_s_out = nullptr, *d_sums = nullptr;
+    int* d_flag = nullptr;
+    // ---- SCD
+    double* d_red = nullptr;
+    unsigned* d_bar = nullptr;
+    int W = 0, R = 0, G = 0;
+    // ---- misc
+    int64_t launches = 0, h2d_bytes = 0, updates = 0, cursor = 0;
+};
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+            return DUHL_E_CUDA;                                                       \
+        }                                                                             \
+    } while (0)
+
+#define TRY(call)                          \
+    do {                                   \
+        duhl_status s_ = (call);           \
+        if (s_ != DUHL_OK) return s_;      \
+    } while (0)
+
+static duhl_status fail(duhl_ctx* ctx, duhl_status s, const std::string& msg) {
+    ctx->err = msg;
+    return s;
+}
+
+// ------------------------------------------------------------------------- helpers
+static ColSrc colsrc(const duhl_ctx* ctx) {
+    ColSrc s;
+    s.pool = ctx->pool;
+    s.ld_dev = ctx->ld_dev;
+    s.host = ctx->h_alias;
+    s.ld_host = ctx->ld_host;
+    s.col_slot = ctx->d_col_slot;
+    return s;
+}
+
+static double wscale(const duhl_ctx* ctx) {
+    return ctx->model == DUHL_LASSO ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n);
+}
+
+static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
+    GapParams p{};
+    p.model = ctx->model;
+    p.d = ctx->d;
+    p.d4 = ctx->d4;
+    p.n = ctx->n;
+    p.src = colsrc(ctx);
+    p.cols = d_cols;
+    p.k = k;
+    p.vt = ctx->d_vt;
+    p.wscale = wscale(ctx);
+    p.alpha = ctx->d_alpha;
+    p.y = ctx->d_y;
+    p.lambda = ctx->lambda;
+    p.B = ctx->B;
+    p.s_acc = ctx->d_s_acc;
+    p.z = ctx->d_z;
+    p.flag = ctx->d_flag;
+    return p;
+}
+
+static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (flag) {
+        CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->st));
+        return fail(ctx, DUHL_E_NUMERIC,
+                    std::string(where) + (flag & 2 ? ": non-finite gap/state" : ": negative duality gap"));
+    }
+    return DUHL_OK;
+}
+
+// gap pass over d_cols[0..k) (nullptr = all n), writing z; optional device outputs
+static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, double* gap_out,
+                            double* s_out, double* sums, bool write_z = true) {
+    GapParams p = gap_params(ctx, d_cols, d_cols ? k : ctx->n);
+    p.gap_out = gap_out;
+    p.s_out = s_out;
+    p.sums = sums;
+    if (!write_z) p.z = nullptr;
+    CK(launch_gap_pass(p, kGapTileRows, ctx->st, &ctx->launches));
+    return DUHL_OK;
+}
+
+static duhl_status upload_slots_changes(duhl_ctx* ctx, const std::vector<int64_t>& cols,
+                                        const std::vector<int>& slots) {
+    if (cols.empty()) return DUHL_OK;
+    CK(cudaMemcpyAsync(ctx->d_chg_cols, cols.data(), cols.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_chg_slots, slots.data(), slots.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ctx->st));
+    CK(launch_set_slots(ctx->d_col_slot, ctx->d_chg_cols, ctx->d_chg_slots, (int64_t)cols.size(),
+                        ctx->st, &ctx->launches));
+    // the uploads read pageable host vectors: make them complete before they go away
+    CK(cudaStreamSynchronize(ctx->st));
+    return DUHL_OK;
+}
+
+// Stage P (ascending) into the slot pool: evict non-members, copy new columns
+// host -> HBM in maximal contiguous runs on the copy stream (Alg. 2 l.4).
+static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& P, int64_t* swaps) {
+    const int64_t m = (int64_t)P.size();
+    std::vector<char> in_new(ctx->n, 0);
+    for (int64_t j : P) in_new[j] = 1;
+    int64_t nsw = 0;
+    std::vector<int64_t> chg_cols;
+    std::vector<int> chg_slots;
+    if (ctx->cfg.hbm_budget_bytes != 0) {
+        std::vector<int> free_slots;
+        for (int64_t s = 0; s < ctx->S; ++s) {
+            int c = ctx->slot_col[s];
+            if (c < 0 || !in_new[c]) {
+                if (c >= 0) {
+                    ctx->col_slot[c] = -1;
+                    chg_cols.push_back(c);
+                    chg_slots.push_back(-1);
+                }
+                ctx->slot_col[s] = -1;
+                free_slots.push_back((int)s);
+            }
+        }
+        // the compute stream may still read evicted slots (previous epoch): order copies after it
+        CK(cudaEventRecord(ctx->ev_copy, ctx->st));
+        CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
+        size_t fi = 0;
+        int64_t run_col = -1, run_slot = -1, run_len = 0;
+        auto flush = [&]() -> duhl_status {
+            if (run_len > 0) {
+                size_t bytes = (size_t)run_len * ctx->ld_dev * sizeof(float);
+                CK(cudaMemcpy2DAsync(ctx->pool + run_slot * ctx->ld_dev, ctx->ld_dev * sizeof(float),
+                                     ctx->h_store + run_col * ctx->ld_host, ctx->ld_host * sizeof(float),
+                                     ctx->ld_dev * sizeof(float), (size_t)run_len,
+                                     cudaMemcpyHostToDevice, ctx->cst));
+                ctx->h2d_bytes += (int64_t)bytes;
+            }
+            run_len = 0;
+            return DUHL_OK;
+        };
+        for (int64_t j : P) {
+            if (ctx->col_slot[j] >= 0) continue;
+            if (fi >= free_slots.size()) return fail(ctx, DUHL_E_INVALID, "working set exceeds the HBM slot pool");
+            int s = free_slots[fi++];
+            ctx->col_slot[j] = s;
+            ctx->slot_col[s] = (int)j;
+            chg_cols.push_back(j);
+            chg_slots.push_back(s);
+            ++nsw;
+            if (run_len > 0 && j == run_col + run_len && s == run_slot + run_len) {
+                ++run_len;
+            } else {
+                TRY(flush());
+                run_col = j;
+                run_slot = s;
+                run_len = 1;
+            }
+        }
+        TRY(flush());
+        CK(cudaEventRecord(ctx->ev_copy, ctx->cst));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0));
+    } else {
+        for (int64_t j : P) if (!ctx->inP[j]) ++nsw;  // logical swaps (everything is resident)
+    }
+    TRY(upload_slots_changes(ctx, chg_cols, chg_slots));
+    std::vector<int> Ps(m);
+    for (int64_t q = 0; q < m; ++q) Ps[q] = ctx->col_slot[P[q]];
+    CK(cudaMemcpyAsync(ctx->d_P, P.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_P_slot, Ps.data(), m * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->P = P;
+    std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
+    for (int64_t j : P) ctx->inP[j] = 1;
+    if (swaps) *swaps = nsw;
+    return DUHL_OK;
+}
+
+static void free_all(duhl_ctx* ctx) {
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    if (ctx->cst) cudaStreamSynchronize(ctx->cst);
+    void* dev_ptrs[] = {ctx->pool, ctx->d_col_slot, ctx->d_alpha, ctx->d_vt, ctx->d_b, ctx->d_y,
+                        ctx->d_norms, ctx->d_z, ctx->d_P, ctx->d_order_j, ctx->d_cols,
+                        ctx->d_chg_cols, ctx->d_P_slot, ctx->d_order_slot, ctx->d_chg_slots,
+                        ctx->d_keys, ctx->d_keys2, ctx->d_idx, ctx->d_idx2, ctx->d_sort_tmp,
+                        ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
+                        ctx->d_red, ctx->d_bar};
+    for (void* p : dev_ptrs)
+        if (p) cudaFree(p);
+    if (ctx->registered) cudaHostUnregister(ctx->h_store);
+    if (ctx->own_store && ctx->h_store) cudaFreeHost(ctx->h_store);
+    if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    if (ctx->cst) cudaStreamDestroy(ctx->cst);
+}
+
+// SCD launch shape: G CTAs own contiguous row ranges of R rows (R % 4 == 0);
+// W = coordinates per Gram block, largest multiple of 4 (<= 32) whose
+// double-buffered stage fits in shared memory.
+static void choose_scd_shape(duhl_ctx* ctx) {
+    int64_t G = ctx->cfg.scd_ctas > 0 ? ctx->cfg.scd_ctas
+                                      : std::min<int64_t>(ctx->nsm, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
+    int64_t R = round4((ctx->d4 + G - 1) / G);
+    G = (ctx->d4 + R - 1) / R;
+    int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 32;
+    W = std::max(4, std::min(32, W / 4 * 4));
+    while (W > 4 && scd_smem_bytes(W, (int)R) > 220 * 1024) W -= 4;
+    ctx->W = W;
+    ctx->R = (int)R;
+    ctx->G = (int)G;
+}
+
+// ============================================================================ C ABI
+extern "C" {
+
+void duhl_default_config(duhl_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->refresh_fraction = 0.05;
+    cfg->cert_every = 10;
+    cfg->seed = 170805357ull;
+}
+
+const char* duhl_last_error(const duhl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambda,
+                        duhl_model model, const duhl_config* cfg_in, duhl_ctx** out) {
+    if (!out) return DUHL_E_INVALID;
+    *out = nullptr;
+    if (!A || !A->values || !b_or_y || A->d < 1 || A->n < 1 || A->ld < A->d) return DUHL_E_INVALID;
+    if (!(lambda > 0.0) || !std::isfinite(lambda)) return DUHL_E_INVALID;
+    if (model != DUHL_LASSO && model != DUHL_SVM_DUAL) return DUHL_E_INVALID;
+    if (A->n > (int64_t)INT32_MAX - 1) return DUHL_E_INVALID;
+    duhl_ctx* ctx = new duhl_ctx();
+    if (cfg_in) ctx->cfg = *cfg_in; else duhl_default_config(&ctx->cfg);
+    if (ctx->cfg.cert_every < 1) ctx->cfg.cert_every = 1;
+    ctx->model = model;
+    ctx->d = A->d;
+    ctx->n = A->n;
+    ctx->d4 = round4(A->d);
+    ctx->lambda = lambda;
+    const int64_t d = ctx->d, n = ctx->n, d4 = ctx->d4;
+    // labels
+    if (model == DUHL_SVM_DUAL) {
+        for (int64_t i = 0; i < n; ++i)
+            if (b_or_y[i] != 1.0 && b_or_y[i] != -1.0) { delete ctx; return DUHL_E_INVALID; }
+    } else {
+        for (int64_t k = 0; k < d; ++k)
+            if (!std::isfinite(b_or_y[k])) { delete ctx; return DUHL_E_INVALID; }
+    }
+    auto bail = [&](duhl_status s) { free_all(ctx); delete ctx; return s; };
+    // device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= ctx->cfg.device) return bail(DUHL_E_CUDA);
+    ctx->dev = ctx->cfg.device;
+    if (cudaSetDevice(ctx->dev) != cudaSuccess) return bail(DUHL_E_CUDA);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, ctx->dev) != cudaSuccess || prop.major != 10) return bail(DUHL_E_CUDA);
+    ctx->nsm = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) != cudaSuccess)
+        return bail(DUHL_E_CUDA);
+    // ---- unit A: pinned host store (column i at h_store + i*ld_host, rows d..d4 zero)
+    const bool can_borrow = ctx->cfg.borrow_host && d % 4 == 0 && A->ld % 4 == 0 &&
+                            ((uintptr_t)A->values % 16 == 0);
+    if (can_borrow) {
+        ctx->h_store = const_cast<float*>(A->values);
+        ctx->ld_host = A->ld;
+        if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float),
+                             cudaHostRegisterMapped | cudaHostRegisterReadOnly) != cudaSuccess) {
+            cudaGetLastError();
+            if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float), cudaHostRegisterMapped) !=
+                cudaSuccess)
+                return bail(DUHL_E_CUDA);
+        }
+        ctx->registered = true;
+    } else {
+        ctx->ld_host = d4;
+        if (cudaHostAlloc((void**)&ctx->h_store, (size_t)n * d4 * sizeof(float), cudaHostAllocMapped) !=
+            cudaSuccess)
+            return bail(DUHL_E_NOMEM);
+        ctx->own_store = true;
+        const float* src = A->values;
+        const int64_t ld = A->ld;
+        float* dst = ctx->h_store;
+        unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([=]() {
+                for (int64_t i = t; i < n; i += nt) {
+                    std::memcpy(dst + i * d4, src + i * ld, (size_t)d * sizeof(float));
+                    for (int64_t k = d; k < d4; ++k) dst[i * d4 + k] = 0.0f;
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    // data validity: finite values (checked on the host copy once, cheap relative to ingest)
+    {
+        std::vector<char> badv(64, 0);
+        unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        const float* hs = ctx->h_store;
+        const int64_t ldh = ctx->ld_host;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([=, &badv]() {
+                for (int64_t i = t; i < n; i += nt)
+                    for (int64_t k = 0; k < d; ++k)
+                        if (!std::isfinite(hs[i * ldh + k])) { badv[t] = 1; break; }
+            });
+        for (auto& x : th) x.join();
+        for (char c : badv)
+            if (c) return bail(DUHL_E_INVALID);
+    }
+    void* alias = nullptr;
+    if (cudaHostGetDevicePointer(&alias, ctx->h_store, 0) != cudaSuccess) return bail(DUHL_E_CUDA);
+    ctx->h_alias = (const float*)alias;
+    // ---- unit B: slot pool
+    ctx->ld_dev = d4;
+    const size_t col_bytes = (size_t)d4 * sizeof(float);
+    if (ctx->cfg.hbm_budget_bytes == 0) {
+        ctx->S = n;
+    } else {
+        ctx->S = std::min<int64_t>(n, (int64_t)(ctx->cfg.hbm_budget_bytes / col_bytes));
+        if (ctx->S < 1) { ctx->err = "HBM budget smaller than one column"; return bail(DUHL_E_INVALID); }
+    }
+    ctx->m_cfg = ctx->cfg.m > 0 ? ctx->cfg.m : ctx->S;
+    if (ctx->m_cfg > n || ctx->m_cfg > ctx->S) return bail(DUHL_E_INVALID);
+    auto dmal = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16) == cudaSuccess; };
+    bool ok = dmal((void**)&ctx->pool, (size_t)ctx->S * col_bytes) &&
+              dmal((void**)&ctx->d_col_slot, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_alpha, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_vt, d4 * sizeof(double)) &&
+              dmal((void**)&ctx->d_b, d4 * sizeof(double)) &&
+              dmal((void**)&ctx->d_y, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_norms, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_z, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_P, n * sizeof(int64_t)) &&
+              dmal((void**)&ctx->d_order_j, n * sizeof(int64_t)) &&
+              dmal((void**)&ctx->d_cols, n * sizeof(int64_t)) &&
+              dmal((void**)&ctx->d_chg_cols, 2 * n * sizeof(int64_t)) &&
+              dmal((void**)&ctx->d_P_slot, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_order_slot, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_chg_slots, 2 * n * sizeof(int)) &&
+              dmal((void**)&ctx->d_keys, n * sizeof(uint64_t)) &&
+              dmal((void**)&ctx->d_keys2, n * sizeof(uint64_t)) &&
+              dmal((void**)&ctx->d_idx, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_idx2, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_s_acc, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_gap_out, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_s_out, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_sums, 8 * sizeof(double)) &&
+              dmal((void**)&ctx->d_flag, sizeof(int));
+    if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
+    ctx->sort_tmp_bytes = sort_temp_bytes(n);
+    if (!dmal(&ctx->d_sort_tmp, ctx->sort_tmp_bytes)) return bail(DUHL_E_NOMEM);
+    choose_scd_shape(ctx);
+    if (!dmal((void**)&ctx->d_red, 3 * (size_t)scd_nred(ctx->W) * sizeof(double)) ||
+        !dmal((void**)&ctx->d_bar, 64))
+        return bail(DUHL_E_NOMEM);
+    ctx->col_slot.assign(n, -1);
+    ctx->slot_col.assign(ctx->S, -1);
+    ctx->inP.assign(n, 0);
+    cudaStream_t st = ctx->st;
+    bool ok2 = true;
+    auto ck = [&](cudaError_t e) { if (e != cudaSuccess) ok2 = false; };
+    ck(cudaMemsetAsync(ctx->d_s_acc, 0, n * sizeof(double), st));
+    ck(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
+    ck(cudaMemsetAsync(ctx->d_alpha, 0, n * sizeof(double), st));
+    ck(cudaMemsetAsync(ctx->d_b, 0, d4 * sizeof(double), st));
+    ck(cudaMemsetAsync(ctx->d_y, 0, n * sizeof(double), st));
+    if (ctx->cfg.hbm_budget_bytes == 0) {  // everything resident: slot i = column i
+        for (int64_t i = 0; i < n; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
+        ck(cudaMemcpy2DAsync(ctx->pool, col_bytes, ctx->h_store, ctx->ld_host * sizeof(float), col_bytes,
+                             (size_t)n, cudaMemcpyHostToDevice, st));
+        ctx->h2d_bytes += (int64_t)(n * col_bytes);
+    }
+    ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (model == DUHL_SVM_DUAL)
+        ck(cudaMemcpyAsync(ctx->d_y, b_or_y, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    else
+        ck(cudaMemcpyAsync(ctx->d_b, b_or_y, d * sizeof(double), cudaMemcpyHostToDevice, st));
+    ck(cudaStreamSynchronize(st));
+    if (!ok2) { cudaGetLastError(); ctx->err = "device setup failed"; return bail(DUHL_E_CUDA); }
+    // ---- precompute (a1): norms, B, initial shared vector, z at alpha = 0
+    ck(launch_col_norms(colsrc(ctx), d4, n, ctx->d_norms, st, &ctx->launches));
+    if (model == DUHL_LASSO) {
+        double h[2] = {0, 0};
+        ck(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), st));
+        ck(launch_vec_sums(ctx->d_b, nullptr, d4, ctx->d_sums, st, &ctx->launches));
+        ck(cudaMemcpyAsync(h, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        ctx->B = h[0] / (2.0 * lambda * (double)d);  // P:848, reading R1
+    }
+    ck(launch_matvec(colsrc(ctx), ctx->d_alpha, 0, d, d4, model == DUHL_LASSO ? ctx->d_b : nullptr,
+                     ctx->d_vt, st, &ctx->launches));  // alpha = 0: v~ = -b, v^ = 0
+    ck(cudaStreamSynchronize(st));
+    if (!ok2) { cudaGetLastError(); ctx->err = "precompute failed"; return bail(DUHL_E_CUDA); }
+    if (run_gaps(ctx, nullptr, n, nullptr, nullptr, nullptr) != DUHL_OK) return bail(DUHL_E_CUDA);
+    if (check_flag(ctx, "initial gaps") != DUHL_OK) return bail(DUHL_E_NUMERIC);
+    *out = ctx;
+    return DUHL_OK;
+}
+
+duhl_status duhl_destroy(duhl_ctx* ctx) {
+    if (!ctx) return DUHL_E_INVALID;
+    cudaSetDevice(ctx->dev);
+    free_all(ctx);
+    delete ctx;
+    return DUHL_OK;
+}
+
+duhl_status duhl_gaps(duhl_ctx* ctx, const int64_t* idx, int64_t k, double* z_out, double* s_out) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    const int64_t* dcols = nullptr;
+    if (idx) {
+        if (k < 0 || k > ctx->n) return fail(ctx, DUHL_E_INVALID, "k out of range");
+        for (int64_t t = 0; t < k; ++t)
+            if (idx[t] < 0 || idx[t] >= ctx->n) return fail(ctx, DUHL_E_INVALID, "index out of range");
+        if (k == 0) return DUHL_OK;
+        CK(cudaMemcpyAsync(ctx->d_cols, idx, k * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        dcols = ctx->d_cols;
+    } else {
+        k = ctx->n;
+    }
+    TRY(run_gaps(ctx, dcols, k, z_out ? ctx->d_gap_out : nullptr, s_out ? ctx->d_s_out : nullptr, nullptr));
+    if (z_out) CK(cudaMemcpyAsync(z_out, ctx->d_gap_out, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    if (s_out) CK(cudaMemcpyAsync(s_out, ctx->d_s_out, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return check_flag(ctx, "duhl_gaps");
+}
+
+static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t round,
+                               int64_t* n_swaps_out) {
+    if (m <= 0) m = ctx->m_cfg;
+    if (m > ctx->n || m > ctx->S) return fail(ctx, DUHL_E_INVALID, "m exceeds n or the HBM slot pool");
+    std::vector<int64_t> P;
+    if (policy == DUHL_SEL_SEQUENTIAL) {  // blocks [k m, min((k+1) m, n)), k = round mod ceil(n/m)
+        int64_t nblk = (ctx->n + m - 1) / m, kb = round % nblk;
+        int64_t lo = kb * m, hi = std::min(ctx->n, lo + m);
+        for (int64_t i = lo; i < hi; ++i) P.push_back(i);
+    } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM) {
+        CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
+                       ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches));
+        P.resize(m);
+        CK(cudaMemcpyAsync(P.data(), ctx->d_P, m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        TRY(check_flag(ctx, "duhl_select"));
+    } else {
+        return fail(ctx, DUHL_E_INVALID, "unknown policy");
+    }
+    return stage_working_set(ctx, P, n_swaps_out);
+}
+
+duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t round, int64_t* P_out,
+                        int64_t* n_swaps_out) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    TRY(select_impl(ctx, policy, m, round, n_swaps_out));
+    if (P_out) std::memcpy(P_out, ctx->P.data(), ctx->P.size() * sizeof(int64_t));
+    return DUHL_OK;
+}
+
+static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
+    ScdParams p{};
+    p.model = ctx->model;
+    p.d = ctx->d;
+    p.d4 = ctx->d4;
+    p.n = ctx->n;
+    p.lambda = ctx->lambda;
+    p.pool = ctx->pool;
+    p.ld_dev = ctx->ld_dev;
+    p.order_j = ctx->d_order_j;
+    p.order_slot = ctx->d_order_slot;
+    p.L = L;
+    p.norms = ctx->d_norms;
+    p.y = ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr;
+    p.alpha = ctx->d_alpha;
+    p.vt = ctx->d_vt;
+    p.W = ctx->W;
+    p.R = ctx->R;
+    p.G = ctx->G;
+    p.red = ctx->d_red;
+    p.bar = ctx->d_bar;
+    CK(cudaMemsetAsync(ctx->d_red, 0, 3 * (size_t)scd_nred(ctx->W) * sizeof(double), ctx->st));
+    CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
+    CK(launch_scd_gram(p, ctx->st, &ctx->launches));
+    ctx->updates += L;
+    return DUHL_OK;
+}
+
+static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
+    const int64_t m = (int64_t)ctx->P.size();
+    for (int pass = 0; pass < passes; ++pass) {
+        CK(launch_perm_keys(ctx->d_P, m, seed, round, pass, ctx->d_keys, ctx->d_idx, ctx->st, &ctx->launches));
+        CK(sort_pairs(ctx->d_sort_tmp, ctx->sort_tmp_bytes, ctx->d_keys, ctx->d_keys2, ctx->d_idx,
+                      ctx->d_idx2, m, ctx->st, &ctx->launches));
+        CK(launch_gather_order(ctx->d_idx2, ctx->d_P, ctx->d_P_slot, m, ctx->d_order_j,
+                               ctx->d_order_slot, ctx->st, &ctx->launches));
+        TRY(scd_launch(ctx, m));
+    }
+    return DUHL_OK;
+}
+
+duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round, const int64_t* perm,
+                           int64_t perm_len) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    if (ctx->P.empty()) return fail(ctx, DUHL_E_INVALID, "no working set: call duhl_select first");
+    if (perm) {
+        if (perm_len < 0 || perm_len > (int64_t)ctx->P.size()) return fail(ctx, DUHL_E_INVALID, "perm_len");
+        std::vector<char> seen(ctx->n, 0);
+        std::vector<int> slots(perm_len);
+        for (int64_t t = 0; t < perm_len; ++t) {
+            int64_t j = perm[t];
+            if (j < 0 || j >= ctx->n || !ctx->inP[j] || seen[j] || ctx->col_slot[j] < 0)
+                return fail(ctx, DUHL_E_INVALID, "perm entries must be distinct resident members of P");
+            seen[j] = 1;
+            slots[t] = ctx->col_slot[j];
+        }
+        CK(cudaMemcpyAsync(ctx->d_order_j, perm, perm_len * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_order_slot, slots.data(), perm_len * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
+        TRY(scd_launch(ctx, perm_len));
+        CK(cudaStreamSynchronize(ctx->st));
+        return DUHL_OK;
+    }
+    if (passes < 1) return fail(ctx, DUHL_E_INVALID, "passes < 1");
+    TRY(scd_passes(ctx, passes, seed, round));
+    CK(cudaStreamSynchronize(ctx->st));
+    return DUHL_OK;
+}
+
+static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, double* dual) {
+    CK(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), ctx->st));
+    TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+    CK(launch_vec_sums(ctx->d_vt, ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
+                       ctx->st, &ctx->launches));
+    double h[8];
+    CK(cudaMemcpyAsync(h, ctx->d_sums, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    TRY(check_flag(ctx, "certificate"));
+    const double dd = (double)ctx->d, nn = (double)ctx->n, lam = ctx->lambda;
+    const double G = h[0], aux = h[1], asum = h[2], vv = h[4], vb = h[5];
+    double amax;
+    std::memcpy(&amax, &h[3], sizeof(double));
+    double O, D;
+    if (ctx->model == DUHL_LASSO) {
+        // w = v~; O = ||w||^2/(2d) + lambda ||alpha||_1;  D = -(u^T b + (d/2)||u||^2) - sum B[|a^T u| - lambda]_+
+        O = vv / (2.0 * dd) + lam * asum;
+        D = -(vb / dd + 0.5 * vv / dd) - aux;
+    } else {
+        // O = -(1/n) sum y a + ||v||^2/(2 lambda n^2);  D = -[(1/n) sum hinge + (lambda/2)||w||^2]
+        O = -asum / nn + vv / (2.0 * lam * nn * nn);
+        D = -(aux / nn + 0.5 * vv / (lam * nn * nn));
+    }
+    if (gap) *gap = G;
+    if (primal) *primal = O;
+    if (dual) *dual = D;
+    if (!std::isfinite(G) || !std::isfinite(O)) return fail(ctx, DUHL_E_NUMERIC, "non-finite certificate");
+    if (ctx->model == DUHL_LASSO && amax > ctx->B * (1.0 + 1e-12))
+        return fail(ctx, DUHL_E_BOUND, "max |alpha_i| exceeds the Lipschitzing bound B (P:848)");
+    return DUHL_OK;
+}
+
+duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double* dual) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    return certificate(ctx, gap, primal, dual);
+}
+
+duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes, duhl_policy policy,
+                       duhl_round_record* trace, int64_t trace_cap, int64_t* rounds_out, double* gap_out) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    if (passes < 1 || max_rounds < 0) return fail(ctx, DUHL_E_INVALID, "passes/max_rounds");
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t n = ctx->n;
+    int64_t kref = (int64_t)std::ceil(ctx->cfg.refresh_fraction * (double)n - 1e-9);
+    kref = std::max<int64_t>(0, std::min(n, kref));
+    std::vector<int64_t> idx(kref);
+    double gap = INFINITY;
+    duhl_status st = DUHL_E_NOT_CONVERGED;
+    int64_t t = 0;
+    for (t = 0; t < max_rounds; ++t) {
+        int64_t swaps = 0;
+        TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                 // Alg. 2 l.3-4
+        if (kref > 0) {                                                       // l.7-10 at alpha^(t)
+            for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
+            ctx->cursor = (ctx->cursor + kref) % n;
+            CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+            TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr));
+        }
+        TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
+        const int64_t m = (int64_t)ctx->P.size();                             // z_P at alpha^(t+1) (R9)
+        TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
+        double cg = -1.0;
+        if ((t + 1) % ctx->cfg.cert_every == 0) {
+            TRY(certificate(ctx, &gap, nullptr, nullptr));
+            cg = gap;
+        } else {
+            CK(cudaStreamSynchronize(ctx->st));  // idx buffer reuse
+            TRY(check_flag(ctx, "duhl_solve"));
+        }
+        if (trace && t < trace_cap) {
+            duhl_round_record& r = trace[t];
+            r.round = t;
+            r.swaps = swaps;
+            r.refreshed = kref;
+            r.cert_gap = cg;
+            r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        if (cg >= 0.0 && gap <= eps) { st = DUHL_OK; ++t; break; }
+    }
+    if (rounds_out) *rounds_out = t;
+    if (gap_out) *gap_out = gap;
+    if (st == DUHL_E_NOT_CONVERGED) ctx->err = "max_rounds reached before the certified gap <= eps";
+    return st;
+}
+
+duhl_status duhl_get_state(duhl_ctx* ctx, double* alpha_out, double* v_out, double* z_out) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    if (alpha_out) CK(cudaMemcpyAsync(alpha_out, ctx->d_alpha, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    if (v_out) CK(cudaMemcpyAsync(v_out, ctx->d_vt, ctx->d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    if (z_out) CK(cudaMemcpyAsync(z_out, ctx->d_z, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return DUHL_OK;
+}
+
+duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
+    if (!ctx || !alpha) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    std::vector<double> y;
+    if (ctx->model == DUHL_SVM_DUAL) {
+        y.resize(ctx->n);
+        CK(cudaMemcpy(y.data(), ctx->d_y, ctx->n * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    for (int64_t i = 0; i < ctx->n; ++i) {
+        if (!std::isfinite(alpha[i])) return fail(ctx, DUHL_E_INVALID, "non-finite alpha");
+        if (ctx->model == DUHL_SVM_DUAL && (y[i] * alpha[i] < 0.0 || y[i] * alpha[i] > 1.0))
+            return fail(ctx, DUHL_E_INVALID, "SVM alpha outside the box y_i alpha_i in [0,1]");
+    }
+    CK(cudaMemcpyAsync(ctx->d_alpha, alpha, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+    CK(launch_matvec(colsrc(ctx), ctx->d_alpha, ctx->n, ctx->d, ctx->d4,
+                     ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
+    TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, nullptr));
+    CK(cudaStreamSynchronize(ctx->st));
+    return check_flag(ctx, "duhl_set_state");
+}
+
+duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {
+    if (!ctx || !stream_out) return DUHL_E_INVALID;
+    *stream_out = (void*)ctx->st;
+    return DUHL_OK;
+}
+
+duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes, int64_t* updates) {
+    if (!ctx) return DUHL_E_INVALID;
+    if (launches) *launches = ctx->launches;
+    if (h2d_bytes) *h2d_bytes = ctx->h2d_bytes;
+    if (updates) *updates = ctx->updates;
+    return DUHL_OK;
+}
+
+}  // extern "C"

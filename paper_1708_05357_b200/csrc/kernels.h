@@ -1,0 +1,86 @@
+// kernels.h -- internal launch interface of the DuHL sm_100a kernels (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace duhl {
+
+// Where column i of A lives: HBM slot (col_slot[i] >= 0) or pinned host memory
+// mapped into the device address space (zero-copy over PCIe).
+struct ColSrc {
+    const float* pool;     // HBM slot pool, slot s at pool + s*ld_dev
+    int64_t ld_dev;        // multiple of 4 floats
+    const float* host;     // device alias of the pinned host store, column i at host + i*ld_host
+    int64_t ld_host;       // multiple of 4 floats
+    const int* col_slot;   // [n] device, -1 = not resident
+};
+
+struct GapParams {
+    int model;
+    int64_t d, d4, n;          // d4 = d rounded up to 4 (zero-padded rows)
+    ColSrc src;
+    const int64_t* cols;       // [k] device column list; nullptr = columns 0..k-1
+    int64_t k;
+    const double* vt;          // shared vector, [d4], zero padded
+    double wscale;             // w = wscale * vt (Lasso 1, SVM 1/(lambda n))
+    const double* alpha;       // [n]
+    const double* y;           // [n] SVM labels (nullptr for Lasso)
+    double lambda, B;
+    double* s_acc;             // [k] partial-dot accumulator (multi-tile passes), zero on entry
+    double* z;                 // [n] gap memory or nullptr
+    double* gap_out;           // [k] or nullptr
+    double* s_out;             // [k] or nullptr
+    double* sums;              // [4] certificate sums or nullptr: sum gap, sum aux, sum |a| / sum y a, max |a| (bits)
+    int* flag;                 // bit0 negative gap, bit1 non-finite
+};
+
+struct ScdParams {
+    int model;
+    int64_t d, d4, n;
+    double lambda;
+    const float* pool;
+    int64_t ld_dev;
+    const int64_t* order_j;    // [L] coordinate processed at position t
+    const int* order_slot;     // [L] its HBM slot
+    int64_t L;
+    const double* norms;       // [n] ||a_j||^2
+    const double* y;           // [n] (SVM) or nullptr
+    double* alpha;             // [n]
+    double* vt;                // [d4] shared vector
+    int W, R, G;               // block size, rows per CTA, CTAs
+    double* red;               // [3 * NRED] zero on entry
+    unsigned* bar;             // grid-barrier counter, zero on entry
+};
+
+int scd_nred(int W);
+size_t scd_smem_bytes(int W, int R);
+int scd_rc(int W);             // row chunks per tile task
+
+cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches);
+cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* norms,
+                             cudaStream_t st, int64_t* launches);
+cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,
+                        int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
+                        int64_t* launches);
+cudaError_t launch_perm_keys(const int64_t* P, int64_t m, uint64_t seed, int64_t round,
+                             int64_t pass, uint64_t* keys, int* idx, cudaStream_t st,
+                             int64_t* launches);
+cudaError_t launch_gather_order(const int* sorted_idx, const int64_t* P, const int* P_slot,
+                                int64_t m, int64_t* order_j, int* order_slot, cudaStream_t st,
+                                int64_t* launches);
+cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
+cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int64_t d,
+                          int64_t d4, const double* b, double* vt, cudaStream_t st,
+                          int64_t* launches);
+cudaError_t launch_set_slots(int* col_slot, const int64_t* cols, const int* slots, int64_t cnt,
+                             cudaStream_t st, int64_t* launches);
+cudaError_t launch_vec_sums(const double* vt, const double* b, int64_t d4, double* out2,
+                            cudaStream_t st, int64_t* launches);
+
+// Radix sort of (key, idx) pairs (CUB, compiled into this library).
+size_t sort_temp_bytes(int64_t m);
+cudaError_t sort_pairs(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
+                       const int* idx_in, int* idx_out, int64_t m, cudaStream_t st,
+                       int64_t* launches);
+
+}  // namespace duhl

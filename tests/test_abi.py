@@ -1,0 +1,64 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports
+every entry point include/duhl.h declares, and fails loudly without a GPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "duhl.h")).read()
+    return sorted(set(re.findall(r"\b(duhl_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1708_05357_b200 as D
+    L = D.lib()
+    declared = _declared()
+    assert {"duhl_create", "duhl_gaps", "duhl_select", "duhl_scd_epoch", "duhl_duality_gap",
+            "duhl_solve"} <= set(declared)
+    missing = [f for f in declared if not hasattr(L, f)]
+    assert not missing, missing
+    assert set(D._abi.FUNCTIONS) == set(declared)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    import paper_1708_05357_b200 as D
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", D.lib_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_sass_uses_bulk_async_copy():
+    """The SCD kernel stages working-set tiles with cp.async.bulk (SASS UBLKCP)."""
+    import subprocess
+    import paper_1708_05357_b200 as D
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", D.lib_path()],
+                          capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass
+
+
+def test_default_config_and_no_gpu_fails_loudly():
+    import torch
+    import paper_1708_05357_b200 as D
+    cfg = D._abi.default_config()
+    assert cfg.refresh_fraction == 0.05 and cfg.cert_every == 10 and cfg.seed == 170805357
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: the no-GPU path is not observable here")
+    A = np.ones((4, 4), dtype=np.float32)
+    with pytest.raises(D.DuhlError):
+        D.create(A, np.ones(4), 0.1, D.LASSO)
+
+
+def test_invalid_arguments_rejected_before_device():
+    import paper_1708_05357_b200 as D
+    A = np.ones((4, 4), dtype=np.float32)
+    for lam, y, model in [(0.0, np.ones(4), D.LASSO), (-1.0, np.ones(4), D.LASSO),
+                          (0.1, np.array([1.0, 2.0, 1.0, -1.0]), D.SVM_DUAL)]:
+        with pytest.raises(D.DuhlError) as e:
+            D.create(A, y, lam, model)
+        assert e.value.status == 2
