@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- the DuHL hot path (arXiv 1708.05357) on B200.
+
+One step = one DuHL round (Algorithm 2) over the configured workload:
+gap-memory top-m selection (Eq. 11) -> staging of A_[P] host -> HBM under the
+budget -> unit-A refresh of a rotating fraction of the gaps (zero-copy from
+pinned host memory) -> `passes` exact SCD passes over the working set (App. D)
+-> refresh of z_P.  The metric is BASELINE.json's: coordinate updates/s (plus
+time-to-certified-gap and gap-pass GB/s as extra keys).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c4|c2|c1] [--impl reference]
+
+Default workload C4 (BASELINE.json configs[3], the config the metric is quoted
+on at 1/2/4/8 GPUs): hinge-SVM dual, 200,704 features x 40,000 samples dense
+fp32 (32.1 GB in pinned host memory), HBM budget 25% (8.03 GB, m = 10,000).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+CONFIGS = {
+    # name: model, d, n, budget fraction of data (0 = all resident), m, lambda (None: 1/n), label
+    "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None,
+               label="C4: hinge-SVM dual, ImageNet-shaped dense synthetic 200704 features x 40000 "
+                     "samples fp32 (32.1 GB pinned host), HBM budget 25% (8.03 GB), m=10000"),
+    "c2": dict(model=1, d=500, n=20000, budget_frac=0.0, m=2000, lam=None,
+               label="C2: hinge-SVM dual, dense synthetic 500 features x 20000 samples, m=10%"),
+    "c1": dict(model=0, d=2000, n=1000, budget_frac=0.0, m=250, lam=0.1,
+               label="C1: Lasso, dense synthetic 2000 samples x 1000 features, lambda=0.1, m=25%"),
+}
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_PATH))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_init(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 2 + k and r[2 + k].lower() == "active"})
+        util = [float(r[6]) for r in self.rows if len(r) > 6 and r[6].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ data
+def make_data(cfg, seed, col_lo=0, col_hi=None):
+    import synth
+    d, n = cfg["d"], cfg["n"]
+    col_hi = n if col_hi is None else col_hi
+    A = np.empty((col_hi - col_lo, d), dtype=np.float32)
+    if cfg["model"] == 1:
+        lab = synth.svm_fill(A, d, n, seed, col_lo=col_lo)
+    else:
+        synth.lasso_fill(A, d, n, seed, col_lo=col_lo)
+        lab = synth.lasso_labels(A, d, seed)
+    return A, lab
+
+
+def lam_of(cfg):
+    return cfg["lam"] if cfg["lam"] is not None else 1.0 / cfg["n"]
+
+
+# ------------------------------------------------------------------ oracle arm
+def oracle_sample(cfg, A, lab, lam, ncols, passes=1):
+    """Time the CPU oracle (single thread, as it stands) on a bounded sample:
+    `passes` sequential SCD passes over `ncols` columns of the same data, plus a
+    gap pass over them.  Returns (updates/s, gap GB/s, seconds)."""
+    import oracle as O
+    Asub = np.ascontiguousarray(A[:ncols])
+    lab_s = lab[:ncols] if cfg["model"] == 1 else lab
+    norms = O.col_norms(Asub)
+    alpha = np.zeros(ncols)
+    vt = np.zeros(cfg["d"]) if cfg["model"] == 1 else -lab_s.copy()
+    y = lab_s if cfg["model"] == 1 else None
+    order = np.arange(ncols)
+    t0 = time.perf_counter()
+    for p in range(passes):
+        O.scd_pass(cfg["model"], Asub, norms, y, lam, alpha, vt, order)
+    t_scd = time.perf_counter() - t0
+    w = O.primal_dual_w(cfg["model"], vt if cfg["model"] == 1 else vt + lab_s,
+                        None if cfg["model"] == 1 else lab_s, cfg["n"], lam)
+    t0 = time.perf_counter()
+    O.coord_gaps(cfg["model"], Asub, alpha, y, w, lam, 1.0)
+    t_gap = time.perf_counter() - t0
+    return passes * ncols / t_scd, ncols * cfg["d"] * 4 / t_gap / 1e9, t_scd + t_gap
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    seed = 170805357 + 3
+    ncols = args.ref_cols
+    A, lab = make_data(cfg, seed, 0, ncols) if cfg["model"] == 1 else make_data(cfg, seed)
+    lam = lam_of(cfg)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, A, lab, lam, min(ncols, 64))
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        u, g, s = oracle_sample(cfg, A, lab, lam, ncols)
+        vals.append(u)
+        secs += s
+    v = float(np.median(vals))
+    sample = (f"per step: 1 sequential SCD pass over {ncols} columns of {args.config.upper()} "
+              f"(d={cfg['d']}) + their gap pass, single-threaded C oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "coord updates/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / max(1, args.steps), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["label"], "oracle_sample_cols": ncols},
+            "cpu_baseline": {"value": v, "unit": "coord updates/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "coord updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ product arm
+def run_duhl(args, cfg, rank, world, local):
+    import torch
+    import paper_1708_05357_b200 as D
+    torch.cuda.set_device(local)
+    seed = 170805357 + 3
+    d, n = cfg["d"], cfg["n"]
+    lam = lam_of(cfg)
+    # CoCoA-style sharding of the columns across ranks (one block per rank)
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    if world > 1:
+        raise SystemExit("bench.py: multi-GPU CoCoA round not implemented in this build")
+    t_gen = time.perf_counter()
+    A, lab = make_data(cfg, seed, lo, hi)
+    t_gen = time.perf_counter() - t_gen
+    col_bytes = ((d + 3) // 4) * 16
+    budget = int(cfg["budget_frac"] * n * col_bytes) if cfg["budget_frac"] > 0 else 0
+    m = cfg["m"]
+    common = dict(hbm_budget_bytes=budget, m=m, device=local, refresh_fraction=args.refresh,
+                  seed=seed, borrow_host=True)
+    policy = {"gap": D.SEL_GAP, "sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM}[args.policy]
+
+    # ---------------- device-timed steady-state rounds
+    t_create = time.perf_counter()
+    P = D.create(A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, **common)
+    t_create = time.perf_counter() - t_create
+    stream = torch.cuda.ExternalStream(P.stream())
+    for t in range(args.warmup):
+        P.round(t, passes=args.passes, policy=policy)
+    barrier(world)
+    torch.cuda.synchronize()
+    c0 = P.counters()
+    k0 = {k: P.kernel_stats(k) for k in range(4)}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    swaps = refreshed = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for t in range(args.warmup, args.warmup + args.steps):
+            r = P.round(t, passes=args.passes, policy=policy)
+            swaps += r.swaps
+            refreshed += r.refreshed
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
+    c1 = P.counters()
+    k1 = {k: P.kernel_stats(k) for k in range(4)}
+    P.close()
+    updates = args.steps * m * args.passes * world
+    value = updates / elapsed
+    ms = {k: k1[k][1] - k0[k][1] for k in range(4)}
+    nl = {k: k1[k][0] - k0[k][0] for k in range(4)}
+    by = {k: k1[k][2] - k0[k][2] for k in range(4)}
+    peak, peak_src = hbm_peak()
+    scd_gbs = by[0] / (ms[0] / 1e3) / 1e9 if ms[0] > 0 else None
+    gap_gbs = by[1] / (ms[1] / 1e3) / 1e9 if ms[1] > 0 else None
+    dom = 0 if ms[0] >= ms[1] else 1
+    dom_gbs = scd_gbs if dom == 0 else gap_gbs
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get(["scd", "gap"][dom])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": ["k_scd_gram", "k_gap_tile"][dom],
+                "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
+                "frac": (dom_gbs / peak) if dom_gbs else None, "traffic": traffic,
+                "peak_source": peak_src,
+                "share_of_step": (ms[dom] / 1e3) / elapsed,
+                "algorithmic_bytes_per_launch": by[dom] / max(1, nl[dom]),
+                "avg_launch_ms": ms[dom] / max(1, nl[dom])}
+
+    # ---------------- end to end: create from host buffers + solve to certified eps
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P2 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, **common)
+        t_c2 = time.perf_counter() - t0
+        r = P2.solve(args.eps, args.max_rounds, passes=args.passes, policy=policy)
+        wall = time.perf_counter() - t0
+        c2 = P2.counters()
+        g_final = r["gap"]
+        P2.close()
+        rounds = max(1, r["rounds"])
+        e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
+               "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
+               "d2h_bytes_per_step": int(m * 8 + 64),
+               "time_to_eps_s": wall, "eps": args.eps, "certified_gap": g_final,
+               "converged": r["status"] == 0, "rounds": r["rounds"], "create_s": t_c2,
+               "note": "duhl_create(host buffers, pinned in place) + duhl_solve to certified gap; "
+                       "h2d = cold fill + swaps (memcpy), zero-copy refresh reads not counted"}
+
+    # ---------------- CPU oracle on a bounded sample of the same workload
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        u, g, s = oracle_sample(cfg, A, lab, lam, min(args.ref_cols, hi - lo))
+        cpu = {"value": u, "unit": "coord updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 sequential SCD pass over {min(args.ref_cols, hi - lo)} columns of the "
+                         f"same {args.config.upper()} data, single-threaded C oracle ({s:.1f} s); "
+                         f"oracle gap pass {g:.2f} GB/s",
+               "gap_pass_GBps": g}
+
+    line = {"metric": METRIC, "value": value, "unit": "coord updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["label"], "d": d, "n": n, "m": m, "passes": args.passes,
+                       "policy": args.policy, "refresh_fraction": args.refresh,
+                       "hbm_budget_GB": budget / 1e9, "lambda": lam,
+                       "l2": "inputs larger than L2 (working set 8 GB >> 126 MB L2)"
+                       if budget else "working set may be L2-resident (small config)",
+                       "parallelism": f"cocoa{world}"},
+            "roofline": roofline,
+            "gap_pass_GBps": gap_gbs, "scd_GBps": scd_gbs,
+            "kernel_ms": {"scd": ms[0], "gap": ms[1], "topm": ms[2], "stage_h2d": ms[3]},
+            "swaps_per_step": swaps / args.steps, "refreshed_per_step": refreshed / args.steps,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": c1["launches"] - c0["launches"],
+            "clocks": clk.summary(),
+            "setup_s": {"generate": t_gen, "create": t_create}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="duhl", choices=["duhl", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--passes", type=int, default=1)
+    ap.add_argument("--refresh", type=float, default=0.01)
+    ap.add_argument("--policy", default="gap", choices=["gap", "sequential", "uniform"])
+    ap.add_argument("--eps", type=float, default=1e-5)
+    ap.add_argument("--max-rounds", type=int, default=2000)
+    ap.add_argument("--cert-every", type=int, default=50)
+    ap.add_argument("--ref-cols", type=int, default=2000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    rank, world, local = dist_init(args.gpus)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_duhl(args, cfg, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

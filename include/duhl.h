@@ -77,6 +77,10 @@ typedef struct {
     int64_t cert_every;       /* certificate (full duality gap) every R rounds in duhl_solve; >= 1 */
     uint64_t seed;            /* seeds the counter-based permutation generator */
     int borrow_host;          /* 1: pin the caller's matrix in place (it must outlive the ctx); 0: copy */
+    int cert_adaptive;        /* 1: duhl_solve also certifies when the gap-memory sum sum_i z_i <= eps */
+    int profile;              /* 1: time every kernel launch with CUDA events (duhl_get_kernel_stats) */
+    int scd_exact;            /* 1: fp64 Gram products -- the SCD pass equals sequential SCD to rounding;
+                                 0: fp32 Gram accumulation inside a warp (fp64 beyond), ~1e-7 relative */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -85,11 +89,13 @@ typedef struct {
     int64_t swaps;            /* |P_t \ P_{t-1}|: columns copied host -> HBM (Fig. 4b) */
     int64_t refreshed;        /* unit-A gap refreshes this round */
     double cert_gap;          /* certified duality gap after the round; -1 if not computed */
-    double time_s;            /* wall seconds since duhl_solve entry, after the round */
+    double z_sum;             /* sum_i z_i after the round: the (time-delayed) gap estimate of the gap memory */
+    double time_s;            /* wall seconds since duhl_solve entry (duhl_round: duration of the round) */
 } duhl_round_record;
 
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,
- * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0. */
+ * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0,
+ * cert_adaptive 1, profile 0, scd_exact 1. */
 void duhl_default_config(duhl_config* cfg);
 
 /* Creates a problem instance.
@@ -122,8 +128,9 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
 
 /* `passes` randomized coordinate-descent passes over the working set (App. D:
  * Lasso soft-threshold step P:804-815 with eta = 0, SVM box step P:824-827),
- * updating alpha_P and the shared vector.  The pass-p order is P sorted by
- * key(seed, round, p, j).  If perm (host int64) is
+ * updating alpha_P and the shared vector.  Position t of pass p processes
+ * P[pi(t)] (P ascending), pi the Feistel bijection keyed by (seed, round, p)
+ * (DESIGN.md "Randomness").  If perm (host int64) is
  * given, exactly one pass is run in the order perm[0..perm_len), whose entries
  * must be distinct, resident members of P.  The kernel executes the sequential
  * SCD semantics exactly (Gram-block reformulation).
@@ -136,6 +143,15 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
  * gap = O - D (D per App. E conjugates).  Any output may be NULL.
  * Errors: DUHL_E_NUMERIC, DUHL_E_BOUND (Lasso max|alpha_i| > B), DUHL_E_CUDA. */
 duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double* dual);
+
+/* One DuHL round t (Alg. 2 body): select (policy) -> stage A_[P] into HBM ->
+ * unit-A refresh of ceil(refresh_fraction n) gaps at the round-start state
+ * (rotating cursor, reading R8) -> `passes` SCD passes (permutation keyed by
+ * (cfg.seed, round, pass)) -> refresh z_P at the new state (reading R9) ->
+ * if certify != 0, the certificate.  rec (host, may be NULL) receives the
+ * round's record (time_s = its duration).  Errors as duhl_select/duhl_scd_epoch. */
+duhl_status duhl_round(duhl_ctx* ctx, int64_t round, int passes, duhl_policy policy, int certify,
+                       duhl_round_record* rec);
 
 /* DuHL rounds (Alg. 2): select -> swap -> [unit-A refresh of
  * ceil(refresh_fraction n) gaps at the round-start state] -> `passes` SCD
@@ -158,6 +174,15 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha);
 /* Device-side view for callers that time kernels on their own stream:
  * returns the CUDA stream (cudaStream_t) all compute of ctx is issued on. */
 duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out);
+
+/* Per-kind kernel timing (cfg.profile = 1), accumulated since creation:
+ * kind 0 = SCD epoch kernel, 1 = gap pass, 2 = top-m select, 3 = working-set
+ * H2D staging (copy stream).  *launches = timed launches, *ms = summed
+ * CUDA-event milliseconds, *bytes = summed ALGORITHMIC bytes (DESIGN.md
+ * "Roofline"): SCD  L (4 d4 + 24) + 16 d4;  gap  k (4 d4 + 24) + 8 d4 tiles;
+ * top-m  8 n x passes;  staging  columns x 4 d4. */
+duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
+                                  double* bytes);
 
 /* Counters since creation: kernel launches issued, bytes copied host->device,
  * SCD coordinate updates.  Any may be NULL. */

@@ -63,6 +63,8 @@ def lib():
         L.or_select_policy.restype = _I
         L.or_select_policy.argtypes = [C.c_int, _I, _I, _I, C.c_uint64, _P, _P]
         L.or_make_perm.argtypes = [_P, _I, C.c_uint64, _I, _I, _P]
+        L.or_perm_index.restype = C.c_int64
+        L.or_perm_index.argtypes = [C.c_uint64, _I, _I, _I, _I]
         L.or_coord_update.restype = C.c_double
         L.or_coord_update.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                       C.c_double, _I, _I]
@@ -165,6 +167,10 @@ def select_policy(policy, n, m, rnd, seed, z=None):
 
 def perm_key(seed, rnd, pas, j):
     return lib().or_perm_key(seed, rnd, pas, j)
+
+
+def perm_index(seed, rnd, pas, m, t):
+    return lib().or_perm_index(seed, rnd, pas, m, t)
 
 
 def make_perm(P, seed, rnd, pas):

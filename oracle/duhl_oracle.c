@@ -199,12 +199,30 @@ i64 or_select_policy(int policy, i64 n, i64 m, i64 round, u64 seed, const double
 }
 
 /* Permutation of the working set for one randomized pass ("randomized
- * passes"; reading R10): P sorted by (key(seed, round, pass, j), j). */
+ * passes"; reading R10): position t of the pass takes
+ * P[pi(t)], where pi is a keyed 8-round Feistel bijection on [0, 4^h),
+ * 4^h >= m, restricted to [0, m) by cycle walking; round function
+ * F_r(x) = mix64(key ^ (r << 56) ^ x) mod 2^h, key = mix64(mix64(mix64(seed) ^ round) ^ pass). */
+i64 or_perm_index(u64 seed, i64 round, i64 pass, i64 m, i64 t) {
+    int h = 1;
+    while (((i64)1 << (2 * h)) < m) ++h;
+    u64 mask = ((u64)1 << h) - 1;
+    u64 key = or_mix64(or_mix64(or_mix64(seed) ^ (u64)round) ^ (u64)pass);
+    u64 x = (u64)t;
+    do {
+        u64 L = x >> h, R = x & mask;
+        for (int r = 0; r < 8; ++r) {
+            u64 F = or_mix64(key ^ ((u64)r << 56) ^ R) & mask;
+            u64 nl = R;
+            R = L ^ F;
+            L = nl;
+        }
+        x = (L << h) | R;
+    } while (x >= (u64)m);
+    return (i64)x;
+}
 void or_make_perm(const i64* P, i64 m, u64 seed, i64 round, i64 pass, i64* out) {
-    u64* key = (u64*)malloc(sizeof(u64) * (size_t)(m > 0 ? m : 1));
-    for (i64 t = 0; t < m; ++t) { out[t] = P[t]; key[t] = or_perm_key(seed, round, pass, P[t]); }
-    or_sort_by_key(key, out, m);
-    free(key);
+    for (i64 t = 0; t < m; ++t) out[t] = P[or_perm_index(seed, round, pass, m, t)];
 }
 
 /* One exact coordinate step (App. D, eta = 0 for Lasso):
@@ -354,7 +372,8 @@ int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
  * R6, R8, R9, R10):
  *   init  alpha = 0 (given alpha is used as is), z_i = gap_i(alpha) for all i      (R6)
  *   round t:
- *     1. P = select(z)   -- Eq. 11 top-m for policy 0; baselines 1/2          (l.3)
+ *     1. P = select(z)   -- Eq. 11 top-m for policy 0; baselines 1/2;
+ *        P is then an ascending index set                                       (l.3)
  *     2. swaps = |P \ P_prev|                                                   (l.4)
  *     3. unit A: z_j := gap_j(alpha^(t)) for the k = refresh_count columns of
  *        the rotating cursor (refresh_count = n: o-DuHL)  at the round-start
@@ -369,6 +388,11 @@ int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
  * SVM w = v^/(lambda n). */
 static void or_shadow_w(int model, const double* vt, i64 d, i64 n, double lambda, double* w) {
     for (i64 k = 0; k < d; ++k) w[k] = (model == OR_LASSO) ? vt[k] : vt[k] / (lambda * (double)n);
+}
+
+static int or_cmp_i64(const void* a, const void* b) {
+    i64 x = *(const i64*)a, y = *(const i64*)b;
+    return (x > y) - (x < y);
 }
 
 typedef struct {
@@ -417,6 +441,7 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
     for (t = 0; t < cfg->max_rounds && s0 == OR_OK; ++t) {
         /* 1. selection */
         i64 mt = or_select_policy(cfg->policy, n, m, t, cfg->seed, z, P);
+        qsort(P, (size_t)mt, sizeof(i64), or_cmp_i64); /* P as an ascending index set */
         /* 2. swap accounting */
         i64 swaps = 0;
         memset(in_cur, 0, (size_t)n);

@@ -14,8 +14,10 @@ STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "
           7: "E_CUDA", 8: "E_NCCL", 9: "E_NOT_CONVERGED"}
 
 FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_destroy", "duhl_gaps", "duhl_select",
-             "duhl_scd_epoch", "duhl_duality_gap", "duhl_solve", "duhl_get_state",
-             "duhl_set_state", "duhl_get_stream", "duhl_get_counters", "duhl_last_error"]
+             "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
+             "duhl_set_state", "duhl_get_stream", "duhl_get_kernel_stats", "duhl_get_counters",
+             "duhl_last_error"]
+KIND_SCD, KIND_GAP, KIND_TOPM, KIND_STAGE = 0, 1, 2, 3
 
 
 class DuhlError(RuntimeError):
@@ -31,12 +33,13 @@ class Matrix(C.Structure):
 class Config(C.Structure):
     _fields_ = [("hbm_budget_bytes", C.c_size_t), ("m", C.c_int64), ("device", C.c_int),
                 ("scd_block", C.c_int), ("scd_ctas", C.c_int), ("refresh_fraction", C.c_double),
-                ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int)]
+                ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
+                ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int)]
 
 
 class RoundRecord(C.Structure):
     _fields_ = [("round", C.c_int64), ("swaps", C.c_int64), ("refreshed", C.c_int64),
-                ("cert_gap", C.c_double), ("time_s", C.c_double)]
+                ("cert_gap", C.c_double), ("z_sum", C.c_double), ("time_s", C.c_double)]
 
 
 _lib = None
@@ -52,7 +55,8 @@ def lib():
     """Load libduhl.so (building it in-tree first if the sources are newer)."""
     global _lib
     if _lib is None:
-        path = _build.build() if os.environ.get("DUHL_NO_BUILD") != "1" else _build.LIB
+        path = os.environ.get("DUHL_LIB") or (
+            _build.build() if os.environ.get("DUHL_NO_BUILD") != "1" else _build.LIB)
         L = C.CDLL(path)
         L.duhl_default_config.argtypes = [C.POINTER(Config)]
         L.duhl_default_config.restype = None
@@ -63,7 +67,9 @@ def lib():
         L.duhl_select.argtypes = [_P, C.c_int, _I, _I, _P, _P]
         L.duhl_scd_epoch.argtypes = [_P, C.c_int, C.c_uint64, _I, _P, _I]
         L.duhl_duality_gap.argtypes = [_P, _P, _P, _P]
+        L.duhl_round.argtypes = [_P, _I, C.c_int, C.c_int, C.c_int, _P]
         L.duhl_solve.argtypes = [_P, C.c_double, _I, C.c_int, C.c_int, _P, _I, _P, _P]
+        L.duhl_get_kernel_stats.argtypes = [_P, C.c_int, _P, _P, _P]
         L.duhl_get_state.argtypes = [_P, _P, _P, _P]
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
@@ -153,6 +159,18 @@ class Problem:
         self._check(lib().duhl_duality_gap(self._h, C.byref(g), C.byref(O), C.byref(D)))
         return g.value, O.value, D.value
 
+    def round(self, t, passes=1, policy=SEL_GAP, certify=False):
+        """duhl_round: one DuHL round; returns its RoundRecord."""
+        rec = RoundRecord()
+        self._check(lib().duhl_round(self._h, t, passes, policy, int(bool(certify)), C.byref(rec)))
+        return rec
+
+    def kernel_stats(self, kind):
+        """duhl_get_kernel_stats: (timed launches, total ms, total algorithmic bytes)."""
+        n, ms, by = C.c_int64(), C.c_double(), C.c_double()
+        self._check(lib().duhl_get_kernel_stats(self._h, kind, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
+
     def solve(self, eps, max_rounds, passes=1, policy=SEL_GAP, trace_cap=None, check=True):
         cap = max_rounds if trace_cap is None else trace_cap
         tr = (RoundRecord * max(cap, 1))()
@@ -185,7 +203,8 @@ class Problem:
 
 
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
-           refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None):
+           refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
+           cert_adaptive=True, profile=False, scd_exact=True):
     """duhl_create.  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -197,7 +216,8 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
     cfg = default_config(hbm_budget_bytes=hbm_budget_bytes, m=m, device=device,
                          scd_block=scd_block, scd_ctas=scd_ctas,
                          refresh_fraction=refresh_fraction, cert_every=cert_every, seed=seed,
-                         borrow_host=int(bool(borrow_host)))
+                         borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
+                         profile=int(bool(profile)), scd_exact=int(bool(scd_exact)))
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -54,20 +55,71 @@ struct duhl_ctx {
     std::vector<char> inP;       // [n]
     int64_t *d_P = nullptr, *d_order_j = nullptr, *d_cols = nullptr, *d_chg_cols = nullptr;
     int *d_P_slot = nullptr, *d_order_slot = nullptr, *d_chg_slots = nullptr;
-    uint64_t *d_keys = nullptr, *d_keys2 = nullptr;
-    int *d_idx = nullptr, *d_idx2 = nullptr;
-    void* d_sort_tmp = nullptr;
-    size_t sort_tmp_bytes = 0;
+    double* d_vsnap = nullptr;   // round-start snapshot of the shared vector (unit-A refresh)
     // ---- gap scratch
     double *d_s_acc = nullptr, *d_gap_out = nullptr, *d_s_out = nullptr, *d_sums = nullptr;
     int* d_flag = nullptr;
     // ---- SCD
     double* d_red = nullptr;
     unsigned* d_bar = nullptr;
-    int W = 0, R = 0, G = 0;
+    int W = 0, R = 0, G = 0, NB = 2;
     // ---- misc
     int64_t launches = 0, h2d_bytes = 0, updates = 0, cursor = 0;
+    // ---- profiling (cfg.profile): CUDA-event pairs per launch, harvested at sync points
+    struct Timed { cudaEvent_t a, b; int kind; double bytes; };
+    std::vector<Timed> pending;
+    std::vector<cudaEvent_t> event_pool;
+    int64_t st_launch[4] = {0, 0, 0, 0};
+    double st_ms[4] = {0, 0, 0, 0}, st_bytes[4] = {0, 0, 0, 0};
 };
+
+// ------------------------------------------------------------------------- profiling
+static cudaEvent_t pool_event(duhl_ctx* ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ProfScope {  // brackets one launch (or copy batch) with events on `st`
+    duhl_ctx* ctx;
+    cudaStream_t st;
+    int kind;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    ProfScope(duhl_ctx* c, cudaStream_t s, int k, double by) : ctx(c), st(s), kind(k), bytes(by) {
+        if (ctx->cfg.profile) {
+            a = pool_event(ctx);
+            cudaEventRecord(a, st);
+        }
+    }
+    void end() {
+        if (a) {
+            cudaEvent_t b = pool_event(ctx);
+            cudaEventRecord(b, st);
+            ctx->pending.push_back({a, b, kind, bytes});
+            a = nullptr;
+        }
+    }
+    ~ProfScope() { end(); }
+};
+static void harvest(duhl_ctx* ctx) {  // call after the streams are synchronized
+    for (auto& t : ctx->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+            ctx->st_launch[t.kind] += 1;
+            ctx->st_ms[t.kind] += ms;
+            ctx->st_bytes[t.kind] += t.bytes;
+        }
+        ctx->event_pool.push_back(t.a);
+        ctx->event_pool.push_back(t.b);
+    }
+    ctx->pending.clear();
+    cudaGetLastError();
+}
 
 #define CK(call)                                                                      \
     do {                                                                              \
@@ -139,12 +191,16 @@ static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
 
 // gap pass over d_cols[0..k) (nullptr = all n), writing z; optional device outputs
 static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, double* gap_out,
-                            double* s_out, double* sums, bool write_z = true) {
+                            double* s_out, double* sums, bool write_z = true,
+                            const double* vt_override = nullptr) {
     GapParams p = gap_params(ctx, d_cols, d_cols ? k : ctx->n);
+    if (vt_override) p.vt = vt_override;
     p.gap_out = gap_out;
     p.s_out = s_out;
     p.sums = sums;
     if (!write_z) p.z = nullptr;
+    const int64_t tiles = (ctx->d4 + kGapTileRows - 1) / kGapTileRows;
+    ProfScope ps(ctx, ctx->st, 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
     CK(launch_gap_pass(p, kGapTileRows, ctx->st, &ctx->launches));
     return DUHL_OK;
 }
@@ -189,6 +245,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
+        ProfScope ps(ctx, ctx->cst, 3, 0.0);
         size_t fi = 0;
         int64_t run_col = -1, run_slot = -1, run_len = 0;
         auto flush = [&]() -> duhl_status {
@@ -199,6 +256,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
                                      ctx->ld_dev * sizeof(float), (size_t)run_len,
                                      cudaMemcpyHostToDevice, ctx->cst));
                 ctx->h2d_bytes += (int64_t)bytes;
+                ps.bytes += (double)bytes;
             }
             run_len = 0;
             return DUHL_OK;
@@ -222,6 +280,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             }
         }
         TRY(flush());
+        ps.end();
         CK(cudaEventRecord(ctx->ev_copy, ctx->cst));
         CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0));
     } else {
@@ -246,13 +305,15 @@ static void free_all(duhl_ctx* ctx) {
     void* dev_ptrs[] = {ctx->pool, ctx->d_col_slot, ctx->d_alpha, ctx->d_vt, ctx->d_b, ctx->d_y,
                         ctx->d_norms, ctx->d_z, ctx->d_P, ctx->d_order_j, ctx->d_cols,
                         ctx->d_chg_cols, ctx->d_P_slot, ctx->d_order_slot, ctx->d_chg_slots,
-                        ctx->d_keys, ctx->d_keys2, ctx->d_idx, ctx->d_idx2, ctx->d_sort_tmp,
+                        ctx->d_vsnap,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->registered) cudaHostUnregister(ctx->h_store);
     if (ctx->own_store && ctx->h_store) cudaFreeHost(ctx->h_store);
+    for (auto& t : ctx->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->st) cudaStreamDestroy(ctx->st);
     if (ctx->cst) cudaStreamDestroy(ctx->cst);
@@ -266,9 +327,13 @@ static void choose_scd_shape(duhl_ctx* ctx) {
                                       : std::min<int64_t>(ctx->nsm, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
     int64_t R = round4((ctx->d4 + G - 1) / G);
     G = (ctx->d4 + R - 1) / R;
-    int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 32;
-    W = std::max(4, std::min(32, W / 4 * 4));
-    while (W > 4 && scd_smem_bytes(W, (int)R) > 220 * 1024) W -= 4;
+    // W <= 16 coordinates per block; 3 TMA stages of W column slices must fit in
+    // shared memory together with the fp64 v slice and per-warp partials
+    int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 16;
+    W = std::max(4, std::min(16, W / 4 * 4));
+    const size_t cap = 225 * 1024;
+    while (W > 4 && scd_smem_bytes(W, (int)R, 3) > cap) W -= 4;
+    ctx->NB = 3;
     ctx->W = W;
     ctx->R = (int)R;
     ctx->G = (int)G;
@@ -282,6 +347,8 @@ void duhl_default_config(duhl_config* cfg) {
     cfg->refresh_fraction = 0.05;
     cfg->cert_every = 10;
     cfg->seed = 170805357ull;
+    cfg->cert_adaptive = 1;
+    cfg->scd_exact = 1;
 }
 
 const char* duhl_last_error(const duhl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -405,20 +472,15 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
               dmal((void**)&ctx->d_P_slot, n * sizeof(int)) &&
               dmal((void**)&ctx->d_order_slot, n * sizeof(int)) &&
               dmal((void**)&ctx->d_chg_slots, 2 * n * sizeof(int)) &&
-              dmal((void**)&ctx->d_keys, n * sizeof(uint64_t)) &&
-              dmal((void**)&ctx->d_keys2, n * sizeof(uint64_t)) &&
-              dmal((void**)&ctx->d_idx, n * sizeof(int)) &&
-              dmal((void**)&ctx->d_idx2, n * sizeof(int)) &&
+              dmal((void**)&ctx->d_vsnap, d4 * sizeof(double)) &&
               dmal((void**)&ctx->d_s_acc, n * sizeof(double)) &&
               dmal((void**)&ctx->d_gap_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_s_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_sums, 8 * sizeof(double)) &&
               dmal((void**)&ctx->d_flag, sizeof(int));
     if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
-    ctx->sort_tmp_bytes = sort_temp_bytes(n);
-    if (!dmal(&ctx->d_sort_tmp, ctx->sort_tmp_bytes)) return bail(DUHL_E_NOMEM);
     choose_scd_shape(ctx);
-    if (!dmal((void**)&ctx->d_red, 3 * (size_t)scd_nred(ctx->W) * sizeof(double)) ||
+    if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
@@ -504,6 +566,7 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
         int64_t lo = kb * m, hi = std::min(ctx->n, lo + m);
         for (int64_t i = lo; i < hi; ++i) P.push_back(i);
     } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM) {
+        ProfScope ps(ctx, ctx->st, 2, 8.0 * ctx->n * 7);
         CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
                        ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches));
         P.resize(m);
@@ -544,11 +607,37 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.W = ctx->W;
     p.R = ctx->R;
     p.G = ctx->G;
+    p.NB = ctx->NB;
+    p.exact = ctx->cfg.scd_exact;
     p.red = ctx->d_red;
     p.bar = ctx->d_bar;
-    CK(cudaMemsetAsync(ctx->d_red, 0, 3 * (size_t)scd_nred(ctx->W) * sizeof(double), ctx->st));
+    CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_doubles(ctx->W) * sizeof(double), ctx->st));
     CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
-    CK(launch_scd_gram(p, ctx->st, &ctx->launches));
+    static const bool trace = std::getenv("DUHL_SCD_TRACE") != nullptr;  // developer phase timing
+    unsigned long long* dtr = nullptr;
+    if (trace) {
+        CK(cudaMalloc((void**)&dtr, 16 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(dtr, 0, 16 * sizeof(unsigned long long), ctx->st));
+    }
+    p.trace = dtr;
+    {
+        ProfScope ps(ctx, ctx->st, 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
+        CK(launch_scd_gram(p, ctx->st, &ctx->launches));
+    }
+    if (trace) {
+        unsigned long long h[16];
+        CK(cudaMemcpyAsync(h, dtr, sizeof(h), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        cudaFree(dtr);
+        const double nb = (double)((L + ctx->W - 1) / ctx->W);
+        std::fprintf(stderr, "scd trace (us/block) W=%d G=%d R=%d: ", ctx->W, ctx->G, ctx->R);
+        const char* nm[8] = {"waitdata", "flush", "WAIT", "sGread", "seq", "vupdate", "tiles", "coords"};
+        for (int c2 = 0; c2 < 2; ++c2) {
+            std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
+            for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / 1e3);
+        }
+        std::fprintf(stderr, "\n");
+    }
     ctx->updates += L;
     return DUHL_OK;
 }
@@ -556,11 +645,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
 static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
     const int64_t m = (int64_t)ctx->P.size();
     for (int pass = 0; pass < passes; ++pass) {
-        CK(launch_perm_keys(ctx->d_P, m, seed, round, pass, ctx->d_keys, ctx->d_idx, ctx->st, &ctx->launches));
-        CK(sort_pairs(ctx->d_sort_tmp, ctx->sort_tmp_bytes, ctx->d_keys, ctx->d_keys2, ctx->d_idx,
-                      ctx->d_idx2, m, ctx->st, &ctx->launches));
-        CK(launch_gather_order(ctx->d_idx2, ctx->d_P, ctx->d_P_slot, m, ctx->d_order_j,
-                               ctx->d_order_slot, ctx->st, &ctx->launches));
+        CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, m, seed, round, pass, ctx->d_order_j,
+                             ctx->d_order_slot, ctx->st, &ctx->launches));
         TRY(scd_launch(ctx, m));
     }
     return DUHL_OK;
@@ -632,48 +718,84 @@ duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double*
     return certificate(ctx, gap, primal, dual);
 }
 
+static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy policy, int certify,
+                              duhl_round_record* rec) {
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t n = ctx->n;
+    int64_t kref = (int64_t)std::ceil(ctx->cfg.refresh_fraction * (double)n - 1e-9);
+    kref = std::max<int64_t>(0, std::min(n, kref));
+    int64_t swaps = 0;
+    TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
+    if (kref > 0) {                                                        // l.7-10 at alpha^(t)
+        std::vector<int64_t> idx(kref);
+        for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
+        ctx->cursor = (ctx->cursor + kref) % n;
+        CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr));
+    }
+    TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                         // l.6, l.11
+    const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
+    TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
+    double cg = -1.0;
+    if (certify) TRY(certificate(ctx, &cg, nullptr, nullptr));
+    CK(cudaMemsetAsync(ctx->d_sums + 6, 0, sizeof(double), ctx->st));
+    CK(launch_sum(ctx->d_z, n, ctx->d_sums + 6, ctx->st, &ctx->launches));
+    double zs = 0.0;
+    CK(cudaMemcpyAsync(&zs, ctx->d_sums + 6, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    TRY(check_flag(ctx, "duhl_round"));
+    harvest(ctx);
+    if (rec) {
+        rec->round = t;
+        rec->swaps = swaps;
+        rec->refreshed = kref;
+        rec->cert_gap = cg;
+        rec->z_sum = zs;
+        rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return DUHL_OK;
+}
+
+duhl_status duhl_round(duhl_ctx* ctx, int64_t round, int passes, duhl_policy policy, int certify,
+                       duhl_round_record* rec) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    if (passes < 1 || round < 0) return fail(ctx, DUHL_E_INVALID, "passes/round");
+    return round_impl(ctx, round, passes, policy, certify, rec);
+}
+
 duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes, duhl_policy policy,
                        duhl_round_record* trace, int64_t trace_cap, int64_t* rounds_out, double* gap_out) {
     if (!ctx) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
     if (passes < 1 || max_rounds < 0) return fail(ctx, DUHL_E_INVALID, "passes/max_rounds");
     auto t0 = std::chrono::steady_clock::now();
-    const int64_t n = ctx->n;
-    int64_t kref = (int64_t)std::ceil(ctx->cfg.refresh_fraction * (double)n - 1e-9);
-    kref = std::max<int64_t>(0, std::min(n, kref));
-    std::vector<int64_t> idx(kref);
     double gap = INFINITY;
     duhl_status st = DUHL_E_NOT_CONVERGED;
-    int64_t t = 0;
+    int64_t t = 0, last_cert = -1, backoff = 1;
+    double zs = INFINITY;
     for (t = 0; t < max_rounds; ++t) {
-        int64_t swaps = 0;
-        TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                 // Alg. 2 l.3-4
-        if (kref > 0) {                                                       // l.7-10 at alpha^(t)
-            for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
-            ctx->cursor = (ctx->cursor + kref) % n;
-            CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
-            TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr));
-        }
-        TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
-        const int64_t m = (int64_t)ctx->P.size();                             // z_P at alpha^(t+1) (R9)
-        TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
-        double cg = -1.0;
-        if ((t + 1) % ctx->cfg.cert_every == 0) {
+        // certify on the fixed schedule, or (adaptive) when the gap memory's own
+        // estimate says we may be done; failed adaptive checks back off 1, 2, 4, ... rounds
+        bool sched = (t + 1) % ctx->cfg.cert_every == 0;
+        bool adapt = ctx->cfg.cert_adaptive && zs <= eps && (t - last_cert) >= backoff;
+        duhl_round_record r{};
+        TRY(round_impl(ctx, t, passes, policy, (sched || adapt) ? 1 : 0, &r));
+        zs = r.z_sum;
+        if (r.cert_gap >= 0.0) {
+            gap = r.cert_gap;
+            if (adapt && !sched && gap > eps) backoff *= 2;
+            last_cert = t;
+        } else if (ctx->cfg.cert_adaptive && zs <= eps && (t - last_cert) >= backoff) {
+            // the estimate crossed eps during this round: certify now rather than next round
             TRY(certificate(ctx, &gap, nullptr, nullptr));
-            cg = gap;
-        } else {
-            CK(cudaStreamSynchronize(ctx->st));  // idx buffer reuse
-            TRY(check_flag(ctx, "duhl_solve"));
+            r.cert_gap = gap;
+            if (gap > eps) backoff *= 2;
+            last_cert = t;
         }
-        if (trace && t < trace_cap) {
-            duhl_round_record& r = trace[t];
-            r.round = t;
-            r.swaps = swaps;
-            r.refreshed = kref;
-            r.cert_gap = cg;
-            r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        }
-        if (cg >= 0.0 && gap <= eps) { st = DUHL_OK; ++t; break; }
+        r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (trace && t < trace_cap) trace[t] = r;
+        if (r.cert_gap >= 0.0 && gap <= eps) { st = DUHL_OK; ++t; break; }
     }
     if (rounds_out) *rounds_out = t;
     if (gap_out) *gap_out = gap;
@@ -715,6 +837,19 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
 duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {
     if (!ctx || !stream_out) return DUHL_E_INVALID;
     *stream_out = (void*)ctx->st;
+    return DUHL_OK;
+}
+
+duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
+                                  double* bytes) {
+    if (!ctx || kind < 0 || kind > 3) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaStreamSynchronize(ctx->st));
+    CK(cudaStreamSynchronize(ctx->cst));
+    harvest(ctx);
+    if (launches) *launches = ctx->st_launch[kind];
+    if (ms) *ms = ctx->st_ms[kind];
+    if (bytes) *bytes = ctx->st_bytes[kind];
     return DUHL_OK;
 }
 

@@ -9,7 +9,8 @@
 // round_up(d, 4) rows so each column is a whole number of 16-byte vectors.
 // All accumulation is fp64 (fp32 x fp32 products are exact in fp64).
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
+
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.h"
@@ -291,271 +292,461 @@ cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint
 }
 
 // =====================================================================================
-// Pass permutation: P sorted by (key(seed, round, pass, j), j).  P is ascending
-// and the radix sort is stable, so equal keys keep index order.
+// Pass permutation: position t takes P[pi(t)], pi a
+// keyed 8-round Feistel bijection on [0, 4^h) >= m, restricted to [0, m) by
+// cycle walking.  One thread per position, no sort.
 // =====================================================================================
-__global__ void k_perm_keys(const int64_t* P, int64_t m, uint64_t seed, int64_t round,
-                            int64_t pass, uint64_t* keys, int* idx) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < m) {
-        keys[t] = perm_key(seed, round, pass, P[t]);
-        idx[t] = (int)t;
-    }
-}
-cudaError_t launch_perm_keys(const int64_t* P, int64_t m, uint64_t seed, int64_t round,
-                             int64_t pass, uint64_t* keys, int* idx, cudaStream_t st,
-                             int64_t* launches) {
-    k_perm_keys<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(P, m, seed, round, pass, keys, idx);
-    ++*launches;
-    return cudaGetLastError();
+__device__ __forceinline__ int64_t feistel_index(uint64_t key, int h, int64_t m, int64_t t) {
+    const uint64_t mask = (1ull << h) - 1;
+    uint64_t x = (uint64_t)t;
+    do {
+        uint64_t L = x >> h, R = x & mask;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            uint64_t F = mix64(key ^ ((uint64_t)r << 56) ^ R) & mask;
+            uint64_t nl = R;
+            R = L ^ F;
+            L = nl;
+        }
+        x = (L << h) | R;
+    } while (x >= (uint64_t)m);
+    return (int64_t)x;
 }
 
-__global__ void k_gather_order(const int* sidx, const int64_t* P, const int* P_slot, int64_t m,
-                               int64_t* order_j, int* order_slot) {
+__global__ void k_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t key, int h,
+                             int64_t* order_j, int* order_slot) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < m) {
-        int q = sidx[t];
+        int64_t q = feistel_index(key, h, m, t);
         order_j[t] = P[q];
         order_slot[t] = P_slot[q];
     }
 }
-cudaError_t launch_gather_order(const int* sorted_idx, const int64_t* P, const int* P_slot,
-                                int64_t m, int64_t* order_j, int* order_slot, cudaStream_t st,
-                                int64_t* launches) {
-    k_gather_order<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(sorted_idx, P, P_slot, m, order_j,
-                                                            order_slot);
+
+cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t seed,
+                              int64_t round, int64_t pass, int64_t* order_j, int* order_slot,
+                              cudaStream_t st, int64_t* launches) {
+    if (m <= 0) return cudaSuccess;
+    int h = 1;
+    while ((1ll << (2 * h)) < m) ++h;
+    uint64_t key = mix64(mix64(mix64(seed) ^ (uint64_t)round) ^ (uint64_t)pass);
+    k_perm_order<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(P, P_slot, m, key, h, order_j, order_slot);
     ++*launches;
     return cudaGetLastError();
 }
 
-size_t sort_temp_bytes(int64_t m) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (const int*)nullptr, (int*)nullptr, (int)m);
-    return bytes;
-}
-cudaError_t sort_pairs(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
-                       const int* idx_in, int* idx_out, int64_t m, cudaStream_t st,
-                       int64_t* launches) {
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, idx_in,
-                                                    idx_out, (int)m, 0, 64, st);
-    *launches += 8;  // onesweep: histogram + exclusive-sum + 8-bit passes (counted conservatively)
-    return e;
-}
-
 // =====================================================================================
 // Exact SCD epoch, Gram-block form (App. D closed forms executed in the exact
-// sequential order).
-//
-// Cooperative persistent kernel, G CTAs, CTA c owns rows [cR, cR + R) of the
-// shared vector v (kept in shared memory, fp64) and of every working-set column.
-// For each block B of W coordinates (positions bW .. bW+W of the order):
-//   1. the TMA engine stages the CTA's row slice of the W columns into shared
-//      memory (cp.async.bulk, double buffered: block b+1 streams in while block
-//      b computes and synchronises);
-//   2. partial s_j = a_j^T v (j in B) and partial Gram G_jk = a_j^T a_k (k < j)
-//      over the CTA's rows, fp64, register-tiled 4x4 per warp task;
-//   3. fp64 atomics into a global reduction buffer + one grid barrier;
-//   4. every CTA (redundantly, identically) runs the W closed-form updates in
-//      sequence with s_j <- s_j + sum_{k<j} G_jk delta_k -- exactly sequential
-//      SCD -- and CTA 0 writes alpha;
-//   5. v_slice += sum_j delta_j a_j (own rows; no atomics).
+// sequential order).  Cooperative persistent kernel,
+// G CTAs; CTA c owns rows [cR, cR + R) of the shared vector v (in shared
+// memory, fp64) and of every working-set column, streamed in by the TMA engine
+// (cp.async.bulk + mbarrier, 3 stages).
 // =====================================================================================
-constexpr int kScdThreads = 512;
+constexpr int kScdThreads = 256;
 constexpr int kScdWarps = kScdThreads / 32;
+constexpr int kScdStages = 3;
+constexpr int kRedBufs = 6;     // rotating reduction buffers (see the zeroing rule below)
+constexpr int kRedGroups = 8;   // CTA c adds into group c % 8 ...
+constexpr int kRedStride = 32;  // ... one 256-byte line per (entry, group): spreads the fp64
+                                // atomics of 148 CTAs over many L2 slices
 
-__host__ __device__ __forceinline__ int scd_rc_dev(int W, int nt) {
-    (void)W;
-    int rc = (kScdWarps + nt - 1) / nt;
-    return rc < 1 ? 1 : rc;
-}
+// Reduction entries of a block of W coordinates:
+//   u_j   = a_j^T v_(block start)           [0, W)
+//   G_jk  = a_j^T a_k, k < j (this block)   W + j(j-1)/2 + k
+//   C_jk  = a_j^T a'_k (previous block)     W + W(W-1)/2 + j W + k
+__host__ __device__ __forceinline__ int scd_off_G(int W) { return W; }
+__host__ __device__ __forceinline__ int scd_off_C(int W) { return W + W * (W - 1) / 2; }
+__host__ __device__ int scd_nred(int W) { return W + W * (W - 1) / 2 + W * W; }
+size_t scd_red_doubles(int W) { return (size_t)kRedBufs * scd_nred(W) * kRedGroups * kRedStride; }
 __host__ __device__ __forceinline__ size_t align_up_dev(size_t x) { return (x + 127) / 128 * 128; }
-int scd_nred(int W) { return W + W * (W - 1) / 2; }
-int scd_rc(int W) {
-    int T = W / 4;
-    return scd_rc_dev(W, T * (T + 1) / 2 + T);
-}
-static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-size_t scd_smem_bytes(int W, int R) {
-    size_t off = 128;                                             // mbarriers
-    off += align_up((size_t)2 * W * R * sizeof(float), 128);      // A slices, 2 stages
-    off += align_up((size_t)R * sizeof(double), 128);             // v slice
-    off += align_up((size_t)scd_rc(W) * scd_nred(W) * sizeof(double), 128);  // CTA partials
-    off += align_up((size_t)scd_nred(W) * sizeof(double), 128);   // reduced s, G
-    off += align_up((size_t)32 * sizeof(double), 128);            // deltas
+size_t scd_smem_bytes(int W, int R, int NB) {
+    (void)NB;
+    size_t off = 128;                                                             // mbarriers
+    off += align_up_dev((size_t)kScdStages * W * R * sizeof(float));              // A stages
+    off += align_up_dev((size_t)R * sizeof(double));                              // v slice
+    off += align_up_dev((size_t)scd_nred(W) * sizeof(double));                    // CTA partials
+    off += align_up_dev((size_t)scd_nred(W) * sizeof(double));                    // reduced block
+    off += align_up_dev((size_t)2 * 16 * sizeof(double));                         // deltas (2 blocks)
     return off;
 }
 
-__device__ __forceinline__ void scd_issue(const ScdParams& p, float* dst, int64_t base, int Wb,
-                                          int64_t r0, int rows, uint64_t* bar) {
-    const unsigned bytes = (unsigned)rows * 4u;
-    mbar_arrive_expect_tx(bar, bytes * (unsigned)Wb);
-    for (int j = 0; j < Wb; ++j) {
-        const float* src = p.pool + (int64_t)p.order_slot[base + j] * p.ld_dev + r0;
-        bulk_g2s(dst + (size_t)j * p.R, src, bytes, bar);
+// Warp reduce-scatter: on return lane l holds the warp-wide sum of g[l % N]
+// (N - 1 shuffles instead of 5 N).
+template <typename T, int N>
+__device__ __forceinline__ T reduce_scatter(T (&g)[N], int lane) {
+#pragma unroll
+    for (int half = N / 2, off = N / 2; half >= 1; half >>= 1, off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            T send = upper ? g[i] : g[i + half];
+            T keep = upper ? g[i + half] : g[i];
+            g[i] = keep + __shfl_xor_sync(~0u, send, off);
+        }
+    }
+    T v = g[0];
+#pragma unroll
+    for (int off = N; off < 32; off <<= 1) v += __shfl_xor_sync(~0u, v, off);
+    return v;
+}
+
+// 4 x KW register tile over rows [lo, hi) (multiples of 4): lane l takes the
+// 4-row group starting at lo + 4 l (+ 128 i), 16-byte shared loads.  Output
+// element (a, q) -> row j = jbase + a, column k = kbase + q of G (LOWER, kept
+// where k < j) or C.  EXACT: fp64 products/accumulation (fp32 -> fp64 exact);
+// fast: fp32 FFMA inside the warp, fp64 from the warp reduction on.
+template <bool EXACT, int KW, bool LOWER>
+__device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float* __restrict__ Ak, int R,
+                                      int lo, int hi, int lane, int jbase, int kbase, double* out,
+                                      int W) {
+    typedef typename std::conditional<EXACT, double, float>::type T;
+    T g[4 * KW];
+#pragma unroll
+    for (int e = 0; e < 4 * KW; ++e) g[e] = T(0);
+    const float4* xj[4];
+    const float4* yk[KW];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) xj[a] = reinterpret_cast<const float4*>(Aj + (size_t)a * R);
+#pragma unroll
+    for (int q = 0; q < KW; ++q) yk[q] = reinterpret_cast<const float4*>(Ak + (size_t)q * R);
+    for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
+        float4 x[4], y[KW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) x[a] = xj[a][r4];
+#pragma unroll
+        for (int q = 0; q < KW; ++q) y[q] = yk[q][r4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int q = 0; q < KW; ++q) {
+                T acc = g[a * KW + q];
+                acc = fma((T)x[a].x, (T)y[q].x, acc);
+                acc = fma((T)x[a].y, (T)y[q].y, acc);
+                acc = fma((T)x[a].z, (T)y[q].z, acc);
+                acc = fma((T)x[a].w, (T)y[q].w, acc);
+                g[a * KW + q] = acc;
+            }
+    }
+    const double v = (double)reduce_scatter<T, 4 * KW>(g, lane);
+    if (lane < 4 * KW) {
+        const int j = jbase + lane / KW, k = kbase + lane % KW;
+        if (LOWER) {
+            if (k < j) out[scd_off_G(W) + j * (j - 1) / 2 + k] = v;
+        } else {
+            out[scd_off_C(W) + j * W + k] = v;
+        }
     }
 }
 
+// u tile: 4 x 1 against the fp64 v slice (always fp64)
+__device__ __forceinline__ void utile(const float* __restrict__ Aj, const double* __restrict__ vs, int R,
+                                      int lo, int hi, int lane, int jbase, double* out) {
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2* v2 = reinterpret_cast<const double2*>(vs);
+    for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
+        const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const float4 x = reinterpret_cast<const float4*>(Aj + (size_t)a * R)[r4];
+            double t = g[a];
+            t = fma((double)x.x, v01.x, t);
+            t = fma((double)x.y, v01.y, t);
+            t = fma((double)x.z, v23.x, t);
+            t = fma((double)x.w, v23.y, t);
+            g[a] = t;
+        }
+    }
+    const double v = reduce_scatter<double, 4>(g, lane);
+    if (lane < 4) out[jbase + lane] = v;
+}
+
+// Exact coordinate step with the reciprocal 1/||a_j||^2 precomputed (same
+// closed forms as coord_step, App. D; zero column -> its 1-D minimiser).
+__device__ __forceinline__ double coord_step_inv(int model, double a, double s, double inv, bool zero,
+                                                 double y, double lam_dn) {
+    if (model == kLasso) {
+        if (zero) return 0.0;
+        double gamma = a - s * inv;               // (a ||a||^2 - s) / ||a||^2
+        double mag = fabs(gamma) - lam_dn * inv;  // tau = lambda d / ||a||^2
+        return mag > 0.0 ? copysign(mag, gamma) : 0.0;
+    }
+    if (zero) return y;
+    double u = fma(lam_dn - y * s, inv, y * a);  // y (a + Delta), Delta = (lambda n y - s)/||a||^2
+    u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
+    return y * u;
+}
+
+// Stage the CTA's row slice of block blk's columns into shared memory with the
+// TMA engine.  Called by a whole warp: lane j fetches the slot of column j (one
+// parallel L2 round trip instead of W dependent ones) and issues its own bulk
+// copy; lane 0 arms the stage's mbarrier with the total byte count first.
+__device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint64_t* mbar, int64_t blk,
+                                          int64_t r0, int rows, int lane) {
+    const int W = p.W;
+    const int64_t base = blk * W;
+    const int Wb = (int)imin64(W, p.L - base);
+    const int st = (int)(blk % kScdStages);
+    float* dst = Abuf + (size_t)st * W * p.R;
+    const unsigned bytes = (unsigned)rows * 4u;
+    const int slot = lane < Wb ? p.order_slot[base + lane] : 0;
+    fence_proxy_async();  // earlier generic reads of this stage before the async-proxy refill
+    if (lane == 0) mbar_arrive_expect_tx(&mbar[st], bytes * (unsigned)Wb);
+    __syncwarp();
+    if (lane < Wb) bulk_g2s(dst + (size_t)lane * p.R, p.pool + (int64_t)slot * p.ld_dev + r0, bytes, &mbar[st]);
+}
+
+// =====================================================================================
+// k_scd_gram: exact sequential SCD epoch, Gram-block form, barrier off the
+// critical path.  Iteration b (blocks b and b+1 resident, b+2 streaming in):
+//   A. partials of block b+1 over the CTA's rows: G_{b+1} (lower), the cross
+//      Gram C_{b+1,b} = A_{b+1}^T A_b and u_{b+1} = A_{b+1}^T v_b (v_b = v at
+//      the start of block b) -> atomics into red[(b+1) % 6] -> ARRIVE(b+1)
+//   B. WAIT(b) (arrived one full phase earlier) -> every CTA redundantly runs
+//      the W closed-form steps of block b in order with
+//        s_j = u_j + sum_k C_jk delta^{(b-1)}_k + sum_{k<j} G_jk delta_k
+//      (== a_j^T v at the moment coordinate j is visited: exactly sequential SCD)
+//   C. v_slice += A_b delta^{(b)}; stage of block b streams block b+3.
+// Zeroing rule: CTA 0 zeroes red[(b+4) % 6] right after WAIT(b); all reads of
+// it (phase B of block b-2) precede everyone's ARRIVE(b), and its next writer
+// (phase A of iteration b+3) waits on ARRIVE(b+2), which CTA 0 issues after
+// zeroing.
+// =====================================================================================
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <bool EXACT>
 __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int W = p.W, R = p.R;
-    const int NRED = W + W * (W - 1) / 2;
-    const int T = W / 4;
-    const int NG = T * (T + 1) / 2;
-    const int NT = NG + T;
-    const int RC = scd_rc_dev(W, NT);
+    const int W = p.W, R = p.R, T = W / 4;
+    const int NRED = scd_nred(W);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
     size_t off = 128;
     float* Abuf = reinterpret_cast<float*>(smem + off);
-    off += align_up_dev((size_t)2 * W * R * sizeof(float));
+    off += align_up_dev((size_t)kScdStages * W * R * sizeof(float));
     double* vs = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)R * sizeof(double));
     double* acc = reinterpret_cast<double*>(smem + off);
-    off += align_up_dev((size_t)RC * NRED * sizeof(double));
+    off += align_up_dev((size_t)NRED * sizeof(double));
     double* sG = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)NRED * sizeof(double));
-    double* delta = reinterpret_cast<double*>(smem + off);
+    double* delta = reinterpret_cast<double*>(smem + off);  // [2][16]
+    __shared__ int64_t cj[2][16];
+    __shared__ double ca[2][16], cinv[2][16], cy[2][16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * R;
     const int rows = (int)imin64(R, p.d4 - r0);
-    const double dd = (double)p.d, nn = (double)p.n;
+    const double lam_dn = p.model == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
+    const size_t bufsz = (size_t)NRED * kRedGroups * kRedStride;
+    const int grp = c % kRedGroups;
 
-    // init: zero the stage buffers (tail rows of the last CTA stay zero), load v slice
-    for (int q = tid; q < 2 * W * R; q += kScdThreads) Abuf[q] = 0.0f;
+    for (int q = tid; q < kScdStages * W * R; q += kScdThreads) Abuf[q] = 0.0f;
     for (int r = tid; r < R; r += kScdThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
-    for (int q = tid; q < RC * NRED; q += kScdThreads) acc[q] = 0.0;
+    for (int q = tid; q < NRED; q += kScdThreads) acc[q] = 0.0;
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int q = 0; q < kScdStages; ++q) mbar_init(&mbar[q], 1);
         fence_mbar_init();
     }
     fence_proxy_async();
     __syncthreads();
 
+    // developer trace (ScdParams::trace): per-phase globaltimer stamps of CTA 0 / CTA G-1
+    const bool tr = p.trace && tid == 0 && (c == 0 || c == p.G - 1);
+    unsigned long long* trc = tr ? p.trace + (c == 0 ? 0 : 8) : nullptr;
+    unsigned long long tprev = tr ? gtimer() : 0;
+    auto stamp = [&](int k) {
+        if (tr) {
+            unsigned long long t = gtimer();
+            trc[k] += t - tprev;
+            tprev = t;
+        }
+    };
     const int64_t nblk = (p.L + W - 1) / W;
-    if (tid == 0 && nblk > 0) scd_issue(p, Abuf, 0, (int)imin64(W, p.L), r0, rows, &mbar[0]);
-
-    for (int64_t b = 0; b < nblk; ++b) {
-        const int buf = (int)(b & 1);
-        const int64_t base = b * W;
-        const int Wb = (int)imin64(W, p.L - base);
-        float* A = Abuf + (size_t)buf * W * R;
-        if (tid == 0 && b + 1 < nblk)
-            scd_issue(p, Abuf + (size_t)(buf ^ 1) * W * R, base + W,
-                      (int)imin64(W, p.L - base - W), r0, rows, &mbar[buf ^ 1]);
-        mbar_wait(&mbar[buf], (unsigned)((b >> 1) & 1));
-
-        // ---- 2. partial dots: tasks = Gram 4x4 tiles (jt >= kt) + s tiles, x RC row chunks
-        const int chunk = (rows + RC - 1) / RC;
-        for (int item = warp; item < NT * RC; item += kScdWarps) {
-            const int task = item % NT, rc = item / NT;
-            const int lo = rc * chunk, hi = min(rows, lo + chunk);
-            double* out = acc + (size_t)rc * NRED;
-            if (task < NG) {
-                int jt = (int)((sqrtf(8.0f * task + 1.0f) - 1.0f) * 0.5f);
-                while ((jt + 1) * (jt + 2) / 2 <= task) ++jt;
-                while (jt * (jt + 1) / 2 > task) --jt;
-                const int kt = task - jt * (jt + 1) / 2;
-                const float* Aj = A + (size_t)(4 * jt) * R;
-                const float* Ak = A + (size_t)(4 * kt) * R;
-                double g[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) g[e] = 0.0;
-                for (int r = lo + lane; r < hi; r += 32) {
-                    double x0 = Aj[r], x1 = Aj[R + r], x2 = Aj[2 * R + r], x3 = Aj[3 * R + r];
-                    double y0 = Ak[r], y1 = Ak[R + r], y2 = Ak[2 * R + r], y3 = Ak[3 * R + r];
-                    g[0] = fma(x0, y0, g[0]); g[1] = fma(x0, y1, g[1]); g[2] = fma(x0, y2, g[2]); g[3] = fma(x0, y3, g[3]);
-                    g[4] = fma(x1, y0, g[4]); g[5] = fma(x1, y1, g[5]); g[6] = fma(x1, y2, g[6]); g[7] = fma(x1, y3, g[7]);
-                    g[8] = fma(x2, y0, g[8]); g[9] = fma(x2, y1, g[9]); g[10] = fma(x2, y2, g[10]); g[11] = fma(x2, y3, g[11]);
-                    g[12] = fma(x3, y0, g[12]); g[13] = fma(x3, y1, g[13]); g[14] = fma(x3, y2, g[14]); g[15] = fma(x3, y3, g[15]);
-                }
-#pragma unroll
-                for (int e = 0; e < 16; ++e) g[e] = warp_sum(g[e]);
-                if (lane == 0) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int j = 4 * jt + (e >> 2), k = 4 * kt + (e & 3);
-                        if (k < j) out[W + j * (j - 1) / 2 + k] += g[e];
+    auto stage = [&](int64_t blk) { return Abuf + (size_t)(blk % kScdStages) * W * R; };
+    auto wait_data = [&](int64_t blk) {
+        mbar_wait(&mbar[blk % kScdStages], (unsigned)((blk / kScdStages) & 1));
+    };
+    // block inputs, read before this CTA arrives at the block's barrier (CTA 0
+    // rewrites alpha right after it)
+    auto load_coords = [&](int64_t blk) {
+        if (warp == 0) {
+            const int64_t bs = blk * W;
+            const int wb = (int)imin64(W, p.L - bs);
+            const int sl = (int)(blk & 1);
+            if (lane < wb) {
+                const int64_t jg = p.order_j[bs + lane];
+                const double nrm = p.norms[jg];
+                cj[sl][lane] = jg;
+                ca[sl][lane] = p.alpha[jg];
+                cinv[sl][lane] = nrm > 0.0 ? 1.0 / nrm : -1.0;  // -1 marks a zero column
+                cy[sl][lane] = p.model == kSvm ? p.y[jg] : 0.0;
+            }
+        }
+    };
+    // phase A for block blk (with_c: the cross Gram against block blk-1).
+    // Work items = register tiles over ALL of the CTA's rows (one warp-reduction
+    // per tile): G rows-groups (4 x 8 / 4 x 4, lower block triangle), C tiles
+    // (4 x 8 / 4 x 4) and u tiles (4 x 1, fp64), listed by decreasing cost and
+    // dealt to warps in snake order.
+    auto partials = [&](int64_t blk, bool with_c) {
+        const float* A1 = stage(blk);
+        const float* A0 = with_c ? stage(blk - 1) : nullptr;
+        // item codes: kind (0 G, 1 C, 2 u), jt, k0, kw
+        int item = 0;
+        for (int cost = 2; cost >= 0; --cost) {        // 2: kw 8 tiles, 1: kw 4 tiles, 0: u tiles
+            for (int kind = 0; kind < 3; ++kind) {
+                if ((kind == 2) != (cost == 0)) continue;
+                if (kind == 1 && !with_c) continue;
+                for (int jt = 0; jt < T; ++jt) {
+                    const int kend = kind == 0 ? 4 * jt + 4 : (kind == 1 ? W : 1);
+                    for (int k0 = 0; k0 < kend; k0 += 8) {
+                        const int kw = kind == 2 ? 1 : (kend - k0 >= 8 ? 8 : 4);
+                        if ((kw == 8) != (cost == 2) && kind != 2) continue;
+                        const int round_ = item / kScdWarps, pos = item % kScdWarps;
+                        const int owner = (round_ & 1) ? kScdWarps - 1 - pos : pos;
+                        ++item;
+                        if (owner != warp) continue;
+                        const float* Aj = A1 + (size_t)(4 * jt) * R;
+                        if (kind == 0) {
+                            if (kw == 8) tile4<EXACT, 8, true>(Aj, A1 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
+                            else tile4<EXACT, 4, true>(Aj, A1 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
+                        } else if (kind == 1) {
+                            if (kw == 8) tile4<EXACT, 8, false>(Aj, A0 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
+                            else tile4<EXACT, 4, false>(Aj, A0 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
+                        } else {
+                            utile(Aj, vs, R, 0, rows, lane, 4 * jt, acc);
+                        }
                     }
                 }
-            } else {
-                const int jt = task - NG;
-                const float* Aj = A + (size_t)(4 * jt) * R;
-                double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-                for (int r = lo + lane; r < hi; r += 32) {
-                    const double v = vs[r];
-                    g0 = fma((double)Aj[r], v, g0);
-                    g1 = fma((double)Aj[R + r], v, g1);
-                    g2 = fma((double)Aj[2 * R + r], v, g2);
-                    g3 = fma((double)Aj[3 * R + r], v, g3);
-                }
-                g0 = warp_sum(g0); g1 = warp_sum(g1); g2 = warp_sum(g2); g3 = warp_sum(g3);
-                if (lane == 0) {
-                    out[4 * jt] += g0; out[4 * jt + 1] += g1; out[4 * jt + 2] += g2; out[4 * jt + 3] += g3;
-                }
+            }
+        }
+        stamp(6);
+        load_coords(blk);
+        __syncthreads();
+        stamp(7);
+        double* red_b = p.red + (size_t)(blk % kRedBufs) * bufsz;
+        const int nq = with_c ? NRED : scd_off_C(W);
+        for (int q = tid; q < nq; q += kScdThreads)
+            atomicAdd(&red_b[((size_t)q * kRedGroups + grp) * kRedStride], acc[q]);
+        __syncthreads();
+        if (tid == 0) {  // ARRIVE(blk) on the counter of blk's parity (see WAIT)
+            __threadfence();
+            atomicAdd(&p.bar[blk & 1], 1u);
+        }
+    };
+
+    if (nblk > 0) {
+        if (warp == 0)
+            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) scd_issue(p, Abuf, mbar, q, r0, rows, lane);
+        wait_data(0);
+        partials(0, false);
+    }
+    for (int64_t b = 0; b < nblk; ++b) {
+        const int64_t base = b * W;
+        const int Wb = (int)imin64(W, p.L - base);
+        // ---- A: block b+1's partials hide block b's barrier latency
+        if (b + 1 < nblk) {
+            wait_data(b + 1);
+            stamp(0);
+            partials(b + 1, true);
+        }
+        stamp(1);
+        // ---- B: WAIT(b), reduced block b -> sequential closed-form steps
+        // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
+        // before WAIT(b) completed everywhere: one counter per block parity then
+        // counts exactly the arrivals of blocks b, b-2, b-4, ...
+        if (tid == 0) {
+            const unsigned target = (unsigned)((b / 2 + 1) * (int64_t)p.G);
+            while (ld_acquire_u32(&p.bar[b & 1]) < target) { __nanosleep(32); }
+            __threadfence();
+        }
+        __syncthreads();
+        stamp(2);
+        if (c == 0)
+            for (int q = tid; q < NRED * kRedGroups; q += kScdThreads)
+                p.red[(size_t)((b + 4) % kRedBufs) * bufsz + (size_t)q * kRedStride] = 0.0;
+        {
+            const double* red_b = p.red + (size_t)(b % kRedBufs) * bufsz;
+            const int nq = b > 0 ? NRED : scd_off_C(W);
+            for (int q = tid; q < nq; q += kScdThreads) {
+                double v = 0.0;
+#pragma unroll
+                for (int g = 0; g < kRedGroups; ++g)
+                    v += ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]);
+                sG[q] = v;
             }
         }
         __syncthreads();
-        // ---- 3. cross-CTA reduction + grid barrier
-        double* red_b = p.red + (size_t)(b % 3) * NRED;
-        for (int q = tid; q < NRED; q += kScdThreads) {
-            double v = 0.0;
-            for (int rc = 0; rc < RC; ++rc) { v += acc[(size_t)rc * NRED + q]; acc[(size_t)rc * NRED + q] = 0.0; }
-            atomicAdd(&red_b[q], v);
-        }
-        grid_barrier(p.bar, (unsigned)((b + 1) * (int64_t)p.G));
-        if (c == 0)  // buffer of block b-1 is no longer read by anyone; block b+2 will use it
-            for (int q = tid; q < NRED; q += kScdThreads) p.red[(size_t)((b + 2) % 3) * NRED + q] = 0.0;
-        for (int q = tid; q < NRED; q += kScdThreads) sG[q] = ld_cg_f64(&red_b[q]);
-        __syncthreads();
-        // ---- 4. W sequential closed-form updates (warp 0; lane j owns coordinate j)
+        stamp(3);
         if (warp == 0) {
+            const int sl = (int)(b & 1);
+            const double* dprev = delta + (size_t)(sl ^ 1) * 16;
             int64_t jg = 0;
-            double a = 0, nrm = 0, yy = 0, sj = 0;
+            double a = 0, inv = 0, yy = 0, sj = 0, afin = 0;
+            bool zero = false;
             if (lane < Wb) {
-                jg = p.order_j[base + lane];
-                a = p.alpha[jg];
-                nrm = p.norms[jg];
-                yy = p.model == kSvm ? p.y[jg] : 0.0;
+                jg = cj[sl][lane];
+                a = ca[sl][lane];
+                inv = cinv[sl][lane];
+                zero = inv < 0.0;
+                if (zero) inv = 0.0;
+                yy = cy[sl][lane];
                 sj = sG[lane];
+                if (b > 0)  // u was taken at the start of block b-1: add its effect
+                    for (int k = 0; k < W; ++k) sj = fma(sG[scd_off_C(W) + lane * W + k], dprev[k], sj);
             }
+            double* dcur = delta + (size_t)sl * 16;
             for (int j = 0; j < Wb; ++j) {
-                double dl = 0.0;
-                if (lane == j) {
-                    double an = coord_step(p.model, a, sj, nrm, yy, p.lambda, dd, nn);
-                    dl = an - a;
-                    if (c == 0) p.alpha[jg] = an;
-                }
-                dl = __shfl_sync(~0u, dl, j);
-                if (lane > j && lane < Wb) sj = fma(sG[W + lane * (lane - 1) / 2 + j], dl, sj);
-                if (lane == 0) delta[j] = dl;
+                const double an = coord_step_inv(p.model, a, sj, inv, zero, yy, lam_dn);
+                if (lane == j) afin = an;
+                const double dl = __shfl_sync(~0u, an - a, j);
+                if (lane > j && lane < Wb) sj = fma(sG[scd_off_G(W) + lane * (lane - 1) / 2 + j], dl, sj);
+                if (lane == 0) dcur[j] = dl;
             }
-            if (lane >= Wb && lane < W) delta[lane] = 0.0;
+            if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
+            if (lane < Wb && c == 0) p.alpha[jg] = afin;
         }
         __syncthreads();
-        // ---- 5. v slice update, sequential order of j (as in the paper's v~ update)
-        for (int r = tid; r < rows; r += kScdThreads) {
-            double v = vs[r];
-            for (int j = 0; j < Wb; ++j) v = fma(delta[j], (double)A[(size_t)j * R + r], v);
-            vs[r] = v;
+        stamp(4);
+        // ---- C: v slice update, sequential order of j; stage b -> block b+3
+        {
+            const float* A = stage(b);
+            const double* dcur = delta + (size_t)(b & 1) * 16;
+            double2* v2 = reinterpret_cast<double2*>(vs);
+            for (int r4 = tid; r4 < (rows >> 2); r4 += kScdThreads) {
+                double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                for (int j = 0; j < Wb; ++j) {
+                    const float4 x = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
+                    const double dj = dcur[j];
+                    v01.x = fma(dj, (double)x.x, v01.x);
+                    v01.y = fma(dj, (double)x.y, v01.y);
+                    v23.x = fma(dj, (double)x.z, v23.x);
+                    v23.y = fma(dj, (double)x.w, v23.y);
+                }
+                v2[2 * r4] = v01;
+                v2[2 * r4 + 1] = v23;
+            }
         }
         __syncthreads();
+        stamp(5);
+        if (warp == 0 && b + kScdStages < nblk) scd_issue(p, Abuf, mbar, b + kScdStages, r0, rows, lane);
     }
     for (int r = tid; r < rows; r += kScdThreads) p.vt[r0 + r] = vs[r];
 }
 
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches) {
     if (p.L <= 0) return cudaSuccess;
-    size_t smem = scd_smem_bytes(p.W, p.R);
-    cudaError_t e = cudaFuncSetAttribute(k_scd_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    size_t smem = scd_smem_bytes(p.W, p.R, kScdStages);
+    const void* fn = p.exact ? (const void*)k_scd_gram<true> : (const void*)k_scd_gram<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     ScdParams q = p;
     void* args[] = {&q};
-    e = cudaLaunchCooperativeKernel((const void*)k_scd_gram, dim3(p.G), dim3(kScdThreads), args,
-                                    smem, st);
+    e = cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(kScdThreads), args, smem, st);
     ++*launches;
     return e;
 }
@@ -590,6 +781,28 @@ cudaError_t launch_set_slots(int* col_slot, const int64_t* cols, const int* slot
                              cudaStream_t st, int64_t* launches) {
     if (cnt <= 0) return cudaSuccess;
     k_set_slots<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(col_slot, cols, slots, cnt);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// out[0] += sum_i x_i
+__global__ void k_sum(const double* x, int64_t n, double* out) {
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s += x[i];
+    s = warp_sum(s);
+    __shared__ double sh[8];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += sh[w];
+        atomicAdd(out, a);
+    }
+}
+cudaError_t launch_sum(const double* x, int64_t n, double* out, cudaStream_t st, int64_t* launches) {
+    k_sum<<<(unsigned)imin64(cdiv(n, 256), 296), 256, 0, st>>>(x, n, out);
     ++*launches;
     return cudaGetLastError();
 }

@@ -47,14 +47,16 @@ struct ScdParams {
     const double* y;           // [n] (SVM) or nullptr
     double* alpha;             // [n]
     double* vt;                // [d4] shared vector
-    int W, R, G;               // block size, rows per CTA, CTAs
-    double* red;               // [3 * NRED] zero on entry
-    unsigned* bar;             // grid-barrier counter, zero on entry
+    int W, R, G, NB;           // block size (<= 16, % 4 == 0), rows per CTA, CTAs, TMA stages (3)
+    int exact;                 // 1: fp64 Gram products (bit-level parity mode); 0: fp32 Gram within a warp
+    double* red;               // [scd_red_doubles(W)] zero on entry
+    unsigned* bar;             // [2] grid-barrier counters (per block parity), zero on entry
+    unsigned long long* trace; // developer phase timer [16] or nullptr
 };
 
-int scd_nred(int W);
-size_t scd_smem_bytes(int W, int R);
-int scd_rc(int W);             // row chunks per tile task
+__host__ __device__ int scd_nred(int W);
+size_t scd_red_doubles(int W);  // size of ScdParams::red
+size_t scd_smem_bytes(int W, int R, int NB);
 
 cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches);
 cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* norms,
@@ -62,25 +64,17 @@ cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* n
 cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,
                         int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
                         int64_t* launches);
-cudaError_t launch_perm_keys(const int64_t* P, int64_t m, uint64_t seed, int64_t round,
-                             int64_t pass, uint64_t* keys, int* idx, cudaStream_t st,
-                             int64_t* launches);
-cudaError_t launch_gather_order(const int* sorted_idx, const int64_t* P, const int* P_slot,
-                                int64_t m, int64_t* order_j, int* order_slot, cudaStream_t st,
-                                int64_t* launches);
+cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t seed,
+                              int64_t round, int64_t pass, int64_t* order_j, int* order_slot,
+                              cudaStream_t st, int64_t* launches);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int64_t d,
                           int64_t d4, const double* b, double* vt, cudaStream_t st,
                           int64_t* launches);
 cudaError_t launch_set_slots(int* col_slot, const int64_t* cols, const int* slots, int64_t cnt,
                              cudaStream_t st, int64_t* launches);
+cudaError_t launch_sum(const double* x, int64_t n, double* out, cudaStream_t st, int64_t* launches);
 cudaError_t launch_vec_sums(const double* vt, const double* b, int64_t d4, double* out2,
                             cudaStream_t st, int64_t* launches);
-
-// Radix sort of (key, idx) pairs (CUB, compiled into this library).
-size_t sort_temp_bytes(int64_t m);
-cudaError_t sort_pairs(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
-                       const int* idx_in, int* idx_out, int64_t m, cudaStream_t st,
-                       int64_t* launches);
 
 }  // namespace duhl

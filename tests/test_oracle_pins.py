@@ -322,11 +322,24 @@ def test_counter_generator_is_splitmix64():
     assert O.lib().or_mix64(0) == 0xE220A8397B1DCDAF
     # second output of the splitmix64 stream from 0 = mix(0x9E37..) step
     assert O.lib().or_mix64(0x9E3779B97F4A7C15) == 0x6E789E6AA1B965F4
-    P = np.arange(10, 60)
-    p1 = O.make_perm(P, 1, 2, 3)
-    assert sorted(p1.tolist()) == P.tolist()
-    keys = [O.perm_key(1, 2, 3, int(j)) for j in p1]
-    assert keys == sorted(keys)
+
+
+def test_pass_permutation_is_a_uniform_bijection():
+    """Feistel + cycle walking: a bijection of P for every m,
+    and positions are uniform over many keys (chi-square), so passes are randomized."""
+    for m in (1, 2, 3, 5, 16, 17, 100, 1000, 4097):
+        P = np.arange(7, 7 + m) * 3
+        p = O.make_perm(P, 5, 1, 2)
+        assert sorted(p.tolist()) == P.tolist()
+    m = 10
+    counts = np.zeros((m, m))
+    for r in range(3000):
+        p = O.make_perm(np.arange(m), 42, r, 0)
+        counts[np.arange(m), p] += 1
+    chi2 = ((counts - 300) ** 2 / 300).sum()
+    assert chi2 < 81 + 5 * np.sqrt(2 * 81)   # dof (m-1)^2 = 81
+    # different passes give different orders
+    assert O.make_perm(np.arange(50), 1, 0, 0).tolist() != O.make_perm(np.arange(50), 1, 0, 1).tolist()
 
 
 # ----------------------------------------------------------------------------- DuHL loop
