@@ -223,7 +223,8 @@ def run_duhl(args, cfg, rank, world, local):
 
     # ---------------- device-timed steady-state rounds
     t_create = time.perf_counter()
-    P = D.create(A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, **common)
+    P = D.create(A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, scd_exact=args.exact,
+                 **common)
     t_create = time.perf_counter() - t_create
     stream = torch.cuda.ExternalStream(P.stream())
     for t in range(args.warmup):
@@ -231,7 +232,7 @@ def run_duhl(args, cfg, rank, world, local):
     barrier(world)
     torch.cuda.synchronize()
     c0 = P.counters()
-    k0 = {k: P.kernel_stats(k) for k in range(4)}
+    k0 = {k: P.kernel_stats(k) for k in range(5)}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     swaps = refreshed = 0
     with ClockSampler(local) as clk:
@@ -246,13 +247,13 @@ def run_duhl(args, cfg, rank, world, local):
     barrier(world)
     elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
     c1 = P.counters()
-    k1 = {k: P.kernel_stats(k) for k in range(4)}
+    k1 = {k: P.kernel_stats(k) for k in range(5)}
     P.close()
     updates = args.steps * m * args.passes * world
     value = updates / elapsed
-    ms = {k: k1[k][1] - k0[k][1] for k in range(4)}
-    nl = {k: k1[k][0] - k0[k][0] for k in range(4)}
-    by = {k: k1[k][2] - k0[k][2] for k in range(4)}
+    ms = {k: k1[k][1] - k0[k][1] for k in range(5)}
+    nl = {k: k1[k][0] - k0[k][0] for k in range(5)}
+    by = {k: k1[k][2] - k0[k][2] for k in range(5)}
     peak, peak_src = hbm_peak()
     scd_gbs = by[0] / (ms[0] / 1e3) / 1e9 if ms[0] > 0 else None
     gap_gbs = by[1] / (ms[1] / 1e3) / 1e9 if ms[1] > 0 else None
@@ -278,7 +279,8 @@ def run_duhl(args, cfg, rank, world, local):
     if not args.no_e2e:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        P2 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, **common)
+        P2 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
+                      **common)
         t_c2 = time.perf_counter() - t0
         r = P2.solve(args.eps, args.max_rounds, passes=args.passes, policy=policy)
         wall = time.perf_counter() - t0
@@ -316,7 +318,9 @@ def run_duhl(args, cfg, rank, world, local):
                        "parallelism": f"cocoa{world}"},
             "roofline": roofline,
             "gap_pass_GBps": gap_gbs, "scd_GBps": scd_gbs,
-            "kernel_ms": {"scd": ms[0], "gap": ms[1], "topm": ms[2], "stage_h2d": ms[3]},
+            "kernel_ms": {"scd": ms[0], "gap_zP": ms[1], "topm": ms[2], "stage_h2d": ms[3],
+                          "refresh_unitA": ms[4]},
+            "refresh_GBps": (by[4] / (ms[4] / 1e3) / 1e9) if ms[4] > 0 else None,
             "swaps_per_step": swaps / args.steps, "refreshed_per_step": refreshed / args.steps,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": c1["launches"] - c0["launches"],
@@ -341,6 +345,7 @@ def main():
     ap.add_argument("--cert-every", type=int, default=50)
     ap.add_argument("--ref-cols", type=int, default=2000)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exact", action="store_true", help="fp64 Gram products in the SCD kernel")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/duhl.h"
+#include "device.cuh"
 #include "kernels.h"
 
 using namespace duhl;
@@ -35,8 +36,8 @@ struct duhl_ctx {
     duhl_config cfg{};
     std::string err;
     int dev = 0, nsm = 0;
-    cudaStream_t st = nullptr, cst = nullptr;
-    cudaEvent_t ev_copy = nullptr;
+    cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
+    cudaEvent_t ev_copy = nullptr, ev_snap = nullptr, ev_ref = nullptr;
     // ---- unit A: pinned host store
     float* h_store = nullptr;
     bool own_store = false, registered = false;
@@ -69,8 +70,21 @@ struct duhl_ctx {
     struct Timed { cudaEvent_t a, b; int kind; double bytes; };
     std::vector<Timed> pending;
     std::vector<cudaEvent_t> event_pool;
-    int64_t st_launch[4] = {0, 0, 0, 0};
-    double st_ms[4] = {0, 0, 0, 0}, st_bytes[4] = {0, 0, 0, 0};
+    int64_t st_launch[5] = {0, 0, 0, 0, 0};
+    double st_ms[5] = {0, 0, 0, 0, 0}, st_bytes[5] = {0, 0, 0, 0, 0};
+    double* d_s_acc2 = nullptr;  // partial-dot accumulator of the concurrent refresh pass
+    // ---- staging overlapped with the SCD epoch
+    typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
+    WriteValue32 write_value = nullptr;  // cuStreamWriteValue32 via cudaGetDriverEntryPoint
+    unsigned* d_progress = nullptr;      // last landed staging copy (sequence number)
+    unsigned batch_seq = 0;
+    std::vector<unsigned> slot_batch;    // [S] sequence number of the copy that filled a slot
+    unsigned *d_P_batch = nullptr, *d_order_batch = nullptr;
+    double *d_order_a = nullptr, *d_order_inv = nullptr, *d_order_y = nullptr;
+    std::vector<int64_t> pend_cols;      // staged columns not yet in the device table
+    std::vector<int> pend_slots;
+    struct Copy { int64_t col; int slot; unsigned seq; };
+    std::vector<Copy> copy_plan;         // planned, not yet enqueued staging copies
 };
 
 // ------------------------------------------------------------------------- profiling
@@ -192,16 +206,19 @@ static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
 // gap pass over d_cols[0..k) (nullptr = all n), writing z; optional device outputs
 static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, double* gap_out,
                             double* s_out, double* sums, bool write_z = true,
-                            const double* vt_override = nullptr) {
+                            const double* vt_override = nullptr, cudaStream_t stream = nullptr,
+                            double* s_acc = nullptr, int tile_rows = kGapTileRows) {
+    cudaStream_t sx = stream ? stream : ctx->st;
     GapParams p = gap_params(ctx, d_cols, d_cols ? k : ctx->n);
     if (vt_override) p.vt = vt_override;
     p.gap_out = gap_out;
     p.s_out = s_out;
     p.sums = sums;
     if (!write_z) p.z = nullptr;
-    const int64_t tiles = (ctx->d4 + kGapTileRows - 1) / kGapTileRows;
-    ProfScope ps(ctx, ctx->st, 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
-    CK(launch_gap_pass(p, kGapTileRows, ctx->st, &ctx->launches));
+    if (s_acc) p.s_acc = s_acc;
+    const int64_t tiles = (ctx->d4 + tile_rows - 1) / tile_rows;
+    ProfScope ps(ctx, sx, stream ? 4 : 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
+    CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches));
     return DUHL_OK;
 }
 
@@ -219,9 +236,86 @@ static duhl_status upload_slots_changes(duhl_ctx* ctx, const std::vector<int64_t
     return DUHL_OK;
 }
 
-// Stage P (ascending) into the slot pool: evict non-members, copy new columns
-// host -> HBM in maximal contiguous runs on the copy stream (Alg. 2 l.4).
-static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& P, int64_t* swaps) {
+// Host copy of the device pass permutation (kernels.cu feistel_index): the
+// position map of pass 0 orders the H2D staging so columns land in the order
+// the SCD kernel consumes them.
+static int64_t feistel_host(uint64_t key, int h, int64_t m, int64_t t) {
+    const uint64_t mask = (1ull << h) - 1;
+    uint64_t x = (uint64_t)t;
+    do {
+        uint64_t L = x >> h, R = x & mask;
+        for (int r = 0; r < 8; ++r) {
+            uint64_t F = mix64(key ^ ((uint64_t)r << 56) ^ R) & mask;
+            uint64_t nl = R;
+            R = L ^ F;
+            L = nl;
+        }
+        x = (L << h) | R;
+    } while (x >= (uint64_t)m);
+    return (int64_t)x;
+}
+
+// Make the device column table point at the columns staged by the last
+// stage_working_set (their copies must have landed: the compute stream waits
+// on the copy stream first).
+static duhl_status issue_staging(duhl_ctx* ctx);
+static duhl_status finalize_staging(duhl_ctx* ctx) {
+    TRY(issue_staging(ctx));
+    if (ctx->pend_cols.empty()) return DUHL_OK;
+    CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0));
+    std::vector<int64_t> cols;
+    std::vector<int> slots;
+    cols.swap(ctx->pend_cols);
+    slots.swap(ctx->pend_slots);
+    return upload_slots_changes(ctx, cols, slots);
+}
+
+// Enqueue the planned host -> HBM copies on the copy stream, each followed by a
+// stream write of its sequence number to d_progress (the SCD kernel waits on
+// it).  Called right after the SCD launch so the host-side enqueue overlaps the
+// epoch.  On a failure the counter is forced to its final value so a waiting
+// kernel can drain, and the error is reported.
+static duhl_status issue_staging(duhl_ctx* ctx) {
+    if (ctx->copy_plan.empty()) return DUHL_OK;
+    duhl_status rc = DUHL_OK;
+    {
+        ProfScope ps(ctx, ctx->cst, 3, 0.0);
+        const size_t col_bytes = (size_t)ctx->ld_dev * sizeof(float);
+        for (const auto& c : ctx->copy_plan) {
+            if (cudaMemcpyAsync(ctx->pool + (int64_t)c.slot * ctx->ld_dev, ctx->h_store + c.col * ctx->ld_host,
+                                col_bytes, cudaMemcpyHostToDevice, ctx->cst) != cudaSuccess) {
+                rc = fail(ctx, DUHL_E_CUDA, "staging cudaMemcpyAsync failed");
+                break;
+            }
+            ctx->h2d_bytes += (int64_t)col_bytes;
+            ps.bytes += (double)col_bytes;
+            if (ctx->write_value &&
+                ctx->write_value(ctx->cst, (unsigned long long)(uintptr_t)ctx->d_progress, c.seq, 0) != 0) {
+                rc = fail(ctx, DUHL_E_CUDA, "cuStreamWriteValue32 failed");
+                break;
+            }
+        }
+    }
+    if (rc != DUHL_OK) {
+        unsigned last = ctx->batch_seq;
+        cudaMemcpy(ctx->d_progress, &last, sizeof(unsigned), cudaMemcpyHostToDevice);
+    }
+    ctx->copy_plan.clear();
+    cudaEventRecord(ctx->ev_copy, ctx->cst);
+    if (!ctx->write_value) cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0);
+    return rc;
+}
+
+// Stage P (ascending) into the slot pool (Alg. 2 l.4): evict non-members (the
+// device table drops them at once, so concurrent gap passes read them from
+// host memory), then plan one host -> HBM copy per new column in the order
+// pass 0 of round `round` visits it (issue_staging enqueues them after the SCD
+// launch; the kernel waits on the copy-progress counter per block, so staging
+// overlaps the epoch).  New columns enter the device table after the epoch
+// (finalize_staging).
+static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& P, int64_t round,
+                                     int64_t* swaps) {
+    TRY(finalize_staging(ctx));
     const int64_t m = (int64_t)P.size();
     std::vector<char> in_new(ctx->n, 0);
     for (int64_t j : P) in_new[j] = 1;
@@ -242,55 +336,47 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
                 free_slots.push_back((int)s);
             }
         }
+        // new columns in pass-0 visiting order
+        int h = 1;
+        while ((1ll << (2 * h)) < m) ++h;
+        const uint64_t key = mix64(mix64(mix64(ctx->cfg.seed) ^ (uint64_t)round) ^ 0ull);
+        std::vector<int64_t> news;
+        news.reserve(m);
+        for (int64_t t = 0; t < m; ++t) {
+            const int64_t j = P[feistel_host(key, h, m, t)];
+            if (ctx->col_slot[j] < 0) news.push_back(j);
+        }
+        if ((int64_t)news.size() > (int64_t)free_slots.size())
+            return fail(ctx, DUHL_E_INVALID, "working set exceeds the HBM slot pool");
+        // plan the copies now (slot, sequence number); issue_staging enqueues them
+        size_t fi = 0;
+        for (int64_t j : news) {
+            const int s = free_slots[fi++];
+            ctx->col_slot[j] = s;
+            ctx->slot_col[s] = (int)j;
+            ctx->pend_cols.push_back(j);
+            ctx->pend_slots.push_back(s);
+            ctx->slot_batch[s] = ctx->write_value ? ++ctx->batch_seq : 0u;
+            ctx->copy_plan.push_back({j, s, ctx->slot_batch[s]});
+            ++nsw;
+        }
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
-        ProfScope ps(ctx, ctx->cst, 3, 0.0);
-        size_t fi = 0;
-        int64_t run_col = -1, run_slot = -1, run_len = 0;
-        auto flush = [&]() -> duhl_status {
-            if (run_len > 0) {
-                size_t bytes = (size_t)run_len * ctx->ld_dev * sizeof(float);
-                CK(cudaMemcpy2DAsync(ctx->pool + run_slot * ctx->ld_dev, ctx->ld_dev * sizeof(float),
-                                     ctx->h_store + run_col * ctx->ld_host, ctx->ld_host * sizeof(float),
-                                     ctx->ld_dev * sizeof(float), (size_t)run_len,
-                                     cudaMemcpyHostToDevice, ctx->cst));
-                ctx->h2d_bytes += (int64_t)bytes;
-                ps.bytes += (double)bytes;
-            }
-            run_len = 0;
-            return DUHL_OK;
-        };
-        for (int64_t j : P) {
-            if (ctx->col_slot[j] >= 0) continue;
-            if (fi >= free_slots.size()) return fail(ctx, DUHL_E_INVALID, "working set exceeds the HBM slot pool");
-            int s = free_slots[fi++];
-            ctx->col_slot[j] = s;
-            ctx->slot_col[s] = (int)j;
-            chg_cols.push_back(j);
-            chg_slots.push_back(s);
-            ++nsw;
-            if (run_len > 0 && j == run_col + run_len && s == run_slot + run_len) {
-                ++run_len;
-            } else {
-                TRY(flush());
-                run_col = j;
-                run_slot = s;
-                run_len = 1;
-            }
-        }
-        TRY(flush());
-        ps.end();
-        CK(cudaEventRecord(ctx->ev_copy, ctx->cst));
-        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0));
+        if (!ctx->write_value) TRY(issue_staging(ctx));  // no overlap: copies first, compute waits
     } else {
         for (int64_t j : P) if (!ctx->inP[j]) ++nsw;  // logical swaps (everything is resident)
     }
     TRY(upload_slots_changes(ctx, chg_cols, chg_slots));
     std::vector<int> Ps(m);
-    for (int64_t q = 0; q < m; ++q) Ps[q] = ctx->col_slot[P[q]];
+    std::vector<unsigned> Pb(m);
+    for (int64_t q = 0; q < m; ++q) {
+        Ps[q] = ctx->col_slot[P[q]];
+        Pb[q] = ctx->slot_batch.empty() ? 0u : ctx->slot_batch[Ps[q]];
+    }
     CK(cudaMemcpyAsync(ctx->d_P, P.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaMemcpyAsync(ctx->d_P_slot, Ps.data(), m * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaMemcpyAsync(ctx->d_P_batch, Pb.data(), m * sizeof(unsigned), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     ctx->P = P;
     std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
@@ -302,10 +388,12 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
 static void free_all(duhl_ctx* ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->cst) cudaStreamSynchronize(ctx->cst);
+    if (ctx->rst) cudaStreamSynchronize(ctx->rst);
     void* dev_ptrs[] = {ctx->pool, ctx->d_col_slot, ctx->d_alpha, ctx->d_vt, ctx->d_b, ctx->d_y,
                         ctx->d_norms, ctx->d_z, ctx->d_P, ctx->d_order_j, ctx->d_cols,
                         ctx->d_chg_cols, ctx->d_P_slot, ctx->d_order_slot, ctx->d_chg_slots,
-                        ctx->d_vsnap,
+                        ctx->d_vsnap, ctx->d_s_acc2, ctx->d_progress, ctx->d_P_batch,
+                        ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar};
     for (void* p : dev_ptrs)
@@ -315,6 +403,9 @@ static void free_all(duhl_ctx* ctx) {
     for (auto& t : ctx->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+    if (ctx->ev_snap) cudaEventDestroy(ctx->ev_snap);
+    if (ctx->ev_ref) cudaEventDestroy(ctx->ev_ref);
+    if (ctx->rst) cudaStreamDestroy(ctx->rst);
     if (ctx->st) cudaStreamDestroy(ctx->st);
     if (ctx->cst) cudaStreamDestroy(ctx->cst);
 }
@@ -389,7 +480,10 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ctx->nsm = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) != cudaSuccess)
+        cudaStreamCreateWithFlags(&ctx->rst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_ref, cudaEventDisableTiming) != cudaSuccess)
         return bail(DUHL_E_CUDA);
     // ---- unit A: pinned host store (column i at h_store + i*ld_host, rows d..d4 zero)
     const bool can_borrow = ctx->cfg.borrow_host && d % 4 == 0 && A->ld % 4 == 0 &&
@@ -473,6 +567,13 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
               dmal((void**)&ctx->d_order_slot, n * sizeof(int)) &&
               dmal((void**)&ctx->d_chg_slots, 2 * n * sizeof(int)) &&
               dmal((void**)&ctx->d_vsnap, d4 * sizeof(double)) &&
+              dmal((void**)&ctx->d_s_acc2, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_progress, 64) &&
+              dmal((void**)&ctx->d_P_batch, n * sizeof(unsigned)) &&
+              dmal((void**)&ctx->d_order_batch, n * sizeof(unsigned)) &&
+              dmal((void**)&ctx->d_order_a, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_order_inv, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_order_y, n * sizeof(double)) &&
               dmal((void**)&ctx->d_s_acc, n * sizeof(double)) &&
               dmal((void**)&ctx->d_gap_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_s_out, n * sizeof(double)) &&
@@ -485,11 +586,25 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
         return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
     ctx->slot_col.assign(ctx->S, -1);
+    ctx->slot_batch.assign(ctx->S, 0u);
+    {   // stream memory ops (copy-progress counter) if the driver offers them
+        int memops = 0;
+        cudaDeviceGetAttribute(&memops, (cudaDeviceAttr)120 /* CAN_USE_STREAM_MEM_OPS_V1 */, ctx->dev);
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && fn && !std::getenv("DUHL_NO_STAGING_OVERLAP"))
+            ctx->write_value = (duhl_ctx::WriteValue32)fn;
+        (void)memops;
+        cudaGetLastError();
+    }
     ctx->inP.assign(n, 0);
     cudaStream_t st = ctx->st;
     bool ok2 = true;
     auto ck = [&](cudaError_t e) { if (e != cudaSuccess) ok2 = false; };
     ck(cudaMemsetAsync(ctx->d_s_acc, 0, n * sizeof(double), st));
+    ck(cudaMemsetAsync(ctx->d_s_acc2, 0, n * sizeof(double), st));
+    ck(cudaMemsetAsync(ctx->d_progress, 0, 64, st));
     ck(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
     ck(cudaMemsetAsync(ctx->d_alpha, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_b, 0, d4 * sizeof(double), st));
@@ -576,7 +691,7 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
     } else {
         return fail(ctx, DUHL_E_INVALID, "unknown policy");
     }
-    return stage_working_set(ctx, P, n_swaps_out);
+    return stage_working_set(ctx, P, round, n_swaps_out);
 }
 
 duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t round, int64_t* P_out,
@@ -610,6 +725,11 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.NB = ctx->NB;
     p.exact = ctx->cfg.scd_exact;
     p.red = ctx->d_red;
+    p.order_batch = ctx->write_value ? ctx->d_order_batch : nullptr;
+    p.order_a = ctx->d_order_a;
+    p.order_inv = ctx->d_order_inv;
+    p.order_y = ctx->d_order_y;
+    p.progress = ctx->write_value ? ctx->d_progress : nullptr;
     p.bar = ctx->d_bar;
     CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_doubles(ctx->W) * sizeof(double), ctx->st));
     CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
@@ -631,7 +751,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         cudaFree(dtr);
         const double nb = (double)((L + ctx->W - 1) / ctx->W);
         std::fprintf(stderr, "scd trace (us/block) W=%d G=%d R=%d: ", ctx->W, ctx->G, ctx->R);
-        const char* nm[8] = {"waitdata", "flush", "WAIT", "sGread", "seq", "vupdate", "tiles", "coords"};
+        const char* nm[8] = {"ctl:issue+coords", "flush", "w0:waitdata", "w0:tiles", "ctl:wait+sG+seq",
+                             "vupdate", "join", "-"};
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
             for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / 1e3);
@@ -642,12 +763,19 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     return DUHL_OK;
 }
 
-static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
+static duhl_status refresh_launch(duhl_ctx* ctx, int64_t kref);
+static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round, int64_t kref = 0) {
     const int64_t m = (int64_t)ctx->P.size();
     for (int pass = 0; pass < passes; ++pass) {
-        CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, m, seed, round, pass, ctx->d_order_j,
-                             ctx->d_order_slot, ctx->st, &ctx->launches));
+        CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
+                             ctx->d_order_j, ctx->d_order_slot, ctx->d_order_batch, ctx->d_order_a,
+                             ctx->d_order_inv, ctx->d_order_y, ctx->d_alpha, ctx->d_norms,
+                             ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr, ctx->st, &ctx->launches));
         TRY(scd_launch(ctx, m));
+        if (pass == 0) {
+            TRY(refresh_launch(ctx, kref));  // unit A beside unit B (after the cooperative launch)
+            TRY(issue_staging(ctx));         // host enqueue of the staging copies overlaps pass 0
+        }
     }
     return DUHL_OK;
 }
@@ -661,21 +789,32 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
         if (perm_len < 0 || perm_len > (int64_t)ctx->P.size()) return fail(ctx, DUHL_E_INVALID, "perm_len");
         std::vector<char> seen(ctx->n, 0);
         std::vector<int> slots(perm_len);
+        std::vector<unsigned> batches(perm_len);
         for (int64_t t = 0; t < perm_len; ++t) {
             int64_t j = perm[t];
             if (j < 0 || j >= ctx->n || !ctx->inP[j] || seen[j] || ctx->col_slot[j] < 0)
                 return fail(ctx, DUHL_E_INVALID, "perm entries must be distinct resident members of P");
             seen[j] = 1;
             slots[t] = ctx->col_slot[j];
+            batches[t] = ctx->slot_batch[slots[t]];
         }
         CK(cudaMemcpyAsync(ctx->d_order_j, perm, perm_len * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_order_slot, slots.data(), perm_len * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->d_order_batch, batches.data(), perm_len * sizeof(unsigned),
+                           cudaMemcpyHostToDevice, ctx->st));
+        CK(launch_perm_order(nullptr, nullptr, nullptr, perm_len, 0, 0, 0, ctx->d_order_j, ctx->d_order_slot,
+                             ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
+                             ctx->d_alpha, ctx->d_norms, ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr,
+                             ctx->st, &ctx->launches));
         TRY(scd_launch(ctx, perm_len));
+        TRY(issue_staging(ctx));
+        TRY(finalize_staging(ctx));
         CK(cudaStreamSynchronize(ctx->st));
         return DUHL_OK;
     }
     if (passes < 1) return fail(ctx, DUHL_E_INVALID, "passes < 1");
     TRY(scd_passes(ctx, passes, seed, round));
+    TRY(finalize_staging(ctx));
     CK(cudaStreamSynchronize(ctx->st));
     return DUHL_OK;
 }
@@ -718,6 +857,18 @@ duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double*
     return certificate(ctx, gap, primal, dual);
 }
 
+// Unit-A refresh of the cursor chunk (columns in d_cols) against the v snapshot:
+// 1024-row tiles (8 KB of shared memory) so a CTA fits beside the SCD kernel's
+// CTA on every SM; PCIe-bound for non-resident columns.
+static duhl_status refresh_launch(duhl_ctx* ctx, int64_t kref) {
+    if (kref <= 0) return DUHL_OK;
+    CK(cudaStreamWaitEvent(ctx->rst, ctx->ev_snap, 0));
+    TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr, true, ctx->d_vsnap, ctx->rst,
+                 ctx->d_s_acc2, 1024));
+    CK(cudaEventRecord(ctx->ev_ref, ctx->rst));
+    return DUHL_OK;
+}
+
 static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy policy, int certify,
                               duhl_round_record* rec) {
     auto t0 = std::chrono::steady_clock::now();
@@ -725,15 +876,25 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     int64_t kref = (int64_t)std::ceil(ctx->cfg.refresh_fraction * (double)n - 1e-9);
     kref = std::max<int64_t>(0, std::min(n, kref));
     int64_t swaps = 0;
+    static const bool htrace = std::getenv("DUHL_ROUND_TRACE") != nullptr;  // developer timing
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto tsel = now();
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
-    if (kref > 0) {                                                        // l.7-10 at alpha^(t)
-        std::vector<int64_t> idx(kref);
+    auto tstaged = now();
+    std::vector<int64_t> idx(kref);
+    if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) from a snapshot of v, launched on its
+                     // own stream right after the SCD kernel (refresh_launch)
         for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
         ctx->cursor = (ctx->cursor + kref) % n;
         CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
-        TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr));
+        CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaEventRecord(ctx->ev_snap, ctx->st));
     }
-    TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                         // l.6, l.11
+    auto tlaunch = now();
+    TRY(scd_passes(ctx, passes, ctx->cfg.seed, t, kref));                   // l.6, l.11
+    TRY(finalize_staging(ctx));                                            // staged columns -> table
+    auto tscd = now();
+    if (kref > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));         // join unit A
     const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
     TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
     double cg = -1.0;
@@ -745,6 +906,13 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     CK(cudaStreamSynchronize(ctx->st));
     TRY(check_flag(ctx, "duhl_round"));
     harvest(ctx);
+    if (htrace) {
+        auto tend = now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "round %lld: select+stage %.2f ms, refresh-launch %.2f, scd+finalize(host) %.2f, "
+                     "tail %.2f, total %.2f\n", (long long)t, ms(tsel, tstaged), ms(tstaged, tlaunch),
+                     ms(tlaunch, tscd), ms(tscd, tend), ms(tsel, tend));
+    }
     if (rec) {
         rec->round = t;
         rec->swaps = swaps;
@@ -842,10 +1010,11 @@ duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {
 
 duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
                                   double* bytes) {
-    if (!ctx || kind < 0 || kind > 3) return DUHL_E_INVALID;
+    if (!ctx || kind < 0 || kind > 4) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
     CK(cudaStreamSynchronize(ctx->st));
     CK(cudaStreamSynchronize(ctx->cst));
+    CK(cudaStreamSynchronize(ctx->rst));
     harvest(ctx);
     if (launches) *launches = ctx->st_launch[kind];
     if (ms) *ms = ctx->st_ms[kind];

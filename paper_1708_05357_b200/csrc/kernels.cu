@@ -313,24 +313,59 @@ __device__ __forceinline__ int64_t feistel_index(uint64_t key, int h, int64_t m,
     return (int64_t)x;
 }
 
-__global__ void k_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t key, int h,
-                             int64_t* order_j, int* order_slot) {
+// Per-position inputs of a pass, gathered once before the launch: the
+// coordinate, its HBM slot and staging sequence number, alpha at the start of
+// the pass (each coordinate is visited once per pass, so this is also its value
+// at the visit), 1/||a_j||^2 (-1 marks a zero column) and y_j.
+struct OrderOut {
+    int64_t* j;
+    int* slot;
+    unsigned* batch;
+    double *a, *inv, *y;
+};
+__device__ __forceinline__ void order_info(const OrderOut& o, int64_t t, int64_t j, const double* alpha,
+                                           const double* norms, const double* y) {
+    const double nrm = norms[j];
+    o.a[t] = alpha[j];
+    o.inv[t] = nrm > 0.0 ? 1.0 / nrm : -1.0;
+    o.y[t] = y ? y[j] : 0.0;
+}
+
+__global__ void k_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
+                             uint64_t key, int h, OrderOut o, const double* alpha, const double* norms,
+                             const double* y) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < m) {
         int64_t q = feistel_index(key, h, m, t);
-        order_j[t] = P[q];
-        order_slot[t] = P_slot[q];
+        const int64_t j = P[q];
+        o.j[t] = j;
+        o.slot[t] = P_slot[q];
+        o.batch[t] = P_batch[q];
+        order_info(o, t, j, alpha, norms, y);
     }
 }
 
-cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t seed,
-                              int64_t round, int64_t pass, int64_t* order_j, int* order_slot,
+__global__ void k_order_info(int64_t L, OrderOut o, const double* alpha, const double* norms, const double* y) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < L) order_info(o, t, o.j[t], alpha, norms, y);
+}
+
+cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
+                              uint64_t seed, int64_t round, int64_t pass, int64_t* order_j,
+                              int* order_slot, unsigned* order_batch, double* order_a, double* order_inv,
+                              double* order_y, const double* alpha, const double* norms, const double* y,
                               cudaStream_t st, int64_t* launches) {
     if (m <= 0) return cudaSuccess;
-    int h = 1;
-    while ((1ll << (2 * h)) < m) ++h;
-    uint64_t key = mix64(mix64(mix64(seed) ^ (uint64_t)round) ^ (uint64_t)pass);
-    k_perm_order<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(P, P_slot, m, key, h, order_j, order_slot);
+    OrderOut o{order_j, order_slot, order_batch, order_a, order_inv, order_y};
+    if (P == nullptr) {  // explicit order already in order_j / slot / batch: gather the rest
+        k_order_info<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(m, o, alpha, norms, y);
+    } else {
+        int h = 1;
+        while ((1ll << (2 * h)) < m) ++h;
+        uint64_t key = mix64(mix64(mix64(seed) ^ (uint64_t)round) ^ (uint64_t)pass);
+        k_perm_order<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(P, P_slot, P_batch, m, key, h, o, alpha,
+                                                              norms, y);
+    }
     ++*launches;
     return cudaGetLastError();
 }
@@ -346,7 +381,10 @@ constexpr int kScdThreads = 256;
 constexpr int kScdWarps = kScdThreads / 32;
 constexpr int kScdStages = 3;
 constexpr int kRedBufs = 6;     // rotating reduction buffers (see the zeroing rule below)
-constexpr int kRedGroups = 8;   // CTA c adds into group c % 8 ...
+#ifndef DUHL_RED_GROUPS
+#define DUHL_RED_GROUPS 8
+#endif
+constexpr int kRedGroups = DUHL_RED_GROUPS;  // CTA c adds into group c % kRedGroups ...
 constexpr int kRedStride = 32;  // ... one 256-byte line per (entry, group): spreads the fp64
                                 // atomics of 148 CTAs over many L2 slices
 
@@ -364,7 +402,7 @@ size_t scd_smem_bytes(int W, int R, int NB) {
     size_t off = 128;                                                             // mbarriers
     off += align_up_dev((size_t)kScdStages * W * R * sizeof(float));              // A stages
     off += align_up_dev((size_t)R * sizeof(double));                              // v slice
-    off += align_up_dev((size_t)scd_nred(W) * sizeof(double));                    // CTA partials
+    off += align_up_dev((size_t)2 * scd_nred(W) * sizeof(double));                // CTA partials (2 halves)
     off += align_up_dev((size_t)scd_nred(W) * sizeof(double));                    // reduced block
     off += align_up_dev((size_t)2 * 16 * sizeof(double));                         // deltas (2 blocks)
     return off;
@@ -489,6 +527,10 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
     float* dst = Abuf + (size_t)st * W * p.R;
     const unsigned bytes = (unsigned)rows * 4u;
     const int slot = lane < Wb ? p.order_slot[base + lane] : 0;
+    if (p.progress && lane < Wb) {  // column still being staged host -> HBM: wait for its copy
+        const unsigned need = p.order_batch[base + lane];
+        while (ld_acquire_u32(p.progress) < need) { __nanosleep(128); }
+    }
     fence_proxy_async();  // earlier generic reads of this stage before the async-proxy refill
     if (lane == 0) mbar_arrive_expect_tx(&mbar[st], bytes * (unsigned)Wb);
     __syncwarp();
@@ -529,7 +571,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     double* vs = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)R * sizeof(double));
     double* acc = reinterpret_cast<double*>(smem + off);
-    off += align_up_dev((size_t)NRED * sizeof(double));
+    off += align_up_dev((size_t)2 * NRED * sizeof(double));
     double* sG = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)NRED * sizeof(double));
     double* delta = reinterpret_cast<double*>(smem + off);  // [2][16]
@@ -546,7 +588,6 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
 
     for (int q = tid; q < kScdStages * W * R; q += kScdThreads) Abuf[q] = 0.0f;
     for (int r = tid; r < R; r += kScdThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
-    for (int q = tid; q < NRED; q += kScdThreads) acc[q] = 0.0;
     if (tid == 0) {
         for (int q = 0; q < kScdStages; ++q) mbar_init(&mbar[q], 1);
         fence_mbar_init();
@@ -555,7 +596,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     __syncthreads();
 
     // developer trace (ScdParams::trace): per-phase globaltimer stamps of CTA 0 / CTA G-1
-    const bool tr = p.trace && tid == 0 && (c == 0 || c == p.G - 1);
+    const bool tr = p.trace && tid == kScdThreads - 32 && (c == 0 || c == p.G - 1);
     unsigned long long* trc = tr ? p.trace + (c == 0 ? 0 : 8) : nullptr;
     unsigned long long tprev = tr ? gtimer() : 0;
     auto stamp = [&](int k) {
@@ -570,109 +611,121 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     auto wait_data = [&](int64_t blk) {
         mbar_wait(&mbar[blk % kScdStages], (unsigned)((blk / kScdStages) & 1));
     };
-    // block inputs, read before this CTA arrives at the block's barrier (CTA 0
-    // rewrites alpha right after it)
-    auto load_coords = [&](int64_t blk) {
-        if (warp == 0) {
-            const int64_t bs = blk * W;
-            const int wb = (int)imin64(W, p.L - bs);
-            const int sl = (int)(blk & 1);
-            if (lane < wb) {
-                const int64_t jg = p.order_j[bs + lane];
-                const double nrm = p.norms[jg];
-                cj[sl][lane] = jg;
-                ca[sl][lane] = p.alpha[jg];
-                cinv[sl][lane] = nrm > 0.0 ? 1.0 / nrm : -1.0;  // -1 marks a zero column
-                cy[sl][lane] = p.model == kSvm ? p.y[jg] : 0.0;
-            }
+    // block inputs (control warp): prefetched into registers one iteration ahead
+    // from the gathered per-position arrays, published to shared slot blk & 1
+    int64_t pf_j = 0;
+    double pf_a = 0, pf_inv = 0, pf_y = 0;
+    auto prefetch_coords = [&](int64_t blk) {
+        const int64_t t = blk * W + lane;
+        if (lane < W && t < p.L) {
+            pf_j = p.order_j[t];
+            pf_a = p.order_a[t];
+            pf_inv = p.order_inv[t];
+            pf_y = p.order_y[t];
         }
     };
-    // phase A for block blk (with_c: the cross Gram against block blk-1).
-    // Work items = register tiles over ALL of the CTA's rows (one warp-reduction
-    // per tile): G rows-groups (4 x 8 / 4 x 4, lower block triangle), C tiles
-    // (4 x 8 / 4 x 4) and u tiles (4 x 1, fp64), listed by decreasing cost and
-    // dealt to warps in snake order.
-    auto partials = [&](int64_t blk, bool with_c) {
-        const float* A1 = stage(blk);
-        const float* A0 = with_c ? stage(blk - 1) : nullptr;
-        // item codes: kind (0 G, 1 C, 2 u), jt, k0, kw
+    auto publish_coords = [&](int64_t blk) {
+        const int sl = (int)(blk & 1);
+        if (lane < W) {
+            cj[sl][lane] = pf_j;
+            ca[sl][lane] = pf_a;
+            cinv[sl][lane] = pf_inv;
+            cy[sl][lane] = pf_y;
+        }
+    };
+    // Warp roles.  Compute warps 0..kCompute-1 build block blk's partials
+    // (tiles over ALL of the CTA's rows, one warp reduction per tile; big tiles
+    // are split into two row halves so the SMSPs stay balanced), dealt in snake
+    // order by decreasing cost.  The control warp (last) streams stages, loads
+    // block inputs, waits on the grid barrier, reads the reduced block and runs
+    // the W sequential closed-form steps -- concurrently with the tiles.
+    constexpr int kCompute = kScdWarps - 1;
+    const bool ctrl = warp == kScdWarps - 1;
+    // per-warp item lists, built once: item = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15
+    __shared__ int witems[kScdWarps][24];
+    __shared__ int wcount[kScdWarps];
+    if (tid == 0) {
+        for (int w = 0; w < kScdWarps; ++w) wcount[w] = 0;
         int item = 0;
-        for (int cost = 2; cost >= 0; --cost) {        // 2: kw 8 tiles, 1: kw 4 tiles, 0: u tiles
+        for (int cost = 2; cost >= 0; --cost)          // 2: kw 8 tiles, 1: kw 4 tiles, 0: u tiles
             for (int kind = 0; kind < 3; ++kind) {
                 if ((kind == 2) != (cost == 0)) continue;
-                if (kind == 1 && !with_c) continue;
                 for (int jt = 0; jt < T; ++jt) {
                     const int kend = kind == 0 ? 4 * jt + 4 : (kind == 1 ? W : 1);
                     for (int k0 = 0; k0 < kend; k0 += 8) {
                         const int kw = kind == 2 ? 1 : (kend - k0 >= 8 ? 8 : 4);
                         if ((kw == 8) != (cost == 2) && kind != 2) continue;
-                        const int round_ = item / kScdWarps, pos = item % kScdWarps;
-                        const int owner = (round_ & 1) ? kScdWarps - 1 - pos : pos;
-                        ++item;
-                        if (owner != warp) continue;
-                        const float* Aj = A1 + (size_t)(4 * jt) * R;
-                        if (kind == 0) {
-                            if (kw == 8) tile4<EXACT, 8, true>(Aj, A1 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
-                            else tile4<EXACT, 4, true>(Aj, A1 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
-                        } else if (kind == 1) {
-                            if (kw == 8) tile4<EXACT, 8, false>(Aj, A0 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
-                            else tile4<EXACT, 4, false>(Aj, A0 + (size_t)k0 * R, R, 0, rows, lane, 4 * jt, k0, acc, W);
-                        } else {
-                            utile(Aj, vs, R, 0, rows, lane, 4 * jt, acc);
+                        const int nparts = kw == 8 ? 2 : 1;  // split the big tiles by rows
+                        for (int part = 0; part < nparts; ++part) {
+                            const int rnd = item / kCompute, pos = item % kCompute;
+                            const int owner = (rnd & 1) ? kCompute - 1 - pos : pos;
+                            ++item;
+                            if (wcount[owner] < 24)
+                                witems[owner][wcount[owner]++] = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15;
                         }
                     }
                 }
             }
+    }
+    __syncthreads();
+    const int half = ((rows >> 2) + 1) / 2 * 4;  // row split point (multiple of 4)
+    auto tiles = [&](int64_t blk, bool with_c) {
+        const float* A1 = stage(blk);
+        const float* A0 = with_c ? stage(blk - 1) : nullptr;
+        const int cnt = wcount[warp];
+        for (int it = 0; it < cnt; ++it) {
+            const int code = witems[warp][it];
+            const int kind = code & 3, jt = (code >> 2) & 15, k0 = (code >> 6) & 31, kw = (code >> 11) & 15,
+                      part = (code >> 15) & 1;
+            if (kind == 1 && !with_c) continue;
+            const int lo = kw == 8 ? (part == 0 ? 0 : half) : 0;
+            const int hi = kw == 8 ? (part == 0 ? half : rows) : rows;
+            double* out = acc + (size_t)part * NRED;
+            const float* Aj = A1 + (size_t)(4 * jt) * R;
+            if (kind == 0) {
+                if (kw == 8) tile4<EXACT, 8, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                else tile4<EXACT, 4, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+            } else if (kind == 1) {
+                if (kw == 8) tile4<EXACT, 8, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                else tile4<EXACT, 4, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+            } else {
+                utile(Aj, vs, R, lo, hi, lane, 4 * jt, out);
+            }
         }
-        stamp(6);
-        load_coords(blk);
-        __syncthreads();
-        stamp(7);
+    };
+    // acc[0] + acc[1] (second row halves of the kw 8 tiles; acc[1] zero elsewhere) -> red
+    auto flush = [&](int64_t blk, bool with_c) {
         double* red_b = p.red + (size_t)(blk % kRedBufs) * bufsz;
         const int nq = with_c ? NRED : scd_off_C(W);
         for (int q = tid; q < nq; q += kScdThreads)
-            atomicAdd(&red_b[((size_t)q * kRedGroups + grp) * kRedStride], acc[q]);
-        __syncthreads();
-        if (tid == 0) {  // ARRIVE(blk) on the counter of blk's parity (see WAIT)
+            atomicAdd(&red_b[((size_t)q * kRedGroups + grp) * kRedStride], acc[q] + acc[NRED + q]);
+    };
+    auto arrive = [&](int64_t blk) {  // by the control warp, after a CTA barrier behind the REDs
+        if (ctrl && lane == 0) {
             __threadfence();
             atomicAdd(&p.bar[blk & 1], 1u);
         }
     };
-
-    if (nblk > 0) {
-        if (warp == 0)
-            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) scd_issue(p, Abuf, mbar, q, r0, rows, lane);
-        wait_data(0);
-        partials(0, false);
-    }
-    for (int64_t b = 0; b < nblk; ++b) {
+    // WAIT(b) + reduced block b -> the W sequential closed-form steps (control warp)
+    auto control = [&](int64_t b) {
         const int64_t base = b * W;
         const int Wb = (int)imin64(W, p.L - base);
-        // ---- A: block b+1's partials hide block b's barrier latency
-        if (b + 1 < nblk) {
-            wait_data(b + 1);
-            stamp(0);
-            partials(b + 1, true);
-        }
-        stamp(1);
-        // ---- B: WAIT(b), reduced block b -> sequential closed-form steps
-        // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
-        // before WAIT(b) completed everywhere: one counter per block parity then
-        // counts exactly the arrivals of blocks b, b-2, b-4, ...
-        if (tid == 0) {
+        if (lane == 0) {
+            // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
+            // before WAIT(b) completed everywhere: one counter per block parity counts
+            // exactly the arrivals of blocks b, b-2, b-4, ...
             const unsigned target = (unsigned)((b / 2 + 1) * (int64_t)p.G);
             while (ld_acquire_u32(&p.bar[b & 1]) < target) { __nanosleep(32); }
             __threadfence();
         }
-        __syncthreads();
-        stamp(2);
+        __syncwarp();
         if (c == 0)
-            for (int q = tid; q < NRED * kRedGroups; q += kScdThreads)
+            for (int q = lane; q < NRED * kRedGroups; q += 32)
                 p.red[(size_t)((b + 4) % kRedBufs) * bufsz + (size_t)q * kRedStride] = 0.0;
         {
             const double* red_b = p.red + (size_t)(b % kRedBufs) * bufsz;
             const int nq = b > 0 ? NRED : scd_off_C(W);
-            for (int q = tid; q < nq; q += kScdThreads) {
+            for (int q = lane; q < nq; q += 32) {
                 double v = 0.0;
 #pragma unroll
                 for (int g = 0; g < kRedGroups; ++g)
@@ -680,60 +733,100 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                 sG[q] = v;
             }
         }
-        __syncthreads();
-        stamp(3);
-        if (warp == 0) {
-            const int sl = (int)(b & 1);
-            const double* dprev = delta + (size_t)(sl ^ 1) * 16;
-            int64_t jg = 0;
-            double a = 0, inv = 0, yy = 0, sj = 0, afin = 0;
-            bool zero = false;
-            if (lane < Wb) {
-                jg = cj[sl][lane];
-                a = ca[sl][lane];
-                inv = cinv[sl][lane];
-                zero = inv < 0.0;
-                if (zero) inv = 0.0;
-                yy = cy[sl][lane];
-                sj = sG[lane];
-                if (b > 0)  // u was taken at the start of block b-1: add its effect
-                    for (int k = 0; k < W; ++k) sj = fma(sG[scd_off_C(W) + lane * W + k], dprev[k], sj);
-            }
-            double* dcur = delta + (size_t)sl * 16;
+        __syncwarp();
+        const int sl = (int)(b & 1);
+        const double* dprev = delta + (size_t)(sl ^ 1) * 16;
+        int64_t jg = 0;
+        double a = 0, inv = 0, yy = 0, sj = 0, afin = 0;
+        bool zero = false;
+        if (lane < Wb) {
+            jg = cj[sl][lane];
+            a = ca[sl][lane];
+            inv = cinv[sl][lane];
+            zero = inv < 0.0;
+            if (zero) inv = 0.0;
+            yy = cy[sl][lane];
+            sj = sG[lane];
+            if (b > 0)  // u was taken at the start of block b-1: add its effect
+                for (int k = 0; k < W; ++k) sj = fma(sG[scd_off_C(W) + lane * W + k], dprev[k], sj);
+        }
+        double* dcur = delta + (size_t)sl * 16;
+        for (int j = 0; j < Wb; ++j) {
+            const double an = coord_step_inv(p.model, a, sj, inv, zero, yy, lam_dn);
+            if (lane == j) afin = an;
+            const double dl = __shfl_sync(~0u, an - a, j);
+            if (lane > j && lane < Wb) sj = fma(sG[scd_off_G(W) + lane * (lane - 1) / 2 + j], dl, sj);
+            if (lane == 0) dcur[j] = dl;
+        }
+        if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
+        if (lane < Wb && c == 0) p.alpha[jg] = afin;
+    };
+    auto vupdate = [&](int64_t b, int t0, int nthreads) {  // v slice += A_b delta_b
+        const int64_t base = b * W;
+        const int Wb = (int)imin64(W, p.L - base);
+        const float* A = stage(b);
+        const double* dcur = delta + (size_t)(b & 1) * 16;
+        double2* v2 = reinterpret_cast<double2*>(vs);
+        for (int r4 = t0; r4 < (rows >> 2); r4 += nthreads) {
+            double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
             for (int j = 0; j < Wb; ++j) {
-                const double an = coord_step_inv(p.model, a, sj, inv, zero, yy, lam_dn);
-                if (lane == j) afin = an;
-                const double dl = __shfl_sync(~0u, an - a, j);
-                if (lane > j && lane < Wb) sj = fma(sG[scd_off_G(W) + lane * (lane - 1) / 2 + j], dl, sj);
-                if (lane == 0) dcur[j] = dl;
+                const float4 x = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
+                const double dj = dcur[j];
+                v01.x = fma(dj, (double)x.x, v01.x);
+                v01.y = fma(dj, (double)x.y, v01.y);
+                v23.x = fma(dj, (double)x.z, v23.x);
+                v23.y = fma(dj, (double)x.w, v23.y);
             }
-            if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
-            if (lane < Wb && c == 0) p.alpha[jg] = afin;
+            v2[2 * r4] = v01;
+            v2[2 * r4 + 1] = v23;
+        }
+    };
+
+    for (int q = tid; q < 2 * NRED; q += kScdThreads) acc[q] = 0.0;
+    if (nblk > 0) {
+        if (ctrl) {
+            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) scd_issue(p, Abuf, mbar, q, r0, rows, lane);
+            prefetch_coords(0);
+            publish_coords(0);
+            prefetch_coords(1);
+        } else {
+            wait_data(0);
+            tiles(0, false);
         }
         __syncthreads();
-        stamp(4);
-        // ---- C: v slice update, sequential order of j; stage b -> block b+3
-        {
-            const float* A = stage(b);
-            const double* dcur = delta + (size_t)(b & 1) * 16;
-            double2* v2 = reinterpret_cast<double2*>(vs);
-            for (int r4 = tid; r4 < (rows >> 2); r4 += kScdThreads) {
-                double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-                for (int j = 0; j < Wb; ++j) {
-                    const float4 x = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
-                    const double dj = dcur[j];
-                    v01.x = fma(dj, (double)x.x, v01.x);
-                    v01.y = fma(dj, (double)x.y, v01.y);
-                    v23.x = fma(dj, (double)x.z, v23.x);
-                    v23.y = fma(dj, (double)x.w, v23.y);
-                }
-                v2[2 * r4] = v01;
-                v2[2 * r4 + 1] = v23;
+        flush(0, false);
+        __syncthreads();
+        arrive(0);
+    }
+    for (int64_t b = 0; b < nblk; ++b) {
+        const bool next = b + 1 < nblk;
+        if (ctrl) {
+            // stage of block b-1 was freed by the last V update: stream block b+2 into it
+            if (next) publish_coords(b + 1);   // block b+1's inputs (prefetched last iteration)
+            if (b + 2 < nblk) prefetch_coords(b + 2);
+            if (b >= 1 && b + 2 < nblk) scd_issue(p, Abuf, mbar, b + 2, r0, rows, lane);
+            stamp(0);
+            control(b);
+            stamp(4);
+        } else if (next) {
+            unsigned long long tw0 = (p.trace && tid == 0 && c == 0) ? gtimer() : 0;
+            wait_data(b + 1);
+            unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? gtimer() : 0;
+            tiles(b + 1, true);
+            if (p.trace && tid == 0 && c == 0) {
+                p.trace[2] += tw1 - tw0;
+                p.trace[3] += gtimer() - tw1;
             }
         }
+        __syncthreads();
+        stamp(6);
+        if (next) flush(b + 1, true);
+        __syncthreads();
+        stamp(1);
+        if (next) arrive(b + 1);
+        if (!ctrl) vupdate(b, tid, kCompute * 32);  // the control warp fences/arrives meanwhile
         __syncthreads();
         stamp(5);
-        if (warp == 0 && b + kScdStages < nblk) scd_issue(p, Abuf, mbar, b + kScdStages, r0, rows, lane);
     }
     for (int r = tid; r < rows; r += kScdThreads) p.vt[r0 + r] = vs[r];
 }

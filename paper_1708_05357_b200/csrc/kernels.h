@@ -52,6 +52,9 @@ struct ScdParams {
     double* red;               // [scd_red_doubles(W)] zero on entry
     unsigned* bar;             // [2] grid-barrier counters (per block parity), zero on entry
     unsigned long long* trace; // developer phase timer [16] or nullptr
+    const unsigned* order_batch;  // [L] staging-copy sequence number of each column (0 = resident)
+    const double *order_a, *order_inv, *order_y;  // [L] alpha at pass start, 1/||a||^2 (-1: zero column), y
+    const unsigned* progress;     // last landed staging copy, written by the copy stream; or nullptr
 };
 
 __host__ __device__ int scd_nred(int W);
@@ -64,8 +67,12 @@ cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* n
 cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,
                         int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
                         int64_t* launches);
-cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, int64_t m, uint64_t seed,
-                              int64_t round, int64_t pass, int64_t* order_j, int* order_slot,
+// Pass order + per-position inputs.  P == nullptr: order_j/slot/batch already
+// hold an explicit order of length m; only alpha / 1/norm / y are gathered.
+cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
+                              uint64_t seed, int64_t round, int64_t pass, int64_t* order_j,
+                              int* order_slot, unsigned* order_batch, double* order_a, double* order_inv,
+                              double* order_y, const double* alpha, const double* norms, const double* y,
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int64_t d,
