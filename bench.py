@@ -59,8 +59,10 @@ def dist_init(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -209,22 +211,30 @@ def run_duhl(args, cfg, rank, world, local):
     lam = lam_of(cfg)
     # CoCoA-style sharding of the columns across ranks (one block per rank)
     lo, hi = rank * n // world, (rank + 1) * n // world
-    if world > 1:
-        raise SystemExit("bench.py: multi-GPU CoCoA round not implemented in this build")
     t_gen = time.perf_counter()
     A, lab = make_data(cfg, seed, lo, hi)
     t_gen = time.perf_counter() - t_gen
     col_bytes = ((d + 3) // 4) * 16
-    budget = int(cfg["budget_frac"] * n * col_bytes) if cfg["budget_frac"] > 0 else 0
-    m = cfg["m"]
+    # strong scaling: the aggregate budget and working set stay those of the config
+    budget = int(cfg["budget_frac"] * n * col_bytes) // world if cfg["budget_frac"] > 0 else 0
+    m = cfg["m"] // world
     common = dict(hbm_budget_bytes=budget, m=m, device=local, refresh_fraction=args.refresh,
-                  seed=seed, borrow_host=True)
+                  seed=seed, borrow_host=True, n_global=n, col_offset=lo,
+                  linesearch=world > 1 or args.linesearch)
+    uid = None
+    if world > 1:  # NCCL group for the dv allreduce: id from rank 0, broadcast by torch.distributed
+        import torch.distributed as dist
+        obj = [D.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
     policy = {"gap": D.SEL_GAP, "sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM}[args.policy]
 
     # ---------------- device-timed steady-state rounds
     t_create = time.perf_counter()
     P = D.create(A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, scd_exact=args.exact,
                  **common)
+    if uid is not None:
+        P.comm_init(uid, world, rank)
     t_create = time.perf_counter() - t_create
     stream = torch.cuda.ExternalStream(P.stream())
     for t in range(args.warmup):
@@ -281,12 +291,16 @@ def run_duhl(args, cfg, rank, world, local):
         t0 = time.perf_counter()
         P2 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
                       **common)
+        if uid is not None:
+            P2.comm_init(uid, world, rank)
         t_c2 = time.perf_counter() - t0
         r = P2.solve(args.eps, args.max_rounds, passes=args.passes, policy=policy)
         wall = time.perf_counter() - t0
         c2 = P2.counters()
         g_final = r["gap"]
         P2.close()
+        wall = max_over_ranks(wall, world)
+        c2["updates"] = int(max_over_ranks(c2["updates"], world)) * world
         rounds = max(1, r["rounds"])
         e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
                "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
@@ -334,7 +348,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=30)
     ap.add_argument("--impl", default="duhl", choices=["duhl", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--passes", type=int, default=1)
@@ -346,6 +360,7 @@ def main():
     ap.add_argument("--ref-cols", type=int, default=2000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exact", action="store_true", help="fp64 Gram products in the SCD kernel")
+    ap.add_argument("--linesearch", action="store_true", help="gamma line search also at N=1")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)

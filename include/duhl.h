@@ -81,6 +81,10 @@ typedef struct {
     int profile;              /* 1: time every kernel launch with CUDA events (duhl_get_kernel_stats) */
     int scd_exact;            /* 1: fp64 Gram products -- the SCD pass equals sequential SCD to rounding;
                                  0: fp32 Gram accumulation inside a warp (fp64 beyond), ~1e-7 relative */
+    int64_t n_global;         /* multi-GPU: total columns of the problem (0 = this matrix is all of it) */
+    int64_t col_offset;       /* multi-GPU: global index of this shard's first column */
+    int linesearch;           /* 1: exact line search on the aggregation weight gamma in [0,1] after each
+                                 round's epoch; 0: gamma = 1 (Alg. 2 l.11) */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -90,12 +94,14 @@ typedef struct {
     int64_t refreshed;        /* unit-A gap refreshes this round */
     double cert_gap;          /* certified duality gap after the round; -1 if not computed */
     double z_sum;             /* sum_i z_i after the round: the (time-delayed) gap estimate of the gap memory */
+    double gamma;             /* aggregation weight applied this round (1 without line search) */
     double time_s;            /* wall seconds since duhl_solve entry (duhl_round: duration of the round) */
 } duhl_round_record;
 
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,
  * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0,
- * cert_adaptive 1, profile 0, scd_exact 1. */
+ * cert_adaptive 1, profile 0, scd_exact 1, n_global 0, col_offset 0,
+ * linesearch 0. */
 void duhl_default_config(duhl_config* cfg);
 
 /* Creates a problem instance.
@@ -170,6 +176,18 @@ duhl_status duhl_get_state(duhl_ctx* ctx, double* alpha_out, double* v_out, doub
 /* Sets alpha (host float64[n]; SVM entries must satisfy y_i alpha_i in [0,1]),
  * recomputes the shared vector exactly from A and resets z to the exact gaps. */
 duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha);
+
+/* Multi-GPU (CoCoA-style): one process per GPU, each
+ * holding a contiguous column shard (cfg.n_global, cfg.col_offset).  The
+ * shared vector v is replicated; each round every rank selects and solves on
+ * its own shard from the common v, then dv is summed with ncclAllReduce over
+ * NVLink and applied with weight gamma (cfg.linesearch).  Certificates sum the
+ * per-column terms over ranks.  duhl_comm_unique_id (one rank) returns the 128
+ * byte NCCL id that the caller broadcasts; every rank then calls
+ * duhl_comm_init on its ctx.  All later calls that reduce must be made by all
+ * ranks in the same order.  Errors: DUHL_E_NCCL (libnccl.so.2 missing / NCCL failure). */
+duhl_status duhl_comm_unique_id(void* id_out);
+duhl_status duhl_comm_init(duhl_ctx* ctx, const void* id, int nranks, int rank);
 
 /* Device-side view for callers that time kernels on their own stream:
  * returns the CUDA stream (cudaStream_t) all compute of ctx is issued on. */

@@ -75,6 +75,11 @@ def lib():
         L.or_solve_scd.restype = C.c_int
         L.or_solve_scd.argtypes = [C.c_int, _P, _I, _I, _I, _P, C.c_double, C.c_double, _I,
                                    C.c_uint64, _P, _P, _P]
+        L.or_linesearch.restype = C.c_double
+        L.or_linesearch.argtypes = [C.c_int, _P, _P, _I, _P, _P, _P, _I, C.c_double, _I]
+        L.or_duhl_solve_cocoa.restype = C.c_int
+        L.or_duhl_solve_cocoa.argtypes = [_P, C.c_int, C.c_int, _P, _I, _I, _I, _P, C.c_double, _P, _P,
+                                          _P, _P, _P, _P]
         L.or_duhl_solve.restype = C.c_int
         L.or_duhl_solve.argtypes = [_P, _P, _I, _I, _I, _P, C.c_double, _P, _P, _P, _P, _P, _P]
         _lib = L
@@ -240,3 +245,33 @@ def duhl_solve(model, A, b_or_y, lam, m, passes=1, policy=SEL_GAP, refresh_count
                              _p(z), C.byref(rounds), C.byref(gap), _p(sw), _p(tg))
     r = rounds.value
     return dict(status=st, alpha=alpha, z=z, rounds=r, gap=gap.value, swaps=sw[:r], gaps=tg[:r])
+
+
+def linesearch(model, v0, dv, a_old, da, y, lam, n):
+    """Exact line search on the aggregation weight gamma in [0, 1] (or_linesearch)."""
+    v0, dv = _f64(v0), _f64(dv)
+    a_old, da = _f64(a_old), _f64(da)
+    yy = _f64(y) if y is not None else np.zeros_like(da)
+    return lib().or_linesearch(model, _p(v0), _p(dv), v0.size, _p(a_old), _p(da), _p(yy), da.size,
+                               lam, n)
+
+
+def duhl_solve_cocoa(model, A, b_or_y, lam, m, K, linesearch=True, passes=1, policy=SEL_GAP,
+                     refresh_count=0, eps=1e-5, max_rounds=100, cert_every=1, seed=0, d=None):
+    """DuHL on K column shards with CoCoA-style aggregation (or_duhl_solve_cocoa).
+    m and refresh_count are per shard.  Returns dict(status, alpha, z, rounds, gap, gaps, gammas)."""
+    A = _f32A(A)
+    n, ld = A.shape
+    d = ld if d is None else d
+    cfg = DuhlCfg(model, policy, m, passes, refresh_count, eps, max_rounds, cert_every, seed)
+    alpha = np.zeros(n)
+    z = np.empty(n)
+    rounds = C.c_int64()
+    gap = C.c_double()
+    tg = np.zeros(max_rounds)
+    gm = np.zeros(max_rounds)
+    st = lib().or_duhl_solve_cocoa(C.byref(cfg), K, int(bool(linesearch)), _p(A), d, n, ld,
+                                   _p(_f64(b_or_y)), lam, _p(alpha), _p(z), C.byref(rounds),
+                                   C.byref(gap), _p(tg), _p(gm))
+    r = rounds.value
+    return dict(status=st, alpha=alpha, z=z, rounds=r, gap=gap.value, gaps=tg[:r], gammas=gm[:r])

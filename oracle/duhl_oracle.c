@@ -483,3 +483,201 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
     free(in_prev); free(in_cur);
     return st;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Multi-GPU aggregation (CoCoA-style; reading R16).
+ *
+ * Exact line search on the aggregation weight gamma in [0,1]: minimise the
+ * global objective along alpha_old + gamma dalpha (v = v0 + gamma dv):
+ *   SVM: O(g) = -(S + g sum_i y_i da_i)/n + ||v0 + g dv||^2/(2 lambda n^2)
+ *                 -> g* = clip((sum y da / n - v0^T dv/(lambda n^2)) / (||dv||^2/(lambda n^2)), 0, 1)
+ *   Lasso: O(g) = ||vt0 + g dv||^2/(2d) + lambda sum_i |a_i + g da_i|  (vt0 = A a - b)
+ *                 convex piecewise quadratic: its right derivative
+ *                 D(g) = (vt0^T dv + g ||dv||^2)/d + lambda sum_i da_i sgn+(a_i + g da_i)
+ *                 is increasing; g* = the smallest g in [0,1] with D(g) >= 0, found by
+ *                 walking the sorted breakpoints g_i = -a_i/da_i.
+ * sgn+(x) = sign(x) for x != 0 and sign(da_i) at x = 0 (the right-limit).
+ * (a_old, da, y) hold the k changed coordinates; v0/vt0, dv are length d. */
+static int or_cmp_d(const void* a, const void* b) {
+    double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+static double or_sgnp(double x, double da) {
+    if (x > 0.0) return 1.0;
+    if (x < 0.0) return -1.0;
+    return da > 0.0 ? 1.0 : (da < 0.0 ? -1.0 : 0.0);
+}
+static double or_lasso_rderiv(double g, const double* a_old, const double* da, i64 k, double vdv,
+                              double dvdv, double lambda, i64 d) {
+    double s = 0.0;
+    for (i64 i = 0; i < k; ++i) s += da[i] * or_sgnp(a_old[i] + g * da[i], da[i]);
+    return (vdv + g * dvdv) / (double)d + lambda * s;
+}
+double or_linesearch(int model, const double* v0, const double* dv, i64 d, const double* a_old,
+                     const double* da, const double* y, i64 k, double lambda, i64 n) {
+    double vdv = 0.0, dvdv = 0.0;
+    for (i64 r = 0; r < d; ++r) { vdv += v0[r] * dv[r]; dvdv += dv[r] * dv[r]; }
+    if (model == OR_SVM) {
+        double ln2 = lambda * (double)n * (double)n, yda = 0.0;
+        for (i64 i = 0; i < k; ++i) yda += y[i] * da[i];
+        if (!(dvdv > 0.0)) return 1.0;
+        double g = (yda / (double)n - vdv / ln2) / (dvdv / ln2);
+        return g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g);
+    }
+    if (or_lasso_rderiv(0.0, a_old, da, k, vdv, dvdv, lambda, d) >= 0.0) return 0.0;
+    if (or_lasso_rderiv(1.0, a_old, da, k, vdv, dvdv, lambda, d) < 0.0) return 1.0;
+    /* breakpoints strictly inside (0, 1) */
+    double* bp = (double*)malloc(sizeof(double) * (size_t)(k + 2));
+    i64 nb = 0;
+    bp[nb++] = 0.0;
+    for (i64 i = 0; i < k; ++i)
+        if (da[i] != 0.0) {
+            double g = -a_old[i] / da[i];
+            if (g > 0.0 && g < 1.0) bp[nb++] = g;
+        }
+    bp[nb++] = 1.0;
+    qsort(bp, (size_t)nb, sizeof(double), or_cmp_d);
+    double g = 1.0;
+    for (i64 q = 0; q + 1 < nb; ++q) {
+        double lo = bp[q], hi = bp[q + 1];
+        if (!(hi > lo)) continue;
+        double mid = 0.5 * (lo + hi);
+        /* on (lo, hi) the sign pattern is constant: D(x) = (vdv + x dvdv)/d + lambda S */
+        double S = 0.0;
+        for (i64 i = 0; i < k; ++i) S += da[i] * or_sgnp(a_old[i] + mid * da[i], da[i]);
+        if (or_lasso_rderiv(lo, a_old, da, k, vdv, dvdv, lambda, d) >= 0.0) { g = lo; break; }
+        double x = dvdv > 0.0 ? (-(double)d * lambda * S - vdv) / dvdv : hi;
+        if (x < hi) { g = x > lo ? x : lo; break; }
+    }
+    free(bp);
+    return g;
+}
+
+/* DuHL on K column shards (CoCoA-style aggregation): shard k
+ * owns columns [k n/K, (k+1) n/K) and keeps its own gap memory, rotating
+ * cursor and working set of m columns.  Round t:
+ *   1. every shard: P_k = its top-m (policy) on its z, ascending
+ *   2. every shard: unit-A refresh of refresh_count of its columns at alpha^(t)
+ *   3. every shard: `passes` SCD passes on P_k from the common v0 (local
+ *      shadow; pass permutation key (seed, t, pass) over P_k's positions),
+ *      giving dv_k = v_k - v0 and dalpha on P_k
+ *   4. dv = sum_k dv_k (shard order); gamma = linesearch (or 1);
+ *      v = v0 + gamma dv, alpha_P = alpha_old + gamma dalpha
+ *      (K = 1 without line search: v = v_1 exactly, == or_duhl_solve)
+ *   5. every shard: z_P refresh at the new state; certificate every cert_every. */
+int or_duhl_solve_cocoa(const or_duhl_cfg* cfg, int K, int linesearch, const float* A, i64 d, i64 n,
+                        i64 ld, const double* b_or_y, double lambda, double* alpha, double* z,
+                        i64* rounds_out, double* gap_out, double* trace_gap, double* trace_gamma) {
+    int model = cfg->model;
+    i64 m = cfg->m;
+    if (K < 1 || m < 1 || m * K > n) return OR_E_INVALID;
+    const double* y = (model == OR_SVM) ? b_or_y : NULL;
+    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    double* norms = (double*)malloc(sizeof(double) * (size_t)n);
+    double* v = (double*)malloc(sizeof(double) * (size_t)d);
+    double* vt = (double*)malloc(sizeof(double) * (size_t)d);
+    double* v0 = (double*)malloc(sizeof(double) * (size_t)d);
+    double* vk = (double*)malloc(sizeof(double) * (size_t)d);
+    double* dv = (double*)malloc(sizeof(double) * (size_t)d);
+    double* w = (double*)malloc(sizeof(double) * (size_t)d);
+    i64* P = (i64*)malloc(sizeof(i64) * (size_t)(m * K));
+    i64* perm = (i64*)malloc(sizeof(i64) * (size_t)m);
+    double* aold = (double*)malloc(sizeof(double) * (size_t)(m * K));
+    double* da = (double*)malloc(sizeof(double) * (size_t)(m * K));
+    double* yP = (double*)malloc(sizeof(double) * (size_t)(m * K));
+    double* gtmp = (double*)malloc(sizeof(double) * (size_t)n);
+    i64* idx = (i64*)malloc(sizeof(i64) * (size_t)n);
+    i64* cursor = (i64*)calloc((size_t)K, sizeof(i64));
+    double* zloc = (double*)malloc(sizeof(double) * (size_t)n);
+    or_col_norms(A, d, n, ld, norms);
+    double B = (model == OR_LASSO) ? or_lasso_B(b, d, lambda) : 0.0;
+    int st = OR_E_NOT_CONVERGED;
+    double gap = INFINITY;
+    or_matvec(A, d, n, ld, alpha, v);
+    for (i64 r = 0; r < d; ++r) vt[r] = (model == OR_LASSO) ? v[r] - b[r] : v[r];
+    or_shadow_w(model, vt, d, n, lambda, w);
+    int s0 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
+    if (s0 != OR_OK) st = s0;
+    i64 t = 0;
+    for (t = 0; t < cfg->max_rounds && s0 == OR_OK; ++t) {
+        /* 1. per-shard selection */
+        i64 nP = 0;
+        for (int k = 0; k < K; ++k) {
+            i64 lo = (i64)k * n / K, hi = (i64)(k + 1) * n / K, nk = hi - lo;
+            for (i64 i = 0; i < nk; ++i) zloc[i] = z[lo + i];
+            i64 mt = or_select_policy(cfg->policy, nk, m, t, cfg->seed, zloc, P + nP);
+            qsort(P + nP, (size_t)mt, sizeof(i64), or_cmp_i64);
+            for (i64 q = 0; q < mt; ++q) P[nP + q] += lo;
+            nP += mt;
+        }
+        /* 2. per-shard unit-A refresh at the round-start state */
+        or_shadow_w(model, vt, d, n, lambda, w);
+        for (int k = 0; k < K; ++k) {
+            i64 lo = (i64)k * n / K, hi = (i64)(k + 1) * n / K, nk = hi - lo;
+            i64 kr = cfg->refresh_count < nk ? cfg->refresh_count : nk;
+            for (i64 q = 0; q < kr; ++q) idx[q] = lo + (cursor[k] + q) % nk;
+            cursor[k] = (cursor[k] + kr) % nk;
+            if (kr > 0) {
+                int s1 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, idx, kr, NULL, gtmp);
+                if (s1 != OR_OK) { st = s1; goto done; }
+                for (i64 q = 0; q < kr; ++q) z[idx[q]] = gtmp[q];
+            }
+        }
+        /* 3. per-shard SCD from the common v0 */
+        memcpy(v0, vt, sizeof(double) * (size_t)d);
+        for (i64 r = 0; r < d; ++r) dv[r] = 0.0;
+        for (i64 q = 0; q < nP; ++q) aold[q] = alpha[P[q]];
+        {
+            i64 off = 0;
+            for (int k = 0; k < K; ++k) {
+                i64 lo = (i64)k * n / K, hi = (i64)(k + 1) * n / K, nk = hi - lo;
+                i64 mk = m < nk ? m : nk;
+                if (cfg->policy == 1) { /* sequential: the block may be short */
+                    mk = 0;
+                    while (off + mk < nP && P[off + mk] < hi) ++mk;
+                }
+                memcpy(vk, v0, sizeof(double) * (size_t)d);
+                for (int p = 0; p < cfg->passes; ++p) {
+                    or_make_perm(P + off, mk, cfg->seed, t, p, perm);
+                    or_scd_pass(model, A, d, n, ld, norms, y, lambda, alpha, vk, perm, mk);
+                }
+                if (K == 1 && !linesearch) memcpy(dv, vk, sizeof(double) * (size_t)d);
+                else for (i64 r = 0; r < d; ++r) dv[r] += vk[r] - v0[r];
+                off += mk;
+                (void)lo;
+            }
+        }
+        /* 4. aggregation */
+        double gamma = 1.0;
+        if (K == 1 && !linesearch) {
+            memcpy(vt, dv, sizeof(double) * (size_t)d);
+        } else {
+            for (i64 q = 0; q < nP; ++q) {
+                da[q] = alpha[P[q]] - aold[q];
+                yP[q] = y ? y[P[q]] : 0.0;
+            }
+            if (linesearch) gamma = or_linesearch(model, v0, dv, d, aold, da, yP, nP, lambda, n);
+            for (i64 r = 0; r < d; ++r) vt[r] = v0[r] + gamma * dv[r];
+            for (i64 q = 0; q < nP; ++q) alpha[P[q]] = aold[q] + gamma * da[q];
+        }
+        if (trace_gamma) trace_gamma[t] = gamma;
+        /* 5. z_P refresh at the new state, certificate */
+        or_shadow_w(model, vt, d, n, lambda, w);
+        int s5 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, P, nP, NULL, gtmp);
+        if (s5 != OR_OK) { st = s5; break; }
+        for (i64 q = 0; q < nP; ++q) z[P[q]] = gtmp[q];
+        if (trace_gap) trace_gap[t] = -1.0;
+        if (cfg->cert_every > 0 && ((t + 1) % cfg->cert_every == 0)) {
+            int s6 = or_duality_gap(model, A, d, n, ld, alpha, b_or_y, lambda, B, &gap, NULL, NULL);
+            if (trace_gap) trace_gap[t] = gap;
+            if (s6 != OR_OK) { st = s6; break; }
+            if (gap <= cfg->eps) { st = OR_OK; ++t; break; }
+        }
+    }
+done:
+    *rounds_out = t;
+    *gap_out = gap;
+    free(norms); free(v); free(vt); free(v0); free(vk); free(dv); free(w); free(P); free(perm);
+    free(aold); free(da); free(yP); free(gtmp); free(idx); free(cursor); free(zloc);
+    return st;
+}

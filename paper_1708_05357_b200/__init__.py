@@ -10,7 +10,7 @@ There is no CPU fallback: importing works anywhere (the symbols load), but any
 call that computes raises ``DuhlError`` unless a B200 is present.
 """
 from ._abi import (LASSO, SVM_DUAL, SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, DuhlError, Problem,
-                   RoundRecord, create, lib, lib_path, exported_symbols)
+                   RoundRecord, create, comm_unique_id, lib, lib_path, exported_symbols)
 
 __all__ = ["LASSO", "SVM_DUAL", "SEL_GAP", "SEL_SEQUENTIAL", "SEL_UNIFORM", "DuhlError", "Problem",
-           "RoundRecord", "create", "lib", "lib_path", "exported_symbols"]
+           "RoundRecord", "create", "comm_unique_id", "lib", "lib_path", "exported_symbols"]

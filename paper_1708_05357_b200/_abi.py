@@ -15,8 +15,8 @@ STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "
 
 FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_destroy", "duhl_gaps", "duhl_select",
              "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
-             "duhl_set_state", "duhl_get_stream", "duhl_get_kernel_stats", "duhl_get_counters",
-             "duhl_last_error"]
+             "duhl_set_state", "duhl_comm_unique_id", "duhl_comm_init", "duhl_get_stream",
+             "duhl_get_kernel_stats", "duhl_get_counters", "duhl_last_error"]
 KIND_SCD, KIND_GAP, KIND_TOPM, KIND_STAGE = 0, 1, 2, 3
 
 
@@ -34,12 +34,14 @@ class Config(C.Structure):
     _fields_ = [("hbm_budget_bytes", C.c_size_t), ("m", C.c_int64), ("device", C.c_int),
                 ("scd_block", C.c_int), ("scd_ctas", C.c_int), ("refresh_fraction", C.c_double),
                 ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
-                ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int)]
+                ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
+                ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int)]
 
 
 class RoundRecord(C.Structure):
     _fields_ = [("round", C.c_int64), ("swaps", C.c_int64), ("refreshed", C.c_int64),
-                ("cert_gap", C.c_double), ("z_sum", C.c_double), ("time_s", C.c_double)]
+                ("cert_gap", C.c_double), ("z_sum", C.c_double), ("gamma", C.c_double),
+                ("time_s", C.c_double)]
 
 
 _lib = None
@@ -70,6 +72,8 @@ def lib():
         L.duhl_round.argtypes = [_P, _I, C.c_int, C.c_int, C.c_int, _P]
         L.duhl_solve.argtypes = [_P, C.c_double, _I, C.c_int, C.c_int, _P, _I, _P, _P]
         L.duhl_get_kernel_stats.argtypes = [_P, C.c_int, _P, _P, _P]
+        L.duhl_comm_unique_id.argtypes = [_P]
+        L.duhl_comm_init.argtypes = [_P, _P, C.c_int, C.c_int]
         L.duhl_get_state.argtypes = [_P, _P, _P, _P]
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
@@ -191,6 +195,11 @@ class Problem:
         a = np.ascontiguousarray(alpha, dtype=np.float64)
         self._check(lib().duhl_set_state(self._h, _p(a)))
 
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """duhl_comm_init: join the NCCL group identified by the 128-byte id."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(lib().duhl_comm_init(self._h, buf, nranks, rank))
+
     def stream(self):
         s = C.c_void_p()
         self._check(lib().duhl_get_stream(self._h, C.byref(s)))
@@ -204,7 +213,8 @@ class Problem:
 
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
-           cert_adaptive=True, profile=False, scd_exact=True):
+           cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
+           linesearch=False):
     """duhl_create.  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -217,7 +227,8 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          scd_block=scd_block, scd_ctas=scd_ctas,
                          refresh_fraction=refresh_fraction, cert_every=cert_every, seed=seed,
                          borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
-                         profile=int(bool(profile)), scd_exact=int(bool(scd_exact)))
+                         profile=int(bool(profile)), scd_exact=int(bool(scd_exact)),
+                         n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)))
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:
@@ -226,3 +237,12 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
     prob.m = cfg.m if cfg.m > 0 else (n if hbm_budget_bytes == 0 else
                                       min(n, hbm_budget_bytes // (((d + 3) // 4) * 16)))
     return prob
+
+
+def comm_unique_id() -> bytes:
+    """duhl_comm_unique_id: a fresh 128-byte NCCL id (call on one rank, broadcast it)."""
+    buf = C.create_string_buffer(128)
+    st = lib().duhl_comm_unique_id(buf)
+    if st != 0:
+        raise DuhlError(st, "duhl_comm_unique_id failed")
+    return buf.raw

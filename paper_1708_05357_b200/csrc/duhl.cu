@@ -6,6 +6,8 @@
 // staged with cudaMemcpyAsync on a copy stream (Alg. 2 l.4); the compute stream
 // waits on an event before the SCD epoch.  See include/duhl.h for the contract.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library dlopen()s libnccl.so.2 at duhl_comm_init
 
 #include <algorithm>
 #include <chrono>
@@ -28,10 +30,43 @@ constexpr int kGapTileRows = 4096;
 inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
 }  // namespace
 
+// ---- NCCL, resolved at run time (shares torch's already-loaded libnccl.so.2 if present)
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+static NcclApi* nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+            api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+            api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+            api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
+        }
+    }
+    return api.ok ? &api : nullptr;
+}
+
 struct duhl_ctx {
-    // ---- problem
+    // ---- problem (this rank's shard: columns [col_offset, col_offset + n) of n_glob)
     int model = 0;
-    int64_t d = 0, d4 = 0, n = 0;
+    int64_t d = 0, d4 = 0, n = 0, n_glob = 0, col_offset = 0;
+    // ---- multi-GPU (CoCoA-style aggregation)
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    double *d_dv = nullptr, *d_aold = nullptr, *d_ls = nullptr;  // dv, alpha_P at round start, line search
     double lambda = 0, B = 0;
     duhl_config cfg{};
     std::string err;
@@ -167,7 +202,15 @@ static ColSrc colsrc(const duhl_ctx* ctx) {
 }
 
 static double wscale(const duhl_ctx* ctx) {
-    return ctx->model == DUHL_LASSO ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n);
+    return ctx->model == DUHL_LASSO ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n_glob);
+}
+
+// In-place sum (or max) allreduce over the group on the compute stream; no-op alone.
+static duhl_status allreduce(duhl_ctx* ctx, double* buf, size_t count, ncclRedOp_t op = ncclSum) {
+    if (!ctx->comm || ctx->nranks < 2) return DUHL_OK;
+    ncclResult_t r = nccl_api()->allReduce(buf, buf, count, ncclDouble, op, ctx->comm, ctx->st);
+    if (r != ncclSuccess) return fail(ctx, DUHL_E_NCCL, std::string("ncclAllReduce: ") + nccl_api()->getErrorString(r));
+    return DUHL_OK;
 }
 
 static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
@@ -175,7 +218,7 @@ static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
     p.model = ctx->model;
     p.d = ctx->d;
     p.d4 = ctx->d4;
-    p.n = ctx->n;
+    p.n = ctx->n_glob;  // gap formulas use the global n (SVM 1/n, w = v/(lambda n))
     p.src = colsrc(ctx);
     p.cols = d_cols;
     p.k = k;
@@ -192,9 +235,15 @@ static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
 }
 
 static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    int fl[2] = {0, 0};
+    CK(cudaMemcpyAsync(fl, ctx->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    const int flag = fl[0];
+    if (fl[1]) {
+        CK(cudaMemsetAsync(ctx->d_flag + 1, 0, sizeof(int), ctx->st));
+        return fail(ctx, DUHL_E_CUDA, std::string(where) + (fl[1] & 1 ? ": staging copy wait timed out"
+                                                                      : ": grid barrier timed out"));
+    }
     if (flag) {
         CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->st));
         return fail(ctx, DUHL_E_NUMERIC,
@@ -393,11 +442,13 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_norms, ctx->d_z, ctx->d_P, ctx->d_order_j, ctx->d_cols,
                         ctx->d_chg_cols, ctx->d_P_slot, ctx->d_order_slot, ctx->d_chg_slots,
                         ctx->d_vsnap, ctx->d_s_acc2, ctx->d_progress, ctx->d_P_batch,
+                        ctx->d_dv, ctx->d_aold, ctx->d_ls,
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
+    if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
     if (ctx->registered) cudaHostUnregister(ctx->h_store);
     if (ctx->own_store && ctx->h_store) cudaFreeHost(ctx->h_store);
     for (auto& t : ctx->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -458,6 +509,9 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ctx->model = model;
     ctx->d = A->d;
     ctx->n = A->n;
+    ctx->n_glob = ctx->cfg.n_global > 0 ? ctx->cfg.n_global : A->n;
+    ctx->col_offset = ctx->cfg.col_offset;
+    if (ctx->col_offset < 0 || ctx->col_offset + A->n > ctx->n_glob) { delete ctx; return DUHL_E_INVALID; }
     ctx->d4 = round4(A->d);
     ctx->lambda = lambda;
     const int64_t d = ctx->d, n = ctx->n, d4 = ctx->d4;
@@ -567,6 +621,9 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
               dmal((void**)&ctx->d_order_slot, n * sizeof(int)) &&
               dmal((void**)&ctx->d_chg_slots, 2 * n * sizeof(int)) &&
               dmal((void**)&ctx->d_vsnap, d4 * sizeof(double)) &&
+              dmal((void**)&ctx->d_dv, d4 * sizeof(double)) &&
+              dmal((void**)&ctx->d_aold, n * sizeof(double)) &&
+              dmal((void**)&ctx->d_ls, 256 * sizeof(double)) &&
               dmal((void**)&ctx->d_s_acc2, n * sizeof(double)) &&
               dmal((void**)&ctx->d_progress, 64) &&
               dmal((void**)&ctx->d_P_batch, n * sizeof(unsigned)) &&
@@ -578,7 +635,7 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
               dmal((void**)&ctx->d_gap_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_s_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_sums, 8 * sizeof(double)) &&
-              dmal((void**)&ctx->d_flag, sizeof(int));
+              dmal((void**)&ctx->d_flag, 4 * sizeof(int));
     if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
     choose_scd_shape(ctx);
     if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
@@ -605,7 +662,7 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ck(cudaMemsetAsync(ctx->d_s_acc, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_s_acc2, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_progress, 0, 64, st));
-    ck(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
+    ck(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), st));
     ck(cudaMemsetAsync(ctx->d_alpha, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_b, 0, d4 * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_y, 0, n * sizeof(double), st));
@@ -708,7 +765,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.model = ctx->model;
     p.d = ctx->d;
     p.d4 = ctx->d4;
-    p.n = ctx->n;
+    p.n = ctx->n_glob;
     p.lambda = ctx->lambda;
     p.pool = ctx->pool;
     p.ld_dev = ctx->ld_dev;
@@ -726,6 +783,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.exact = ctx->cfg.scd_exact;
     p.red = ctx->d_red;
     p.order_batch = ctx->write_value ? ctx->d_order_batch : nullptr;
+    p.err = ctx->d_flag + 1;
     p.order_a = ctx->d_order_a;
     p.order_inv = ctx->d_order_inv;
     p.order_y = ctx->d_order_y;
@@ -809,26 +867,26 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
         TRY(scd_launch(ctx, perm_len));
         TRY(issue_staging(ctx));
         TRY(finalize_staging(ctx));
-        CK(cudaStreamSynchronize(ctx->st));
-        return DUHL_OK;
+        return check_flag(ctx, "duhl_scd_epoch");
     }
     if (passes < 1) return fail(ctx, DUHL_E_INVALID, "passes < 1");
     TRY(scd_passes(ctx, passes, seed, round));
     TRY(finalize_staging(ctx));
-    CK(cudaStreamSynchronize(ctx->st));
-    return DUHL_OK;
+    return check_flag(ctx, "duhl_scd_epoch");
 }
 
 static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, double* dual) {
     CK(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), ctx->st));
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+    TRY(allreduce(ctx, ctx->d_sums, 3));           // per-column sums over the shards
+    TRY(allreduce(ctx, ctx->d_sums + 3, 1, ncclMax));
     CK(launch_vec_sums(ctx->d_vt, ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
-                       ctx->st, &ctx->launches));
+                       ctx->st, &ctx->launches));     // v is replicated: no reduction
     double h[8];
     CK(cudaMemcpyAsync(h, ctx->d_sums, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     TRY(check_flag(ctx, "certificate"));
-    const double dd = (double)ctx->d, nn = (double)ctx->n, lam = ctx->lambda;
+    const double dd = (double)ctx->d, nn = (double)ctx->n_glob, lam = ctx->lambda;
     const double G = h[0], aux = h[1], asum = h[2], vv = h[4], vb = h[5];
     double amax;
     std::memcpy(&amax, &h[3], sizeof(double));
@@ -857,6 +915,82 @@ duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double*
     return certificate(ctx, gap, primal, dual);
 }
 
+// CoCoA-style aggregation after the local epoch (R16):
+// dv = sum over ranks of (v_local - v0); gamma = exact line search on [0, 1] of
+// the global objective along (alpha_old + gamma dalpha, v0 + gamma dv), or 1;
+// then v = v0 + gamma dv and alpha_P = alpha_old + gamma dalpha.
+//   SVM: closed form from sum y dalpha (allreduced), v0^T dv, ||dv||^2
+//   Lasso: the right derivative D(g) = (v~0^T dv + g ||dv||^2)/d
+//                  + lambda sum dalpha sgn+(alpha_old + g dalpha) is increasing:
+//                  bracket its sign change on 64-point grids (one allreduce each),
+//                  then solve the linear piece inside the final bracket.
+static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
+    const int64_t m = (int64_t)ctx->P.size();
+    const double dd = (double)ctx->d, nn = (double)ctx->n_glob, lam = ctx->lambda;
+    CK(launch_delta_v(ctx->d_vt, ctx->d_vsnap, ctx->d4, ctx->d_dv, ctx->d_ls + 64, ctx->st, &ctx->launches));
+    TRY(allreduce(ctx, ctx->d_dv, (size_t)ctx->d4));
+    CK(cudaMemsetAsync(ctx->d_ls, 0, 8 * sizeof(double), ctx->st));
+    CK(launch_vec_sums(ctx->d_dv, ctx->d_vsnap, ctx->d4, ctx->d_ls, ctx->st, &ctx->launches));  // |dv|^2, v0.dv
+    double gamma = 1.0;
+    if (ctx->cfg.linesearch) {
+        if (ctx->model == DUHL_SVM_DUAL) {
+            CK(launch_ydalpha(ctx->d_alpha, ctx->d_y, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 2, ctx->st,
+                              &ctx->launches));
+            TRY(allreduce(ctx, ctx->d_ls + 2, 1));
+            double h[3];
+            CK(cudaMemcpyAsync(h, ctx->d_ls, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            const double dvdv = h[0], vdv = h[1], yda = h[2], ln2 = lam * nn * nn;
+            if (dvdv > 0.0) {
+                gamma = (yda / nn - vdv / ln2) / (dvdv / ln2);
+                gamma = gamma < 0.0 ? 0.0 : (gamma > 1.0 ? 1.0 : gamma);
+            }
+        } else {
+            double h[2];
+            CK(cudaMemcpyAsync(h, ctx->d_ls, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            const double dvdv = h[0], vdv = h[1];
+            auto Dfun = [&](double g, double S) { return (vdv + g * dvdv) / dd + lam * S; };
+            double lo = 0.0, hi = 1.0, gam[64], S[64];
+            bool done = false;
+            for (int it = 0; it < 5 && !done; ++it) {
+                const int ng = 64;
+                for (int q = 0; q < ng; ++q) gam[q] = it == 0 ? (double)q / (ng - 1) : lo + (hi - lo) * (q + 1) / ng;
+                if (it == 4) { gam[0] = 0.5 * (lo + hi); }  // final: the pattern inside the bracket
+                const int nq = it == 4 ? 1 : ng;
+                CK(cudaMemcpyAsync(ctx->d_ls + 128, gam, nq * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+                CK(cudaMemsetAsync(ctx->d_ls + 192, 0, nq * sizeof(double), ctx->st));
+                CK(launch_lasso_dgrid(ctx->d_alpha, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 128, nq, ctx->d_ls + 192,
+                                      ctx->st, &ctx->launches));
+                TRY(allreduce(ctx, ctx->d_ls + 192, (size_t)nq));
+                CK(cudaMemcpyAsync(S, ctx->d_ls + 192, nq * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+                CK(cudaStreamSynchronize(ctx->st));
+                if (it == 0) {
+                    if (Dfun(0.0, S[0]) >= 0.0) { gamma = 0.0; done = true; break; }
+                    if (Dfun(1.0, S[ng - 1]) < 0.0) { gamma = 1.0; done = true; break; }
+                    int q = 1;
+                    while (q < ng && Dfun(gam[q], S[q]) < 0.0) ++q;
+                    lo = gam[q - 1];
+                    hi = gam[q];
+                } else if (it < 4) {
+                    int q = 0;
+                    while (q < ng && Dfun(gam[q], S[q]) < 0.0) ++q;
+                    if (q > 0) lo = gam[q - 1];
+                    hi = gam[q < ng ? q : ng - 1];
+                } else {
+                    const double x = dvdv > 0.0 ? (-dd * lam * S[0] - vdv) / dvdv : hi;
+                    gamma = x < lo ? lo : (x > hi ? hi : x);
+                    done = true;
+                }
+            }
+        }
+    }
+    CK(launch_apply_gamma(ctx->d_vt, ctx->d_vsnap, ctx->d_dv, ctx->d4, ctx->d_alpha, ctx->d_P, ctx->d_aold, m,
+                          gamma, ctx->st, &ctx->launches));
+    if (gamma_out) *gamma_out = gamma;
+    return DUHL_OK;
+}
+
 // Unit-A refresh of the cursor chunk (columns in d_cols) against the v snapshot:
 // 1024-row tiles (8 KB of shared memory) so a CTA fits beside the SCD kernel's
 // CTA on every SM; PCIe-bound for non-resident columns.
@@ -882,12 +1016,19 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
     auto tstaged = now();
     std::vector<int64_t> idx(kref);
+    const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
+    if (agg) {  // round-start state for the aggregation: v0 and alpha_P
+        CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+        CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, (int64_t)ctx->P.size(), ctx->d_aold, ctx->st,
+                             &ctx->launches));
+    }
     if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) from a snapshot of v, launched on its
                      // own stream right after the SCD kernel (refresh_launch)
         for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
         ctx->cursor = (ctx->cursor + kref) % n;
         CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
-        CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+        if (!agg)
+            CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
     }
     auto tlaunch = now();
@@ -895,12 +1036,15 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     TRY(finalize_staging(ctx));                                            // staged columns -> table
     auto tscd = now();
     if (kref > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));         // join unit A
+    double gamma = 1.0;
+    if (agg) TRY(aggregate(ctx, &gamma));                                   // l.11 across ranks
     const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
     TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
     double cg = -1.0;
     if (certify) TRY(certificate(ctx, &cg, nullptr, nullptr));
     CK(cudaMemsetAsync(ctx->d_sums + 6, 0, sizeof(double), ctx->st));
     CK(launch_sum(ctx->d_z, n, ctx->d_sums + 6, ctx->st, &ctx->launches));
+    TRY(allreduce(ctx, ctx->d_sums + 6, 1));
     double zs = 0.0;
     CK(cudaMemcpyAsync(&zs, ctx->d_sums + 6, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -919,6 +1063,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->refreshed = kref;
         rec->cert_gap = cg;
         rec->z_sum = zs;
+        rec->gamma = gamma;
         rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     return DUHL_OK;
@@ -1000,6 +1145,34 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, nullptr));
     CK(cudaStreamSynchronize(ctx->st));
     return check_flag(ctx, "duhl_set_state");
+}
+
+duhl_status duhl_comm_unique_id(void* id_out) {
+    if (!id_out) return DUHL_E_INVALID;
+    NcclApi* api = nccl_api();
+    if (!api) return DUHL_E_NCCL;
+    ncclUniqueId id;
+    if (api->getUniqueId(&id) != ncclSuccess) return DUHL_E_NCCL;
+    std::memcpy(id_out, &id, sizeof(id));
+    return DUHL_OK;
+}
+
+duhl_status duhl_comm_init(duhl_ctx* ctx, const void* id, int nranks, int rank) {
+    if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    NcclApi* api = nccl_api();
+    if (!api) return fail(ctx, DUHL_E_NCCL, "libnccl.so.2 not found");
+    if (ctx->comm) return fail(ctx, DUHL_E_INVALID, "communicator already initialised");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = api->commInitRank(&ctx->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        ctx->comm = nullptr;
+        return fail(ctx, DUHL_E_NCCL, std::string("ncclCommInitRank: ") + api->getErrorString(r));
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return DUHL_OK;
 }
 
 duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {

@@ -514,6 +514,17 @@ __device__ __forceinline__ double coord_step_inv(int model, double a, double s, 
     return y * u;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded spin-waits: a wait that cannot be satisfied (e.g. a profiler that
+// serialises the copy stream behind this kernel) sets ScdParams::err and lets
+// the kernel drain instead of hanging the device; the host reports DUHL_E_CUDA.
+constexpr unsigned long long kSpinTimeoutNs = 4000000000ull;  // 4 s
+
 // Stage the CTA's row slice of block blk's columns into shared memory with the
 // TMA engine.  Called by a whole warp: lane j fetches the slot of column j (one
 // parallel L2 round trip instead of W dependent ones) and issues its own bulk
@@ -529,7 +540,11 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
     const int slot = lane < Wb ? p.order_slot[base + lane] : 0;
     if (p.progress && lane < Wb) {  // column still being staged host -> HBM: wait for its copy
         const unsigned need = p.order_batch[base + lane];
-        while (ld_acquire_u32(p.progress) < need) { __nanosleep(128); }
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire_u32(p.progress) < need) {
+            __nanosleep(128);
+            if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 1); break; }  // never hang the GPU
+        }
     }
     fence_proxy_async();  // earlier generic reads of this stage before the async-proxy refill
     if (lane == 0) mbar_arrive_expect_tx(&mbar[st], bytes * (unsigned)Wb);
@@ -553,12 +568,6 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
 // (phase A of iteration b+3) waits on ARRIVE(b+2), which CTA 0 issues after
 // zeroing.
 // =====================================================================================
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
 template <bool EXACT>
 __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -715,7 +724,11 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             // before WAIT(b) completed everywhere: one counter per block parity counts
             // exactly the arrivals of blocks b, b-2, b-4, ...
             const unsigned target = (unsigned)((b / 2 + 1) * (int64_t)p.G);
-            while (ld_acquire_u32(&p.bar[b & 1]) < target) { __nanosleep(32); }
+            const unsigned long long t0 = gtimer();
+            while (ld_acquire_u32(&p.bar[b & 1]) < target) {
+                __nanosleep(32);
+                if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 2); break; }
+            }
             __threadfence();
         }
         __syncwarp();
@@ -896,6 +909,96 @@ __global__ void k_sum(const double* x, int64_t n, double* out) {
 }
 cudaError_t launch_sum(const double* x, int64_t n, double* out, cudaStream_t st, int64_t* launches) {
     k_sum<<<(unsigned)imin64(cdiv(n, 256), 296), 256, 0, st>>>(x, n, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// ---- CoCoA-style aggregation helpers ------------------------------
+// out[q] = x[idx[q]]
+__global__ void k_gather_f64(const double* x, const int64_t* idx, int64_t k, double* out) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < k) out[q] = x[idx[q]];
+}
+// dv = v - v0 ; sums[0] += v0^T dv, sums[1] += dv^T dv
+__global__ void k_delta_v(const double* v, const double* v0, int64_t d4, double* dv, double* sums) {
+    double s0 = 0, s1 = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < d4; r += (int64_t)gridDim.x * blockDim.x) {
+        const double x = v[r] - v0[r];
+        dv[r] = x;
+        s0 = fma(v0[r], x, s0);
+        s1 = fma(x, x, s1);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if ((threadIdx.x & 31) == 0) { atomicAdd(&sums[0], s0); atomicAdd(&sums[1], s1); }
+}
+// SVM: sums[0] += sum_q y_j (alpha_j - aold_q),  j = P[q]
+__global__ void k_ydalpha(const double* alpha, const double* y, const int64_t* P, const double* aold, int64_t k,
+                          double* sums) {
+    double s = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x)
+        s += y[P[q]] * (alpha[P[q]] - aold[q]);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&sums[0], s);
+}
+// Lasso: out[g] += sum_q da_q sgn+(aold_q + gam[g] da_q), da_q = alpha_j - aold_q  (g < ng)
+__global__ void k_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
+                              const double* gam, int ng, double* out) {
+    __shared__ double sh[64];
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) sh[g] = 0.0;
+    __syncthreads();
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x) {
+        const double a0 = aold[q], da = alpha[P[q]] - a0;
+        if (da == 0.0) continue;
+        for (int g = 0; g < ng; ++g) {
+            const double x = fma(gam[g], da, a0);
+            const double sg = x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (da > 0.0 ? 1.0 : -1.0));
+            atomicAdd(&sh[g], da * sg);
+        }
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) atomicAdd(&out[g], sh[g]);
+}
+// v = v0 + gamma dv ; alpha_P = aold + gamma (alpha_P - aold)
+__global__ void k_apply_gamma(double* v, const double* v0, const double* dv, int64_t d4, double* alpha,
+                              const int64_t* P, const double* aold, int64_t k, double gamma) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < d4; r += stride) v[r] = fma(gamma, dv[r], v0[r]);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += stride) {
+        const int64_t j = P[q];
+        alpha[j] = fma(gamma, alpha[j] - aold[q], aold[q]);
+    }
+}
+cudaError_t launch_gather_f64(const double* x, const int64_t* idx, int64_t k, double* out, cudaStream_t st,
+                              int64_t* launches) {
+    if (k <= 0) return cudaSuccess;
+    k_gather_f64<<<(unsigned)cdiv(k, 256), 256, 0, st>>>(x, idx, k, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_delta_v(const double* v, const double* v0, int64_t d4, double* dv, double* sums,
+                           cudaStream_t st, int64_t* launches) {
+    k_delta_v<<<(unsigned)imin64(cdiv(d4, 256), 296), 256, 0, st>>>(v, v0, d4, dv, sums);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_ydalpha(const double* alpha, const double* y, const int64_t* P, const double* aold, int64_t k,
+                           double* sums, cudaStream_t st, int64_t* launches) {
+    k_ydalpha<<<(unsigned)imin64(cdiv(k, 256), 148), 256, 0, st>>>(alpha, y, P, aold, k, sums);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
+                               const double* gam, int ng, double* out, cudaStream_t st, int64_t* launches) {
+    k_lasso_dgrid<<<(unsigned)imin64(cdiv(k, 256), 148), 256, 0, st>>>(alpha, P, aold, k, gam, ng, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_apply_gamma(double* v, const double* v0, const double* dv, int64_t d4, double* alpha,
+                               const int64_t* P, const double* aold, int64_t k, double gamma, cudaStream_t st,
+                               int64_t* launches) {
+    k_apply_gamma<<<(unsigned)imin64(cdiv(d4 > k ? d4 : k, 256), 296), 256, 0, st>>>(v, v0, dv, d4, alpha, P,
+                                                                                     aold, k, gamma);
     ++*launches;
     return cudaGetLastError();
 }

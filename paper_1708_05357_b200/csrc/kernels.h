@@ -55,6 +55,7 @@ struct ScdParams {
     const unsigned* order_batch;  // [L] staging-copy sequence number of each column (0 = resident)
     const double *order_a, *order_inv, *order_y;  // [L] alpha at pass start, 1/||a||^2 (-1: zero column), y
     const unsigned* progress;     // last landed staging copy, written by the copy stream; or nullptr
+    int* err;                     // set (bit 0: staging wait, bit 1: grid barrier) on a wait timeout
 };
 
 __host__ __device__ int scd_nred(int W);
@@ -80,6 +81,17 @@ cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int
                           int64_t* launches);
 cudaError_t launch_set_slots(int* col_slot, const int64_t* cols, const int* slots, int64_t cnt,
                              cudaStream_t st, int64_t* launches);
+cudaError_t launch_gather_f64(const double* x, const int64_t* idx, int64_t k, double* out, cudaStream_t st,
+                              int64_t* launches);
+cudaError_t launch_delta_v(const double* v, const double* v0, int64_t d4, double* dv, double* sums,
+                           cudaStream_t st, int64_t* launches);
+cudaError_t launch_ydalpha(const double* alpha, const double* y, const int64_t* P, const double* aold, int64_t k,
+                           double* sums, cudaStream_t st, int64_t* launches);
+cudaError_t launch_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
+                               const double* gam, int ng, double* out, cudaStream_t st, int64_t* launches);
+cudaError_t launch_apply_gamma(double* v, const double* v0, const double* dv, int64_t d4, double* alpha,
+                               const int64_t* P, const double* aold, int64_t k, double gamma, cudaStream_t st,
+                               int64_t* launches);
 cudaError_t launch_sum(const double* x, int64_t n, double* out, cudaStream_t st, int64_t* launches);
 cudaError_t launch_vec_sums(const double* vt, const double* b, int64_t d4, double* out2,
                             cudaStream_t st, int64_t* launches);

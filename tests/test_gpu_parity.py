@@ -313,3 +313,53 @@ def test_budget_smaller_than_data_swaps(D):
     sw = np.array([t.swaps for t in r["trace"]])
     assert sw[0] == m and sw[-len(sw) // 4:].mean() <= sw[:len(sw) // 4].mean()
     assert c["h2d_bytes"] >= sw.sum() * d * 4
+
+
+# ------------------------------------------------------------------------- multi-GPU path (8(e))
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_aggregation_linesearch_matches_oracle(D, model, with_comm):
+    """The CoCoA aggregation path (dv, exact gamma line search, apply) on one rank,
+    with and without a 1-rank NCCL communicator, against or_duhl_solve_cocoa(K=1)."""
+    d, n = (300, 800) if model == O.LASSO else (80, 800)
+    A, lab = _data(model, d, n, seed=400 + model)
+    lam = _lam(model, n)
+    m, eps = 200, 1e-6
+    ref = O.duhl_solve_cocoa(model, A, lab, lam, m=m, K=1, linesearch=True, passes=2,
+                             refresh_count=40, eps=eps, max_rounds=3000, cert_every=1, seed=7)
+    assert ref["status"] == O.OK
+    with D.create(A, lab, lam, model, m=m, refresh_fraction=0.05, cert_every=1, seed=7,
+                  linesearch=True) as P:
+        if with_comm:
+            P.comm_init(D.comm_unique_id(), 1, 0)
+        r = P.solve(eps, 3000, passes=2)
+        g, Ob, Db = P.duality_gap()
+    assert r["status"] == 0 and g <= eps
+    gam = np.array([t.gamma for t in r["trace"]])
+    k = min(4, len(gam), len(ref["gammas"]))
+    np.testing.assert_allclose(gam[:k], ref["gammas"][:k], atol=1e-8)
+    gg = np.array([t.cert_gap for t in r["trace"]])
+    np.testing.assert_allclose(gg[:k], ref["gaps"][:k], rtol=1e-7)
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    st, G_ref, O_ref, _ = O.duality_gap(model, A, ref["alpha"], lab, lam, B)
+    assert abs(Ob - O_ref) <= 1e-4 * abs(O_ref)
+
+
+def test_shard_offsets_global_n(D):
+    """A shard (col_offset, n_global) evaluates the same gaps as the full problem's columns."""
+    d, n = 200, 600
+    A, y = synth.svm_dense(d, n, seed=9)
+    lam = 1.0 / n
+    lo, hi = 200, 400
+    rng = np.random.default_rng(2)
+    alpha = y * rng.random(n) * (rng.random(n) < 0.5)
+    alpha[:lo] = 0
+    alpha[hi:] = 0                     # only the shard's columns are nonzero: same v on both
+    with D.create(A, y, lam, D.SVM_DUAL) as Pf:
+        Pf.set_state(alpha)
+        gf = Pf.gaps()
+    with D.create(np.ascontiguousarray(A[lo:hi]), y[lo:hi], lam, D.SVM_DUAL, n_global=n,
+                  col_offset=lo) as Ps:
+        Ps.set_state(alpha[lo:hi])
+        gs = Ps.gaps()
+    np.testing.assert_allclose(gs, gf[lo:hi], rtol=1e-12, atol=1e-15)
