@@ -809,8 +809,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         cudaFree(dtr);
         const double nb = (double)((L + ctx->W - 1) / ctx->W);
         std::fprintf(stderr, "scd trace (us/block) W=%d G=%d R=%d: ", ctx->W, ctx->G, ctx->R);
-        const char* nm[8] = {"ctl:issue+coords", "flush", "w0:waitdata", "w0:tiles", "ctl:wait+sG+seq",
-                             "vupdate", "join", "-"};
+        const char* nm[8] = {"ctl:issue", "flush", "ctl:WAIT", "ctl:sGread", "ctl:seq", "vupdate", "join",
+                             "w0:tiles"};
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
             for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / 1e3);

@@ -382,7 +382,7 @@ constexpr int kScdWarps = kScdThreads / 32;
 constexpr int kScdStages = 3;
 constexpr int kRedBufs = 6;     // rotating reduction buffers (see the zeroing rule below)
 #ifndef DUHL_RED_GROUPS
-#define DUHL_RED_GROUPS 8
+#define DUHL_RED_GROUPS 2
 #endif
 constexpr int kRedGroups = DUHL_RED_GROUPS;  // CTA c adds into group c % kRedGroups ...
 constexpr int kRedStride = 32;  // ... one 256-byte line per (entry, group): spreads the fp64
@@ -529,24 +529,29 @@ constexpr unsigned long long kSpinTimeoutNs = 4000000000ull;  // 4 s
 // TMA engine.  Called by a whole warp: lane j fetches the slot of column j (one
 // parallel L2 round trip instead of W dependent ones) and issues its own bulk
 // copy; lane 0 arms the stage's mbarrier with the total byte count first.
+// Stage the CTA's row slice of block blk's columns into shared memory with the
+// TMA engine.  Called by a whole warp: lane j issues the bulk copy of column j
+// (slot / staging sequence number prefetched by the caller); lane 0 arms the
+// stage's mbarrier with the total byte count first.  A column still in flight
+// host -> HBM is waited for on the copy-progress counter (cached per lane).
 __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint64_t* mbar, int64_t blk,
-                                          int64_t r0, int rows, int lane) {
+                                          int64_t r0, int rows, int lane, int slot, unsigned need,
+                                          unsigned& seen) {
     const int W = p.W;
     const int64_t base = blk * W;
     const int Wb = (int)imin64(W, p.L - base);
     const int st = (int)(blk % kScdStages);
     float* dst = Abuf + (size_t)st * W * p.R;
     const unsigned bytes = (unsigned)rows * 4u;
-    const int slot = lane < Wb ? p.order_slot[base + lane] : 0;
-    if (p.progress && lane < Wb) {  // column still being staged host -> HBM: wait for its copy
-        const unsigned need = p.order_batch[base + lane];
+    if (p.progress && lane < Wb && need > seen) {
         const unsigned long long t0 = gtimer();
-        while (ld_acquire_u32(p.progress) < need) {
+        while ((seen = ld_acquire_u32(p.progress)) < need) {
             __nanosleep(128);
             if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 1); break; }  // never hang the GPU
         }
     }
-    fence_proxy_async();  // earlier generic reads of this stage before the async-proxy refill
+    // (the stage's last generic accesses are reads, completed before the CTA barrier
+    // that precedes this refill: no proxy fence is needed for that order)
     if (lane == 0) mbar_arrive_expect_tx(&mbar[st], bytes * (unsigned)Wb);
     __syncwarp();
     if (lane < Wb) bulk_g2s(dst + (size_t)lane * p.R, p.pool + (int64_t)slot * p.ld_dev + r0, bytes, &mbar[st]);
@@ -631,6 +636,15 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             pf_a = p.order_a[t];
             pf_inv = p.order_inv[t];
             pf_y = p.order_y[t];
+        }
+    };
+    int pf_slot = 0;
+    unsigned pf_need = 0, seen = 0;
+    auto prefetch_slot = [&](int64_t blk) {
+        const int64_t t = blk * W + lane;
+        if (lane < W && t < p.L) {
+            pf_slot = p.order_slot[t];
+            pf_need = p.order_batch ? p.order_batch[t] : 0u;
         }
     };
     auto publish_coords = [&](int64_t blk) {
@@ -732,21 +746,34 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             __threadfence();
         }
         __syncwarp();
+        stamp(2);
         if (c == 0)
             for (int q = lane; q < NRED * kRedGroups; q += 32)
                 p.red[(size_t)((b + 4) % kRedBufs) * bufsz + (size_t)q * kRedStride] = 0.0;
-        {
+        {   // all loads of the reduced block in flight at once (8 entries per lane per batch)
             const double* red_b = p.red + (size_t)(b % kRedBufs) * bufsz;
             const int nq = b > 0 ? NRED : scd_off_C(W);
-            for (int q = lane; q < nq; q += 32) {
-                double v = 0.0;
+            for (int q0 = 0; q0 < nq; q0 += 8 * 32) {
+                double v[8][kRedGroups];
 #pragma unroll
-                for (int g = 0; g < kRedGroups; ++g)
-                    v += ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]);
-                sG[q] = v;
+                for (int u = 0; u < 8; ++u) {
+                    const int q = q0 + u * 32 + lane;
+#pragma unroll
+                    for (int g = 0; g < kRedGroups; ++g)
+                        v[u][g] = q < nq ? ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int q = q0 + u * 32 + lane;
+                    double s = 0.0;
+#pragma unroll
+                    for (int g = 0; g < kRedGroups; ++g) s += v[u][g];
+                    if (q < nq) sG[q] = s;
+                }
             }
         }
         __syncwarp();
+        stamp(3);
         const int sl = (int)(b & 1);
         const double* dprev = delta + (size_t)(sl ^ 1) * 16;
         int64_t jg = 0;
@@ -764,11 +791,17 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                 for (int k = 0; k < W; ++k) sj = fma(sG[scd_off_C(W) + lane * W + k], dprev[k], sj);
         }
         double* dcur = delta + (size_t)sl * 16;
-        for (int j = 0; j < Wb; ++j) {
+        double grow[16];  // this lane's row of the block Gram, k < lane
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            grow[j] = (j < lane && lane < Wb) ? sG[scd_off_G(W) + lane * (lane - 1) / 2 + j] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j >= Wb) break;
             const double an = coord_step_inv(p.model, a, sj, inv, zero, yy, lam_dn);
             if (lane == j) afin = an;
             const double dl = __shfl_sync(~0u, an - a, j);
-            if (lane > j && lane < Wb) sj = fma(sG[scd_off_G(W) + lane * (lane - 1) / 2 + j], dl, sj);
+            sj = fma(grow[j], dl, sj);  // grow[j] = 0 unless j < lane < Wb
             if (lane == 0) dcur[j] = dl;
         }
         if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
@@ -798,7 +831,11 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     for (int q = tid; q < 2 * NRED; q += kScdThreads) acc[q] = 0.0;
     if (nblk > 0) {
         if (ctrl) {
-            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) scd_issue(p, Abuf, mbar, q, r0, rows, lane);
+            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) {
+                prefetch_slot(q);
+                scd_issue(p, Abuf, mbar, q, r0, rows, lane, pf_slot, pf_need, seen);
+            }
+            prefetch_slot(kScdStages);
             prefetch_coords(0);
             publish_coords(0);
             prefetch_coords(1);
@@ -817,7 +854,10 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             // stage of block b-1 was freed by the last V update: stream block b+2 into it
             if (next) publish_coords(b + 1);   // block b+1's inputs (prefetched last iteration)
             if (b + 2 < nblk) prefetch_coords(b + 2);
-            if (b >= 1 && b + 2 < nblk) scd_issue(p, Abuf, mbar, b + 2, r0, rows, lane);
+            if (b >= 1 && b + 2 < nblk) {       // slot/sequence of block b+2 prefetched last time
+                scd_issue(p, Abuf, mbar, b + 2, r0, rows, lane, pf_slot, pf_need, seen);
+                prefetch_slot(b + 3);
+            }
             stamp(0);
             control(b);
             stamp(4);
@@ -827,8 +867,8 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? gtimer() : 0;
             tiles(b + 1, true);
             if (p.trace && tid == 0 && c == 0) {
-                p.trace[2] += tw1 - tw0;
-                p.trace[3] += gtimer() - tw1;
+                p.trace[7] += gtimer() - tw1;
+                (void)tw0;
             }
         }
         __syncthreads();
