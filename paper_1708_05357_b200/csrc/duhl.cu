@@ -808,12 +808,16 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         CK(cudaStreamSynchronize(ctx->st));
         cudaFree(dtr);
         const double nb = (double)((L + ctx->W - 1) / ctx->W);
-        std::fprintf(stderr, "scd trace (us/block) W=%d G=%d R=%d: ", ctx->W, ctx->G, ctx->R);
+        int clk_khz = 0;
+        cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, ctx->dev);
+        const double cyc_per_us = clk_khz > 0 ? clk_khz / 1e3 : 1965.0;
+        std::fprintf(stderr, "scd trace (us/block at %.0f MHz) W=%d G=%d R=%d: ", cyc_per_us, ctx->W, ctx->G,
+                     ctx->R);
         const char* nm[8] = {"ctl:issue", "flush", "ctl:WAIT", "ctl:sGread", "ctl:seq", "vupdate", "join",
                              "w0:tiles"};
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
-            for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / 1e3);
+            for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / cyc_per_us);
         }
         std::fprintf(stderr, "\n");
     }

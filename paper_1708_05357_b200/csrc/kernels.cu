@@ -498,22 +498,6 @@ __device__ __forceinline__ void utile(const float* __restrict__ Aj, const double
     if (lane < 4) out[jbase + lane] = v;
 }
 
-// Exact coordinate step with the reciprocal 1/||a_j||^2 precomputed (same
-// closed forms as coord_step, App. D; zero column -> its 1-D minimiser).
-__device__ __forceinline__ double coord_step_inv(int model, double a, double s, double inv, bool zero,
-                                                 double y, double lam_dn) {
-    if (model == kLasso) {
-        if (zero) return 0.0;
-        double gamma = a - s * inv;               // (a ||a||^2 - s) / ||a||^2
-        double mag = fabs(gamma) - lam_dn * inv;  // tau = lambda d / ||a||^2
-        return mag > 0.0 ? copysign(mag, gamma) : 0.0;
-    }
-    if (zero) return y;
-    double u = fma(lam_dn - y * s, inv, y * a);  // y (a + Delta), Delta = (lambda n y - s)/||a||^2
-    u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
-    return y * u;
-}
-
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -573,7 +557,16 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
 // (phase A of iteration b+3) waits on ARRIVE(b+2), which CTA 0 issues after
 // zeroing.
 // =====================================================================================
-template <bool EXACT>
+#ifndef DUHL_CTRL_ALONE
+#define DUHL_CTRL_ALONE 1
+#endif
+// The control warp gets an SMSP to itself (warps w and w+4 share SMSP w % 4):
+// control = warp 3, compute = warps 0,1,2,4,5,6; warp 7 only joins the
+// all-thread phases.  (DUHL_CTRL_ALONE=0: control = warp 7, 7 compute warps.)
+constexpr int kCompute = DUHL_CTRL_ALONE ? kScdWarps - 2 : kScdWarps - 1;
+constexpr int kCtrlWarp = DUHL_CTRL_ALONE ? 3 : kScdWarps - 1;
+
+template <bool EXACT, int MODEL>
 __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int W = p.W, R = p.R, T = W / 4;
@@ -591,12 +584,14 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     double* delta = reinterpret_cast<double*>(smem + off);  // [2][16]
     __shared__ int64_t cj[2][16];
     __shared__ double ca[2][16], cinv[2][16], cy[2][16];
+    __shared__ double sT[16], sP[16], sA[16], sC[16 * 16];
+    __shared__ int sZ[16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * R;
     const int rows = (int)imin64(R, p.d4 - r0);
-    const double lam_dn = p.model == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
+    const double lam_dn = MODEL == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
     const size_t bufsz = (size_t)NRED * kRedGroups * kRedStride;
     const int grp = c % kRedGroups;
 
@@ -610,13 +605,16 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     __syncthreads();
 
     // developer trace (ScdParams::trace): per-phase globaltimer stamps of CTA 0 / CTA G-1
-    const bool tr = p.trace && tid == kScdThreads - 32 && (c == 0 || c == p.G - 1);
-    unsigned long long* trc = tr ? p.trace + (c == 0 ? 0 : 8) : nullptr;
-    unsigned long long tprev = tr ? gtimer() : 0;
+    const bool tr = p.trace && tid == kCtrlWarp * 32 && (c == 0 || c == p.G - 1);
+    unsigned long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // registers; written once at the end
+    // SM cycle counter (globaltimer ticks too coarsely for sub-microsecond phases)
+    unsigned long long tprev = tr ? (unsigned long long)clock64() : 0;
     auto stamp = [&](int k) {
         if (tr) {
-            unsigned long long t = gtimer();
-            trc[k] += t - tprev;
+            unsigned long long t = (unsigned long long)clock64();
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q == k) trc[q] += t - tprev;
             tprev = t;
         }
     };
@@ -662,8 +660,9 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     // order by decreasing cost.  The control warp (last) streams stages, loads
     // block inputs, waits on the grid barrier, reads the reduced block and runs
     // the W sequential closed-form steps -- concurrently with the tiles.
-    constexpr int kCompute = kScdWarps - 1;
-    const bool ctrl = warp == kScdWarps - 1;
+    const bool ctrl = warp == kCtrlWarp;
+    // compute-warp index (-1: none)
+    const int cw = ctrl ? -1 : (DUHL_CTRL_ALONE ? (warp < 3 ? warp : (warp < 7 ? warp - 1 : -1)) : warp);
     // per-warp item lists, built once: item = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15
     __shared__ int witems[kScdWarps][24];
     __shared__ int wcount[kScdWarps];
@@ -695,9 +694,10 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     auto tiles = [&](int64_t blk, bool with_c) {
         const float* A1 = stage(blk);
         const float* A0 = with_c ? stage(blk - 1) : nullptr;
-        const int cnt = wcount[warp];
+        if (cw < 0) return;
+        const int cnt = wcount[cw];
         for (int it = 0; it < cnt; ++it) {
-            const int code = witems[warp][it];
+            const int code = witems[cw][it];
             const int kind = code & 3, jt = (code >> 2) & 15, k0 = (code >> 6) & 31, kw = (code >> 11) & 15,
                       part = (code >> 15) & 1;
             if (kind == 1 && !with_c) continue;
@@ -757,10 +757,12 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                 double v[8][kRedGroups];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int q = q0 + u * 32 + lane;
+                    // unconditional loads (index clamped, store predicated) so all of them
+                    // are in flight together: one L2 round trip instead of one per entry
+                    const int q = min(q0 + u * 32 + lane, nq - 1);
 #pragma unroll
                     for (int g = 0; g < kRedGroups; ++g)
-                        v[u][g] = q < nq ? ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]) : 0.0;
+                        v[u][g] = ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -776,33 +778,70 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
         stamp(3);
         const int sl = (int)(b & 1);
         const double* dprev = delta + (size_t)(sl ^ 1) * 16;
+        // Lane j < Wb owns coordinate j.  Keep the step's pre-activation t_j and
+        // fold every correction into it with one DFMA:
+        //   Lasso: t = gamma = a - s/||a||^2,  alpha' = soft(t, lambda d/||a||^2)
+        //   SVM:   t = y a + (lambda n - y s)/||a||^2,  alpha' = y clip(t, 0, 1)
+        // s_j <- s_j + G_jk delta_k  becomes  t_j <- t_j + c_jk delta_k with
+        // c_jk = -G_jk/||a_j||^2 (Lasso) or -y_j G_jk/||a_j||^2 (SVM).
         int64_t jg = 0;
-        double a = 0, inv = 0, yy = 0, sj = 0, afin = 0;
-        bool zero = false;
+        double a = 0, t = 0, tau = 0, cy_ = 0, scale = 0, afin = 0;
+        bool zero = true;
         if (lane < Wb) {
             jg = cj[sl][lane];
             a = ca[sl][lane];
-            inv = cinv[sl][lane];
+            double inv = cinv[sl][lane];
             zero = inv < 0.0;
             if (zero) inv = 0.0;
-            yy = cy[sl][lane];
-            sj = sG[lane];
+            const double yy = cy[sl][lane];
+            double sj = sG[lane];
             if (b > 0)  // u was taken at the start of block b-1: add its effect
-                for (int k = 0; k < W; ++k) sj = fma(sG[scd_off_C(W) + lane * W + k], dprev[k], sj);
+                for (int k2 = 0; k2 < W; ++k2) sj = fma(sG[scd_off_C(W) + lane * W + k2], dprev[k2], sj);
+            if (MODEL == kLasso) {
+                t = a - sj * inv;
+                tau = lam_dn * inv;
+                scale = -inv;
+            } else {
+                t = fma(lam_dn - yy * sj, inv, yy * a);
+                cy_ = yy;
+                scale = -yy * inv;
+            }
         }
         double* dcur = delta + (size_t)sl * 16;
-        double grow[16];  // this lane's row of the block Gram, k < lane
+        // Stage every coordinate's t_j and scaled Gram row in shared memory, then let
+        // every lane run all Wb steps redundantly: no per-step cross-lane traffic
+        // (a shuffle per step queues behind the compute warps' shared-memory loads).
+        if (lane < 16) {
+            sT[lane] = t;
+            sP[lane] = MODEL == kLasso ? tau : cy_;
+            sZ[lane] = zero ? 1 : 0;
+            sA[lane] = a;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            grow[j] = (j < lane && lane < Wb) ? sG[scd_off_G(W) + lane * (lane - 1) / 2 + j] : 0.0;
+            for (int j = 0; j < 16; ++j)
+                sC[lane * 16 + j] = (j < lane && lane < Wb) ? scale * sG[scd_off_G(W) + lane * (lane - 1) / 2 + j] : 0.0;
+        }
+        __syncwarp();
+        double tq[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) tq[q] = sT[q];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             if (j >= Wb) break;
-            const double an = coord_step_inv(p.model, a, sj, inv, zero, yy, lam_dn);
+            const double aj = sA[j], pj = sP[j];
+            double an;
+            if (MODEL == kLasso) {
+                const double mag = fabs(tq[j]) - pj;
+                an = mag > 0.0 ? copysign(mag, tq[j]) : 0.0;
+                if (sZ[j]) an = 0.0;
+            } else {
+                const double u = tq[j] < 0.0 ? 0.0 : (tq[j] > 1.0 ? 1.0 : tq[j]);
+                an = sZ[j] ? pj : pj * u;
+            }
+            const double dl = an - aj;
             if (lane == j) afin = an;
-            const double dl = __shfl_sync(~0u, an - a, j);
-            sj = fma(grow[j], dl, sj);  // grow[j] = 0 unless j < lane < Wb
             if (lane == 0) dcur[j] = dl;
+#pragma unroll
+            for (int q = j + 1; q < 16; ++q) tq[q] = fma(sC[q * 16 + j], dl, tq[q]);
         }
         if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
         if (lane < Wb && c == 0) p.alpha[jg] = afin;
@@ -829,6 +868,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     };
 
     for (int q = tid; q < 2 * NRED; q += kScdThreads) acc[q] = 0.0;
+    unsigned long long w0tiles = 0;
     if (nblk > 0) {
         if (ctrl) {
             for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) {
@@ -862,14 +902,10 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             control(b);
             stamp(4);
         } else if (next) {
-            unsigned long long tw0 = (p.trace && tid == 0 && c == 0) ? gtimer() : 0;
             wait_data(b + 1);
-            unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? gtimer() : 0;
+            unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? (unsigned long long)clock64() : 0;
             tiles(b + 1, true);
-            if (p.trace && tid == 0 && c == 0) {
-                p.trace[7] += gtimer() - tw1;
-                (void)tw0;
-            }
+            if (p.trace && tid == 0 && c == 0) w0tiles += (unsigned long long)clock64() - tw1;
         }
         __syncthreads();
         stamp(6);
@@ -877,17 +913,23 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
         __syncthreads();
         stamp(1);
         if (next) arrive(b + 1);
-        if (!ctrl) vupdate(b, tid, kCompute * 32);  // the control warp fences/arrives meanwhile
+        if (!ctrl)  // the control warp fences/arrives meanwhile; the others share the rows
+            vupdate(b, tid < kCtrlWarp * 32 ? tid : tid - 32, kScdThreads - 32);
         __syncthreads();
         stamp(5);
     }
     for (int r = tid; r < rows; r += kScdThreads) p.vt[r0 + r] = vs[r];
+    if (tr)
+        for (int q = 0; q < 7; ++q) p.trace[(c == 0 ? 0 : 8) + q] += trc[q];
+    if (p.trace && tid == 0 && c == 0) p.trace[7] += w0tiles;
 }
 
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches) {
     if (p.L <= 0) return cudaSuccess;
     size_t smem = scd_smem_bytes(p.W, p.R, kScdStages);
-    const void* fn = p.exact ? (const void*)k_scd_gram<true> : (const void*)k_scd_gram<false>;
+    const void* fn = p.model == kLasso
+                         ? (p.exact ? (const void*)k_scd_gram<true, kLasso> : (const void*)k_scd_gram<false, kLasso>)
+                         : (p.exact ? (const void*)k_scd_gram<true, kSvm> : (const void*)k_scd_gram<false, kSvm>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     ScdParams q = p;
