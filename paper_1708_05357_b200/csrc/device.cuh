@@ -84,6 +84,16 @@ __device__ __forceinline__ double coord_gap(int model, double alpha, double s, d
     return (t1 + t2 - t3) / nn;
 }
 
+// ---------------------------------------------------------------- packed fp32 (sm_100 FFMA2)
+// c += a * b on two fp32 lanes with one instruction (fma.rn.f32x2).
+__device__ __forceinline__ void ffma2(float2& c, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%0, %1};\n\t"
+        "fma.rn.f32x2 rc, ra, rb, rc;\n\tmov.b64 {%0, %1}, rc;\n\t}"
+        : "+f"(c.x), "+f"(c.y)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -439,31 +439,53 @@ __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float*
                                       int W) {
     typedef typename std::conditional<EXACT, double, float>::type T;
     T g[4 * KW];
-#pragma unroll
-    for (int e = 0; e < 4 * KW; ++e) g[e] = T(0);
     const float4* xj[4];
     const float4* yk[KW];
 #pragma unroll
     for (int a = 0; a < 4; ++a) xj[a] = reinterpret_cast<const float4*>(Aj + (size_t)a * R);
 #pragma unroll
     for (int q = 0; q < KW; ++q) yk[q] = reinterpret_cast<const float4*>(Ak + (size_t)q * R);
-    for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
-        float4 x[4], y[KW];
+    if (EXACT) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) x[a] = xj[a][r4];
+        for (int e = 0; e < 4 * KW; ++e) g[e] = T(0);
+        for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
+            float4 x[4], y[KW];
 #pragma unroll
-        for (int q = 0; q < KW; ++q) y[q] = yk[q][r4];
+            for (int a = 0; a < 4; ++a) x[a] = xj[a][r4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+            for (int q = 0; q < KW; ++q) y[q] = yk[q][r4];
 #pragma unroll
-            for (int q = 0; q < KW; ++q) {
-                T acc = g[a * KW + q];
-                acc = fma((T)x[a].x, (T)y[q].x, acc);
-                acc = fma((T)x[a].y, (T)y[q].y, acc);
-                acc = fma((T)x[a].z, (T)y[q].z, acc);
-                acc = fma((T)x[a].w, (T)y[q].w, acc);
-                g[a * KW + q] = acc;
-            }
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int q = 0; q < KW; ++q) {
+                    T acc = g[a * KW + q];
+                    acc = fma((T)x[a].x, (T)y[q].x, acc);
+                    acc = fma((T)x[a].y, (T)y[q].y, acc);
+                    acc = fma((T)x[a].z, (T)y[q].z, acc);
+                    acc = fma((T)x[a].w, (T)y[q].w, acc);
+                    g[a * KW + q] = acc;
+                }
+        }
+    } else {  // packed: rows (r, r+1) and (r+2, r+3) of a lane's 4-row group in FFMA2 halves
+        float2 g2[4 * KW];
+#pragma unroll
+        for (int e = 0; e < 4 * KW; ++e) g2[e] = make_float2(0.f, 0.f);
+        for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
+            float4 x[4], y[KW];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) x[a] = xj[a][r4];
+#pragma unroll
+            for (int q = 0; q < KW; ++q) y[q] = yk[q][r4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int q = 0; q < KW; ++q) {
+                    ffma2(g2[a * KW + q], x[a].x, x[a].y, y[q].x, y[q].y);
+                    ffma2(g2[a * KW + q], x[a].z, x[a].w, y[q].z, y[q].w);
+                }
+        }
+#pragma unroll
+        for (int e = 0; e < 4 * KW; ++e) g[e] = (T)(g2[e].x + g2[e].y);
     }
     const double v = (double)reduce_scatter<T, 4 * KW>(g, lane);
     if (lane < 4 * KW) {
