@@ -330,19 +330,29 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
     {
         ProfScope ps(ctx, ctx->cst, 3, 0.0);
         const size_t col_bytes = (size_t)ctx->ld_dev * sizeof(float);
-        for (const auto& c : ctx->copy_plan) {
-            if (cudaMemcpyAsync(ctx->pool + (int64_t)c.slot * ctx->ld_dev, ctx->h_store + c.col * ctx->ld_host,
-                                col_bytes, cudaMemcpyHostToDevice, ctx->cst) != cudaSuccess) {
+        const size_t np = ctx->copy_plan.size();
+        for (size_t q = 0; q < np;) {
+            // maximal run of consecutive columns into consecutive slots with one sequence number
+            const auto& c0 = ctx->copy_plan[q];
+            size_t e = q + 1;
+            while (e < np && ctx->copy_plan[e].seq == c0.seq && ctx->copy_plan[e].col == c0.col + (int64_t)(e - q) &&
+                   ctx->copy_plan[e].slot == c0.slot + (int)(e - q) && ctx->ld_host == ctx->ld_dev)
+                ++e;
+            const size_t bytes = (e - q) * col_bytes;
+            if (cudaMemcpyAsync(ctx->pool + (int64_t)c0.slot * ctx->ld_dev, ctx->h_store + c0.col * ctx->ld_host,
+                                bytes, cudaMemcpyHostToDevice, ctx->cst) != cudaSuccess) {
                 rc = fail(ctx, DUHL_E_CUDA, "staging cudaMemcpyAsync failed");
                 break;
             }
-            ctx->h2d_bytes += (int64_t)col_bytes;
-            ps.bytes += (double)col_bytes;
-            if (ctx->write_value &&
-                ctx->write_value(ctx->cst, (unsigned long long)(uintptr_t)ctx->d_progress, c.seq, 0) != 0) {
+            ctx->h2d_bytes += (int64_t)bytes;
+            ps.bytes += (double)bytes;
+            const bool last_of_seq = e == np || ctx->copy_plan[e].seq != c0.seq;
+            if (ctx->write_value && last_of_seq &&
+                ctx->write_value(ctx->cst, (unsigned long long)(uintptr_t)ctx->d_progress, c0.seq, 0) != 0) {
                 rc = fail(ctx, DUHL_E_CUDA, "cuStreamWriteValue32 failed");
                 break;
             }
+            q = e;
         }
     }
     if (rc != DUHL_OK) {
@@ -397,18 +407,30 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         }
         if ((int64_t)news.size() > (int64_t)free_slots.size())
             return fail(ctx, DUHL_E_INVALID, "working set exceeds the HBM slot pool");
-        // plan the copies now (slot, sequence number); issue_staging enqueues them
+        // plan the copies now (slot, sequence number); issue_staging enqueues them.
+        // Light rounds: one copy per column in pass-0 order, a progress write every
+        // 4 columns, so the epoch starts at once.  Heavy rounds (more than half of P
+        // new): columns in index order with consecutive slots, so runs coalesce into
+        // large copies at full PCIe rate, and one progress write at the end.
+        const bool heavy = (int64_t)news.size() * 2 > m;
+        if (heavy) std::sort(news.begin(), news.end());
         size_t fi = 0;
-        for (int64_t j : news) {
+        const unsigned heavy_seq = ctx->write_value && heavy ? ctx->batch_seq + 1 : 0u;
+        for (size_t q = 0; q < news.size(); ++q) {
+            const int64_t j = news[q];
             const int s = free_slots[fi++];
             ctx->col_slot[j] = s;
             ctx->slot_col[s] = (int)j;
             ctx->pend_cols.push_back(j);
             ctx->pend_slots.push_back(s);
-            ctx->slot_batch[s] = ctx->write_value ? ++ctx->batch_seq : 0u;
-            ctx->copy_plan.push_back({j, s, ctx->slot_batch[s]});
+            unsigned seq = 0;
+            if (ctx->write_value) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
+            ctx->slot_batch[s] = seq;
+            ctx->copy_plan.push_back({j, s, seq});
             ++nsw;
         }
+        if (ctx->write_value && !news.empty())
+            ctx->batch_seq = heavy ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
