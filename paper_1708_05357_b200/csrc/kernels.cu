@@ -683,6 +683,12 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     // block inputs, waits on the grid barrier, reads the reduced block and runs
     // the W sequential closed-form steps -- concurrently with the tiles.
     const bool ctrl = warp == kCtrlWarp;
+    // producer (stage issue, block inputs): the spare warp 7 when the control warp
+    // has its own SMSP, else the control warp itself
+#ifndef DUHL_PROD_SPARE
+#define DUHL_PROD_SPARE 0
+#endif
+    const bool prod = (DUHL_CTRL_ALONE && DUHL_PROD_SPARE) ? warp == kScdWarps - 1 : ctrl;
     // compute-warp index (-1: none)
     const int cw = ctrl ? -1 : (DUHL_CTRL_ALONE ? (warp < 3 ? warp : (warp < 7 ? warp - 1 : -1)) : warp);
     // per-warp item lists, built once: item = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15
@@ -892,7 +898,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     for (int q = tid; q < 2 * NRED; q += kScdThreads) acc[q] = 0.0;
     unsigned long long w0tiles = 0;
     if (nblk > 0) {
-        if (ctrl) {
+        if (prod) {
             for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) {
                 prefetch_slot(q);
                 scd_issue(p, Abuf, mbar, q, r0, rows, lane, pf_slot, pf_need, seen);
@@ -901,7 +907,8 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             prefetch_coords(0);
             publish_coords(0);
             prefetch_coords(1);
-        } else {
+        }
+        if (!ctrl && !prod) {
             wait_data(0);
             tiles(0, false);
         }
@@ -912,7 +919,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     }
     for (int64_t b = 0; b < nblk; ++b) {
         const bool next = b + 1 < nblk;
-        if (ctrl) {
+        if (prod) {
             // stage of block b-1 was freed by the last V update: stream block b+2 into it
             if (next) publish_coords(b + 1);   // block b+1's inputs (prefetched last iteration)
             if (b + 2 < nblk) prefetch_coords(b + 2);
@@ -920,10 +927,12 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                 scd_issue(p, Abuf, mbar, b + 2, r0, rows, lane, pf_slot, pf_need, seen);
                 prefetch_slot(b + 3);
             }
+        }
+        if (ctrl) {
             stamp(0);
             control(b);
             stamp(4);
-        } else if (next) {
+        } else if (next && !prod) {
             wait_data(b + 1);
             unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? (unsigned long long)clock64() : 0;
             tiles(b + 1, true);
