@@ -355,6 +355,10 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
             q = e;
         }
     }
+    if (std::getenv("DUHL_STAGE_TRACE"))
+        std::fprintf(stderr, "issue_staging: %zu copies, seq %u..%u, batch_seq %u\n", ctx->copy_plan.size(),
+                     ctx->copy_plan.empty() ? 0u : ctx->copy_plan.front().seq,
+                     ctx->copy_plan.empty() ? 0u : ctx->copy_plan.back().seq, ctx->batch_seq);
     if (rc != DUHL_OK) {
         unsigned last = ctx->batch_seq;
         cudaMemcpy(ctx->d_progress, &last, sizeof(unsigned), cudaMemcpyHostToDevice);
@@ -561,6 +565,7 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
         cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_ref, cudaEventDisableTiming) != cudaSuccess)
         return bail(DUHL_E_CUDA);
+    if (preload_kernels() != cudaSuccess) return bail(DUHL_E_CUDA);  // no lazy loads mid-epoch
     // ---- unit A: pinned host store (column i at h_store + i*ld_host, rows d..d4 zero)
     const bool can_borrow = ctx->cfg.borrow_host && d % 4 == 0 && A->ld % 4 == 0 &&
                             ((uintptr_t)A->values % 16 == 0);
@@ -826,6 +831,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     }
     if (trace) {
         unsigned long long h[16];
+        TRY(issue_staging(ctx));  // the synchronize below must not starve a waiting epoch
         CK(cudaMemcpyAsync(h, dtr, sizeof(h), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         cudaFree(dtr);

@@ -1145,4 +1145,26 @@ cudaError_t launch_vec_sums(const double* vt, const double* b, int64_t d4, doubl
     return cudaGetLastError();
 }
 
+
+// Load every kernel of the library now.  Under lazy module loading (the CUDA 12
+// default) the first launch of a kernel loads it, and that load can wait for the
+// device to go idle -- fatal while the SCD kernel waits on staging copies the
+// host has yet to enqueue (the refresh kernel is launched in between).
+cudaError_t preload_kernels() {
+    const void* fns[] = {
+        (const void*)k_gap_tile,    (const void*)k_gap_finalize, (const void*)k_col_norms,
+        (const void*)k_topm,        (const void*)k_perm_order,   (const void*)k_order_info,
+        (const void*)k_scd_gram<true, kLasso>, (const void*)k_scd_gram<false, kLasso>,
+        (const void*)k_scd_gram<true, kSvm>,   (const void*)k_scd_gram<false, kSvm>,
+        (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
+        (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
+        (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums};
+    for (const void* f : fns) {
+        cudaFuncAttributes a;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace duhl

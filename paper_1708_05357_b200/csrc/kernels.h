@@ -76,6 +76,7 @@ cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigne
                               double* order_y, const double* alpha, const double* norms, const double* y,
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
+cudaError_t preload_kernels();
 cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int64_t d,
                           int64_t d4, const double* b, double* vt, cudaStream_t st,
                           int64_t* launches);

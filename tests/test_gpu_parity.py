@@ -4,6 +4,7 @@ seeded inputs (SURVEY 8(c) tolerances).
 Sizes: small enough for the oracle to finish in seconds, large enough to span
 several row tiles / CTAs / Gram blocks, with ragged tails (d % 4 != 0, m % W != 0).
 """
+import os
 import numpy as np
 import pytest
 
@@ -363,3 +364,16 @@ def test_shard_offsets_global_n(D):
         Ps.set_state(alpha[lo:hi])
         gs = Ps.gaps()
     np.testing.assert_allclose(gs, gf[lo:hi], rtol=1e-12, atol=1e-15)
+
+
+def test_first_solve_in_a_fresh_process():
+    """The staging overlap in a process whose kernels were never launched before:
+    the SCD epoch waits on copies that the host enqueues after launching the
+    refresh kernel, so no kernel may be lazily loaded in between (a lazy load
+    would wait for the device and starve the epoch)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import __graft_entry__ as g; g.smoke()")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
