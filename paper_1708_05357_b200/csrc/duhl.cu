@@ -111,6 +111,7 @@ struct duhl_ctx {
     // ---- staging overlapped with the SCD epoch
     typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
     WriteValue32 write_value = nullptr;  // cuStreamWriteValue32 via cudaGetDriverEntryPoint
+    bool overlap = false;  // this round's copies overlap the epoch (progress counter); else copies first
     unsigned* d_progress = nullptr;      // last landed staging copy (sequence number)
     unsigned batch_seq = 0;
     std::vector<unsigned> slot_batch;    // [S] sequence number of the copy that filled a slot
@@ -347,7 +348,7 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
             ctx->h2d_bytes += (int64_t)bytes;
             ps.bytes += (double)bytes;
             const bool last_of_seq = e == np || ctx->copy_plan[e].seq != c0.seq;
-            if (ctx->write_value && last_of_seq &&
+            if (ctx->overlap && last_of_seq &&
                 ctx->write_value(ctx->cst, (unsigned long long)(uintptr_t)ctx->d_progress, c0.seq, 0) != 0) {
                 rc = fail(ctx, DUHL_E_CUDA, "cuStreamWriteValue32 failed");
                 break;
@@ -365,7 +366,7 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
     }
     ctx->copy_plan.clear();
     cudaEventRecord(ctx->ev_copy, ctx->cst);
-    if (!ctx->write_value) cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0);
+    if (!ctx->overlap) cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0);
     return rc;
 }
 
@@ -419,7 +420,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         const bool heavy = (int64_t)news.size() * 2 > m;
         if (heavy) std::sort(news.begin(), news.end());
         size_t fi = 0;
-        const unsigned heavy_seq = ctx->write_value && heavy ? ctx->batch_seq + 1 : 0u;
+        const unsigned heavy_seq = ctx->overlap && heavy ? ctx->batch_seq + 1 : 0u;
         for (size_t q = 0; q < news.size(); ++q) {
             const int64_t j = news[q];
             const int s = free_slots[fi++];
@@ -428,17 +429,16 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             ctx->pend_cols.push_back(j);
             ctx->pend_slots.push_back(s);
             unsigned seq = 0;
-            if (ctx->write_value) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
+            if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
             ctx->slot_batch[s] = seq;
             ctx->copy_plan.push_back({j, s, seq});
             ++nsw;
         }
-        if (ctx->write_value && !news.empty())
+        if (ctx->overlap && !news.empty())
             ctx->batch_seq = heavy ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
-        if (!ctx->write_value) TRY(issue_staging(ctx));  // no overlap: copies first, compute waits
     } else {
         for (int64_t j : P) if (!ctx->inP[j]) ++nsw;  // logical swaps (everything is resident)
     }
@@ -782,6 +782,8 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
                         int64_t* n_swaps_out) {
     if (!ctx) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
+    TRY(finalize_staging(ctx));
+    ctx->overlap = ctx->write_value != nullptr;
     TRY(select_impl(ctx, policy, m, round, n_swaps_out));
     if (P_out) std::memcpy(P_out, ctx->P.data(), ctx->P.size() * sizeof(int64_t));
     return DUHL_OK;
@@ -809,12 +811,12 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.NB = ctx->NB;
     p.exact = ctx->cfg.scd_exact;
     p.red = ctx->d_red;
-    p.order_batch = ctx->write_value ? ctx->d_order_batch : nullptr;
+    p.order_batch = ctx->overlap ? ctx->d_order_batch : nullptr;
     p.err = ctx->d_flag + 1;
     p.order_a = ctx->d_order_a;
     p.order_inv = ctx->d_order_inv;
     p.order_y = ctx->d_order_y;
-    p.progress = ctx->write_value ? ctx->d_progress : nullptr;
+    p.progress = ctx->overlap ? ctx->d_progress : nullptr;
     p.bar = ctx->d_bar;
     CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_doubles(ctx->W) * sizeof(double), ctx->st));
     CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
@@ -853,19 +855,19 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     return DUHL_OK;
 }
 
-static duhl_status refresh_launch(duhl_ctx* ctx, int64_t kref);
-static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round, int64_t kref = 0) {
+// The epoch on the working set.  Staging copies planned by the last select are
+// enqueued after the pass-0 launch when they overlap it (the kernel waits on the
+// progress counter per block), else before it (the compute stream waits).
+static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
     const int64_t m = (int64_t)ctx->P.size();
+    if (!ctx->overlap) TRY(issue_staging(ctx));
     for (int pass = 0; pass < passes; ++pass) {
         CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
                              ctx->d_order_j, ctx->d_order_slot, ctx->d_order_batch, ctx->d_order_a,
                              ctx->d_order_inv, ctx->d_order_y, ctx->d_alpha, ctx->d_norms,
                              ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr, ctx->st, &ctx->launches));
         TRY(scd_launch(ctx, m));
-        if (pass == 0) {
-            TRY(refresh_launch(ctx, kref));  // unit A beside unit B (after the cooperative launch)
-            TRY(issue_staging(ctx));         // host enqueue of the staging copies overlaps pass 0
-        }
+        if (pass == 0) TRY(issue_staging(ctx));  // no-op unless overlapping: host enqueue overlaps pass 0
     }
     return DUHL_OK;
 }
@@ -888,6 +890,7 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
             slots[t] = ctx->col_slot[j];
             batches[t] = ctx->slot_batch[slots[t]];
         }
+        if (!ctx->overlap) TRY(issue_staging(ctx));
         CK(cudaMemcpyAsync(ctx->d_order_j, perm, perm_len * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_order_slot, slots.data(), perm_len * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_order_batch, batches.data(), perm_len * sizeof(unsigned),
@@ -1023,14 +1026,14 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
     return DUHL_OK;
 }
 
-// Unit-A refresh of the cursor chunk (columns in d_cols) against the v snapshot:
-// 1024-row tiles (8 KB of shared memory) so a CTA fits beside the SCD kernel's
-// CTA on every SM; PCIe-bound for non-resident columns.
+// Unit-A refresh of the cursor chunk (columns in d_cols) against the v snapshot,
+// on its own stream beside the staging copies; PCIe-bound (zero-copy reads) for
+// non-resident columns.
 static duhl_status refresh_launch(duhl_ctx* ctx, int64_t kref) {
     if (kref <= 0) return DUHL_OK;
     CK(cudaStreamWaitEvent(ctx->rst, ctx->ev_snap, 0));
     TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr, true, ctx->d_vsnap, ctx->rst,
-                 ctx->d_s_acc2, 1024));
+                 ctx->d_s_acc2));
     CK(cudaEventRecord(ctx->ev_ref, ctx->rst));
     return DUHL_OK;
 }
@@ -1045,6 +1048,11 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     static const bool htrace = std::getenv("DUHL_ROUND_TRACE") != nullptr;  // developer timing
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto tsel = now();
+    // Copies overlap the epoch only when unit A is idle: with a refresh, PCIe is
+    // shared by the staging copies and the zero-copy refresh reads, so both run
+    // first, side by side, and the epoch follows at full HBM rate.
+    TRY(finalize_staging(ctx));
+    ctx->overlap = ctx->write_value != nullptr && kref == 0;
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
     auto tstaged = now();
     std::vector<int64_t> idx(kref);
@@ -1054,20 +1062,22 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, (int64_t)ctx->P.size(), ctx->d_aold, ctx->st,
                              &ctx->launches));
     }
-    if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) from a snapshot of v, launched on its
-                     // own stream right after the SCD kernel (refresh_launch)
+    if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) on its own stream, beside the
+                     // staging copies; the epoch waits for it (it holds the SMs the
+                     // cooperative launch needs, and PCIe is the shared bound anyway)
         for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
         ctx->cursor = (ctx->cursor + kref) % n;
         CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         if (!agg)
             CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
+        TRY(refresh_launch(ctx, kref));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));
     }
     auto tlaunch = now();
-    TRY(scd_passes(ctx, passes, ctx->cfg.seed, t, kref));                   // l.6, l.11
+    TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
     TRY(finalize_staging(ctx));                                            // staged columns -> table
     auto tscd = now();
-    if (kref > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));         // join unit A
     double gamma = 1.0;
     if (agg) TRY(aggregate(ctx, &gamma));                                   // l.11 across ranks
     const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
