@@ -36,6 +36,9 @@ HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 CONFIGS = {
     # name: model, d, n, budget fraction of data (0 = all resident), m, lambda (None: 1/n), label
+    "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07,
+               label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "
+                     "(32.1 GB pinned host), HBM budget 25% (8.03 GB), m=50176, lambda=0.07 lambda_max"),
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None,
                label="C4: hinge-SVM dual, ImageNet-shaped dense synthetic 200704 features x 40000 "
                      "samples fp32 (32.1 GB pinned host), HBM budget 25% (8.03 GB), m=10000"),
@@ -129,8 +132,37 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
 
 
+def pcie_h2d_peak(local):
+    """Measured copy-engine H2D bandwidth of this box (1 GiB pinned -> HBM, best of 5)."""
+    import torch
+    x = torch.empty(1 << 28, dtype=torch.float32).pin_memory()
+    g = torch.empty(1 << 28, dtype=torch.float32, device=f"cuda:{local}")
+    best = 0.0
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.copy_(x, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, x.numel() * 4 / (a.elapsed_time(b) / 1e3) / 1e9)
+    del x, g
+    return best
+
+
 # ------------------------------------------------------------------ data
-def make_data(cfg, seed, col_lo=0, col_hi=None):
+def _allreduce_host(x, world, op="sum"):
+    """Sum / max of a host float64 array over the ranks (set-up only, not timed)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
+def make_data(cfg, seed, col_lo=0, col_hi=None, world=1):
+    """The columns [col_lo, col_hi) of the config's matrix and the (global) labels."""
     import synth
     d, n = cfg["d"], cfg["n"]
     col_hi = n if col_hi is None else col_hi
@@ -139,12 +171,20 @@ def make_data(cfg, seed, col_lo=0, col_hi=None):
         lab = synth.svm_fill(A, d, n, seed, col_lo=col_lo)
     else:
         synth.lasso_fill(A, d, n, seed, col_lo=col_lo)
-        lab = synth.lasso_labels(A, d, seed)
+        sig = synth.lasso_signal(A, d, seed, col_lo=col_lo, n_total=n)
+        lab = synth.lasso_finish(_allreduce_host(sig, world), d, seed)
     return A, lab
 
 
-def lam_of(cfg):
-    return cfg["lam"] if cfg["lam"] is not None else 1.0 / cfg["n"]
+def lam_of(cfg, A=None, lab=None, world=1):
+    """lambda: given, 1/n (SVM), or lam_rel * lambda_max with lambda_max = ||A^T b||_inf / d."""
+    if cfg["lam"] is not None:
+        return cfg["lam"]
+    if cfg.get("lam_rel") is None:
+        return 1.0 / cfg["n"]
+    s = np.abs(A @ lab.astype(np.float32)).max()
+    lmax = float(_allreduce_host(np.array([s], dtype=np.float64), world, "max")[0]) / cfg["d"]
+    return cfg["lam_rel"] * lmax
 
 
 # ------------------------------------------------------------------ oracle arm
@@ -178,7 +218,7 @@ def run_reference(args, cfg, rank, world):
     seed = 170805357 + 3
     ncols = args.ref_cols
     A, lab = make_data(cfg, seed, 0, ncols) if cfg["model"] == 1 else make_data(cfg, seed)
-    lam = lam_of(cfg)
+    lam = lam_of(cfg, A, lab)
     for _ in range(args.warmup):
         oracle_sample(cfg, A, lab, lam, min(ncols, 64))
     vals, secs = [], 0.0
@@ -208,11 +248,11 @@ def run_duhl(args, cfg, rank, world, local):
     torch.cuda.set_device(local)
     seed = 170805357 + 3
     d, n = cfg["d"], cfg["n"]
-    lam = lam_of(cfg)
     # CoCoA-style sharding of the columns across ranks (one block per rank)
     lo, hi = rank * n // world, (rank + 1) * n // world
     t_gen = time.perf_counter()
-    A, lab = make_data(cfg, seed, lo, hi)
+    A, lab = make_data(cfg, seed, lo, hi, world)
+    lam = lam_of(cfg, A, lab, world)
     t_gen = time.perf_counter() - t_gen
     col_bytes = ((d + 3) // 4) * 16
     # strong scaling: the aggregate budget and working set stay those of the config
@@ -220,7 +260,7 @@ def run_duhl(args, cfg, rank, world, local):
     m = cfg["m"] // world
     common = dict(hbm_budget_bytes=budget, m=m, device=local, refresh_fraction=args.refresh,
                   seed=seed, borrow_host=True, n_global=n, col_offset=lo,
-                  linesearch=world > 1 or args.linesearch)
+                  linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas)
     uid = None
     if world > 1:  # NCCL group for the dv allreduce: id from rank 0, broadcast by torch.distributed
         import torch.distributed as dist
@@ -257,6 +297,16 @@ def run_duhl(args, cfg, rank, world, local):
     barrier(world)
     elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3, world)
     c1 = P.counters()
+    pcie_peak = pcie_h2d_peak(local)
+    pcie_bytes = (c1["h2d_bytes"] - c0["h2d_bytes"] + c1["zc_bytes"] - c0["zc_bytes"]) / args.steps
+    pcie = {"bytes_per_step": pcie_bytes,
+            "copy_bytes_per_step": (c1["h2d_bytes"] - c0["h2d_bytes"]) / args.steps,
+            "zero_copy_bytes_per_step": (c1["zc_bytes"] - c0["zc_bytes"]) / args.steps,
+            "achieved_GBps": pcie_bytes / (elapsed / args.steps) / 1e9,
+            "peak_GBps": pcie_peak, "frac": pcie_bytes / (elapsed / args.steps) / 1e9 / pcie_peak,
+            "note": "the step's binding resource when the working set changes: staging copies + "
+                    "unit-A zero-copy refresh reads over PCIe; peak = 1 GiB pinned H2D copy measured "
+                    "in this run"}
     k1 = {k: P.kernel_stats(k) for k in range(5)}
     # kernel-only SCD roofline: extra passes over the working set now resident in HBM
     # (no staging waits inside the launch), outside the timed region
@@ -312,6 +362,7 @@ def run_duhl(args, cfg, rank, world, local):
         rounds = max(1, r["rounds"])
         e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
                "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
+               "zero_copy_bytes_per_step": int(c2["zc_bytes"] / rounds),
                "d2h_bytes_per_step": int(m * 8 + 64),
                "time_to_eps_s": max_over_ranks(t_solve, world), "eps": args.eps,
                "certified_gap": g_final, "create_plus_solve_s": wall,
@@ -319,7 +370,8 @@ def run_duhl(args, cfg, rank, world, local):
                "note": "value = updates / (duhl_create from host buffers (pin in place, norms, z at "
                        "alpha=0 over PCIe) + duhl_solve to the certified gap); time_to_eps_s = "
                        "duhl_solve alone (data resident in pinned host memory, cold HBM fill "
-                       "included); h2d = cold fill + swaps (memcpy), zero-copy refresh reads not counted"}
+                       "included); h2d = cold fill + swaps (memcpy); zero-copy = refresh + certificate reads of "
+                       "non-resident columns"}
 
     # ---------------- baselines: same library, budget and kernels, batch selection
     # sequential blocks [Yu 2012] / uniform instead of gap top-m
@@ -366,6 +418,7 @@ def run_duhl(args, cfg, rank, world, local):
                        if budget else "working set may be L2-resident (small config)",
                        "parallelism": f"cocoa{world}"},
             "roofline": roofline,
+            "pcie": pcie,
             "roofline_scd_kernel_only": {"bound": "hbm", "kernel": "k_scd_gram", "unit": "GB/s",
                                          "achieved": ko_bytes / (ko_ms / 1e3) / 1e9,
                                          "peak": peak, "frac": ko_bytes / (ko_ms / 1e3) / 1e9 / peak,
@@ -406,6 +459,8 @@ def main():
                     help="also time the sequential / uniform batch baselines to eps (capped rounds)")
     ap.add_argument("--baseline-rounds", type=int, default=600)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--unit-a-ctas", type=int, default=0,
+                    help="CTAs of the unit-A refresh beside the epoch (0 auto, -1 off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     rank, world, local = dist_init(args.gpus)

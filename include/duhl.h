@@ -85,6 +85,10 @@ typedef struct {
     int64_t col_offset;       /* multi-GPU: global index of this shard's first column */
     int linesearch;           /* 1: exact line search on the aggregation weight gamma in [0,1] after each
                                  round's epoch; 0: gamma = 1 (Alg. 2 l.11) */
+    int unit_a_ctas;          /* unit-A refresh beside the epoch: CTAs of its persistent gap kernel; the
+                                 SCD grid leaves them their SMs.  0 = auto (16 when the data exceeds the
+                                 budget and refresh_fraction > 0), -1 = off (the refresh runs on the
+                                 whole GPU before the epoch) */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -101,7 +105,7 @@ typedef struct {
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,
  * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0,
  * cert_adaptive 1, profile 0, scd_exact 1, n_global 0, col_offset 0,
- * linesearch 0. */
+ * linesearch 0, unit_a_ctas 0. */
 void duhl_default_config(duhl_config* cfg);
 
 /* Creates a problem instance.
@@ -203,10 +207,12 @@ duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out);
 duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
                                   double* bytes);
 
-/* Counters since creation: kernel launches issued, bytes copied host->device,
- * SCD coordinate updates.  Any may be NULL. */
+/* Counters since creation: kernel launches issued, bytes copied host->device
+ * (copy engine: cold fill + swaps), bytes the gap kernels read from pinned host
+ * memory over PCIe (zero-copy: unit-A refresh + certificates of non-resident
+ * columns, 4 d4 per column), SCD coordinate updates.  Any may be NULL. */
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes,
-                              int64_t* updates);
+                              int64_t* zc_bytes, int64_t* updates);
 
 const char* duhl_last_error(const duhl_ctx* ctx);
 

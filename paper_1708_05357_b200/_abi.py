@@ -35,7 +35,8 @@ class Config(C.Structure):
                 ("scd_block", C.c_int), ("scd_ctas", C.c_int), ("refresh_fraction", C.c_double),
                 ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
                 ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
-                ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int)]
+                ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int),
+                ("unit_a_ctas", C.c_int)]
 
 
 class RoundRecord(C.Structure):
@@ -77,7 +78,7 @@ def lib():
         L.duhl_get_state.argtypes = [_P, _P, _P, _P]
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
-        L.duhl_get_counters.argtypes = [_P, _P, _P, _P]
+        L.duhl_get_counters.argtypes = [_P, _P, _P, _P, _P]
         L.duhl_last_error.argtypes = [_P]
         L.duhl_last_error.restype = C.c_char_p
         for f in FUNCTIONS:
@@ -206,15 +207,15 @@ class Problem:
         return s.value
 
     def counters(self):
-        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
-        self._check(lib().duhl_get_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
-        return dict(launches=a.value, h2d_bytes=b.value, updates=c.value)
+        a, b, z, c = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().duhl_get_counters(self._h, C.byref(a), C.byref(b), C.byref(z), C.byref(c)))
+        return dict(launches=a.value, h2d_bytes=b.value, zc_bytes=z.value, updates=c.value)
 
 
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
            cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
-           linesearch=False):
+           linesearch=False, unit_a_ctas=0):
     """duhl_create.  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -228,7 +229,8 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          refresh_fraction=refresh_fraction, cert_every=cert_every, seed=seed,
                          borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
                          profile=int(bool(profile)), scd_exact=int(bool(scd_exact)),
-                         n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)))
+                         n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)),
+                         unit_a_ctas=unit_a_ctas)
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

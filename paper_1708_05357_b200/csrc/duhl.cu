@@ -70,7 +70,7 @@ struct duhl_ctx {
     double lambda = 0, B = 0;
     duhl_config cfg{};
     std::string err;
-    int dev = 0, nsm = 0;
+    int dev = 0, nsm = 0, unit_a_ctas = 0;
     cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
     cudaEvent_t ev_copy = nullptr, ev_snap = nullptr, ev_ref = nullptr;
     // ---- unit A: pinned host store
@@ -100,7 +100,7 @@ struct duhl_ctx {
     unsigned* d_bar = nullptr;
     int W = 0, R = 0, G = 0, NB = 2;
     // ---- misc
-    int64_t launches = 0, h2d_bytes = 0, updates = 0, cursor = 0;
+    int64_t launches = 0, h2d_bytes = 0, zc_bytes = 0, updates = 0, cursor = 0;
     // ---- profiling (cfg.profile): CUDA-event pairs per launch, harvested at sync points
     struct Timed { cudaEvent_t a, b; int kind; double bytes; };
     std::vector<Timed> pending;
@@ -257,7 +257,7 @@ static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
 static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, double* gap_out,
                             double* s_out, double* sums, bool write_z = true,
                             const double* vt_override = nullptr, cudaStream_t stream = nullptr,
-                            double* s_acc = nullptr, int tile_rows = kGapTileRows) {
+                            double* s_acc = nullptr, int tile_rows = kGapTileRows, int max_ctas = 0) {
     cudaStream_t sx = stream ? stream : ctx->st;
     GapParams p = gap_params(ctx, d_cols, d_cols ? k : ctx->n);
     if (vt_override) p.vt = vt_override;
@@ -268,7 +268,7 @@ static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, dou
     if (s_acc) p.s_acc = s_acc;
     const int64_t tiles = (ctx->d4 + tile_rows - 1) / tile_rows;
     ProfScope ps(ctx, sx, stream ? 4 : 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
-    CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches));
+    CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches, max_ctas));
     return DUHL_OK;
 }
 
@@ -491,8 +491,10 @@ static void free_all(duhl_ctx* ctx) {
 // W = coordinates per Gram block, largest multiple of 4 (<= 32) whose
 // double-buffered stage fits in shared memory.
 static void choose_scd_shape(duhl_ctx* ctx) {
-    int64_t G = ctx->cfg.scd_ctas > 0 ? ctx->cfg.scd_ctas
-                                      : std::min<int64_t>(ctx->nsm, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
+    // the unit-A refresh grid keeps its SMs while the epoch runs
+    const int64_t sms = std::max<int64_t>(1, ctx->nsm - std::max(0, ctx->unit_a_ctas));
+    int64_t G = ctx->cfg.scd_ctas > 0 ? std::min<int64_t>(ctx->cfg.scd_ctas, sms)
+                                      : std::min<int64_t>(sms, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
     int64_t R = round4((ctx->d4 + G - 1) / G);
     G = (ctx->d4 + R - 1) / R;
     // W <= 16 coordinates per block; 3 TMA stages of W column slices must fit in
@@ -664,6 +666,9 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
               dmal((void**)&ctx->d_sums, 8 * sizeof(double)) &&
               dmal((void**)&ctx->d_flag, 4 * sizeof(int));
     if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
+    ctx->unit_a_ctas = ctx->cfg.unit_a_ctas > 0 ? std::min(ctx->cfg.unit_a_ctas, ctx->nsm / 2)
+                       : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 &&
+                          ctx->cfg.refresh_fraction > 0.0) ? 16 : 0;
     choose_scd_shape(ctx);
     if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
         !dmal((void**)&ctx->d_bar, 64))
@@ -912,6 +917,9 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
 
 static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, double* dual) {
     CK(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), ctx->st));
+    int64_t resident = 0;
+    for (int64_t s = 0; s < ctx->S; ++s) resident += ctx->slot_col[s] >= 0;
+    ctx->zc_bytes += (ctx->n - resident) * ctx->ld_dev * (int64_t)sizeof(float);
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
     TRY(allreduce(ctx, ctx->d_sums, 3));           // per-column sums over the shards
     TRY(allreduce(ctx, ctx->d_sums + 3, 1, ncclMax));
@@ -1033,7 +1041,7 @@ static duhl_status refresh_launch(duhl_ctx* ctx, int64_t kref) {
     if (kref <= 0) return DUHL_OK;
     CK(cudaStreamWaitEvent(ctx->rst, ctx->ev_snap, 0));
     TRY(run_gaps(ctx, ctx->d_cols, kref, nullptr, nullptr, nullptr, true, ctx->d_vsnap, ctx->rst,
-                 ctx->d_s_acc2));
+                 ctx->d_s_acc2, kGapTileRows, ctx->unit_a_ctas));
     CK(cudaEventRecord(ctx->ev_ref, ctx->rst));
     return DUHL_OK;
 }
@@ -1063,21 +1071,28 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
                              &ctx->launches));
     }
     if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) on its own stream, beside the
-                     // staging copies; the epoch waits for it (it holds the SMs the
-                     // cooperative launch needs, and PCIe is the shared bound anyway)
-        for (int64_t q = 0; q < kref; ++q) idx[q] = (ctx->cursor + q) % n;
+                     // staging copies and (unit_a_ctas > 0) the epoch on the remaining SMs;
+                     // otherwise the epoch waits for it (it would hold the SMs the
+                     // cooperative launch needs)
+        int64_t host_cols = 0;
+        for (int64_t q = 0; q < kref; ++q) {
+            idx[q] = (ctx->cursor + q) % n;
+            host_cols += ctx->col_slot[idx[q]] < 0;
+        }
+        ctx->zc_bytes += host_cols * ctx->ld_dev * (int64_t)sizeof(float);
         ctx->cursor = (ctx->cursor + kref) % n;
         CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         if (!agg)
             CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
         TRY(refresh_launch(ctx, kref));
-        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));
+        if (ctx->unit_a_ctas <= 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));
     }
     auto tlaunch = now();
     TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
     TRY(finalize_staging(ctx));                                            // staged columns -> table
     auto tscd = now();
+    if (kref > 0 && ctx->unit_a_ctas > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));  // join unit A
     double gamma = 1.0;
     if (agg) TRY(aggregate(ctx, &gamma));                                   // l.11 across ranks
     const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
@@ -1237,10 +1252,12 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
     return DUHL_OK;
 }
 
-duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes, int64_t* updates) {
+duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes, int64_t* zc_bytes,
+                              int64_t* updates) {
     if (!ctx) return DUHL_E_INVALID;
     if (launches) *launches = ctx->launches;
     if (h2d_bytes) *h2d_bytes = ctx->h2d_bytes;
+    if (zc_bytes) *zc_bytes = ctx->zc_bytes;
     if (updates) *updates = ctx->updates;
     return DUHL_OK;
 }

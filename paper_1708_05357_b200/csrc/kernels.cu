@@ -97,19 +97,28 @@ __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
     }
 }
 
-__global__ void __launch_bounds__(kGapThreads) k_gap_tile(GapParams p, int tile_rows, int ntiles) {
+// Work item vb = (column group vb % ngroups, row tile vb / ngroups); a grid
+// smaller than the item count loops (a persistent unit-A grid beside the SCD epoch).
+__global__ void __launch_bounds__(kGapThreads) k_gap_tile(GapParams p, int tile_rows, int ntiles, int64_t ngroups) {
     extern __shared__ double ws[];
-    const int64_t r0 = (int64_t)blockIdx.y * tile_rows;
-    const int rows = (int)imin64(tile_rows, p.d4 - r0);  // multiple of 4
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) ws[r] = p.vt[r0 + r] * p.wscale;
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t t0 = (int64_t)blockIdx.x * kGapColsPerCta;
-    const int64_t t1 = imin64(p.k, t0 + kGapColsPerCta);
-    const int nv = rows >> 2;
     const double2* w2 = reinterpret_cast<const double2*>(ws);
     SumAcc acc;
     int flag = 0;
+    int64_t cur_tile = -1;
+    for (int64_t vb = blockIdx.x; vb < ngroups * ntiles; vb += gridDim.x) {
+    const int64_t tile = vb / ngroups;
+    const int64_t r0 = tile * tile_rows;
+    const int rows = (int)imin64(tile_rows, p.d4 - r0);  // multiple of 4
+    if (tile != cur_tile) {
+        __syncthreads();
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) ws[r] = p.vt[r0 + r] * p.wscale;
+        __syncthreads();
+        cur_tile = tile;
+    }
+    const int64_t t0 = (vb % ngroups) * kGapColsPerCta;
+    const int64_t t1 = imin64(p.k, t0 + kGapColsPerCta);
+    const int nv = rows >> 2;
     for (int64_t t = t0 + warp; t < t1; t += nw) {
         const int64_t i = p.cols ? p.cols[t] : t;
         const float4* a = reinterpret_cast<const float4*>(col_ptr(p.src, i) + r0);
@@ -144,6 +153,7 @@ __global__ void __launch_bounds__(kGapThreads) k_gap_tile(GapParams p, int tile_
             else atomicAdd(&p.s_acc[t], s);
         }
     }
+    }
     if (ntiles == 1) block_flush_sums(p, acc, flag);
 }
 
@@ -159,13 +169,19 @@ __global__ void __launch_bounds__(kGapThreads) k_gap_finalize(GapParams p) {
     block_flush_sums(p, acc, flag);
 }
 
-cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches) {
+cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches, int max_ctas) {
     if (p.k <= 0) return cudaSuccess;
     int ntiles = (int)cdiv(p.d4, tile_rows);
     if (ntiles == 1) tile_rows = (int)p.d4;
-    dim3 grid((unsigned)cdiv(p.k, kGapColsPerCta), (unsigned)ntiles);
+    const int64_t ngroups = cdiv(p.k, kGapColsPerCta);
+    int64_t items = ngroups * ntiles;
+    if (max_ctas > 0 && items > max_ctas) items = max_ctas;
     size_t smem = (size_t)tile_rows * sizeof(double);
-    k_gap_tile<<<grid, kGapThreads, smem, st>>>(p, tile_rows, ntiles);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_gap_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_gap_tile<<<(unsigned)items, kGapThreads, smem, st>>>(p, tile_rows, ntiles, ngroups);
     ++*launches;
     if (ntiles > 1) {
         k_gap_finalize<<<(unsigned)cdiv(p.k, kGapThreads), kGapThreads, 0, st>>>(p);

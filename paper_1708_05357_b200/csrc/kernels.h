@@ -62,7 +62,8 @@ __host__ __device__ int scd_nred(int W);
 size_t scd_red_doubles(int W);  // size of ScdParams::red
 size_t scd_smem_bytes(int W, int R, int NB);
 
-cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches);
+cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches,
+                            int max_ctas = 0);
 cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* norms,
                              cudaStream_t st, int64_t* launches);
 cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,

@@ -149,17 +149,28 @@ def lasso_truth(n: int, seed: int, support: float = 0.1):
     return at
 
 
-def lasso_labels(A: np.ndarray, d: int, seed: int, support: float = 0.1, noise: float = 0.1):
-    """b = A alpha_true + noise N(0,1), rescaled to ||b||^2 = d (normalised data, reading R12)."""
-    n = A.shape[0]
-    at = lasso_truth(n, seed, support)
-    nz = np.nonzero(at)[0]
+def lasso_signal(A: np.ndarray, d: int, seed: int, support: float = 0.1, col_lo: int = 0,
+                 n_total: int | None = None) -> np.ndarray:
+    """A_shard alpha_true[shard] for the columns [col_lo, col_lo + len(A)) of an
+    n_total-column problem (fp64 accumulation in column order)."""
+    n_total = A.shape[0] + col_lo if n_total is None else n_total
+    at = lasso_truth(n_total, seed, support)[col_lo:col_lo + A.shape[0]]
     b = np.zeros(d)
-    for i in nz:
+    for i in np.nonzero(at)[0]:
         b += at[i] * A[i, :d].astype(np.float64)
-    b += noise * _rng(seed, 0, stream=3).standard_normal(d)
+    return b
+
+
+def lasso_finish(signal: np.ndarray, d: int, seed: int, noise: float = 0.1) -> np.ndarray:
+    """b = signal + noise N(0,1), rescaled to ||b||^2 = d (normalised data, reading R12)."""
+    b = signal + noise * _rng(seed, 0, stream=3).standard_normal(d)
     b *= math.sqrt(d) / np.linalg.norm(b)
     return b
+
+
+def lasso_labels(A: np.ndarray, d: int, seed: int, support: float = 0.1, noise: float = 0.1):
+    """b = A alpha_true + noise N(0,1), rescaled to ||b||^2 = d (normalised data, reading R12)."""
+    return lasso_finish(lasso_signal(A, d, seed, support), d, seed, noise)
 
 
 def lasso_dense(d: int, n: int, seed: int = SEED0, corr: float = 0.0, support: float = 0.1,
