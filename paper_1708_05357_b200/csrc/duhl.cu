@@ -242,8 +242,12 @@ static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
     const int flag = fl[0];
     if (fl[1]) {
         CK(cudaMemsetAsync(ctx->d_flag + 1, 0, sizeof(int), ctx->st));
-        return fail(ctx, DUHL_E_CUDA, std::string(where) + (fl[1] & 1 ? ": staging copy wait timed out"
-                                                                      : ": grid barrier timed out"));
+        // bits: 1 staging copy, 2 grid barrier, 4 stage-free, 8 stage-data, 16 delta (SCD kernel waits)
+        std::string what;
+        const char* nm[5] = {"staging copy", "grid barrier", "stage-free", "stage-data", "delta"};
+        for (int k = 0; k < 5; ++k)
+            if (fl[1] & (1 << k)) what += std::string(what.empty() ? "" : ", ") + nm[k];
+        return fail(ctx, DUHL_E_CUDA, std::string(where) + ": " + what + " wait timed out");
     }
     if (flag) {
         CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->st));
@@ -848,8 +852,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         const double cyc_per_us = clk_khz > 0 ? clk_khz / 1e3 : 1965.0;
         std::fprintf(stderr, "scd trace (us/block at %.0f MHz) W=%d G=%d R=%d: ", cyc_per_us, ctx->W, ctx->G,
                      ctx->R);
-        const char* nm[8] = {"ctl:issue", "flush", "ctl:WAIT", "ctl:sGread", "ctl:seq", "vupdate", "join",
-                             "w0:tiles"};
+        const char* nm[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
+                             "cmp:vupdate", "cmp:tiles"};
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
             for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / cyc_per_us);

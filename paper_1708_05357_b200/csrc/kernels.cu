@@ -398,11 +398,14 @@ constexpr int kScdWarps = kScdThreads / 32;
 constexpr int kScdStages = 3;
 constexpr int kRedBufs = 6;     // rotating reduction buffers (see the zeroing rule below)
 #ifndef DUHL_RED_GROUPS
-#define DUHL_RED_GROUPS 2
+#define DUHL_RED_GROUPS 1
 #endif
 constexpr int kRedGroups = DUHL_RED_GROUPS;  // CTA c adds into group c % kRedGroups ...
-constexpr int kRedStride = 32;  // ... one 256-byte line per (entry, group): spreads the fp64
-                                // atomics of 148 CTAs over many L2 slices
+#ifndef DUHL_RED_STRIDE
+#define DUHL_RED_STRIDE 4
+#endif
+constexpr int kRedStride = DUHL_RED_STRIDE;  // ... one 32-byte sector per (entry, group): the fp64
+                                // atomics of 148 CTAs spread over sectors, the read-back over few lines
 
 // Reduction entries of a block of W coordinates:
 //   u_j   = a_j^T v_(block start)           [0, W)
@@ -418,7 +421,6 @@ size_t scd_smem_bytes(int W, int R, int NB) {
     size_t off = 128;                                                             // mbarriers
     off += align_up_dev((size_t)kScdStages * W * R * sizeof(float));              // A stages
     off += align_up_dev((size_t)R * sizeof(double));                              // v slice
-    off += align_up_dev((size_t)2 * scd_nred(W) * sizeof(double));                // CTA partials (2 halves)
     off += align_up_dev((size_t)scd_nred(W) * sizeof(double));                    // reduced block
     off += align_up_dev((size_t)2 * 16 * sizeof(double));                         // deltas (2 blocks)
     return off;
@@ -449,9 +451,19 @@ __device__ __forceinline__ T reduce_scatter(T (&g)[N], int lane) {
 // element (a, q) -> row j = jbase + a, column k = kbase + q of G (LOWER, kept
 // where k < j) or C.  EXACT: fp64 products/accumulation (fp32 -> fp64 exact);
 // fast: fp32 FFMA inside the warp, fp64 from the warp reduction on.
+// Where a tile's reduced entries go: fp64 REDs into the block's rotating
+// reduction buffer, group grp (see kRedGroups), one 256-byte line per entry.
+struct RedOut {
+    double* buf;
+    int grp;
+    __device__ __forceinline__ void add(int q, double v) const {
+        atomicAdd(&buf[((size_t)q * kRedGroups + grp) * kRedStride], v);
+    }
+};
+
 template <bool EXACT, int KW, bool LOWER>
 __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float* __restrict__ Ak, int R,
-                                      int lo, int hi, int lane, int jbase, int kbase, double* out,
+                                      int lo, int hi, int lane, int jbase, int kbase, const RedOut& out,
                                       int W) {
     typedef typename std::conditional<EXACT, double, float>::type T;
     T g[4 * KW];
@@ -507,16 +519,16 @@ __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float*
     if (lane < 4 * KW) {
         const int j = jbase + lane / KW, k = kbase + lane % KW;
         if (LOWER) {
-            if (k < j) out[scd_off_G(W) + j * (j - 1) / 2 + k] = v;
+            if (k < j) out.add(scd_off_G(W) + j * (j - 1) / 2 + k, v);
         } else {
-            out[scd_off_C(W) + j * W + k] = v;
+            out.add(scd_off_C(W) + j * W + k, v);
         }
     }
 }
 
 // u tile: 4 x 1 against the fp64 v slice (always fp64)
 __device__ __forceinline__ void utile(const float* __restrict__ Aj, const double* __restrict__ vs, int R,
-                                      int lo, int hi, int lane, int jbase, double* out) {
+                                      int lo, int hi, int lane, int jbase, const RedOut& out) {
     double g[4] = {0.0, 0.0, 0.0, 0.0};
     const double2* v2 = reinterpret_cast<const double2*>(vs);
     for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
@@ -533,7 +545,7 @@ __device__ __forceinline__ void utile(const float* __restrict__ Aj, const double
         }
     }
     const double v = reduce_scatter<double, 4>(g, lane);
-    if (lane < 4) out[jbase + lane] = v;
+    if (lane < 4) out.add(jbase + lane, v);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -580,49 +592,52 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
 }
 
 // =====================================================================================
-// k_scd_gram: exact sequential SCD epoch, Gram-block form, barrier off the
-// critical path.  Iteration b (blocks b and b+1 resident, b+2 streaming in):
-//   A. partials of block b+1 over the CTA's rows: G_{b+1} (lower), the cross
-//      Gram C_{b+1,b} = A_{b+1}^T A_b and u_{b+1} = A_{b+1}^T v_b (v_b = v at
-//      the start of block b) -> atomics into red[(b+1) % 6] -> ARRIVE(b+1)
-//   B. WAIT(b) (arrived one full phase earlier) -> every CTA redundantly runs
-//      the W closed-form steps of block b in order with
+// k_scd_gram: exact sequential SCD epoch, Gram-block form, warp-specialised.
+// Per block b of W coordinates (in visiting order):
+//   compute warps (6): v_slice += A_{b-1} delta^{(b-1)} (the previous block's
+//      update), then the partials of block b+1 over the CTA's rows -- G_{b+1}
+//      (lower), the cross Gram C_{b+1,b} = A_{b+1}^T A_b and u_{b+1} = A_{b+1}^T v_b
+//      (v_b = v at the start of block b) -- REDed straight from the tile registers
+//      into red[(b+1) % 6]; the last warp done ARRIVEs(b+1) on the grid barrier.
+//   control warp: WAIT(b) (arrived while block b-1 was being solved) -> reads the
+//      reduced block -> runs the W closed-form steps in order with
 //        s_j = u_j + sum_k C_jk delta^{(b-1)}_k + sum_{k<j} G_jk delta_k
 //      (== a_j^T v at the moment coordinate j is visited: exactly sequential SCD)
-//   C. v_slice += A_b delta^{(b)}; stage of block b streams block b+3.
-// Zeroing rule: CTA 0 zeroes red[(b+4) % 6] right after WAIT(b); all reads of
-// it (phase B of block b-2) precede everyone's ARRIVE(b), and its next writer
-// (phase A of iteration b+3) waits on ARRIVE(b+2), which CTA 0 issues after
-// zeroing.
+//      -> publishes delta^{(b)} (mbarrier dfull[b & 1]).
+//   producer warp: streams block b+3 into the stage block b freed (mbarrier
+//      empty[] per stage, TMA bulk copies completing on full[]).
+// The control chain (read + steps) and the compute chain (update + tiles) of
+// consecutive blocks overlap; the grid barrier's latency hides behind both.
+// Zeroing rule: CTA 0's control warp zeroes red[(b+4) % 6] right after WAIT(b).
+// All reads of it (control(b-2), every CTA) precede every CTA's ARRIVE(b)
+// (compute warps arrive only after consuming delta^{(b-2)}); its next writer
+// (partials of block b+4, iteration b+3) waits on delta^{(b+2)}, which needs
+// CTA 0's ARRIVE(b+2), issued after CTA 0 consumed delta^{(b)} (after the zeroing).
 // =====================================================================================
-#ifndef DUHL_CTRL_ALONE
-#define DUHL_CTRL_ALONE 1
-#endif
-// The control warp gets an SMSP to itself (warps w and w+4 share SMSP w % 4):
-// control = warp 3, compute = warps 0,1,2,4,5,6; warp 7 only joins the
-// all-thread phases.  (DUHL_CTRL_ALONE=0: control = warp 7, 7 compute warps.)
-constexpr int kCompute = DUHL_CTRL_ALONE ? kScdWarps - 2 : kScdWarps - 1;
-constexpr int kCtrlWarp = DUHL_CTRL_ALONE ? 3 : kScdWarps - 1;
+// Warp layout (warps w and w+4 share SMSP w % 4): control = warp 3 (its SMSP
+// otherwise holds only the mostly-waiting producer, warp 7); compute = 0,1,2,4,5,6.
+constexpr int kCompute = kScdWarps - 2;
+constexpr int kCtrlWarp = 3;
+constexpr int kProdWarp = kScdWarps - 1;
+constexpr int kBarCompute = 1;  // named barrier id: compute warps only
 
 template <bool EXACT, int MODEL>
 __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int W = p.W, R = p.R, T = W / 4;
     const int NRED = scd_nred(W);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [3] stage data landed
+    uint64_t* empty = full + kScdStages;                 // [3] stage consumed
+    uint64_t* dfull = empty + kScdStages;                // [2] delta of a block published
     size_t off = 128;
     float* Abuf = reinterpret_cast<float*>(smem + off);
     off += align_up_dev((size_t)kScdStages * W * R * sizeof(float));
     double* vs = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)R * sizeof(double));
-    double* acc = reinterpret_cast<double*>(smem + off);
-    off += align_up_dev((size_t)2 * NRED * sizeof(double));
     double* sG = reinterpret_cast<double*>(smem + off);
     off += align_up_dev((size_t)NRED * sizeof(double));
     double* delta = reinterpret_cast<double*>(smem + off);  // [2][16]
-    __shared__ int64_t cj[2][16];
-    __shared__ double ca[2][16], cinv[2][16], cy[2][16];
-    __shared__ double sT[16], sP[16], sA[16], sC[16 * 16];
+    __shared__ double sT[16], sP[16], sA[16], sS[16], sC[16 * 16];
     __shared__ int sZ[16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -636,16 +651,22 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     for (int q = tid; q < kScdStages * W * R; q += kScdThreads) Abuf[q] = 0.0f;
     for (int r = tid; r < R; r += kScdThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
     if (tid == 0) {
-        for (int q = 0; q < kScdStages; ++q) mbar_init(&mbar[q], 1);
+        for (int q = 0; q < kScdStages; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kCompute);
+        }
+        mbar_init(&dfull[0], 1);
+        mbar_init(&dfull[1], 1);
         fence_mbar_init();
     }
     fence_proxy_async();
     __syncthreads();
 
-    // developer trace (ScdParams::trace): per-phase globaltimer stamps of CTA 0 / CTA G-1
-    const bool tr = p.trace && tid == kCtrlWarp * 32 && (c == 0 || c == p.G - 1);
+    // developer trace (ScdParams::trace): per-phase cycle counts of CTA 0 / CTA G-1
+    // (control warp lane 0: slots 0-4; compute warp 0 lane 0: slots 5-7)
+    const bool trc_cta = p.trace && (c == 0 || c == p.G - 1);
+    const bool tr = trc_cta && (tid == kCtrlWarp * 32 || tid == 0);
     unsigned long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // registers; written once at the end
-    // SM cycle counter (globaltimer ticks too coarsely for sub-microsecond phases)
     unsigned long long tprev = tr ? (unsigned long long)clock64() : 0;
     auto stamp = [&](int k) {
         if (tr) {
@@ -658,60 +679,14 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     };
     const int64_t nblk = (p.L + W - 1) / W;
     auto stage = [&](int64_t blk) { return Abuf + (size_t)(blk % kScdStages) * W * R; };
-    auto wait_data = [&](int64_t blk) {
-        mbar_wait(&mbar[blk % kScdStages], (unsigned)((blk / kScdStages) & 1));
-    };
-    // block inputs (control warp): prefetched into registers one iteration ahead
-    // from the gathered per-position arrays, published to shared slot blk & 1
-    int64_t pf_j = 0;
-    double pf_a = 0, pf_inv = 0, pf_y = 0;
-    auto prefetch_coords = [&](int64_t blk) {
-        const int64_t t = blk * W + lane;
-        if (lane < W && t < p.L) {
-            pf_j = p.order_j[t];
-            pf_a = p.order_a[t];
-            pf_inv = p.order_inv[t];
-            pf_y = p.order_y[t];
-        }
-    };
-    int pf_slot = 0;
-    unsigned pf_need = 0, seen = 0;
-    auto prefetch_slot = [&](int64_t blk) {
-        const int64_t t = blk * W + lane;
-        if (lane < W && t < p.L) {
-            pf_slot = p.order_slot[t];
-            pf_need = p.order_batch ? p.order_batch[t] : 0u;
-        }
-    };
-    auto publish_coords = [&](int64_t blk) {
-        const int sl = (int)(blk & 1);
-        if (lane < W) {
-            cj[sl][lane] = pf_j;
-            ca[sl][lane] = pf_a;
-            cinv[sl][lane] = pf_inv;
-            cy[sl][lane] = pf_y;
-        }
-    };
-    // Warp roles.  Compute warps 0..kCompute-1 build block blk's partials
-    // (tiles over ALL of the CTA's rows, one warp reduction per tile; big tiles
-    // are split into two row halves so the SMSPs stay balanced), dealt in snake
-    // order by decreasing cost.  The control warp (last) streams stages, loads
-    // block inputs, waits on the grid barrier, reads the reduced block and runs
-    // the W sequential closed-form steps -- concurrently with the tiles.
-    const bool ctrl = warp == kCtrlWarp;
-    // producer (stage issue, block inputs): the spare warp 7 when the control warp
-    // has its own SMSP, else the control warp itself
-#ifndef DUHL_PROD_SPARE
-#define DUHL_PROD_SPARE 0
-#endif
-    const bool prod = (DUHL_CTRL_ALONE && DUHL_PROD_SPARE) ? warp == kScdWarps - 1 : ctrl;
-    // compute-warp index (-1: none)
-    const int cw = ctrl ? -1 : (DUHL_CTRL_ALONE ? (warp < 3 ? warp : (warp < 7 ? warp - 1 : -1)) : warp);
-    // per-warp item lists, built once: item = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15
-    __shared__ int witems[kScdWarps][24];
-    __shared__ int wcount[kScdWarps];
+    const bool ctrl = warp == kCtrlWarp, prod = warp == kProdWarp;
+    const int cw = warp < kCtrlWarp ? warp : (warp > kCtrlWarp && warp < kProdWarp ? warp - 1 : -1);
+
+    // per-compute-warp tile lists, built once: item = kind | jt << 2 | k0 << 6 | kw << 11 | part << 15
+    __shared__ int witems[kCompute][24];
+    __shared__ int wcount[kCompute];
     if (tid == 0) {
-        for (int w = 0; w < kScdWarps; ++w) wcount[w] = 0;
+        for (int w = 0; w < kCompute; ++w) wcount[w] = 0;
         int item = 0;
         for (int cost = 2; cost >= 0; --cost)          // 2: kw 8 tiles, 1: kw 4 tiles, 0: u tiles
             for (int kind = 0; kind < 3; ++kind) {
@@ -735,240 +710,306 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     }
     __syncthreads();
     const int half = ((rows >> 2) + 1) / 2 * 4;  // row split point (multiple of 4)
-    auto tiles = [&](int64_t blk, bool with_c) {
-        const float* A1 = stage(blk);
-        const float* A0 = with_c ? stage(blk - 1) : nullptr;
-        if (cw < 0) return;
-        const int cnt = wcount[cw];
-        for (int it = 0; it < cnt; ++it) {
-            const int code = witems[cw][it];
-            const int kind = code & 3, jt = (code >> 2) & 15, k0 = (code >> 6) & 31, kw = (code >> 11) & 15,
-                      part = (code >> 15) & 1;
-            if (kind == 1 && !with_c) continue;
-            const int lo = kw == 8 ? (part == 0 ? 0 : half) : 0;
-            const int hi = kw == 8 ? (part == 0 ? half : rows) : rows;
-            double* out = acc + (size_t)part * NRED;
-            const float* Aj = A1 + (size_t)(4 * jt) * R;
-            if (kind == 0) {
-                if (kw == 8) tile4<EXACT, 8, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
-                else tile4<EXACT, 4, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
-            } else if (kind == 1) {
-                if (kw == 8) tile4<EXACT, 8, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
-                else tile4<EXACT, 4, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
-            } else {
-                utile(Aj, vs, R, lo, hi, lane, 4 * jt, out);
-            }
-        }
-    };
-    // acc[0] + acc[1] (second row halves of the kw 8 tiles; acc[1] zero elsewhere) -> red
-    auto flush = [&](int64_t blk, bool with_c) {
-        double* red_b = p.red + (size_t)(blk % kRedBufs) * bufsz;
-        const int nq = with_c ? NRED : scd_off_C(W);
-        for (int q = tid; q < nq; q += kScdThreads)
-            atomicAdd(&red_b[((size_t)q * kRedGroups + grp) * kRedStride], acc[q] + acc[NRED + q]);
-    };
-    auto arrive = [&](int64_t blk) {  // by the control warp, after a CTA barrier behind the REDs
-        if (ctrl && lane == 0) {
-            __threadfence();
-            atomicAdd(&p.bar[blk & 1], 1u);
-        }
-    };
-    // WAIT(b) + reduced block b -> the W sequential closed-form steps (control warp)
-    auto control = [&](int64_t b) {
-        const int64_t base = b * W;
-        const int Wb = (int)imin64(W, p.L - base);
-        if (lane == 0) {
-            // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
-            // before WAIT(b) completed everywhere: one counter per block parity counts
-            // exactly the arrivals of blocks b, b-2, b-4, ...
-            const unsigned target = (unsigned)((b / 2 + 1) * (int64_t)p.G);
-            const unsigned long long t0 = gtimer();
-            while (ld_acquire_u32(&p.bar[b & 1]) < target) {
-                __nanosleep(32);
-                if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 2); break; }
-            }
-            __threadfence();
-        }
-        __syncwarp();
-        stamp(2);
-        if (c == 0)
-            for (int q = lane; q < NRED * kRedGroups; q += 32)
-                p.red[(size_t)((b + 4) % kRedBufs) * bufsz + (size_t)q * kRedStride] = 0.0;
-        {   // all loads of the reduced block in flight at once (8 entries per lane per batch)
-            const double* red_b = p.red + (size_t)(b % kRedBufs) * bufsz;
-            const int nq = b > 0 ? NRED : scd_off_C(W);
-            for (int q0 = 0; q0 < nq; q0 += 8 * 32) {
-                double v[8][kRedGroups];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    // unconditional loads (index clamped, store predicated) so all of them
-                    // are in flight together: one L2 round trip instead of one per entry
-                    const int q = min(q0 + u * 32 + lane, nq - 1);
-#pragma unroll
-                    for (int g = 0; g < kRedGroups; ++g)
-                        v[u][g] = ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int q = q0 + u * 32 + lane;
-                    double s = 0.0;
-#pragma unroll
-                    for (int g = 0; g < kRedGroups; ++g) s += v[u][g];
-                    if (q < nq) sG[q] = s;
-                }
-            }
-        }
-        __syncwarp();
-        stamp(3);
-        const int sl = (int)(b & 1);
-        const double* dprev = delta + (size_t)(sl ^ 1) * 16;
-        // Lane j < Wb owns coordinate j.  Keep the step's pre-activation t_j and
-        // fold every correction into it with one DFMA:
-        //   Lasso: t = gamma = a - s/||a||^2,  alpha' = soft(t, lambda d/||a||^2)
-        //   SVM:   t = y a + (lambda n - y s)/||a||^2,  alpha' = y clip(t, 0, 1)
-        // s_j <- s_j + G_jk delta_k  becomes  t_j <- t_j + c_jk delta_k with
-        // c_jk = -G_jk/||a_j||^2 (Lasso) or -y_j G_jk/||a_j||^2 (SVM).
-        int64_t jg = 0;
-        double a = 0, t = 0, tau = 0, cy_ = 0, scale = 0, afin = 0;
-        bool zero = true;
-        if (lane < Wb) {
-            jg = cj[sl][lane];
-            a = ca[sl][lane];
-            double inv = cinv[sl][lane];
-            zero = inv < 0.0;
-            if (zero) inv = 0.0;
-            const double yy = cy[sl][lane];
-            double sj = sG[lane];
-            if (b > 0)  // u was taken at the start of block b-1: add its effect
-                for (int k2 = 0; k2 < W; ++k2) sj = fma(sG[scd_off_C(W) + lane * W + k2], dprev[k2], sj);
-            if (MODEL == kLasso) {
-                t = a - sj * inv;
-                tau = lam_dn * inv;
-                scale = -inv;
-            } else {
-                t = fma(lam_dn - yy * sj, inv, yy * a);
-                cy_ = yy;
-                scale = -yy * inv;
-            }
-        }
-        double* dcur = delta + (size_t)sl * 16;
-        // Stage every coordinate's t_j and scaled Gram row in shared memory, then let
-        // every lane run all Wb steps redundantly: no per-step cross-lane traffic
-        // (a shuffle per step queues behind the compute warps' shared-memory loads).
-        if (lane < 16) {
-            sT[lane] = t;
-            sP[lane] = MODEL == kLasso ? tau : cy_;
-            sZ[lane] = zero ? 1 : 0;
-            sA[lane] = a;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                sC[lane * 16 + j] = (j < lane && lane < Wb) ? scale * sG[scd_off_G(W) + lane * (lane - 1) / 2 + j] : 0.0;
-        }
-        __syncwarp();
-        double tq[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) tq[q] = sT[q];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (j >= Wb) break;
-            const double aj = sA[j], pj = sP[j];
-            double an;
-            if (MODEL == kLasso) {
-                const double mag = fabs(tq[j]) - pj;
-                an = mag > 0.0 ? copysign(mag, tq[j]) : 0.0;
-                if (sZ[j]) an = 0.0;
-            } else {
-                const double u = tq[j] < 0.0 ? 0.0 : (tq[j] > 1.0 ? 1.0 : tq[j]);
-                an = sZ[j] ? pj : pj * u;
-            }
-            const double dl = an - aj;
-            if (lane == j) afin = an;
-            if (lane == 0) dcur[j] = dl;
-#pragma unroll
-            for (int q = j + 1; q < 16; ++q) tq[q] = fma(sC[q * 16 + j], dl, tq[q]);
-        }
-        if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
-        if (lane < Wb && c == 0) p.alpha[jg] = afin;
-    };
-    auto vupdate = [&](int64_t b, int t0, int nthreads) {  // v slice += A_b delta_b
-        const int64_t base = b * W;
-        const int Wb = (int)imin64(W, p.L - base);
-        const float* A = stage(b);
-        const double* dcur = delta + (size_t)(b & 1) * 16;
-        double2* v2 = reinterpret_cast<double2*>(vs);
-        for (int r4 = t0; r4 < (rows >> 2); r4 += nthreads) {
-            double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-            for (int j = 0; j < Wb; ++j) {
-                const float4 x = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
-                const double dj = dcur[j];
-                v01.x = fma(dj, (double)x.x, v01.x);
-                v01.y = fma(dj, (double)x.y, v01.y);
-                v23.x = fma(dj, (double)x.z, v23.x);
-                v23.y = fma(dj, (double)x.w, v23.y);
-            }
-            v2[2 * r4] = v01;
-            v2[2 * r4 + 1] = v23;
-        }
-    };
 
-    for (int q = tid; q < 2 * NRED; q += kScdThreads) acc[q] = 0.0;
-    unsigned long long w0tiles = 0;
-    if (nblk > 0) {
-        if (prod) {
-            for (int64_t q = 0; q < imin64(kScdStages, nblk); ++q) {
-                prefetch_slot(q);
-                scd_issue(p, Abuf, mbar, q, r0, rows, lane, pf_slot, pf_need, seen);
+    if (prod) {
+        // ---------------------------------------------------------------- producer
+        int pf_slot = 0;
+        unsigned pf_need = 0, seen = 0;
+        auto prefetch_slot = [&](int64_t blk) {
+            const int64_t t = blk * W + lane;
+            if (lane < W && t < p.L) {
+                pf_slot = p.order_slot[t];
+                pf_need = p.order_batch ? p.order_batch[t] : 0u;
             }
-            prefetch_slot(kScdStages);
-            prefetch_coords(0);
-            publish_coords(0);
-            prefetch_coords(1);
+        };
+        prefetch_slot(0);
+        for (int64_t q = 0; q < nblk; ++q) {
+            const int slot = pf_slot;
+            const unsigned need = pf_need;
+            if (q + 1 < nblk) prefetch_slot(q + 1);
+            if (q >= kScdStages)  // block q-3 consumed: its stage is free
+                mbar_wait_bounded(&empty[q % kScdStages], (unsigned)((q / kScdStages - 1) & 1), p.err, 4,
+                                  kSpinTimeoutNs);
+            scd_issue(p, Abuf, full, q, r0, rows, lane, slot, need, seen);
         }
-        if (!ctrl && !prod) {
+    } else if (ctrl) {
+        // ---------------------------------------------------------------- control
+        int64_t pf_j = 0;
+        double pf_a = 0, pf_inv = 0, pf_y = 0;
+        auto prefetch_coords = [&](int64_t blk) {
+            const int64_t t = blk * W + lane;
+            if (lane < W && t < p.L) {
+                pf_j = p.order_j[t];
+                pf_a = p.order_a[t];
+                pf_inv = p.order_inv[t];
+                pf_y = p.order_y[t];
+            }
+        };
+        prefetch_coords(0);
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int64_t base = b * W;
+            const int Wb = (int)imin64(W, p.L - base);
+            // this block's inputs (prefetched one block ahead), then start the next block's loads
+            const int64_t jg = pf_j;
+            const double a_in = pf_a, inv_in = pf_inv, y_in = pf_y;
+            if (b + 1 < nblk) prefetch_coords(b + 1);
+            stamp(0);
+            if (lane == 0) {
+                // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
+                // before WAIT(b) completed everywhere: one counter per block parity counts
+                // exactly the arrivals of blocks b, b-2, b-4, ...
+                const unsigned target = (unsigned)((b / 2 + 1) * (int64_t)p.G);
+                const unsigned long long t0 = gtimer();
+                while (ld_acquire_u32(&p.bar[b & 1]) < target) {
+                    __nanosleep(32);
+                    if (gtimer() - t0 > kSpinTimeoutNs) {
+                        atomicOr(p.err, 2);
+#ifdef DUHL_DEBUG_WAITS
+                        printf("WAIT timeout CTA %d b %lld bar %u target %u G %d nblk %lld\n", c, (long long)b,
+                               ld_acquire_u32(&p.bar[b & 1]), target, p.G, (long long)nblk);
+#endif
+                        break;
+                    }
+                }
+                __threadfence();
+            }
+            __syncwarp();
+            stamp(2);
+            if (c == 0)
+                for (int q = lane; q < NRED * kRedGroups; q += 32)
+                    p.red[(size_t)((b + 4) % kRedBufs) * bufsz + (size_t)q * kRedStride] = 0.0;
+#ifdef DUHL_EXP_CTRLTRACE
+            stamp(5);
+#endif
+            {   // all loads of the reduced block in flight at once (8 entries per lane per batch)
+                const double* red_b = p.red + (size_t)(b % kRedBufs) * bufsz;
+                const int nq = b > 0 ? NRED : scd_off_C(W);
+                for (int q0 = 0; q0 < nq; q0 += 8 * 32) {
+                    double v[8][kRedGroups];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        // unconditional loads (index clamped, store predicated) so all of them
+                        // are in flight together: one L2 round trip instead of one per entry
+                        const int q = min(q0 + u * 32 + lane, nq - 1);
+#pragma unroll
+                        for (int g = 0; g < kRedGroups; ++g)
+                            v[u][g] = ld_cg_f64(&red_b[((size_t)q * kRedGroups + g) * kRedStride]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int q = q0 + u * 32 + lane;
+                        double s = 0.0;
+#pragma unroll
+                        for (int g = 0; g < kRedGroups; ++g) s += v[u][g];
+                        if (q < nq) sG[q] = s;
+                    }
+                }
+            }
+            __syncwarp();
+            stamp(3);
+            const double* dprev = delta + (size_t)((b & 1) ^ 1) * 16;
+            // Lane j < Wb owns coordinate j.  Keep the step's pre-activation t_j and
+            // fold every correction into it with one DFMA:
+            //   Lasso: t = gamma = a - s/||a||^2,  alpha' = soft(t, lambda d/||a||^2)
+            //   SVM:   t = y a + (lambda n - y s)/||a||^2,  alpha' = y clip(t, 0, 1)
+            // s_j <- s_j + G_jk delta_k  becomes  t_j <- t_j + c_jk delta_k with
+            // c_jk = -G_jk/||a_j||^2 (Lasso) or -y_j G_jk/||a_j||^2 (SVM).
+            double a = 0, t = 0, tau = 0, cy_ = 0, scale = 0, afin = 0;
+            bool zero = true;
+            if (lane < Wb) {
+                a = a_in;
+                double inv = inv_in;
+                zero = inv < 0.0;
+                if (zero) inv = 0.0;
+                const double yy = y_in;
+                double sj = sG[lane];
+                if (b > 0)  // u was taken at the start of block b-1: add its effect
+                    for (int k2 = 0; k2 < W; ++k2) sj = fma(sG[scd_off_C(W) + lane * W + k2], dprev[k2], sj);
+                if (MODEL == kLasso) {
+                    t = a - sj * inv;
+                    tau = lam_dn * inv;
+                    scale = -inv;
+                } else {
+                    t = fma(lam_dn - yy * sj, inv, yy * a);
+                    cy_ = yy;
+                    scale = -yy * inv;
+                }
+            }
+#ifdef DUHL_EXP_CTRLTRACE
+            __syncwarp();
+            stamp(6);
+#endif
+            double* dcur = delta + (size_t)(b & 1) * 16;
+            // Stage every coordinate's t_j and scaled Gram row in shared memory, then let
+            // every lane run all Wb steps redundantly: no per-step cross-lane traffic.
+            if (lane < 16) {
+                sT[lane] = t;
+                sP[lane] = MODEL == kLasso ? tau : cy_;
+                sZ[lane] = zero ? 1 : 0;
+                sA[lane] = a;
+                sS[lane] = scale;
+            }
+            __syncwarp();
+            // scaled Gram rows, written entry-by-lane (consecutive doubles: no bank conflicts)
+#pragma unroll
+            for (int e0 = 0; e0 < 256; e0 += 32) {
+                const int e = e0 + lane, q = e >> 4, j = e & 15;
+                sC[e] = (j < q && q < Wb) ? sS[q] * sG[scd_off_G(W) + q * (q - 1) / 2 + j] : 0.0;
+            }
+            __syncwarp();
+            double tq[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) tq[q] = sT[q];
+#ifdef DUHL_EXP_CTRLTRACE
+            stamp(7);
+#endif
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (j >= Wb) break;
+                const double aj = sA[j], pj = sP[j];
+                double an;
+                if (MODEL == kLasso) {
+                    const double mag = fabs(tq[j]) - pj;
+                    an = mag > 0.0 ? copysign(mag, tq[j]) : 0.0;
+                    if (sZ[j]) an = 0.0;
+                } else {
+                    const double u = tq[j] < 0.0 ? 0.0 : (tq[j] > 1.0 ? 1.0 : tq[j]);
+                    an = sZ[j] ? pj : pj * u;
+                }
+                const double dl = an - aj;
+                if (lane == j) afin = an;
+                if (lane == 0) dcur[j] = dl;
+#pragma unroll
+                for (int q = j + 1; q < 16; ++q) tq[q] = fma(sC[q * 16 + j], dl, tq[q]);
+            }
+            if (lane >= Wb && lane < 16) dcur[lane] = 0.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dfull[b & 1]);  // publish delta^{(b)} to the compute warps
+#ifdef DUHL_DEBUG_WAITS
+            if (lane == 0 && c == 0 && b < 4) printf("ctrl CTA0 published delta %lld\n", (long long)b);
+#endif
+            if (lane < Wb && c == 0) p.alpha[jg] = afin;
+            stamp(4);
+        }
+    } else {
+        // ---------------------------------------------------------------- compute
+        const int ctid = cw * 32 + lane;
+        const bool tr0 = trc_cta && tid == 0;
+        unsigned long long tc = tr0 ? (unsigned long long)clock64() : 0;
+        auto cstamp = [&](int k) {
+#ifdef DUHL_EXP_CTRLTRACE
+            return;
+#endif
+            if (tr0) {
+                unsigned long long t = (unsigned long long)clock64();
+#pragma unroll
+                for (int q = 5; q < 8; ++q)
+                    if (q == k) trc[q] += t - tc;
+                tc = t;
+            }
+        };
+        auto tiles = [&](int64_t blk, bool with_c) {  // partials of block blk -> red[blk % 6]
+            const float* A1 = stage(blk);
+            const float* A0 = with_c ? stage(blk - 1) : nullptr;
+            const RedOut out{p.red + (size_t)(blk % kRedBufs) * bufsz, grp};
+            const int cnt = wcount[cw];
+            for (int it = 0; it < cnt; ++it) {
+                const int code = witems[cw][it];
+                const int kind = code & 3, jt = (code >> 2) & 15, k0 = (code >> 6) & 31, kw = (code >> 11) & 15,
+                          part = (code >> 15) & 1;
+                if (kind == 1 && !with_c) continue;
+                const int lo = kw == 8 ? (part == 0 ? 0 : half) : 0;
+                const int hi = kw == 8 ? (part == 0 ? half : rows) : rows;
+                const float* Aj = A1 + (size_t)(4 * jt) * R;
+                if (kind == 0) {
+                    if (kw == 8) tile4<EXACT, 8, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                    else tile4<EXACT, 4, true>(Aj, A1 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                } else if (kind == 1) {
+                    if (kw == 8) tile4<EXACT, 8, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                    else tile4<EXACT, 4, false>(Aj, A0 + (size_t)k0 * R, R, lo, hi, lane, 4 * jt, k0, out, W);
+                } else {
+                    utile(Aj, vs, R, lo, hi, lane, 4 * jt, out);
+                }
+            }
+            // ARRIVE(blk): the compute warps' REDs are ordered before one cumulative fence
+            named_sync(kBarCompute, kCompute * 32);
+            if (ctid == 0) {
+                __threadfence();
+                atomicAdd(&p.bar[blk & 1], 1u);
+#ifdef DUHL_DEBUG_WAITS
+                if (blk < 2) printf("arrive CTA %d blk %lld\n", c, (long long)blk);
+#endif
+            }
+        };
+        auto vupdate = [&](int64_t b) {  // v slice += A_b delta_b (rows split over the compute warps)
+            const int Wb = (int)imin64(W, p.L - b * W);
+            const float* A = stage(b);
+            const double* dcur = delta + (size_t)(b & 1) * 16;
+            double2* v2 = reinterpret_cast<double2*>(vs);
+            for (int r4 = ctid; r4 < (rows >> 2); r4 += kCompute * 32) {
+                double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                for (int j = 0; j < Wb; ++j) {
+                    const float4 x = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
+                    const double dj = dcur[j];
+                    v01.x = fma(dj, (double)x.x, v01.x);
+                    v01.y = fma(dj, (double)x.y, v01.y);
+                    v23.x = fma(dj, (double)x.z, v23.x);
+                    v23.y = fma(dj, (double)x.w, v23.y);
+                }
+                v2[2 * r4] = v01;
+                v2[2 * r4 + 1] = v23;
+            }
+        };
+        auto wait_data = [&](int64_t blk) {
+            mbar_wait_bounded(&full[blk % kScdStages], (unsigned)((blk / kScdStages) & 1), p.err, 8,
+                              kSpinTimeoutNs);
+        };
+        auto wait_delta = [&](int64_t blk) {
+            mbar_wait_bounded(&dfull[blk & 1], (unsigned)((blk >> 1) & 1), p.err, 16, kSpinTimeoutNs);
+        };
+        if (nblk > 0) {
             wait_data(0);
             tiles(0, false);
         }
-        __syncthreads();
-        flush(0, false);
-        __syncthreads();
-        arrive(0);
-    }
-    for (int64_t b = 0; b < nblk; ++b) {
-        const bool next = b + 1 < nblk;
-        if (prod) {
-            // stage of block b-1 was freed by the last V update: stream block b+2 into it
-            if (next) publish_coords(b + 1);   // block b+1's inputs (prefetched last iteration)
-            if (b + 2 < nblk) prefetch_coords(b + 2);
-            if (b >= 1 && b + 2 < nblk) {       // slot/sequence of block b+2 prefetched last time
-                scd_issue(p, Abuf, mbar, b + 2, r0, rows, lane, pf_slot, pf_need, seen);
-                prefetch_slot(b + 3);
+        for (int64_t b = 0; b < nblk; ++b) {
+            named_sync(kBarCompute, kCompute * 32);  // every warp is done reading v for block b's u
+            if (b >= 1) {
+                cstamp(7);
+#ifdef DUHL_DEBUG_WAITS
+                if (lane == 0 && c == 0 && b < 4) printf("cmp CTA0 warp %d waits delta %lld\n", warp, (long long)(b - 1));
+#endif
+                wait_delta(b - 1);
+#ifdef DUHL_DEBUG_WAITS
+                if (lane == 0 && c == 0 && b < 4) printf("cmp CTA0 warp %d got delta %lld\n", warp, (long long)(b - 1));
+#endif
+                cstamp(5);
+                vupdate(b - 1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[(b - 1) % kScdStages]);  // block b-1's stage is free
+                named_sync(kBarCompute, kCompute * 32);  // v_b complete before the u tiles read it
+                cstamp(6);
+            }
+            if (b + 1 < nblk) {
+                wait_data(b + 1);
+#ifdef DUHL_DEBUG_WAITS
+                if (lane == 0 && c == 0 && b < 4) printf("cmp CTA0 warp %d got data %lld\n", warp, (long long)(b + 1));
+#endif
+                tiles(b + 1, true);
             }
         }
-        if (ctrl) {
-            stamp(0);
-            control(b);
-            stamp(4);
-        } else if (next && !prod) {
-            wait_data(b + 1);
-            unsigned long long tw1 = (p.trace && tid == 0 && c == 0) ? (unsigned long long)clock64() : 0;
-            tiles(b + 1, true);
-            if (p.trace && tid == 0 && c == 0) w0tiles += (unsigned long long)clock64() - tw1;
+        if (nblk > 0) {
+            cstamp(7);
+            wait_delta(nblk - 1);
+            cstamp(5);
+            vupdate(nblk - 1);
+            cstamp(6);
         }
-        __syncthreads();
-        stamp(6);
-        if (next) flush(b + 1, true);
-        __syncthreads();
-        stamp(1);
-        if (next) arrive(b + 1);
-        if (!ctrl)  // the control warp fences/arrives meanwhile; the others share the rows
-            vupdate(b, tid < kCtrlWarp * 32 ? tid : tid - 32, kScdThreads - 32);
-        __syncthreads();
-        stamp(5);
     }
+    __syncthreads();
     for (int r = tid; r < rows; r += kScdThreads) p.vt[r0 + r] = vs[r];
     if (tr)
-        for (int q = 0; q < 7; ++q) p.trace[(c == 0 ? 0 : 8) + q] += trc[q];
-    if (p.trace && tid == 0 && c == 0) p.trace[7] += w0tiles;
+        for (int q = 0; q < 8; ++q)
+            if (trc[q]) atomicAdd(&p.trace[(c == 0 ? 0 : 8) + q], trc[q]);
 }
 
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches) {
