@@ -99,7 +99,7 @@ __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
 
 // Work item vb = (column group vb % ngroups, row tile vb / ngroups); a grid
 // smaller than the item count loops (a persistent unit-A grid beside the SCD epoch).
-__global__ void __launch_bounds__(kGapThreads) k_gap_tile(GapParams p, int tile_rows, int ntiles, int64_t ngroups) {
+__global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int tile_rows, int ntiles, int64_t ngroups) {
     extern __shared__ double ws[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const double2* w2 = reinterpret_cast<const double2*>(ws);
