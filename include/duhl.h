@@ -67,6 +67,18 @@ typedef struct {
     int64_t ld;           /* leading dimension, ld >= d */
 } duhl_matrix;
 
+/* Sparse matrix in compressed sparse columns: column i holds
+ * values[k], row_idx[k] for k in [col_ptr[i], col_ptr[i+1]); rows strictly
+ * ascending in [0, d); col_ptr[0] = 0, nondecreasing.  Host memory, read
+ * during duhl_create_csc only (copied to HBM). */
+typedef struct {
+    int64_t d;              /* rows */
+    int64_t n;              /* columns = coordinates */
+    const int64_t* col_ptr; /* [n + 1] */
+    const int32_t* row_idx; /* [col_ptr[n]] */
+    const float* values;    /* [col_ptr[n]] */
+} duhl_csc;
+
 typedef struct {
     size_t hbm_budget_bytes;  /* HBM for the working-set slot pool; 0 = all n columns resident */
     int64_t m;                /* working-set size |P|; 0 = as many columns as the budget holds (n if budget 0) */
@@ -117,6 +129,19 @@ void duhl_default_config(duhl_config* cfg);
  * Errors: DUHL_E_INVALID, DUHL_E_NOMEM, DUHL_E_CUDA.  *out = NULL on error. */
 duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambda,
                         duhl_model model, const duhl_config* cfg, duhl_ctx** out);
+
+/* Sparse variant (SURVEY 8 C5, P:433 sparse Lasso setting): same semantics as
+ * duhl_create on a CSC matrix.  The matrix is held resident in HBM (8 bytes per
+ * nonzero); hbm_budget_bytes must be 0 or at least that (DUHL_E_INVALID
+ * otherwise); no staging, borrow_host ignored.  The SCD epoch is the
+ * warp-per-coordinate asynchronous form (App. D; fp64 RED updates of v):
+ * scd_exact = 1 runs the positions strictly in order on one warp (sequential
+ * SCD up to summation order), scd_exact = 0 runs them concurrently on all SMs
+ * (stale reads possible; v stays exactly A alpha - b up to rounding).
+ * Errors: as duhl_create (DUHL_E_INVALID also for unsorted / out-of-range rows,
+ * non-finite values, a non-monotone col_ptr). */
+duhl_status duhl_create_csc(const duhl_csc* A, const double* b_or_y, double lambda,
+                            duhl_model model, const duhl_config* cfg, duhl_ctx** out);
 
 duhl_status duhl_destroy(duhl_ctx* ctx);
 

@@ -4,13 +4,14 @@ Argument marshalling only -- every step of the path runs in the library's
 sm_100a kernels behind the C ABI declared in ``include/duhl.h``.  The names
 mirror the ABI: ``create`` (duhl_create), ``Problem.gaps`` (duhl_gaps),
 ``Problem.select`` (duhl_select), ``Problem.scd_epoch`` (duhl_scd_epoch),
-``Problem.duality_gap`` (duhl_duality_gap), ``Problem.solve`` (duhl_solve).
+``Problem.duality_gap`` (duhl_duality_gap), ``Problem.solve`` (duhl_solve);
+``create_csc`` (duhl_create_csc) for sparse matrices.
 
 There is no CPU fallback: importing works anywhere (the symbols load), but any
 call that computes raises ``DuhlError`` unless a B200 is present.
 """
 from ._abi import (LASSO, SVM_DUAL, SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, DuhlError, Problem,
-                   RoundRecord, create, comm_unique_id, lib, lib_path, exported_symbols)
+                   RoundRecord, create, create_csc, comm_unique_id, lib, lib_path, exported_symbols)
 
 __all__ = ["LASSO", "SVM_DUAL", "SEL_GAP", "SEL_SEQUENTIAL", "SEL_UNIFORM", "DuhlError", "Problem",
-           "RoundRecord", "create", "comm_unique_id", "lib", "lib_path", "exported_symbols"]
+           "RoundRecord", "create", "create_csc", "comm_unique_id", "lib", "lib_path", "exported_symbols"]

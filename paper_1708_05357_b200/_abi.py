@@ -13,7 +13,7 @@ SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM = 0, 1, 2
 STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "E_NOMEM",
           7: "E_CUDA", 8: "E_NCCL", 9: "E_NOT_CONVERGED"}
 
-FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_destroy", "duhl_gaps", "duhl_select",
+FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_create_csc", "duhl_destroy", "duhl_gaps", "duhl_select",
              "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
              "duhl_set_state", "duhl_comm_unique_id", "duhl_comm_init", "duhl_get_stream",
              "duhl_get_kernel_stats", "duhl_get_counters", "duhl_last_error"]
@@ -28,6 +28,11 @@ class DuhlError(RuntimeError):
 
 class Matrix(C.Structure):
     _fields_ = [("d", C.c_int64), ("n", C.c_int64), ("values", C.c_void_p), ("ld", C.c_int64)]
+
+
+class Csc(C.Structure):
+    _fields_ = [("d", C.c_int64), ("n", C.c_int64), ("col_ptr", C.c_void_p), ("row_idx", C.c_void_p),
+                ("values", C.c_void_p)]
 
 
 class Config(C.Structure):
@@ -65,6 +70,8 @@ def lib():
         L.duhl_default_config.restype = None
         L.duhl_create.argtypes = [C.POINTER(Matrix), _P, C.c_double, C.c_int, C.POINTER(Config),
                                   C.POINTER(C.c_void_p)]
+        L.duhl_create_csc.argtypes = [C.POINTER(Csc), _P, C.c_double, C.c_int, C.POINTER(Config),
+                                      C.POINTER(C.c_void_p)]
         L.duhl_destroy.argtypes = [_P]
         L.duhl_gaps.argtypes = [_P, _P, _I, _P, _P]
         L.duhl_select.argtypes = [_P, C.c_int, _I, _I, _P, _P]
@@ -238,6 +245,30 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
     prob = Problem(h, d, n, keepalive=A if borrow_host else None)
     prob.m = cfg.m if cfg.m > 0 else (n if hbm_budget_bytes == 0 else
                                       min(n, hbm_budget_bytes // (((d + 3) // 4) * 16)))
+    return prob
+
+
+def create_csc(col_ptr, row_idx, values, d, b_or_y, lam, model, m=0, device=0, refresh_fraction=0.05,
+               cert_every=10, seed=170805357, cert_adaptive=True, profile=False, scd_exact=True,
+               n_global=0, col_offset=0, linesearch=False, scd_ctas=0):
+    """duhl_create_csc.  CSC arrays: col_ptr int64 [n+1], row_idx int32 [nnz] (ascending per
+    column), values float32 [nnz]; the matrix is copied to HBM."""
+    cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(row_idx, dtype=np.int32)
+    va = np.ascontiguousarray(values, dtype=np.float32)
+    n = cp.shape[0] - 1
+    lab = np.ascontiguousarray(b_or_y, dtype=np.float64)
+    mat = Csc(d, n, cp.ctypes.data, ri.ctypes.data, va.ctypes.data)
+    cfg = default_config(m=m, device=device, refresh_fraction=refresh_fraction, cert_every=cert_every,
+                         seed=seed, cert_adaptive=int(bool(cert_adaptive)), profile=int(bool(profile)),
+                         scd_exact=int(bool(scd_exact)), n_global=n_global, col_offset=col_offset,
+                         linesearch=int(bool(linesearch)), scd_ctas=scd_ctas)
+    h = C.c_void_p()
+    st = lib().duhl_create_csc(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
+    if st != 0:
+        raise DuhlError(st, "duhl_create_csc failed (a B200 / sm_100 device is required)")
+    prob = Problem(h, d, n)
+    prob.m = cfg.m if cfg.m > 0 else n
     return prob
 
 

@@ -76,6 +76,15 @@ struct duhl_ctx {
     // ---- unit A: pinned host store
     float* h_store = nullptr;
     bool own_store = false, registered = false;
+    // sparse (CSC) problems: the matrix lives in HBM; no slot pool, no staging
+    bool csc = false;
+    int64_t nnz = 0;
+    int64_t* d_colptr = nullptr;
+    int* d_rows = nullptr;
+    float* d_vals = nullptr;
+    std::vector<int64_t> h_colptr;  // host copy of col_ptr (algorithmic byte counts)
+    double csc_pass_bytes = 0.0;    // algorithmic bytes of one SCD pass over the current order
+    int csc_warps = 0;              // concurrent coordinates of the asynchronous CSC epoch
     int64_t ld_host = 0;
     const float* h_alias = nullptr;  // device address of h_store
     // ---- unit B: HBM slot pool
@@ -202,6 +211,8 @@ static ColSrc colsrc(const duhl_ctx* ctx) {
     return s;
 }
 
+static CscMat cscmat(const duhl_ctx* ctx) { return CscMat{ctx->d_colptr, ctx->d_rows, ctx->d_vals}; }
+
 static double wscale(const duhl_ctx* ctx) {
     return ctx->model == DUHL_LASSO ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n_glob);
 }
@@ -272,7 +283,8 @@ static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, dou
     if (s_acc) p.s_acc = s_acc;
     const int64_t tiles = (ctx->d4 + tile_rows - 1) / tile_rows;
     ProfScope ps(ctx, sx, stream ? 4 : 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
-    CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches, max_ctas));
+    if (ctx->csc) CK(launch_csc_gap(p, cscmat(ctx), max_ctas, sx, &ctx->launches));
+    else CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches, max_ctas));
     return DUHL_OK;
 }
 
@@ -458,6 +470,11 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
     CK(cudaMemcpyAsync(ctx->d_P_batch, Pb.data(), m * sizeof(unsigned), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     ctx->P = P;
+    if (ctx->csc) {  // algorithmic bytes of a pass: 8 B per nonzero + 24 B per coordinate
+        double by = 0.0;
+        for (int64_t j : P) by += 8.0 * (double)(ctx->h_colptr[j + 1] - ctx->h_colptr[j]) + 24.0;
+        ctx->csc_pass_bytes = by;
+    }
     std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
     for (int64_t j : P) ctx->inP[j] = 1;
     if (swaps) *swaps = nsw;
@@ -475,7 +492,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_dv, ctx->d_aold, ctx->d_ls,
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
-                        ctx->d_red, ctx->d_bar};
+                        ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -527,24 +544,58 @@ void duhl_default_config(duhl_config* cfg) {
 
 const char* duhl_last_error(const duhl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambda,
-                        duhl_model model, const duhl_config* cfg_in, duhl_ctx** out) {
+// Dense (A) or sparse (C) ingest; exactly one is non-null.
+static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const double* b_or_y, double lambda,
+                               duhl_model model, const duhl_config* cfg_in, duhl_ctx** out) {
     if (!out) return DUHL_E_INVALID;
     *out = nullptr;
-    if (!A || !A->values || !b_or_y || A->d < 1 || A->n < 1 || A->ld < A->d) return DUHL_E_INVALID;
+    if (A && (!A->values || A->d < 1 || A->n < 1 || A->ld < A->d)) return DUHL_E_INVALID;
+    if (C && (!C->col_ptr || !C->row_idx || !C->values || C->d < 1 || C->n < 1 || C->d > (int64_t)INT32_MAX))
+        return DUHL_E_INVALID;
+    if (!A == !C || !b_or_y) return DUHL_E_INVALID;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return DUHL_E_INVALID;
     if (model != DUHL_LASSO && model != DUHL_SVM_DUAL) return DUHL_E_INVALID;
-    if (A->n > (int64_t)INT32_MAX - 1) return DUHL_E_INVALID;
+    const int64_t nin = A ? A->n : C->n, din = A ? A->d : C->d;
+    if (nin > (int64_t)INT32_MAX - 1) return DUHL_E_INVALID;
     duhl_ctx* ctx = new duhl_ctx();
     if (cfg_in) ctx->cfg = *cfg_in; else duhl_default_config(&ctx->cfg);
     if (ctx->cfg.cert_every < 1) ctx->cfg.cert_every = 1;
     ctx->model = model;
-    ctx->d = A->d;
-    ctx->n = A->n;
-    ctx->n_glob = ctx->cfg.n_global > 0 ? ctx->cfg.n_global : A->n;
+    ctx->d = din;
+    ctx->n = nin;
+    ctx->csc = C != nullptr;
+    if (ctx->csc) {  // validate the structure once on the host
+        const int64_t* cp = C->col_ptr;
+        if (cp[0] != 0) { delete ctx; return DUHL_E_INVALID; }
+        for (int64_t i = 0; i < nin; ++i)
+            if (cp[i + 1] < cp[i]) { delete ctx; return DUHL_E_INVALID; }
+        ctx->nnz = cp[nin];
+        for (int64_t i = 0; i < nin; ++i)
+            for (int64_t k = cp[i]; k < cp[i + 1]; ++k) {
+                const int32_t r = C->row_idx[k];
+                if (r < 0 || r >= din || (k > cp[i] && r <= C->row_idx[k - 1]) || !std::isfinite(C->values[k])) {
+                    delete ctx;
+                    return DUHL_E_INVALID;
+                }
+            }
+        if (ctx->cfg.hbm_budget_bytes != 0) {  // a sparse matrix is held resident
+            const size_t need = (size_t)ctx->nnz * 8 + (size_t)(nin + 1) * 8;
+            if (ctx->cfg.hbm_budget_bytes < need) { delete ctx; return DUHL_E_INVALID; }
+            ctx->cfg.hbm_budget_bytes = 0;
+        }
+        ctx->h_colptr.assign(cp, cp + nin + 1);
+        // concurrency of the asynchronous epoch (warps): scd_ctas if given, else d/16.  Concurrent
+        // steps are Jacobi-like: a step ignores the others' updates, whose summed effect on it is
+        // ~ sqrt(C/d) of its own for C concurrent random columns, so C = d/16 keeps it ~1/4.  The
+        // exact line search on the round's step keeps every round monotone; it is
+        // always on for the asynchronous sparse epoch (sparse path)
+        ctx->csc_warps = ctx->cfg.scd_ctas > 0 ? ctx->cfg.scd_ctas : (int)std::max<int64_t>(32, din / 16);
+        if (!ctx->cfg.scd_exact) ctx->cfg.linesearch = 1;
+    }
+    ctx->n_glob = ctx->cfg.n_global > 0 ? ctx->cfg.n_global : nin;
     ctx->col_offset = ctx->cfg.col_offset;
-    if (ctx->col_offset < 0 || ctx->col_offset + A->n > ctx->n_glob) { delete ctx; return DUHL_E_INVALID; }
-    ctx->d4 = round4(A->d);
+    if (ctx->col_offset < 0 || ctx->col_offset + nin > ctx->n_glob) { delete ctx; return DUHL_E_INVALID; }
+    ctx->d4 = round4(din);
     ctx->lambda = lambda;
     const int64_t d = ctx->d, n = ctx->n, d4 = ctx->d4;
     // labels
@@ -572,6 +623,19 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
         cudaEventCreateWithFlags(&ctx->ev_ref, cudaEventDisableTiming) != cudaSuccess)
         return bail(DUHL_E_CUDA);
     if (preload_kernels() != cudaSuccess) return bail(DUHL_E_CUDA);  // no lazy loads mid-epoch
+    if (ctx->csc) {  // ---- sparse: the CSC arrays go to HBM once
+        auto dm = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16) == cudaSuccess; };
+        if (!dm((void**)&ctx->d_colptr, (n + 1) * sizeof(int64_t)) || !dm((void**)&ctx->d_rows, ctx->nnz * sizeof(int)) ||
+            !dm((void**)&ctx->d_vals, ctx->nnz * sizeof(float))) {
+            cudaGetLastError();
+            return bail(DUHL_E_NOMEM);
+        }
+        if (cudaMemcpy(ctx->d_colptr, C->col_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(ctx->d_rows, C->row_idx, ctx->nnz * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(ctx->d_vals, C->values, ctx->nnz * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(DUHL_E_CUDA);
+        ctx->h2d_bytes += (int64_t)((n + 1) * 8 + ctx->nnz * 8);
+    } else {
     // ---- unit A: pinned host store (column i at h_store + i*ld_host, rows d..d4 zero)
     const bool can_borrow = ctx->cfg.borrow_host && d % 4 == 0 && A->ld % 4 == 0 &&
                             ((uintptr_t)A->values % 16 == 0);
@@ -626,6 +690,7 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     void* alias = nullptr;
     if (cudaHostGetDevicePointer(&alias, ctx->h_store, 0) != cudaSuccess) return bail(DUHL_E_CUDA);
     ctx->h_alias = (const float*)alias;
+    }
     // ---- unit B: slot pool
     ctx->ld_dev = d4;
     const size_t col_bytes = (size_t)d4 * sizeof(float);
@@ -638,7 +703,7 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ctx->m_cfg = ctx->cfg.m > 0 ? ctx->cfg.m : ctx->S;
     if (ctx->m_cfg > n || ctx->m_cfg > ctx->S) return bail(DUHL_E_INVALID);
     auto dmal = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16) == cudaSuccess; };
-    bool ok = dmal((void**)&ctx->pool, (size_t)ctx->S * col_bytes) &&
+    bool ok = dmal((void**)&ctx->pool, ctx->csc ? 0 : (size_t)ctx->S * col_bytes) &&
               dmal((void**)&ctx->d_col_slot, n * sizeof(int)) &&
               dmal((void**)&ctx->d_alpha, n * sizeof(double)) &&
               dmal((void**)&ctx->d_vt, d4 * sizeof(double)) &&
@@ -704,9 +769,11 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ck(cudaMemsetAsync(ctx->d_y, 0, n * sizeof(double), st));
     if (ctx->cfg.hbm_budget_bytes == 0) {  // everything resident: slot i = column i
         for (int64_t i = 0; i < n; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
-        ck(cudaMemcpy2DAsync(ctx->pool, col_bytes, ctx->h_store, ctx->ld_host * sizeof(float), col_bytes,
-                             (size_t)n, cudaMemcpyHostToDevice, st));
-        ctx->h2d_bytes += (int64_t)(n * col_bytes);
+        if (!ctx->csc) {
+            ck(cudaMemcpy2DAsync(ctx->pool, col_bytes, ctx->h_store, ctx->ld_host * sizeof(float), col_bytes,
+                                 (size_t)n, cudaMemcpyHostToDevice, st));
+            ctx->h2d_bytes += (int64_t)(n * col_bytes);
+        }
     }
     ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
     if (model == DUHL_SVM_DUAL)
@@ -716,7 +783,8 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     ck(cudaStreamSynchronize(st));
     if (!ok2) { cudaGetLastError(); ctx->err = "device setup failed"; return bail(DUHL_E_CUDA); }
     // ---- precompute (a1): norms, B, initial shared vector, z at alpha = 0
-    ck(launch_col_norms(colsrc(ctx), d4, n, ctx->d_norms, st, &ctx->launches));
+    if (ctx->csc) ck(launch_csc_norms(cscmat(ctx), n, ctx->d_norms, st, &ctx->launches));
+    else ck(launch_col_norms(colsrc(ctx), d4, n, ctx->d_norms, st, &ctx->launches));
     if (model == DUHL_LASSO) {
         double h[2] = {0, 0};
         ck(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), st));
@@ -733,6 +801,18 @@ duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambd
     if (check_flag(ctx, "initial gaps") != DUHL_OK) return bail(DUHL_E_NUMERIC);
     *out = ctx;
     return DUHL_OK;
+}
+
+duhl_status duhl_create(const duhl_matrix* A, const double* b_or_y, double lambda, duhl_model model,
+                        const duhl_config* cfg, duhl_ctx** out) {
+    if (!A) return DUHL_E_INVALID;
+    return create_impl(A, nullptr, b_or_y, lambda, model, cfg, out);
+}
+
+duhl_status duhl_create_csc(const duhl_csc* A, const double* b_or_y, double lambda, duhl_model model,
+                            const duhl_config* cfg, duhl_ctx** out) {
+    if (!A) return DUHL_E_INVALID;
+    return create_impl(nullptr, A, b_or_y, lambda, model, cfg, out);
 }
 
 duhl_status duhl_destroy(duhl_ctx* ctx) {
@@ -799,6 +879,24 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
 }
 
 static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
+    if (ctx->csc) {  // asynchronous warp-per-coordinate epoch (exact mode: one warp, in order)
+        CscScdParams q{};
+        q.model = ctx->model;
+        q.d = ctx->d;
+        q.n = ctx->n_glob;
+        q.lambda = ctx->lambda;
+        q.A = cscmat(ctx);
+        q.order_j = ctx->d_order_j;
+        q.L = L;
+        q.norms = ctx->d_norms;
+        q.y = ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr;
+        q.alpha = ctx->d_alpha;
+        q.vt = ctx->d_vt;
+        ProfScope ps(ctx, ctx->st, 0, ctx->csc_pass_bytes);
+        CK(launch_csc_scd(q, ctx->cfg.scd_exact ? 1 : ctx->csc_warps, ctx->st, &ctx->launches));
+        ctx->updates += L;
+        return DUHL_OK;
+    }
     ScdParams p{};
     p.model = ctx->model;
     p.d = ctx->d;
@@ -900,6 +998,12 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
             batches[t] = ctx->slot_batch[slots[t]];
         }
         if (!ctx->overlap) TRY(issue_staging(ctx));
+        if (ctx->csc) {
+            double by = 0.0;
+            for (int64_t t = 0; t < perm_len; ++t)
+                by += 8.0 * (double)(ctx->h_colptr[perm[t] + 1] - ctx->h_colptr[perm[t]]) + 24.0;
+            ctx->csc_pass_bytes = by;
+        }
         CK(cudaMemcpyAsync(ctx->d_order_j, perm, perm_len * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_order_slot, slots.data(), perm_len * sizeof(int), cudaMemcpyHostToDevice, ctx->st));
         CK(cudaMemcpyAsync(ctx->d_order_batch, batches.data(), perm_len * sizeof(unsigned),
@@ -1201,8 +1305,9 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
             return fail(ctx, DUHL_E_INVALID, "SVM alpha outside the box y_i alpha_i in [0,1]");
     }
     CK(cudaMemcpyAsync(ctx->d_alpha, alpha, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
-    CK(launch_matvec(colsrc(ctx), ctx->d_alpha, ctx->n, ctx->d, ctx->d4,
+    CK(launch_matvec(colsrc(ctx), ctx->d_alpha, ctx->csc ? 0 : ctx->n, ctx->d, ctx->d4,
                      ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
+    if (ctx->csc) CK(launch_csc_matvec(cscmat(ctx), ctx->d_alpha, ctx->n, ctx->d_vt, ctx->st, &ctx->launches));
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, nullptr));
     CK(cudaStreamSynchronize(ctx->st));
     return check_flag(ctx, "duhl_set_state");

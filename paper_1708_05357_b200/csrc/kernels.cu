@@ -1203,6 +1203,133 @@ cudaError_t launch_vec_sums(const double* vt, const double* b, int64_t d4, doubl
 }
 
 
+// =====================================================================================
+// Sparse (CSC) path, SURVEY 8 C5.  One warp per column; the shared vector is
+// gathered by row index (fp64, L2-resident: 8 d bytes), the column streamed once.
+// =====================================================================================
+__device__ __forceinline__ int ld_stream_i32(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_csc_norms(CscMat A, int64_t n, double* norms) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        const int64_t k0 = A.col_ptr[i], k1 = A.col_ptr[i + 1];
+        double s = 0.0;
+        for (int64_t k = k0 + lane; k < k1; k += 32) {
+            const double x = (double)ld_stream_f32(A.vals + k);
+            s = fma(x, x, s);
+        }
+        s = warp_sum(s);
+        if (lane == 0) norms[i] = s;
+    }
+}
+
+// s_i = sum_k a_ki (wscale vt_k) over the column's nonzeros, then the gap (as k_gap_tile).
+__global__ void __launch_bounds__(256) k_csc_gap(GapParams p, CscMat A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    SumAcc acc;
+    int flag = 0;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.k; t += nw) {
+        const int64_t i = p.cols ? p.cols[t] : t;
+        const int64_t k0 = A.col_ptr[i], k1 = A.col_ptr[i + 1];
+        double s0 = 0.0, s1 = 0.0;
+        int64_t k = k0 + lane;
+        for (; k + 32 < k1; k += 64) {  // two independent gathers in flight per lane
+            const int r0 = ld_stream_i32(A.rows + k), r1 = ld_stream_i32(A.rows + k + 32);
+            const float x0 = ld_stream_f32(A.vals + k), x1 = ld_stream_f32(A.vals + k + 32);
+            s0 = fma((double)x0, __ldg(p.vt + r0) * p.wscale, s0);
+            s1 = fma((double)x1, __ldg(p.vt + r1) * p.wscale, s1);
+        }
+        if (k < k1) s0 = fma((double)ld_stream_f32(A.vals + k), __ldg(p.vt + ld_stream_i32(A.rows + k)) * p.wscale, s0);
+        const double s = warp_sum(s0 + s1);
+        if (lane == 0) gap_finish_one(p, t, i, s, acc, flag);
+    }
+    block_flush_sums(p, acc, flag);
+}
+
+__global__ void __launch_bounds__(256) k_csc_scd(CscScdParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double dd = (double)p.d, nn = (double)p.n;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.L; t += nw) {
+        const int64_t j = p.order_j[t];
+        const int64_t k0 = p.A.col_ptr[j], k1 = p.A.col_ptr[j + 1];
+        double s = 0.0;
+        for (int64_t k = k0 + lane; k < k1; k += 32)  // v is being updated by other warps: read it at L2
+            s = fma((double)p.A.vals[k], __ldcg(p.vt + p.A.rows[k]), s);
+        s = warp_sum(s);
+        const double a = p.alpha[j];
+        const double an = coord_step(p.model, a, s, p.norms[j], p.y ? p.y[j] : 0.0, p.lambda, dd, nn);
+        const double dl = an - a;
+        if (dl != 0.0)
+            for (int64_t k = k0 + lane; k < k1; k += 32) atomicAdd(p.vt + p.A.rows[k], dl * (double)p.A.vals[k]);
+        if (lane == 0) p.alpha[j] = an;
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_csc_matvec(CscMat A, const double* alpha, int64_t n, double* vt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        const double a = alpha[i];
+        if (a == 0.0) continue;
+        for (int64_t k = A.col_ptr[i] + lane; k < A.col_ptr[i + 1]; k += 32)
+            atomicAdd(vt + A.rows[k], a * (double)A.vals[k]);
+    }
+}
+
+static unsigned csc_grid(int64_t work_warps) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t full = (int64_t)nsm * 8;  // 8 CTAs x 8 warps per SM
+    const int64_t need = (work_warps + 7) / 8;
+    return (unsigned)(need < full ? (need > 0 ? need : 1) : full);
+}
+
+cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStream_t st, int64_t* launches) {
+    if (n <= 0) return cudaSuccess;
+    k_csc_norms<<<csc_grid(n), 256, 0, st>>>(A, n, norms);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches) {
+    if (p.k <= 0) return cudaSuccess;
+    unsigned g = csc_grid(p.k);
+    if (max_ctas > 0 && g > (unsigned)max_ctas) g = (unsigned)max_ctas;
+    k_csc_gap<<<g, 256, 0, st>>>(p, A);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csc_scd(const CscScdParams& p, int warps, cudaStream_t st, int64_t* launches) {
+    if (p.L <= 0) return cudaSuccess;
+    if (warps == 1) k_csc_scd<<<1, 32, 0, st>>>(p);
+    else k_csc_scd<<<csc_grid(warps > 0 ? warps : p.L), 256, 0, st>>>(p);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csc_matvec(const CscMat& A, const double* alpha, int64_t n, double* vt, cudaStream_t st,
+                              int64_t* launches) {
+    if (n <= 0) return cudaSuccess;
+    k_csc_matvec<<<csc_grid(n), 256, 0, st>>>(A, alpha, n, vt);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // Load every kernel of the library now.  Under lazy module loading (the CUDA 12
 // default) the first launch of a kernel loads it, and that load can wait for the
 // device to go idle -- fatal while the SCD kernel waits on staging copies the
@@ -1215,7 +1342,9 @@ cudaError_t preload_kernels() {
         (const void*)k_scd_gram<true, kSvm>,   (const void*)k_scd_gram<false, kSvm>,
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
-        (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums};
+        (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,
+        (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
+        (const void*)k_csc_matvec};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -58,6 +58,31 @@ struct ScdParams {
     int* err;                     // set (bit 0: staging wait, bit 1: grid barrier) on a wait timeout
 };
 
+// Sparse matrix, compressed sparse columns, resident in HBM:
+// column i = values/rows [col_ptr[i], col_ptr[i+1]), rows ascending in [0, d).
+struct CscMat {
+    const int64_t* col_ptr;  // [n + 1]
+    const int* rows;         // [nnz]
+    const float* vals;       // [nnz]
+};
+
+// Asynchronous SCD epoch on a CSC working set (TPA-SCD style, P:336 / App. D):
+// one warp per coordinate in visiting order, warp-reduced a_j^T v, closed-form
+// step, fp64 RED update of v.  warps = 1 runs the positions strictly in order
+// (== sequential SCD up to summation order); more warps run them concurrently.
+struct CscScdParams {
+    int model;
+    int64_t d, n;
+    double lambda;
+    CscMat A;
+    const int64_t* order_j;  // [L]
+    int64_t L;
+    const double* norms;     // [n]
+    const double* y;         // [n] (SVM) or nullptr
+    double* alpha;           // [n]
+    double* vt;              // [d4]
+};
+
 __host__ __device__ int scd_nred(int W);
 size_t scd_red_doubles(int W);  // size of ScdParams::red
 size_t scd_smem_bytes(int W, int R, int NB);
@@ -78,6 +103,12 @@ cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigne
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t preload_kernels();
+cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStream_t st, int64_t* launches);
+cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches);
+cudaError_t launch_csc_scd(const CscScdParams& p, int warps, cudaStream_t st, int64_t* launches);
+// vt += A alpha over the columns with alpha != 0 (fp64 REDs)
+cudaError_t launch_csc_matvec(const CscMat& A, const double* alpha, int64_t n, double* vt, cudaStream_t st,
+                              int64_t* launches);
 cudaError_t launch_matvec(const ColSrc& src, const double* alpha, int64_t n, int64_t d,
                           int64_t d4, const double* b, double* vt, cudaStream_t st,
                           int64_t* launches);

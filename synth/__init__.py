@@ -183,6 +183,89 @@ def lasso_dense(d: int, n: int, seed: int = SEED0, corr: float = 0.0, support: f
     return A, b
 
 
+# --------------------------------------------------------------------------- sparse (CSC)
+def _csc_block(d: int, density: float, seed: int, blk: int, lo: int, hi: int):
+    """Columns [lo, hi) of counter block blk: each row is a nonzero independently
+    with probability `density` (so nnz_i ~ Binomial(d, density) and, given the
+    count, the rows are uniform without replacement), drawn as geometric gaps;
+    values N(0, 1).  Returns (counts, rows, vals) of the block's columns."""
+    r = _rng(seed, blk, stream=5)
+    nb = hi - lo
+    mean = d * density
+    g = int(mean + 8.0 * math.sqrt(max(mean, 1.0)) + 16)
+    gaps = r.geometric(density, size=(nb, g)).astype(np.int64)
+    pos = np.cumsum(gaps, axis=1) - 1            # row positions, ascending per column
+    counts = (pos < d).sum(axis=1)
+    short = np.nonzero(counts == g)[0]           # (vanishingly rare) ran out of draws: extend
+    rows_list = None
+    if short.size:
+        rows_list = [pos[q, :counts[q]] for q in range(nb)]
+        for q in short:
+            ext = [pos[q]]
+            last = pos[q, -1]
+            while last < d:
+                more = np.cumsum(r.geometric(density, size=g).astype(np.int64)) + last
+                ext.append(more)
+                last = more[-1]
+            allp = np.concatenate(ext)
+            rows_list[q] = allp[allp < d]
+        counts = np.array([x.size for x in rows_list], dtype=np.int64)
+        rows = np.concatenate(rows_list).astype(np.int32)
+    else:
+        rows = pos[pos < d].astype(np.int32)     # row-major mask keeps column order
+    vals = r.standard_normal(rows.size, dtype=np.float32)
+    return counts, rows, vals
+
+
+def csc_lasso(d: int, n: int, seed: int = SEED0 + 5, density: float = 0.01, col_lo: int = 0,
+              col_hi: int | None = None):
+    """Sparse Lasso design (C5): columns [col_lo, col_hi) of a d x n matrix, CSC
+    (col_ptr int64 [k+1], rows int32 ascending per column, values float32)."""
+    col_hi = n if col_hi is None else col_hi
+    b0, b1 = col_lo // BLOCK, (col_hi - 1) // BLOCK
+    jobs = [(blk, max(col_lo, blk * BLOCK), min(col_hi, (blk + 1) * BLOCK)) for blk in range(b0, b1 + 1)]
+
+    def one(job):
+        blk, lo, hi = job
+        c, r_, v = _csc_block(d, density, seed, blk, blk * BLOCK, min(n, (blk + 1) * BLOCK))
+        skip = lo - blk * BLOCK
+        take = hi - lo
+        starts = np.concatenate([[0], np.cumsum(c)])
+        return c[skip:skip + take], r_[starts[skip]:starts[skip + take]], v[starts[skip]:starts[skip + take]]
+
+    with ThreadPoolExecutor(_threads(len(jobs))) as ex:
+        parts = list(ex.map(one, jobs))
+    counts = np.concatenate([p[0] for p in parts])
+    col_ptr = np.zeros(counts.size + 1, dtype=np.int64)
+    np.cumsum(counts, out=col_ptr[1:])
+    rows = np.concatenate([p[1] for p in parts]) if parts else np.zeros(0, np.int32)
+    vals = np.concatenate([p[2] for p in parts]) if parts else np.zeros(0, np.float32)
+    return col_ptr, rows, vals
+
+
+def csc_lasso_signal(col_ptr, rows, vals, d: int, seed: int, support: float = 0.002, col_lo: int = 0,
+                     n_total: int | None = None) -> np.ndarray:
+    """A_shard alpha_true[shard] (fp64) for CSC columns [col_lo, col_lo + k)."""
+    k = col_ptr.size - 1
+    n_total = k + col_lo if n_total is None else n_total
+    at = lasso_truth(n_total, seed, support)[col_lo:col_lo + k]
+    b = np.zeros(d)
+    for i in np.nonzero(at)[0]:
+        sl = slice(col_ptr[i], col_ptr[i + 1])
+        np.add.at(b, rows[sl], at[i] * vals[sl].astype(np.float64))
+    return b
+
+
+def csc_to_dense(col_ptr, rows, vals, d: int, ld: int | None = None) -> np.ndarray:
+    """The (n, ld) float32 dense layout of a CSC matrix (test helper)."""
+    ld = d if ld is None else ld
+    n = col_ptr.size - 1
+    A = np.zeros((n, ld), dtype=np.float32)
+    cols = np.repeat(np.arange(n), np.diff(col_ptr))
+    A[cols, rows] = vals
+    return A
+
+
 # --------------------------------------------------------------------------- structured
 def hadamard(d: int) -> np.ndarray:
     """Sylvester Hadamard matrix H_d (d a power of two), entries +-1, H^T H = d I."""

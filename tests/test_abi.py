@@ -62,3 +62,25 @@ def test_invalid_arguments_rejected_before_device():
         with pytest.raises(D.DuhlError) as e:
             D.create(A, y, lam, model)
         assert e.value.status == 2
+
+
+def test_invalid_csc_rejected_before_device():
+    """duhl_create_csc validates the structure on the host (DUHL_E_INVALID, status 2)."""
+    import paper_1708_05357_b200 as D
+    b = np.ones(5)
+    good = (np.array([0, 2, 3]), np.array([0, 3], np.int32), np.array([1.0, 2.0], np.float32))
+    cases = [
+        (np.array([0, 2, 3]), np.array([3, 0, 1], np.int32), np.ones(3, np.float32)),   # unsorted rows
+        (np.array([0, 2, 3]), np.array([0, 5, 1], np.int32), np.ones(3, np.float32)),   # row >= d
+        (np.array([0, 2, 1]), np.array([0, 1, 1], np.int32), np.ones(3, np.float32)),   # col_ptr decreasing
+        (np.array([1, 2, 3]), np.array([0, 1, 1], np.int32), np.ones(3, np.float32)),   # col_ptr[0] != 0
+        (np.array([0, 2, 3]), np.array([0, 1, 1], np.int32),
+         np.array([1.0, np.nan, 1.0], np.float32)),                                    # non-finite value
+    ]
+    for cp, ri, va in cases:
+        with pytest.raises(D.DuhlError) as e:
+            D.create_csc(cp, ri, va, 5, b, 0.1, D.LASSO)
+        assert e.value.status == 2
+    with pytest.raises(D.DuhlError) as e:           # lambda must be > 0
+        D.create_csc(*good, 5, b, 0.0, D.LASSO)
+    assert e.value.status == 2

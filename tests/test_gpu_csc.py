@@ -1,0 +1,127 @@
+"""GPU parity of the sparse (CSC) path against the CPU oracle.
+
+The oracle is the dense one applied to csc_to_dense(A): a sparse dot product is the
+dense one with the zero terms dropped, so both compute the same definition (the
+order of the nonzero terms is the same ascending row order).  The SCD epoch is
+compared in exact mode (one warp, positions in order == sequential SCD); the
+asynchronous multi-warp mode is checked by its certified convergence and the
+converged objective (north_star: within 1e-4)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from test_gpu_parity import KAPPA, TOL
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    import paper_1708_05357_b200 as D
+    return D
+
+
+def _problem(model, d, n, density, seed):
+    cp, rows, vals = synth.csc_lasso(d, n, seed=seed, density=density)
+    A = synth.csc_to_dense(cp, rows, vals, d)
+    if model == O.LASSO:
+        lab = synth.lasso_finish(synth.csc_lasso_signal(cp, rows, vals, d, seed, support=0.05), d, seed)
+        lam = 0.1 * np.abs(A.astype(np.float64) @ lab).max() / d
+    else:
+        lab = synth.svm_labels(n, seed)[1]
+        lam = 1.0 / n
+    return (cp, rows, vals), A, lab, lam
+
+
+def _random_state(model, n, lab, rng):
+    if model == O.LASSO:
+        return rng.standard_normal(n) * (rng.random(n) < 0.3) * 0.1
+    return lab * rng.random(n) * (rng.random(n) < 0.5)
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_csc_gaps_and_certificate_match_oracle(D, model):
+    d, n = (3001, 2000) if model == O.LASSO else (2999, 1500)
+    csc, A, lab, lam = _problem(model, d, n, 0.01, seed=31 + model)
+    assert (np.diff(csc[0]) == 0).any() or True  # empty columns are allowed (density 1 %)
+    rng = np.random.default_rng(7)
+    alpha = _random_state(model, n, lab, rng)
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    with D.create_csc(*csc, d, lab, lam, model) as P:
+        P.set_state(alpha)
+        g_gpu, s_gpu = P.gaps(want_s=True)
+        G, Ob, Db = P.duality_gap()
+    v = O.matvec(A, alpha)
+    if model == O.LASSO:
+        w = O.primal_dual_w(O.LASSO, v, lab, n, lam)
+        _, s_or, g_or = O.coord_gaps(O.LASSO, A, alpha, None, w, lam, B)
+    else:
+        w = O.primal_dual_w(O.SVM, v, None, n, lam)
+        _, s_or, g_or = O.coord_gaps(O.SVM, A, alpha, lab, w, lam)
+    An = np.linalg.norm(A.astype(np.float64), axis=1)
+    floor = KAPPA * An * np.linalg.norm(w)
+    assert np.all(np.abs(s_gpu - s_or) <= TOL * np.maximum(np.abs(s_or), floor) + 1e-300)
+    c = (np.abs(alpha) + B) / d if model == O.LASSO else (np.abs(alpha) + 1) / n
+    assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), KAPPA * c * An * np.linalg.norm(w)) + 1e-300)
+    st, G_ref, O_ref, D_ref = O.duality_gap(model, A, alpha, lab, lam, B)
+    assert abs(G - G_ref) <= 1e-9 * max(1.0, abs(G_ref))
+    assert abs(Ob - O_ref) <= 1e-9 * max(1.0, abs(O_ref))
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_csc_exact_epoch_matches_sequential_oracle(D, model):
+    d, n, m = 2000, 1200, 700
+    csc, A, lab, lam = _problem(model, d, n, 0.02, seed=41 + model)
+    y = lab if model == O.SVM else None
+    order = synth.permutation(np.arange(m), 3)
+    with D.create_csc(*csc, d, lab, lam, model, m=m, scd_exact=True) as P:
+        sel, _ = P.select(D.SEL_SEQUENTIAL, m=m, round=0)
+        assert sel.tolist() == list(range(m))
+        P.scd_epoch(perm=order)
+        P.scd_epoch(perm=order[::-1].copy())
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = -lab.copy() if model == O.LASSO else np.zeros(d)
+    norms = O.col_norms(A)
+    O.scd_pass(model, A, norms, y, lam, alpha, vt, order)
+    O.scd_pass(model, A, norms, y, lam, alpha, vt, order[::-1].copy())
+    assert np.abs(a_gpu - alpha).max() <= 1e-11 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
+
+
+def test_csc_exact_duhl_solve_follows_algorithm_2(D):
+    """scd_exact: DuHL rounds on the CSC problem follow the oracle's Alg. 2 trajectory."""
+    model = O.LASSO
+    d, n, m = 1500, 1000, 250
+    csc, A, lab, lam = _problem(model, d, n, 0.02, seed=51)
+    eps = 1e-6
+    ref = O.duhl_solve(model, A, lab, lam, m=m, passes=2, refresh_count=50, eps=eps, max_rounds=2000,
+                       cert_every=1, seed=5)
+    assert ref["status"] == O.OK
+    with D.create_csc(*csc, d, lab, lam, model, m=m, refresh_fraction=0.05, cert_every=1, seed=5,
+                      scd_exact=True) as P:
+        r = P.solve(eps, 2000, passes=2)
+    assert r["status"] == 0 and r["gap"] <= eps
+    g_gpu = np.array([t.cert_gap for t in r["trace"]])
+    k = min(5, len(g_gpu), len(ref["gaps"]))
+    np.testing.assert_allclose(g_gpu[:k], ref["gaps"][:k], rtol=1e-8)
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_csc_async_solve_certifies_and_matches_objective(D, model):
+    d, n = (4000, 3000) if model == O.LASSO else (3000, 2000)
+    csc, A, lab, lam = _problem(model, d, n, 0.01, seed=61 + model)
+    eps = 1e-6
+    with D.create_csc(*csc, d, lab, lam, model, m=n // 4, refresh_fraction=0.1, cert_every=5,
+                      scd_exact=False) as P:
+        r = P.solve(eps, 5000, passes=2)
+        a, v, _ = P.get_state()
+        G, Ob, Db = P.duality_gap()
+    assert r["status"] == 0 and G <= eps
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    st, G_o, O_o, D_o = O.duality_gap(model, A, a, lab, lam, B)   # the oracle certifies the GPU's alpha
+    assert G_o <= 1.01 * eps and abs(O_o - Ob) <= 1e-9 * max(1.0, abs(O_o))
+    ref = O.solve_scd(model, A, lab, lam, 1e-9, 20000)
+    _, _, O_ref, _ = O.duality_gap(model, A, ref[1], lab, lam, B)
+    assert abs(Ob - O_ref) <= 1e-4 * abs(O_ref)
