@@ -42,6 +42,14 @@ CONFIGS = {
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None,
                label="C4: hinge-SVM dual, ImageNet-shaped dense synthetic 200704 features x 40000 "
                      "samples fp32 (32.1 GB pinned host), HBM budget 25% (8.03 GB), m=10000"),
+    "c5": dict(model=0, sparse=True, d=40000, n=10_000_000, density=0.01, budget_frac=0.0, m=2_500_000,
+               lam=None, lam_rel=0.1, support=0.002,
+               label="C5: sparse Lasso, CSC synthetic 40000 samples x 10M features, 1% density (4e9 nonzeros, "
+                     "32 GB), resident in HBM, m=25% of local columns, lambda=0.1 lambda_max"),
+    "c5s": dict(model=0, sparse=True, d=40000, n=1_250_000, density=0.01, budget_frac=0.0, m=312_500,
+                lam=None, lam_rel=0.1, support=0.002,
+                label="C5 shard: sparse Lasso, CSC 40000 samples x 1.25M features (one of C5's 8 feature "
+                      "blocks), 1% density, resident, m=25%, lambda=0.1 lambda_max"),
     "c2": dict(model=1, d=500, n=20000, budget_frac=0.0, m=2000, lam=None,
                label="C2: hinge-SVM dual, dense synthetic 500 features x 20000 samples, m=10%"),
     "c1": dict(model=0, d=2000, n=1000, budget_frac=0.0, m=250, lam=0.1,
@@ -161,11 +169,42 @@ def _allreduce_host(x, world, op="sum"):
     return t.cpu().numpy()
 
 
+class Sparse:
+    """A CSC column block (col_ptr, rows, vals) of a sparse config."""
+
+    def __init__(self, cp, rows, vals, d):
+        self.cp, self.rows, self.vals, self.d = cp, rows, vals, d
+        self.shape = (cp.size - 1, d)
+
+    def dense(self, ncols):
+        import synth
+        k = min(ncols, self.shape[0])
+        e = self.cp[k]
+        return synth.csc_to_dense(self.cp[:k + 1], self.rows[:e], self.vals[:e], self.d)
+
+    def __matmul__(self, b):  # A^T b over the block's columns (lambda_max)
+        out = np.add.reduceat(self.vals.astype(np.float64) * b[self.rows], self.cp[:-1])
+        return np.where(np.diff(self.cp) > 0, out, 0.0)
+
+
+def create(D, A, lab, lam, model, **kw):
+    """duhl_create (dense) or duhl_create_csc (sparse) with the bench's options."""
+    if isinstance(A, Sparse):
+        for k in ("hbm_budget_bytes", "borrow_host", "unit_a_ctas"):
+            kw.pop(k, None)
+        return D.create_csc(A.cp, A.rows, A.vals, A.d, lab, lam, model, **kw)
+    return D.create(A, lab, lam, model, **kw)
+
+
 def make_data(cfg, seed, col_lo=0, col_hi=None, world=1):
     """The columns [col_lo, col_hi) of the config's matrix and the (global) labels."""
     import synth
     d, n = cfg["d"], cfg["n"]
     col_hi = n if col_hi is None else col_hi
+    if cfg.get("sparse"):
+        cp, rows, vals = synth.csc_lasso(d, n, seed, density=cfg["density"], col_lo=col_lo, col_hi=col_hi)
+        sig = synth.csc_lasso_signal(cp, rows, vals, d, seed, support=cfg["support"], col_lo=col_lo, n_total=n)
+        return Sparse(cp, rows, vals, d), synth.lasso_finish(_allreduce_host(sig, world), d, seed)
     A = np.empty((col_hi - col_lo, d), dtype=np.float32)
     if cfg["model"] == 1:
         lab = synth.svm_fill(A, d, n, seed, col_lo=col_lo)
@@ -182,7 +221,7 @@ def lam_of(cfg, A=None, lab=None, world=1):
         return cfg["lam"]
     if cfg.get("lam_rel") is None:
         return 1.0 / cfg["n"]
-    s = np.abs(A @ lab.astype(np.float32)).max()
+    s = np.abs(A @ (lab if isinstance(A, Sparse) else lab.astype(np.float32))).max()
     lmax = float(_allreduce_host(np.array([s], dtype=np.float64), world, "max")[0]) / cfg["d"]
     return cfg["lam_rel"] * lmax
 
@@ -193,7 +232,7 @@ def oracle_sample(cfg, A, lab, lam, ncols, passes=1):
     `passes` sequential SCD passes over `ncols` columns of the same data, plus a
     gap pass over them.  Returns (updates/s, gap GB/s, seconds)."""
     import oracle as O
-    Asub = np.ascontiguousarray(A[:ncols])
+    Asub = A.dense(ncols) if isinstance(A, Sparse) else np.ascontiguousarray(A[:ncols])
     lab_s = lab[:ncols] if cfg["model"] == 1 else lab
     norms = O.col_norms(Asub)
     alpha = np.zeros(ncols)
@@ -217,7 +256,8 @@ def run_reference(args, cfg, rank, world):
         return
     seed = 170805357 + 3
     ncols = args.ref_cols
-    A, lab = make_data(cfg, seed, 0, ncols) if cfg["model"] == 1 else make_data(cfg, seed)
+    A, lab = (make_data(cfg, seed, 0, ncols) if cfg["model"] == 1 or cfg.get("sparse") else
+              make_data(cfg, seed))
     lam = lam_of(cfg, A, lab)
     for _ in range(args.warmup):
         oracle_sample(cfg, A, lab, lam, min(ncols, 64))
@@ -271,7 +311,7 @@ def run_duhl(args, cfg, rank, world, local):
 
     # ---------------- device-timed steady-state rounds
     t_create = time.perf_counter()
-    P = D.create(A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, scd_exact=args.exact,
+    P = create(D, A, lab, lam, cfg["model"], profile=True, cert_every=1 << 40, scd_exact=args.exact,
                  **common)
     if uid is not None:
         P.comm_init(uid, world, rank)
@@ -299,7 +339,7 @@ def run_duhl(args, cfg, rank, world, local):
     c1 = P.counters()
     pcie_peak = pcie_h2d_peak(local)
     pcie_bytes = (c1["h2d_bytes"] - c0["h2d_bytes"] + c1["zc_bytes"] - c0["zc_bytes"]) / args.steps
-    pcie = {"bytes_per_step": pcie_bytes,
+    pcie = None if budget == 0 else {"bytes_per_step": pcie_bytes,
             "copy_bytes_per_step": (c1["h2d_bytes"] - c0["h2d_bytes"]) / args.steps,
             "zero_copy_bytes_per_step": (c1["zc_bytes"] - c0["zc_bytes"]) / args.steps,
             "achieved_GBps": pcie_bytes / (elapsed / args.steps) / 1e9,
@@ -345,7 +385,7 @@ def run_duhl(args, cfg, rank, world, local):
     if not args.no_e2e:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        P2 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
+        P2 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
                       **common)
         if uid is not None:
             P2.comm_init(uid, world, rank)
@@ -382,7 +422,7 @@ def run_duhl(args, cfg, rank, world, local):
             pol = {"sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM}[pol_name]
             t0 = time.perf_counter()
             cb = dict(common, refresh_fraction=0.0)  # batch baselines do not read z
-            P3 = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
+            P3 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
                           **cb)
             if uid is not None:
                 P3.comm_init(uid, world, rank)
@@ -414,8 +454,10 @@ def run_duhl(args, cfg, rank, world, local):
             "config": {"workload": cfg["label"], "d": d, "n": n, "m": m, "passes": args.passes,
                        "policy": args.policy, "refresh_fraction": args.refresh,
                        "hbm_budget_GB": budget / 1e9, "lambda": lam,
-                       "l2": "inputs larger than L2 (working set 8 GB >> 126 MB L2)"
-                       if budget else "working set may be L2-resident (small config)",
+                       "l2": ("inputs larger than L2 (CSC matrix resident in HBM >> 126 MB L2)"
+                              if cfg.get("sparse") else
+                              "inputs larger than L2 (working set 8 GB >> 126 MB L2)" if budget
+                              else "working set may be L2-resident (small config)"),
                        "parallelism": f"cocoa{world}"},
             "roofline": roofline,
             "pcie": pcie,

@@ -282,7 +282,12 @@ static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, dou
     if (!write_z) p.z = nullptr;
     if (s_acc) p.s_acc = s_acc;
     const int64_t tiles = (ctx->d4 + tile_rows - 1) / tile_rows;
-    ProfScope ps(ctx, sx, stream ? 4 : 1, (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
+    // algorithmic bytes: dense 4 d4 + 24 per column (+ w tiles); CSC 8 per nonzero + 24 per column
+    const double by = !ctx->csc ? (double)p.k * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles
+                      : !d_cols ? 8.0 * (double)ctx->nnz + 24.0 * (double)ctx->n
+                      : d_cols == ctx->d_P ? ctx->csc_pass_bytes
+                      : (double)p.k * (8.0 * (double)ctx->nnz / (double)ctx->n + 24.0);
+    ProfScope ps(ctx, sx, stream ? 4 : 1, by);
     if (ctx->csc) CK(launch_csc_gap(p, cscmat(ctx), max_ctas, sx, &ctx->launches));
     else CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches, max_ctas));
     return DUHL_OK;
