@@ -85,6 +85,7 @@ struct duhl_ctx {
     std::vector<int64_t> h_colptr;  // host copy of col_ptr (algorithmic byte counts)
     double csc_pass_bytes = 0.0;    // algorithmic bytes of one SCD pass over the current order
     int csc_warps = 0;              // concurrent coordinates of the asynchronous CSC epoch
+    void* d_topm_work = nullptr;    // scratch of the multi-CTA top-m
     int64_t ld_host = 0;
     const float* h_alias = nullptr;  // device address of h_store
     // ---- unit B: HBM slot pool
@@ -497,7 +498,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_dv, ctx->d_aold, ctx->d_ls,
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
-                        ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals};
+                        ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -744,6 +745,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
                        : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 &&
                           ctx->cfg.refresh_fraction > 0.0) ? 16 : 0;
     choose_scd_shape(ctx);
+    if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes())) return bail(DUHL_E_NOMEM);
     if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
@@ -861,7 +863,7 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
     } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM) {
         ProfScope ps(ctx, ctx->st, 2, 8.0 * ctx->n * 7);
         CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
-                       ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches));
+                       ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches, ctx->d_topm_work));
         P.resize(m);
         CK(cudaMemcpyAsync(P.data(), ctx->d_P, m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));

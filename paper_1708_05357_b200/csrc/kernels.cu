@@ -8,6 +8,7 @@
 // Data layout: A column-major float32; every column padded with zeros to d4 =
 // round_up(d, 4) rows so each column is a whole number of 16-byte vectors.
 // All accumulation is fp64 (fp32 x fp32 products are exact in fp64).
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <type_traits>
@@ -228,6 +229,7 @@ cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* n
 constexpr int kTopThreads = 1024;
 constexpr int kRadixBits = 11;
 constexpr int kBins = 1 << kRadixBits;
+constexpr int64_t kTopmSmallN = 1 << 17;  // one CTA up to here, the multi-CTA form beyond
 
 __device__ __forceinline__ uint64_t select_key(const double* z, int64_t i, int keymode,
                                                uint64_t seed, int64_t round, int* bad) {
@@ -299,13 +301,167 @@ __global__ void __launch_bounds__(kTopThreads) k_topm(const double* z, int64_t n
     if (bad) atomicOr(flag, 1);
 }
 
+// ---- multi-CTA form for large n (same semantics, same output): per digit, a
+// grid-wide histogram of the candidate keys + a one-CTA pick of the digit; then
+// per-chunk counts, a one-CTA scan of the chunk offsets, and an in-order write.
+struct TopmState {
+    unsigned long long prefix, pmask;
+    long long need;
+};
+constexpr int kTopChunks = 1024;  // CTAs (and contiguous index chunks) of the multi-CTA form
+
+__global__ void __launch_bounds__(kTopThreads) k_topm_hist(const double* z, int64_t n, int keymode, uint64_t seed,
+                                                           int64_t round, const TopmState* stt, int shift,
+                                                           int nbits, int* ghist, int* flag) {
+    __shared__ int hist[kBins];
+    const int tid = threadIdx.x;
+    for (int b = tid; b < kBins; b += kTopThreads) hist[b] = 0;
+    __syncthreads();
+    const unsigned long long prefix = stt->prefix, pmask = stt->pmask, dmask = (1ull << nbits) - 1;
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * kTopThreads + tid; i < n; i += (int64_t)gridDim.x * kTopThreads) {
+        const uint64_t k = select_key(z, i, keymode, seed, round, &bad);
+        if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & dmask], 1);
+    }
+    __syncthreads();
+    for (int b = tid; b < kBins; b += kTopThreads)
+        if (hist[b]) atomicAdd(&ghist[b], hist[b]);
+    if (bad && shift == 64 - kRadixBits) atomicOr(flag, 1);
+}
+
+__global__ void __launch_bounds__(kTopThreads) k_topm_pick(int* ghist, TopmState* stt, int shift, int nbits) {
+    typedef cub::BlockScan<int, kTopThreads> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_digit, s_above;
+    const int tid = threadIdx.x;
+    const long long need = stt->need;
+    const int e0 = kBins - 1 - 2 * tid, e1 = e0 - 1;
+    const int c0 = ghist[e0], c1 = ghist[e1];
+    int excl;
+    Scan(scan_tmp).ExclusiveSum(c0 + c1, excl);
+    if (excl < need && need <= excl + c0) { s_digit = e0; s_above = excl; }
+    else if (excl + c0 < need && need <= excl + c0 + c1) { s_digit = e1; s_above = excl + c0; }
+    __syncthreads();
+    ghist[e0] = 0;  // ready for the next digit
+    ghist[e1] = 0;
+    if (tid == 0) {
+        stt->need = need - s_above;
+        stt->prefix |= (unsigned long long)s_digit << shift;
+        stt->pmask |= ((1ull << nbits) - 1) << shift;
+    }
+}
+
+// per chunk: keys above the threshold and keys equal to it
+__global__ void __launch_bounds__(kTopThreads) k_topm_count(const double* z, int64_t n, int keymode, uint64_t seed,
+                                                            int64_t round, const TopmState* stt, int64_t chunk,
+                                                            int* cnt) {
+    typedef cub::BlockReduce<int, kTopThreads> Red;
+    __shared__ typename Red::TempStorage tmp;
+    const unsigned long long thr = stt->prefix;
+    int gt = 0, eq = 0, bad = 0;
+    const int64_t lo = (int64_t)blockIdx.x * chunk, hi = imin64(n, lo + chunk);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kTopThreads) {
+        const uint64_t k = select_key(z, i, keymode, seed, round, &bad);
+        gt += k > thr;
+        eq += k == thr;
+    }
+    gt = Red(tmp).Sum(gt);
+    __syncthreads();
+    eq = Red(tmp).Sum(eq);
+    if (threadIdx.x == 0) {
+        cnt[2 * blockIdx.x] = gt;
+        cnt[2 * blockIdx.x + 1] = eq;
+    }
+}
+
+// chunk offsets: eq keys before the chunk, then the output position of its first kept key
+__global__ void __launch_bounds__(kTopThreads) k_topm_offsets(int* cnt, const TopmState* stt, int nch) {
+    typedef cub::BlockScan<long long, kTopThreads> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int c = threadIdx.x;
+    const long long gt = c < nch ? cnt[2 * c] : 0, eq = c < nch ? cnt[2 * c + 1] : 0;
+    long long eq_before;
+    Scan(tmp).ExclusiveSum(eq, eq_before);
+    __syncthreads();
+    const long long need = stt->need;
+    long long eq_take = need - eq_before;
+    eq_take = eq_take < 0 ? 0 : (eq_take > eq ? eq : eq_take);
+    long long out;
+    Scan(tmp).ExclusiveSum(gt + eq_take, out);
+    if (c < nch) {
+        cnt[2 * c] = (int)out;         // output offset of the chunk
+        cnt[2 * c + 1] = (int)eq_before;  // equal keys before the chunk
+    }
+}
+
+__global__ void __launch_bounds__(kTopThreads) k_topm_write(const double* z, int64_t n, int keymode, uint64_t seed,
+                                                            int64_t round, const TopmState* stt, int64_t chunk,
+                                                            const int* cnt, int64_t* P_out) {
+    typedef cub::BlockScan<int, kTopThreads> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    const int tid = threadIdx.x;
+    const unsigned long long thr = stt->prefix;
+    const long long need = stt->need;
+    long long base = cnt[2 * blockIdx.x], eqbase = cnt[2 * blockIdx.x + 1];
+    int bad = 0;
+    const int64_t lo = (int64_t)blockIdx.x * chunk, hi = imin64(n, lo + chunk);
+    for (int64_t i0 = lo; i0 < hi; i0 += kTopThreads) {
+        const int64_t i = i0 + tid;
+        int gt = 0, eq = 0;
+        if (i < hi) {
+            const uint64_t k = select_key(z, i, keymode, seed, round, &bad);
+            gt = k > thr;
+            eq = k == thr;
+        }
+        int eq_excl, eq_tot;
+        Scan(scan_tmp).ExclusiveSum(eq, eq_excl, eq_tot);
+        __syncthreads();
+        const int take = gt || (eq && (eqbase + eq_excl) < need);
+        int pos, tot;
+        Scan(scan_tmp).ExclusiveSum(take, pos, tot);
+        if (take) P_out[base + pos] = i;
+        base += tot;
+        eqbase += eq_tot;
+        __syncthreads();
+    }
+}
+
 cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,
                         int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
-                        int64_t* launches) {
-    k_topm<<<1, kTopThreads, 0, st>>>(z, n, m, keymode, seed, round, P_out, flag);
-    ++*launches;
+                        int64_t* launches, void* work) {
+    if (m <= 0) return cudaSuccess;
+    if (n <= kTopmSmallN || !work) {
+        k_topm<<<1, kTopThreads, 0, st>>>(z, n, m, keymode, seed, round, P_out, flag);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    // work: TopmState | ghist[kBins] | cnt[2 kTopChunks]  (launch_topm_work_bytes)
+    TopmState* stt = reinterpret_cast<TopmState*>(work);
+    int* ghist = reinterpret_cast<int*>(reinterpret_cast<char*>(work) + 64);
+    int* cnt = ghist + kBins;
+    TopmState init{0ull, 0ull, (long long)m};
+    cudaError_t e = cudaMemcpyAsync(stt, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ghist, 0, kBins * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)imin64(kTopChunks, cdiv(n, 4 * kTopThreads));
+    for (int hi = 64; hi > 0;) {
+        const int nbits = hi < kRadixBits ? hi : kRadixBits;
+        const int shift = hi - nbits;
+        k_topm_hist<<<grid, kTopThreads, 0, st>>>(z, n, keymode, seed, round, stt, shift, nbits, ghist, flag);
+        k_topm_pick<<<1, kTopThreads, 0, st>>>(ghist, stt, shift, nbits);
+        *launches += 2;
+        hi = shift;
+    }
+    const int64_t chunk = cdiv(n, grid);
+    k_topm_count<<<grid, kTopThreads, 0, st>>>(z, n, keymode, seed, round, stt, chunk, cnt);
+    k_topm_offsets<<<1, kTopThreads, 0, st>>>(cnt, stt, grid);
+    k_topm_write<<<grid, kTopThreads, 0, st>>>(z, n, keymode, seed, round, stt, chunk, cnt, P_out);
+    *launches += 3;
     return cudaGetLastError();
 }
+
+size_t launch_topm_work_bytes() { return 64 + kBins * sizeof(int) + 2 * kTopChunks * sizeof(int); }
 
 // =====================================================================================
 // Pass permutation: position t takes P[pi(t)], pi a
@@ -1344,7 +1500,8 @@ cudaError_t preload_kernels() {
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,
         (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
-        (const void*)k_csc_matvec};
+        (const void*)k_csc_matvec,  (const void*)k_topm_hist,    (const void*)k_topm_pick,
+        (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);

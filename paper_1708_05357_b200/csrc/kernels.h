@@ -91,9 +91,11 @@ cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, 
                             int max_ctas = 0);
 cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* norms,
                              cudaStream_t st, int64_t* launches);
+// work: device scratch of launch_topm_work_bytes() (multi-CTA form for large n; nullptr = one CTA)
 cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint64_t seed,
                         int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
-                        int64_t* launches);
+                        int64_t* launches, void* work = nullptr);
+size_t launch_topm_work_bytes();
 // Pass order + per-position inputs.  P == nullptr: order_j/slot/batch already
 // hold an explicit order of length m; only alpha / 1/norm / y are gathered.
 cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,

@@ -377,3 +377,20 @@ def test_first_solve_in_a_fresh_process():
     code = ("import __graft_entry__ as g; g.smoke()")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,m", [(300_001, 7_000), (1_000_000, 250_000)])
+def test_select_multi_cta_large_n_with_ties(D, n, m):
+    """The multi-CTA top-m (n > 2^17) against the oracle's rule, on gaps with massive exact
+    ties (columns in 6 scale classes, some zero) and on the uniform-baseline keys."""
+    rng = np.random.default_rng(n)
+    A = np.zeros((n, 4), dtype=np.float32)
+    A[:, 0] = rng.choice(np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0], dtype=np.float32), n)
+    with D.create(A, np.ones(4), 0.1, D.LASSO, m=m) as P:
+        z = P.gaps()
+        sel, _ = P.select(D.SEL_GAP, m=m, round=0)
+    assert len(np.unique(z)) <= 6
+    assert sel.tolist() == np.sort(O.select_topm(z, m)).tolist()
+    with D.create(A, np.ones(4), 0.1, D.LASSO, m=m, seed=9) as P:
+        sel_u, _ = P.select(D.SEL_UNIFORM, m=m, round=3)
+    assert sel_u.tolist() == np.sort(O.select_policy(O.SEL_UNIFORM, n, m, 3, 9)).tolist()
