@@ -86,6 +86,13 @@ struct duhl_ctx {
     double csc_pass_bytes = 0.0;    // algorithmic bytes of one SCD pass over the current order
     int csc_warps = 0;              // concurrent coordinates of the asynchronous CSC epoch
     void* d_topm_work = nullptr;    // scratch of the multi-CTA top-m
+    // resident problems (no slot pool) keep P on the device: the host copy and inP are
+    // refreshed only when an ABI call needs them
+    int* d_stamp = nullptr;         // [n] id of the select that last took column j
+    unsigned long long* d_rsel = nullptr;  // [2] swaps, nnz over P
+    int sel_id = 0;
+    int64_t m_cur = 0;              // |P|
+    bool P_host_valid = true;
     int64_t ld_host = 0;
     const float* h_alias = nullptr;  // device address of h_store
     // ---- unit B: HBM slot pool
@@ -399,6 +406,33 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
 // launch; the kernel waits on the copy-progress counter per block, so staging
 // overlaps the epoch).  New columns enter the device table after the epoch
 // (finalize_staging).
+// Resident problem: d_P holds the new working set (m entries); slots/batches,
+// swap count and the CSC pass bytes come from one device pass (no O(n) host work).
+static duhl_status resident_commit(duhl_ctx* ctx, int64_t m, int64_t* swaps) {
+    ++ctx->sel_id;
+    CK(launch_resident_select(ctx->d_P, m, ctx->d_stamp, ctx->sel_id, ctx->d_P_slot, ctx->d_P_batch,
+                              ctx->csc ? ctx->d_colptr : nullptr, ctx->d_rsel, ctx->st, &ctx->launches));
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, ctx->d_rsel, sizeof(h), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->m_cur = m;
+    if (ctx->csc) ctx->csc_pass_bytes = 8.0 * (double)h[1] + 24.0 * (double)m;
+    if (swaps) *swaps = (int64_t)h[0];
+    return DUHL_OK;
+}
+
+// The host copy of P (and inP) for the calls that need it (explicit-order epochs, P_out).
+static duhl_status ensure_host_P(duhl_ctx* ctx) {
+    if (ctx->P_host_valid) return DUHL_OK;
+    ctx->P.resize(ctx->m_cur);
+    CK(cudaMemcpyAsync(ctx->P.data(), ctx->d_P, ctx->m_cur * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
+    for (int64_t j : ctx->P) ctx->inP[j] = 1;
+    ctx->P_host_valid = true;
+    return DUHL_OK;
+}
+
 static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& P, int64_t round,
                                      int64_t* swaps) {
     TRY(finalize_staging(ctx));
@@ -461,8 +495,14 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
-    } else {
-        for (int64_t j : P) if (!ctx->inP[j]) ++nsw;  // logical swaps (everything is resident)
+    } else {  // everything resident: bookkeeping on the device
+        CK(cudaMemcpyAsync(ctx->d_P, P.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        TRY(resident_commit(ctx, m, swaps));
+        ctx->P = P;
+        std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
+        for (int64_t j : P) ctx->inP[j] = 1;
+        ctx->P_host_valid = true;
+        return DUHL_OK;
     }
     TRY(upload_slots_changes(ctx, chg_cols, chg_slots));
     std::vector<int> Ps(m);
@@ -476,11 +516,8 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
     CK(cudaMemcpyAsync(ctx->d_P_batch, Pb.data(), m * sizeof(unsigned), cudaMemcpyHostToDevice, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     ctx->P = P;
-    if (ctx->csc) {  // algorithmic bytes of a pass: 8 B per nonzero + 24 B per coordinate
-        double by = 0.0;
-        for (int64_t j : P) by += 8.0 * (double)(ctx->h_colptr[j + 1] - ctx->h_colptr[j]) + 24.0;
-        ctx->csc_pass_bytes = by;
-    }
+    ctx->m_cur = m;
+    ctx->P_host_valid = true;
     std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
     for (int64_t j : P) ctx->inP[j] = 1;
     if (swaps) *swaps = nsw;
@@ -498,7 +535,8 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_dv, ctx->d_aold, ctx->d_ls,
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
-                        ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work};
+                        ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
+                        ctx->d_stamp, ctx->d_rsel};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -745,7 +783,10 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
                        : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 &&
                           ctx->cfg.refresh_fraction > 0.0) ? 16 : 0;
     choose_scd_shape(ctx);
-    if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes())) return bail(DUHL_E_NOMEM);
+    if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
+        !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)))
+        return bail(DUHL_E_NOMEM);
+    if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
     if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
@@ -861,9 +902,17 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
         int64_t lo = kb * m, hi = std::min(ctx->n, lo + m);
         for (int64_t i = lo; i < hi; ++i) P.push_back(i);
     } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM) {
-        ProfScope ps(ctx, ctx->st, 2, 8.0 * ctx->n * 7);
-        CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
-                       ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches, ctx->d_topm_work));
+        {
+            ProfScope ps(ctx, ctx->st, 2, 8.0 * ctx->n * 7);
+            CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
+                           ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches, ctx->d_topm_work));
+        }
+        if (ctx->cfg.hbm_budget_bytes == 0) {  // resident: P stays on the device
+            TRY(finalize_staging(ctx));
+            TRY(resident_commit(ctx, m, n_swaps_out));
+            ctx->P_host_valid = false;
+            return check_flag(ctx, "duhl_select");
+        }
         P.resize(m);
         CK(cudaMemcpyAsync(P.data(), ctx->d_P, m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
@@ -881,7 +930,10 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
     TRY(finalize_staging(ctx));
     ctx->overlap = ctx->write_value != nullptr;
     TRY(select_impl(ctx, policy, m, round, n_swaps_out));
-    if (P_out) std::memcpy(P_out, ctx->P.data(), ctx->P.size() * sizeof(int64_t));
+    if (P_out) {
+        TRY(ensure_host_P(ctx));
+        std::memcpy(P_out, ctx->P.data(), ctx->P.size() * sizeof(int64_t));
+    }
     return DUHL_OK;
 }
 
@@ -973,7 +1025,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
 // enqueued after the pass-0 launch when they overlap it (the kernel waits on the
 // progress counter per block), else before it (the compute stream waits).
 static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
-    const int64_t m = (int64_t)ctx->P.size();
+    const int64_t m = ctx->m_cur;
     if (!ctx->overlap) TRY(issue_staging(ctx));
     for (int pass = 0; pass < passes; ++pass) {
         CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
@@ -990,8 +1042,9 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
                            int64_t perm_len) {
     if (!ctx) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
-    if (ctx->P.empty()) return fail(ctx, DUHL_E_INVALID, "no working set: call duhl_select first");
+    if (ctx->m_cur == 0) return fail(ctx, DUHL_E_INVALID, "no working set: call duhl_select first");
     if (perm) {
+        TRY(ensure_host_P(ctx));
         if (perm_len < 0 || perm_len > (int64_t)ctx->P.size()) return fail(ctx, DUHL_E_INVALID, "perm_len");
         std::vector<char> seen(ctx->n, 0);
         std::vector<int> slots(perm_len);
@@ -1083,7 +1136,7 @@ duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double*
 //                  bracket its sign change on 64-point grids (one allreduce each),
 //                  then solve the linear piece inside the final bracket.
 static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
-    const int64_t m = (int64_t)ctx->P.size();
+    const int64_t m = ctx->m_cur;
     const double dd = (double)ctx->d, nn = (double)ctx->n_glob, lam = ctx->lambda;
     CK(launch_delta_v(ctx->d_vt, ctx->d_vsnap, ctx->d4, ctx->d_dv, ctx->d_ls + 64, ctx->st, &ctx->launches));
     TRY(allreduce(ctx, ctx->d_dv, (size_t)ctx->d4));
@@ -1182,7 +1235,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
     if (agg) {  // round-start state for the aggregation: v0 and alpha_P
         CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
-        CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, (int64_t)ctx->P.size(), ctx->d_aold, ctx->st,
+        CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, ctx->m_cur, ctx->d_aold, ctx->st,
                              &ctx->launches));
     }
     if (kref > 0) {  // unit A (l.7-10): gaps at alpha^(t) on its own stream, beside the
@@ -1210,7 +1263,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     if (kref > 0 && ctx->unit_a_ctas > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));  // join unit A
     double gamma = 1.0;
     if (agg) TRY(aggregate(ctx, &gamma));                                   // l.11 across ranks
-    const int64_t m = (int64_t)ctx->P.size();                              // z_P at alpha^(t+1) (R9)
+    const int64_t m = ctx->m_cur;                                          // z_P at alpha^(t+1) (R9)
     TRY(run_gaps(ctx, ctx->d_P, m, nullptr, nullptr, nullptr));
     double cg = -1.0;
     if (certify) TRY(certificate(ctx, &cg, nullptr, nullptr));

@@ -1486,6 +1486,41 @@ cudaError_t launch_csc_matvec(const CscMat& A, const double* alpha, int64_t n, d
     return cudaGetLastError();
 }
 
+// Resident working set (no slot pool): slot of P[q] = P[q], no staging; count the
+// coordinates not selected last time (stamp[j] == sel - 1) and, for CSC, the
+// algorithmic bytes of a pass over P; stamp the new members with sel.
+__global__ void k_resident_select(const int64_t* P, int64_t m, int* stamp, int sel, int* P_slot,
+                                  unsigned* P_batch, const int64_t* col_ptr, unsigned long long* out) {
+    unsigned long long sw = 0, by = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = P[q];
+        P_slot[q] = (int)j;
+        P_batch[q] = 0u;
+        sw += stamp[j] != sel - 1;
+        stamp[j] = sel;
+        if (col_ptr) by += (unsigned long long)(col_ptr[j + 1] - col_ptr[j]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sw += __shfl_xor_sync(~0u, sw, o);
+        by += __shfl_xor_sync(~0u, by, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (sw) atomicAdd(&out[0], sw);
+        if (by) atomicAdd(&out[1], by);
+    }
+}
+
+cudaError_t launch_resident_select(const int64_t* P, int64_t m, int* stamp, int sel, int* P_slot,
+                                   unsigned* P_batch, const int64_t* col_ptr, unsigned long long* out,
+                                   cudaStream_t st, int64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess || m <= 0) return e;
+    k_resident_select<<<(unsigned)imin64(cdiv(m, 256), 1184), 256, 0, st>>>(P, m, stamp, sel, P_slot, P_batch,
+                                                                           col_ptr, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // Load every kernel of the library now.  Under lazy module loading (the CUDA 12
 // default) the first launch of a kernel loads it, and that load can wait for the
 // device to go idle -- fatal while the SCD kernel waits on staging copies the
@@ -1501,7 +1536,8 @@ cudaError_t preload_kernels() {
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,
         (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
         (const void*)k_csc_matvec,  (const void*)k_topm_hist,    (const void*)k_topm_pick,
-        (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write};
+        (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write,
+        (const void*)k_resident_select};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -96,6 +96,10 @@ cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint
                         int64_t round, int64_t* P_out, int* flag, cudaStream_t st,
                         int64_t* launches, void* work = nullptr);
 size_t launch_topm_work_bytes();
+// resident working set bookkeeping on the device (see k_resident_select); out[0] swaps, out[1] nnz over P
+cudaError_t launch_resident_select(const int64_t* P, int64_t m, int* stamp, int sel, int* P_slot,
+                                   unsigned* P_batch, const int64_t* col_ptr, unsigned long long* out,
+                                   cudaStream_t st, int64_t* launches);
 // Pass order + per-position inputs.  P == nullptr: order_j/slot/batch already
 // hold an explicit order of length m; only alpha / 1/norm / y are gathered.
 cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
