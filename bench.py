@@ -505,12 +505,12 @@ def main():
                     help="CTAs of the unit-A refresh beside the epoch (0 auto, -1 off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
-    rank, world, local = dist_init(args.gpus)
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
-    else:
-        run_duhl(args, cfg, rank, world, local)
+    if args.impl == "reference":  # the CPU oracle: rank 0 alone, no process group needed
+        run_reference(args, cfg, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    rank, world, local = dist_init(args.gpus)
+    run_duhl(args, cfg, rank, world, local)
 
 
 if __name__ == "__main__":
