@@ -101,6 +101,11 @@ typedef struct {
                                  SCD grid leaves them their SMs.  0 = auto (16 when the data exceeds the
                                  budget and refresh_fraction > 0), -1 = off (the refresh runs on the
                                  whole GPU before the epoch) */
+    int scd_kernel;           /* dense exact SCD kernel: 1 = warp-specialised (a control warp in every CTA,
+                                 W <= 16); 2 = pipelined (one control CTA runs the sequential steps; Gram
+                                 tiles of block b+1 run before delta_{b-1} is known; W <= 32); 0 = auto
+                                 (pipelined where shared memory holds W >= 24).  Both execute the same
+                                 sequential order (App. D), up to summation order. */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -117,7 +122,7 @@ typedef struct {
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,
  * refresh_fraction 0.05, cert_every 10, seed 170805357, borrow_host 0,
  * cert_adaptive 1, profile 0, scd_exact 1, n_global 0, col_offset 0,
- * linesearch 0, unit_a_ctas 0. */
+ * linesearch 0, unit_a_ctas 0, scd_kernel 0. */
 void duhl_default_config(duhl_config* cfg);
 
 /* Creates a problem instance.

@@ -41,7 +41,7 @@ class Config(C.Structure):
                 ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
                 ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
                 ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int),
-                ("unit_a_ctas", C.c_int)]
+                ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int)]
 
 
 class RoundRecord(C.Structure):
@@ -222,7 +222,7 @@ class Problem:
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
            cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
-           linesearch=False, unit_a_ctas=0):
+           linesearch=False, unit_a_ctas=0, scd_kernel=0):
     """duhl_create.  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -237,7 +237,7 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
                          profile=int(bool(profile)), scd_exact=int(bool(scd_exact)),
                          n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)),
-                         unit_a_ctas=unit_a_ctas)
+                         unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel)
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

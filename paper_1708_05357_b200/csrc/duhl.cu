@@ -71,6 +71,7 @@ struct duhl_ctx {
     duhl_config cfg{};
     std::string err;
     int dev = 0, nsm = 0, unit_a_ctas = 0;
+    bool pipe = false;  // SCD epoch runs k_scd_pipe (else k_scd_gram); see choose_scd_shape
     cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
     cudaEvent_t ev_copy = nullptr, ev_snap = nullptr, ev_ref = nullptr;
     // ---- unit A: pinned host store
@@ -552,12 +553,41 @@ static void free_all(duhl_ctx* ctx) {
     if (ctx->cst) cudaStreamDestroy(ctx->cst);
 }
 
+static size_t scd_red_bytes(const duhl_ctx* ctx) {
+    return (ctx->pipe ? pipe_red_doubles(ctx->W) : scd_red_doubles(ctx->W)) * sizeof(double);
+}
+
 // SCD launch shape: G CTAs own contiguous row ranges of R rows (R % 4 == 0);
 // W = coordinates per Gram block, largest multiple of 4 (<= 32) whose
 // double-buffered stage fits in shared memory.
 static void choose_scd_shape(duhl_ctx* ctx) {
     // the unit-A refresh grid keeps its SMs while the epoch runs
     const int64_t sms = std::max<int64_t>(1, ctx->nsm - std::max(0, ctx->unit_a_ctas));
+    // pipelined kernel (scd_pipe.cuh): G compute CTAs + 1 control CTA; W <= 32 with 3 (else 4)
+    // TMA stages.  Auto (scd_kernel 0) takes it where shared memory allows W >= 24 (short row
+    // slices, e.g. C3: 2x fewer blocks than W = 16, measured 14.7 vs 25 ms per pass); at W <= 16
+    // the warp-specialised kernel is as fast or faster (C4, W = 12: 6.6 vs 7.3 ms).
+    if (ctx->cfg.scd_kernel != 1) {
+        const int64_t smax = std::max<int64_t>(1, sms - 1);
+        int64_t G = ctx->cfg.scd_ctas > 0 ? std::min<int64_t>(ctx->cfg.scd_ctas, smax)
+                                          : std::min<int64_t>(smax, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
+        int64_t R = round4((ctx->d4 + G - 1) / G);
+        G = (ctx->d4 + R - 1) / R;
+        const size_t cap = 225 * 1024;
+        int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 32;
+        W = std::max(4, std::min(32, W / 4 * 4));
+        while (W > 4 && pipe_smem_bytes(W, (int)R, 3) > cap) W -= 4;
+        if (ctx->cfg.scd_kernel == 2 || W >= 24) {
+            ctx->pipe = true;
+            ctx->NB = pipe_smem_bytes(W, (int)R, 4) <= cap ? 4 : 3;
+            if (const char* e = std::getenv("DUHL_SCD_STAGES")) ctx->NB = std::max(3, std::min(4, std::atoi(e)));
+            ctx->W = W;
+            ctx->R = (int)R;
+            ctx->G = (int)G;
+            return;
+        }
+    }
+    ctx->pipe = false;
     int64_t G = ctx->cfg.scd_ctas > 0 ? std::min<int64_t>(ctx->cfg.scd_ctas, sms)
                                       : std::min<int64_t>(sms, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
     int64_t R = round4((ctx->d4 + G - 1) / G);
@@ -787,7 +817,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)))
         return bail(DUHL_E_NOMEM);
     if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
-    if (!dmal((void**)&ctx->d_red, scd_red_doubles(ctx->W) * sizeof(double)) ||
+    if (!dmal((void**)&ctx->d_red, scd_red_bytes(ctx)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
@@ -984,7 +1014,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.order_y = ctx->d_order_y;
     p.progress = ctx->overlap ? ctx->d_progress : nullptr;
     p.bar = ctx->d_bar;
-    CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_doubles(ctx->W) * sizeof(double), ctx->st));
+    CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_bytes(ctx), ctx->st));
     CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
     static const bool trace = std::getenv("DUHL_SCD_TRACE") != nullptr;  // developer phase timing
     unsigned long long* dtr = nullptr;
@@ -995,7 +1025,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.trace = dtr;
     {
         ProfScope ps(ctx, ctx->st, 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
-        CK(launch_scd_gram(p, ctx->st, &ctx->launches));
+        CK(ctx->pipe ? launch_scd_pipe(p, ctx->st, &ctx->launches)
+                                    : launch_scd_gram(p, ctx->st, &ctx->launches));
     }
     if (trace) {
         unsigned long long h[16];
@@ -1009,11 +1040,16 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         const double cyc_per_us = clk_khz > 0 ? clk_khz / 1e3 : 1965.0;
         std::fprintf(stderr, "scd trace (us/block at %.0f MHz) W=%d G=%d R=%d: ", cyc_per_us, ctx->W, ctx->G,
                      ctx->R);
-        const char* nm[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
-                             "cmp:vupdate", "cmp:tiles"};
+        const char* nm0[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
+                              "cmp:vupdate", "cmp:tiles"};
+        const char* nm1[8] = {"ctl:poll", "ctl:read", "ctl:steps", "ctl:other", "ctl:publish", "-", "-", "-"};
+        const char* nm1c[8] = {"cmp:wait-data", "cmp:GC", "cmp:wait-delta", "cmp:vupd", "cmp:u", "cmp:arrive",
+                               "-", "cmp:other"};
+        const bool pipe = ctx->pipe;
         for (int c2 = 0; c2 < 2; ++c2) {
-            std::fprintf(stderr, "%s", c2 ? " | last: " : "cta0: ");
-            for (int k = 0; k < 8; ++k) std::fprintf(stderr, "%s %.2f ", nm[k], h[c2 * 8 + k] / nb / cyc_per_us);
+            std::fprintf(stderr, "%s", pipe ? (c2 ? " | cta0: " : "control: ") : (c2 ? " | last: " : "cta0: "));
+            for (int k = 0; k < 8; ++k)
+                std::fprintf(stderr, "%s %.2f ", pipe ? (c2 ? nm1c[k] : nm1[k]) : nm0[k], h[c2 * 8 + k] / nb / cyc_per_us);
         }
         std::fprintf(stderr, "\n");
     }

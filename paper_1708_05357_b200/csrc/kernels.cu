@@ -617,7 +617,9 @@ struct RedOut {
     }
 };
 
-template <bool EXACT, int KW, bool LOWER>
+// XL (the pipelined kernel's expanded layout, see pipe_ne): G_jk at W + k W + j,
+// C_jk at W + W^2 + k W + j, so the control warp reads rows with consecutive lanes.
+template <bool EXACT, int KW, bool LOWER, bool XL = false>
 __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float* __restrict__ Ak, int R,
                                       int lo, int hi, int lane, int jbase, int kbase, const RedOut& out,
                                       int W) {
@@ -675,9 +677,9 @@ __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float*
     if (lane < 4 * KW) {
         const int j = jbase + lane / KW, k = kbase + lane % KW;
         if (LOWER) {
-            if (k < j) out.add(scd_off_G(W) + j * (j - 1) / 2 + k, v);
+            if (k < j) out.add(XL ? W + k * W + j : scd_off_G(W) + j * (j - 1) / 2 + k, v);
         } else {
-            out.add(scd_off_C(W) + j * W + k, v);
+            out.add(XL ? W + W * W + k * W + j : scd_off_C(W) + j * W + k, v);
         }
     }
 }
@@ -1183,6 +1185,8 @@ cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launch
     return e;
 }
 
+#include "scd_pipe.cuh"
+
 // =====================================================================================
 // v = A alpha (- b): exact shared-vector recompute for set_state.  CTA per row
 // tile of 1024 rows; loops over the columns with alpha_i != 0.
@@ -1531,6 +1535,8 @@ cudaError_t preload_kernels() {
         (const void*)k_topm,        (const void*)k_perm_order,   (const void*)k_order_info,
         (const void*)k_scd_gram<true, kLasso>, (const void*)k_scd_gram<false, kLasso>,
         (const void*)k_scd_gram<true, kSvm>,   (const void*)k_scd_gram<false, kSvm>,
+        (const void*)k_scd_pipe<true, kLasso>, (const void*)k_scd_pipe<false, kLasso>,
+        (const void*)k_scd_pipe<true, kSvm>,   (const void*)k_scd_pipe<false, kSvm>,
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,

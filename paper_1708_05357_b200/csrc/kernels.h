@@ -47,7 +47,8 @@ struct ScdParams {
     const double* y;           // [n] (SVM) or nullptr
     double* alpha;             // [n]
     double* vt;                // [d4] shared vector
-    int W, R, G, NB;           // block size (<= 16, % 4 == 0), rows per CTA, CTAs, TMA stages (3)
+    int W, R, G, NB;           // block size (% 4 == 0; <= 16 legacy, <= 32 pipe), rows per CTA, (compute) CTAs, TMA stages
+    // pipe kernel: bar = cnt[4] (arrivals per reduction buffer) + flg[4] at bar + 8 (delta tags)
     int exact;                 // 1: fp64 Gram products (bit-level parity mode); 0: fp32 Gram within a warp
     double* red;               // [scd_red_doubles(W)] zero on entry
     unsigned* bar;             // [2] grid-barrier counters (per block parity), zero on entry
@@ -108,6 +109,10 @@ cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigne
                               double* order_y, const double* alpha, const double* norms, const double* y,
                               cudaStream_t st, int64_t* launches);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
+// pipelined form (scd_pipe.cuh): p.G compute CTAs + one control CTA, W <= 32, p.NB in {3, 4}
+size_t pipe_red_doubles(int W);   // size of ScdParams::red (reduction + delta buffers)
+size_t pipe_smem_bytes(int W, int R, int NS);
+cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t preload_kernels();
 cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches);

@@ -1,0 +1,581 @@
+// scd_pipe.cuh -- pipelined exact SCD epoch (App. D closed forms in the exact
+// sequential order).  Included by kernels.cu (uses its
+// tile4 / utile helpers, the RED layout constants and the bounded waits).
+//
+// Why a second kernel: in k_scd_gram every CTA runs the W sequential steps in a
+// control warp that shares the SM's shared-memory / shuffle pipe with six
+// compute warps saturating it, and a block's Gram tiles wait for delta_{b-1}.
+// Measured (DUHL_SCD_TRACE, C4 / C3 shapes): ~7.8 us per block, of which the
+// control chain (barrier wait + read-back + steps) is ~7.6 us and the tiles ~6 us,
+// against 1.5 us (C4) / 0.3 us (C3) of HBM time.  This kernel
+//   * gives the sequential part its own CTA (the control CTA, blockIdx.x == G):
+//     it waits for block b's reduction, reads it back with all of its threads,
+//     runs the W steps on one warp (lane j owns coordinate j; delta_j is
+//     broadcast by one shuffle per step) and publishes delta_b to global memory
+//     with a release flag;
+//   * lets the G compute CTAs build block b+1's delta-independent partials
+//     (G_{b+1} and the cross Gram C_{b+1,b}) as soon as the TMA engine has
+//     landed the columns, and only then wait for delta_{b-1} to apply
+//     v += A_{b-1} delta_{b-1} and take u_{b+1} = A_{b+1}^T v_b;
+//   * allows W <= 32 coordinates per block where shared memory holds 3 stages.
+// Per block the control CTA computes, for coordinate j of block b (visiting order),
+//   s_j = u_j + sum_k C_jk delta^{(b-1)}_k + sum_{k<j} G_jk delta^{(b)}_k  (== a_j^T v at its visit)
+// exactly as k_scd_gram does; the result is sequential SCD up to summation order.
+//
+// Synchronisation (all global, K = kPipeRot rotating buffers):
+//   red[b % K]   fp64 REDs of block b's partials by every compute CTA, then
+//                cnt[b % K] += 1 per CTA (after a gpu-scope fence);
+//   control:     waits cnt[b % K] == G (acquire), reads red[b % K] into shared
+//                memory, zeroes red[b % K] and cnt[b % K], runs the steps, writes
+//                dbuf[b % K] and releases flg[b % K] = b + 1;
+//   compute:     before applying delta_b, waits flg[b % K] >= b + 1 (acquire).
+// Reuse of red/cnt[b % K] by block b + K: its first RED is issued (compute
+// iteration b + K - 1) after that CTA acquired delta_{b+K-3} >= delta_b, which the
+// control CTA released after zeroing -- safe for K >= 3.  dbuf[b % K] is
+// rewritten for block b + K only after every CTA arrived for block b + K, i.e.
+// after each consumed delta_b (iteration b + 1 <= b + K - 1) -- safe for K >= 2.
+#pragma once
+
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
+static_assert(kRedGroups == 1, "the pipelined kernel assumes one reduction group");
+constexpr int kPipeWMax = 32;
+constexpr int kPipeRot = 4;
+constexpr int kPipeThreads = 256;
+constexpr int kPipeCompute = 7;   // compute warps 0..6 of a compute CTA
+constexpr int kPipeProd = 7;      // producer warp (TMA)
+constexpr int kBarPipe = 2;       // named barrier: the compute warps of a compute CTA
+
+// Reduction entries of one block (expanded layout, see tile4<..., XL>):
+//   u_j [0, W),  G_jk (k < j) at W + k W + j,  C_jk at W + W^2 + k W + j.
+__host__ __device__ __forceinline__ int pipe_ne(int W) { return W + 2 * W * W; }
+size_t pipe_red_doubles(int W) {
+    return (size_t)kPipeRot * pipe_ne(W) * kRedStride + (size_t)kPipeRot * kPipeWMax;  // + delta buffers
+}
+// Column stride of a stage in shared memory: R rounded so that R/4 is odd -- the
+// 16-byte chunks of 8 consecutive columns at one row then fall in 8 distinct bank groups.
+__host__ __device__ __forceinline__ int pipe_stride(int R) { return ((R >> 2) & 1) ? R : R + 4; }
+size_t pipe_smem_bytes(int W, int R, int NS) {
+    const size_t compute = 128 + align_up_dev((size_t)NS * W * pipe_stride(R) * sizeof(float)) +
+                           align_up_dev((size_t)R * sizeof(double)) +
+                           align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float)) +
+                           align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double));
+    const size_t control = 128 + align_up_dev((size_t)pipe_ne(W) * sizeof(double));
+    return compute > control ? compute : control;
+}
+
+// One warp's share of a block's Gram partials: the W x 2W block M = A1^T [A1 | A0]
+// (M_jk = G_jk for k < W, C_j,k-W for k >= W; global entry W + k W + j) over rows
+// [4 r4lo, 4 r4hi).  Lane (jg, kg) = (lane & 3, lane >> 2) owns rows j = jg + 4a and
+// columns k = kg + 8b (a, b < T = W/4): one 16-byte load per owned column and 4-row
+// step feeds 4 T^2 FMAs, and the 4 (8) distinct columns a load instruction touches are
+// consecutive, i.e. conflict-free with the padded stride.  Fast mode: fp32 FMA (FFMA2
+// over row pairs), the partial of every lane-entry written to `part` (slot (a T + b) 32
+// + lane) for the cross-warp sum; exact mode: fp64 products, REDs straight from here.
+template <bool EXACT, int T, int B0, int NBK>  // columns k = kg + 8 b, b in [B0, B0 + NBK)
+__device__ __forceinline__ void gc_warp_part(const float* __restrict__ A1, const float* __restrict__ A0, int Rs,
+                                             int W, int r4lo, int r4hi, int lane, float* __restrict__ part,
+                                             const RedOut& out) {
+    const int jg = lane & 3, kg = lane >> 2;
+    // (a, b) pairs whose every lane-entry is strictly upper G (k >= 8b > 4a + 3 >= j, k < W): skipped
+    auto upper = [](int a, int b) { return 8 * b + 7 < 4 * T && a < 2 * b; };
+    // 32-bit shared-window addresses
+    uint32_t xa[T], ya[NBK];
+#pragma unroll
+    for (int a = 0; a < T; ++a) xa[a] = smem_addr(A1 + (size_t)(jg + 4 * a) * Rs);
+#pragma unroll
+    for (int b = 0; b < NBK; ++b) {
+        const int k = kg + 8 * (B0 + b);
+        ya[b] = smem_addr(k < W ? A1 + (size_t)k * Rs : A0 + (size_t)(k - W) * Rs);
+    }
+    if (EXACT) {
+        double acc[T][NBK];
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) acc[a][b] = 0.0;
+#pragma unroll 2
+        for (int r4 = r4lo; r4 < r4hi; ++r4) {
+            float4 x[T];
+#pragma unroll
+            for (int a = 0; a < T; ++a) x[a] = lds_f4(xa[a] + 16u * r4);
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) {
+                const float4 y = lds_f4(ya[b] + 16u * r4);
+#pragma unroll
+                for (int a = 0; a < T; ++a) {
+                    if (upper(a, B0 + b)) continue;
+                    double t = acc[a][b];
+                    t = fma((double)x[a].x, (double)y.x, t);
+                    t = fma((double)x[a].y, (double)y.y, t);
+                    t = fma((double)x[a].z, (double)y.z, t);
+                    t = fma((double)x[a].w, (double)y.w, t);
+                    acc[a][b] = t;
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) {
+                const int j = jg + 4 * a, k = kg + 8 * (B0 + b);
+                if (k >= W || k < j) out.add(W + k * W + j, acc[a][b]);
+            }
+    } else {
+        float2 acc[T][NBK];
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) acc[a][b] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (int r4 = r4lo; r4 < r4hi; ++r4) {
+            float4 x[T];
+#pragma unroll
+            for (int a = 0; a < T; ++a) x[a] = lds_f4(xa[a] + 16u * r4);
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) {
+                const float4 y = lds_f4(ya[b] + 16u * r4);
+#pragma unroll
+                for (int a = 0; a < T; ++a) {
+                    if (upper(a, B0 + b)) continue;
+                    ffma2(acc[a][b], x[a].x, x[a].y, y.x, y.y);
+                    ffma2(acc[a][b], x[a].z, x[a].w, y.z, y.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) part[(a * T + B0 + b) * 32 + lane] = acc[a][b].x + acc[a][b].y;
+    }
+}
+template <bool EXACT, int T>
+__device__ __forceinline__ void gc_warp(const float* A1, const float* A0, int Rs, int W, int r4lo, int r4hi,
+                                        int lane, float* part, const RedOut& out) {
+    if (T <= 4) {
+        gc_warp_part<EXACT, T, 0, T>(A1, A0, Rs, W, r4lo, r4hi, lane, part, out);
+    } else {
+        gc_warp_part<EXACT, T, 0, 4>(A1, A0, Rs, W, r4lo, r4hi, lane, part, out);
+        gc_warp_part<EXACT, T, 4, (T > 4 ? T - 4 : 1)>(A1, A0, Rs, W, r4lo, r4hi, lane, part, out);
+    }
+}
+
+// Cross-warp sum of the fast-mode partials (fp32 within the CTA, fp64 REDs across CTAs).
+template <int T>
+__device__ __forceinline__ void gc_sum(const float* __restrict__ part, int W, int tid, const RedOut& out) {
+    constexpr int nslot = 32 * T * T;
+    for (int sl = tid; sl < nslot; sl += kPipeCompute * 32) {
+        const int ln = sl & 31, e = sl >> 5, a = e / T, bb = e - a * T;
+        const int j = (ln & 3) + 4 * a, k = (ln >> 2) + 8 * bb;
+        if (k >= W || k < j) {
+            float sum = 0.f;
+#pragma unroll
+            for (int w = 0; w < kPipeCompute; ++w) sum += part[w * 2 * 16 * T * T + sl];
+            out.add(W + k * W + j, (double)sum);
+        }
+    }
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Stage block blk's row slice (W column slices of `rows` floats, stride R) into
+// stage blk % NS.  Whole producer warp; lane j copies column j.
+__device__ __forceinline__ void pipe_issue(const ScdParams& p, float* Abuf, uint64_t* full, int64_t blk,
+                                           int64_t r0, int rows, int lane, int slot, unsigned need,
+                                           unsigned& seen, int Rs) {
+    const int W = p.W;
+    const int Wb = (int)imin64(W, p.L - blk * W);
+    const int st = (int)(blk % p.NB);
+    float* dst = Abuf + (size_t)st * W * Rs;
+    const unsigned bytes = (unsigned)rows * 4u;
+    if (p.progress && lane < Wb && need > seen) {
+        const unsigned long long t0 = gtimer();
+        while ((seen = ld_acquire_u32(p.progress)) < need) {
+            __nanosleep(128);
+            if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 1); break; }
+        }
+    }
+    if (lane == 0) mbar_arrive_expect_tx(&full[st], bytes * (unsigned)Wb);
+    __syncwarp();
+    if (lane < Wb) bulk_g2s(dst + (size_t)lane * Rs, p.pool + (int64_t)slot * p.ld_dev + r0, bytes, &full[st]);
+}
+
+template <bool EXACT, int MODEL>
+__global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int W = p.W, R = p.R, NS = p.NB, G = p.G;
+    const int NE = pipe_ne(W);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t nblk = (p.L + W - 1) / W;
+    unsigned* cnt = p.bar;       // [kPipeRot]
+    unsigned* flg = p.bar + 8;   // [kPipeRot]
+    const size_t rbsz = (size_t)NE * kRedStride;
+    double* dbuf = p.red + (size_t)kPipeRot * rbsz;  // [kPipeRot][kPipeWMax]
+    const double lam_dn = MODEL == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
+    const bool tr = p.trace != nullptr && (tid == 0) && (c == G || c == 0);
+    unsigned long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tprev = tr ? (unsigned long long)clock64() : 0;
+    auto stamp = [&](int k) {
+        if (tr) {
+            const unsigned long long t = (unsigned long long)clock64();
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q == k) trc[q] += t - tprev;
+            tprev = t;
+        }
+    };
+
+    if (c == G) {
+        // ============================================================ control CTA
+        double* sRed = reinterpret_cast<double*>(smem + 128);  // [NE]
+        __shared__ double sDprev[kPipeWMax];
+        if (tid < kPipeWMax) sDprev[tid] = 0.0;
+        int64_t pf_j = 0;
+        double pf_a = 0, pf_inv = 0, pf_y = 0;
+        auto prefetch = [&](int64_t blk) {
+            const int64_t t = blk * W + lane;
+            if (warp == 0 && lane < W && t < p.L) {
+                pf_j = p.order_j[t];
+                pf_a = p.order_a[t];
+                pf_inv = p.order_inv[t];
+                pf_y = p.order_y[t];
+            }
+        };
+        prefetch(0);
+        __syncthreads();
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int rb = (int)(b % kPipeRot);
+            const int Wb = (int)imin64(W, p.L - b * W);
+            const int64_t jg = pf_j;
+            const double a_in = pf_a, inv_in = pf_inv, y_in = pf_y;
+            if (b + 1 < nblk) prefetch(b + 1);
+            stamp(3);
+            if (tid == 0) {
+                const unsigned long long t0 = gtimer();
+                while (ld_acquire_u32(&cnt[rb]) < (unsigned)G) {
+                    if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 2); break; }
+                }
+            }
+            __syncthreads();
+            stamp(0);
+            {   // read back (all loads in flight), then zero the buffer for block b + K
+                double* red_b = p.red + (size_t)rb * rbsz;
+                double v[(kPipeWMax + 2 * kPipeWMax * kPipeWMax + kPipeThreads - 1) / kPipeThreads];
+                constexpr int kPer = (kPipeWMax + 2 * kPipeWMax * kPipeWMax + kPipeThreads - 1) / kPipeThreads;
+#pragma unroll
+                for (int u = 0; u < kPer; ++u) {
+                    const int q = tid + u * kPipeThreads;
+                    v[u] = q < NE ? ld_cg_f64(&red_b[(size_t)q * kRedStride]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kPer; ++u) {
+                    const int q = tid + u * kPipeThreads;
+                    if (q < NE) {
+                        sRed[q] = v[u];
+                        __stcg(&red_b[(size_t)q * kRedStride], 0.0);
+                    }
+                }
+                if (tid == 0) cnt[rb] = 0u;
+            }
+            __syncthreads();
+            stamp(1);
+            if (warp == 0) {
+                double a = 0, t = 0, tau = 0, cy = 0, scale = 0;
+                bool zero = true;
+                if (lane < Wb) {
+                    a = a_in;
+                    double inv = inv_in;
+                    zero = inv < 0.0;
+                    if (zero) inv = 0.0;
+                    double sj = sRed[lane];
+                    if (b > 0)
+                        for (int k = 0; k < W; ++k) sj = fma(sRed[W + W * W + k * W + lane], sDprev[k], sj);
+                    if (MODEL == kLasso) {
+                        t = a - sj * inv;
+                        tau = lam_dn * inv;
+                        scale = -inv;
+                    } else {
+                        t = fma(lam_dn - y_in * sj, inv, y_in * a);
+                        cy = y_in;
+                        scale = -y_in * inv;
+                    }
+                }
+                // lane j's scaled Gram row: t_j += cg[k] delta_k for k < j (zero for k >= j)
+                double cg[kPipeWMax];
+#pragma unroll
+                for (int k = 0; k < kPipeWMax; ++k)
+                    cg[k] = (k < W && lane < Wb) ? scale * sRed[W + k * W + lane] : 0.0;
+                double afin = a;
+                double* dout = dbuf + (size_t)rb * kPipeWMax;
+#pragma unroll
+                for (int j = 0; j < kPipeWMax; ++j) {
+                    if (j >= Wb) break;
+                    double an;
+                    if (MODEL == kLasso) {
+                        const double mag = fabs(t) - tau;
+                        an = mag > 0.0 ? copysign(mag, t) : 0.0;
+                        if (zero) an = 0.0;
+                    } else {
+                        const double u = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+                        an = zero ? cy : cy * u;
+                    }
+                    double dl = an - a;
+                    if (lane == j) afin = an;
+                    dl = __shfl_sync(0xffffffffu, dl, j);
+                    t = fma(cg[j], dl, t);
+                    if (lane == 0) {  // every lane has delta_j: lane 0 publishes (its own stores, then release)
+                        __stcg(&dout[j], dl);
+                        sDprev[j] = dl;
+                    }
+                }
+                if (lane == 0)
+                    for (int j = Wb; j < W; ++j) {
+                        __stcg(&dout[j], 0.0);
+                        sDprev[j] = 0.0;
+                    }
+                stamp(2);
+                if (lane == 0) st_release_u32(&flg[rb], (unsigned)(b + 1));
+                if (lane < Wb) p.alpha[jg] = afin;
+                __syncwarp();
+                stamp(4);
+            }
+        }
+    } else {
+        // ============================================================ compute CTA c
+        // Shared memory: mbarriers | NS stages of W column slices (stride Rs) | v slice (fp64) |
+        // per-warp fp32 partials of the Gram block (fast mode) | per-warp u partials.
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [NS]
+        uint64_t* empty = full + 4;                          // [NS]
+        const int Rs = pipe_stride(R);
+        float* Abuf = reinterpret_cast<float*>(smem + 128);
+        size_t off = 128 + align_up_dev((size_t)NS * W * Rs * sizeof(float));
+        double* vs = reinterpret_cast<double*>(smem + off);
+        off += align_up_dev((size_t)R * sizeof(double));
+        float* part = reinterpret_cast<float*>(smem + off);  // [kPipeCompute][2 W^2]
+        off += align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float));
+        double* upart = reinterpret_cast<double*>(smem + off);  // [kPipeCompute][32]
+        __shared__ double sDelta[2][kPipeWMax];
+        const int64_t r0 = (int64_t)c * R;
+        const int rows = (int)imin64(R, p.d4 - r0);
+        for (int q = tid; q < NS * W * Rs; q += kPipeThreads) Abuf[q] = 0.0f;
+        for (int r = tid; r < R; r += kPipeThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
+        if (tid == 0) {
+            for (int q = 0; q < NS; ++q) {
+                mbar_init(&full[q], 1);
+                mbar_init(&empty[q], kPipeCompute);
+            }
+            fence_mbar_init();
+        }
+        fence_proxy_async();
+        __syncthreads();
+
+        if (warp == kPipeProd) {
+            int pf_slot = 0;
+            unsigned pf_need = 0, seen = 0;
+            auto prefetch_slot = [&](int64_t blk) {
+                const int64_t t = blk * W + lane;
+                if (lane < W && t < p.L) {
+                    pf_slot = p.order_slot[t];
+                    pf_need = p.order_batch ? p.order_batch[t] : 0u;
+                }
+            };
+            prefetch_slot(0);
+            for (int64_t q = 0; q < nblk; ++q) {
+                const int slot = pf_slot;
+                const unsigned need = pf_need;
+                if (q + 1 < nblk) prefetch_slot(q + 1);
+                if (q >= NS)
+                    mbar_wait_bounded(&empty[q % NS], (unsigned)((q / NS - 1) & 1), p.err, 4, kSpinTimeoutNs);
+                pipe_issue(p, Abuf, full, q, r0, rows, lane, slot, need, seen, Rs);
+            }
+        } else {
+            const int cw = warp;
+            const int n4 = rows >> 2;
+            const int w4lo = (cw * n4) / kPipeCompute, w4hi = ((cw + 1) * n4) / kPipeCompute;  // this warp's rows
+            auto stage = [&](int64_t blk) { return Abuf + (size_t)(blk % NS) * W * Rs; };
+            auto wait_data = [&](int64_t blk) {
+                mbar_wait_bounded(&full[blk % NS], (unsigned)((blk / NS) & 1), p.err, 8, kSpinTimeoutNs);
+            };
+            auto out_of = [&](int64_t blk) { return RedOut{p.red + (size_t)(blk % kPipeRot) * rbsz, 0}; };
+            // G_{blk} (lower) and C_{blk,blk-1}: every warp takes the whole W x 2W block over its
+            // own rows (no cross-lane reduction); fp32 partials are summed across warps in fp64.
+            auto gc_block = [&](int64_t blk, bool with_c) {
+                const float* A1 = stage(blk);
+                const float* A0 = with_c ? stage(blk - 1) : A1;  // block 0: C is never read
+                const RedOut out = out_of(blk);
+                float* mypart = part + (size_t)cw * 2 * W * W;
+                switch (W >> 2) {
+                    case 1: gc_warp<EXACT, 1>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 2: gc_warp<EXACT, 2>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 3: gc_warp<EXACT, 3>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 4: gc_warp<EXACT, 4>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 5: gc_warp<EXACT, 5>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 6: gc_warp<EXACT, 6>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    case 7: gc_warp<EXACT, 7>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                    default: gc_warp<EXACT, 8>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                }
+                if (!EXACT) {  // sum the warps' partials and add one (fp64) RED per entry
+                    named_sync(kBarPipe, kPipeCompute * 32);
+                    switch (W >> 2) {
+                        case 1: gc_sum<1>(part, W, tid, out); break;
+                        case 2: gc_sum<2>(part, W, tid, out); break;
+                        case 3: gc_sum<3>(part, W, tid, out); break;
+                        case 4: gc_sum<4>(part, W, tid, out); break;
+                        case 5: gc_sum<5>(part, W, tid, out); break;
+                        case 6: gc_sum<6>(part, W, tid, out); break;
+                        case 7: gc_sum<7>(part, W, tid, out); break;
+                        default: gc_sum<8>(part, W, tid, out); break;
+                    }
+                }
+            };
+            // u_blk = A_blk^T v over this warp's rows (lane j = column j), fp64; summed across warps
+            auto u_block = [&](int64_t blk) {
+                // lane (jq, rs) = (lane & 3, lane >> 2): columns jq + 4a, rows r4 = rs mod 8 of the slice
+                const float* A1 = stage(blk);
+                const int jq = lane & 3, rs = lane >> 2, T = W >> 2;
+                const double2* v2 = reinterpret_cast<const double2*>(vs);
+                double acc[8];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) acc[a] = 0.0;
+                for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
+                    const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        if (a >= T) break;
+                        const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
+                        acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
+                                     fma((double)x.w, v23.y, acc[a]))));
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    if (a >= T) break;
+                    double t = acc[a];
+                    t += __shfl_xor_sync(0xffffffffu, t, 4);
+                    t += __shfl_xor_sync(0xffffffffu, t, 8);
+                    t += __shfl_xor_sync(0xffffffffu, t, 16);
+                    if (rs == 0) upart[cw * kPipeWMax + jq + 4 * a] = t;
+                }
+                named_sync(kBarPipe, kPipeCompute * 32);
+                if (tid < W) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < kPipeCompute; ++w) sum += upart[w * kPipeWMax + tid];
+                    out_of(blk).add(tid, sum);
+                }
+            };
+            auto arrive = [&](int64_t blk) {  // this CTA's partials of block blk are complete
+                named_sync(kBarPipe, kPipeCompute * 32);
+                if (tid == 0) {
+                    __threadfence();
+                    atomicAdd(&cnt[blk % kPipeRot], 1u);
+                }
+            };
+            auto wait_delta = [&](int64_t blk) {  // delta_blk -> sDelta[blk & 1]
+                if (cw == 0) {
+                    const unsigned* f = &flg[blk % kPipeRot];
+                    const unsigned long long t0 = gtimer();
+                    while (ld_acquire_u32(f) < (unsigned)(blk + 1)) {
+                        if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 16); break; }
+                    }
+                    if (lane < W) sDelta[blk & 1][lane] = ld_cg_f64(&dbuf[(size_t)(blk % kPipeRot) * kPipeWMax + lane]);
+                }
+                named_sync(kBarPipe, kPipeCompute * 32);
+            };
+            auto vupdate = [&](int64_t blk) {  // v slice += A_blk delta_blk (delta = 0 beyond the block)
+                const float* A = stage(blk);
+                const double* dl = sDelta[blk & 1];
+                double2* v2 = reinterpret_cast<double2*>(vs);
+                const uint32_t a0 = smem_addr(A);
+                for (int r4 = tid; r4 < n4; r4 += kPipeCompute * 32) {
+                    double2 p01 = make_double2(0.0, 0.0), p23 = p01, q01 = p01, q23 = p01;
+                    for (int j = 0; j < W; j += 4) {  // W % 4 == 0: two independent chains
+#pragma unroll
+                        for (int u = 0; u < 4; u += 2) {
+                            const float4 x = lds_f4(a0 + 4u * (uint32_t)((j + u) * Rs) + 16u * r4);
+                            const float4 y = lds_f4(a0 + 4u * (uint32_t)((j + u + 1) * Rs) + 16u * r4);
+                            const double dx = dl[j + u], dy = dl[j + u + 1];
+                            p01.x = fma(dx, (double)x.x, p01.x);
+                            p01.y = fma(dx, (double)x.y, p01.y);
+                            p23.x = fma(dx, (double)x.z, p23.x);
+                            p23.y = fma(dx, (double)x.w, p23.y);
+                            q01.x = fma(dy, (double)y.x, q01.x);
+                            q01.y = fma(dy, (double)y.y, q01.y);
+                            q23.x = fma(dy, (double)y.z, q23.x);
+                            q23.y = fma(dy, (double)y.w, q23.y);
+                        }
+                    }
+                    double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                    v01.x += p01.x + q01.x;
+                    v01.y += p01.y + q01.y;
+                    v23.x += p23.x + q23.x;
+                    v23.y += p23.y + q23.y;
+                    v2[2 * r4] = v01;
+                    v2[2 * r4 + 1] = v23;
+                }
+            };
+            if (nblk > 0) {
+                wait_data(0);
+                gc_block(0, false);
+                u_block(0);
+                arrive(0);
+            }
+            for (int64_t b = 0; b < nblk; ++b) {
+                stamp(7);
+                if (b + 1 < nblk) {
+                    wait_data(b + 1);
+                    stamp(0);
+                    gc_block(b + 1, true);
+                    stamp(1);
+                }
+                if (b >= 1) {
+                    wait_delta(b - 1);
+                    stamp(2);
+                    vupdate(b - 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[(b - 1) % NS]);
+                    named_sync(kBarPipe, kPipeCompute * 32);  // v_b complete before the u tiles read it
+                    stamp(3);
+                }
+                if (b + 1 < nblk) {
+                    u_block(b + 1);
+                    stamp(4);
+                    arrive(b + 1);
+                    stamp(5);
+                }
+            }
+            if (nblk > 0) {
+                wait_delta(nblk - 1);
+                vupdate(nblk - 1);
+            }
+            named_sync(kBarPipe, kPipeCompute * 32);
+        }
+        __syncthreads();
+        for (int r = tid; r < rows; r += kPipeThreads) p.vt[r0 + r] = vs[r];
+    }
+    if (tr)
+        for (int q = 0; q < 8; ++q)
+            if (trc[q]) atomicAdd(&p.trace[(c == G ? 0 : 8) + q], trc[q]);
+}
+
+cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launches) {
+    if (p.L <= 0) return cudaSuccess;
+    const size_t smem = pipe_smem_bytes(p.W, p.R, p.NB);
+    const void* fn = p.model == kLasso
+                         ? (p.exact ? (const void*)k_scd_pipe<true, kLasso> : (const void*)k_scd_pipe<false, kLasso>)
+                         : (p.exact ? (const void*)k_scd_pipe<true, kSvm> : (const void*)k_scd_pipe<false, kSvm>);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ScdParams q = p;
+    void* args[] = {&q};
+    e = cudaLaunchCooperativeKernel(fn, dim3(p.G + 1), dim3(kPipeThreads), args, smem, st);
+    ++*launches;
+    return e;
+}

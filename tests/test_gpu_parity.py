@@ -170,21 +170,25 @@ def test_select_uniform_and_sequential_match_oracle(D):
 
 
 # ------------------------------------------------------------------------- SCD epoch (a5)
+@pytest.mark.parametrize("kernel", [1, 2])   # warp-specialised / pipelined (control CTA)
 @pytest.mark.parametrize("model,d,n,m,W", [
     (O.LASSO, 2000, 1000, 250, 0),      # C1 shape, 25% working set
     (O.SVM, 500, 4000, 400, 0),         # C2 aspect, 10% working set
     (O.LASSO, 20001, 200, 150, 16),     # tall: many CTAs, ragged d, ragged last block
     (O.SVM, 3001, 900, 333, 12),
     (O.LASSO, 300, 700, 700, 4),
+    (O.LASSO, 40000, 300, 299, 32),     # C3 row count: 32-wide blocks (pipelined only), ragged tail
+    (O.SVM, 9998, 500, 477, 24),
+    (O.LASSO, 1003, 400, 390, 20),
 ])
-def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W):
+def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
     """P12: same order, fp64 -> GPU epoch == oracle sequential epoch to ~1e-12."""
     A, lab = _data(model, d, n, seed=200 + d)
     lam = _lam(model, n)
     y = lab if model == O.SVM else None
     P_set = np.arange(m)                       # sequential block 0: known without either side
     order = synth.permutation(P_set, 5)
-    with D.create(A, lab, lam, model, scd_block=W, m=m) as P:
+    with D.create(A, lab, lam, model, scd_block=W, m=m, scd_kernel=kernel) as P:
         sel, _ = P.select(D.SEL_SEQUENTIAL, m=m, round=0)
         assert sel.tolist() == P_set.tolist()
         P.scd_epoch(perm=order)
@@ -195,6 +199,29 @@ def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W):
     scale_a = max(1e-300, np.abs(alpha).max())
     assert np.abs(a_gpu - alpha).max() <= 1e-11 * scale_a
     assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("model,d,n,m", [(O.LASSO, 40000, 400, 390), (O.SVM, 200704 // 8, 300, 290)])
+def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
+    """Fast mode (scd_exact=0, the bench's): fp32 Gram partials inside a CTA (k_scd_pipe) or a
+    warp (k_scd_gram), fp64 across CTAs and everywhere else.  The Gram entries only correct s_j
+    for the updates of the current / previous block, so the epoch stays within ~1e-6 of the
+    oracle's sequential epoch (relative to max |alpha|); a wrong index or sign is O(1)."""
+    A, lab = _data(model, d, n, seed=300 + d)
+    lam = _lam(model, n)
+    y = lab if model == O.SVM else None
+    P_set = np.arange(m)
+    order = synth.permutation(P_set, 7)
+    with D.create(A, lab, lam, model, m=m, scd_kernel=kernel, scd_exact=False) as P:
+        P.select(D.SEL_SEQUENTIAL, m=m, round=0)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = -lab.copy() if model == O.LASSO else np.zeros(d)
+    O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
+    assert np.abs(a_gpu - alpha).max() <= 1e-6 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-6 * max(1.0, np.abs(vt).max())
 
 
 def test_scd_internal_permutation_generator_matches_oracle(D):
@@ -214,7 +241,8 @@ def test_scd_internal_permutation_generator_matches_oracle(D):
     assert np.abs(a_gpu - alpha).max() <= 1e-11 * np.abs(alpha).max()
 
 
-def test_P7_hadamard_one_epoch_on_gpu(D):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_P7_hadamard_one_epoch_on_gpu(D, kernel):
     d, n = 2048, 1024
     A = synth.hadamard_columns(d, n)
     rng = np.random.default_rng(0)
@@ -222,7 +250,7 @@ def test_P7_hadamard_one_epoch_on_gpu(D):
     lam = 0.1
     c = A.astype(np.float64) @ b
     astar = np.sign(c) * np.maximum(np.abs(c) - lam * d, 0) / d
-    with D.create(A, b, lam, D.LASSO) as P:
+    with D.create(A, b, lam, D.LASSO, scd_kernel=kernel) as P:
         P.select(D.SEL_GAP, m=n)
         P.scd_epoch(passes=1, seed=1)
         a, v, _ = P.get_state()
@@ -231,13 +259,14 @@ def test_P7_hadamard_one_epoch_on_gpu(D):
     assert g < 1e-10
 
 
-def test_P8_orthogonal_svm_one_epoch_on_gpu(D):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_P8_orthogonal_svm_one_epoch_on_gpu(D, kernel):
     d, n = 256, 128
     rng = np.random.default_rng(1)
     A = synth.hadamard_columns(d, n, rng.uniform(0.5, 2.0, n))
     y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
     lam = 0.5
-    with D.create(A, y, lam, D.SVM_DUAL) as P:
+    with D.create(A, y, lam, D.SVM_DUAL, scd_kernel=kernel) as P:
         P.select(D.SEL_GAP, m=n)
         P.scd_epoch(passes=1, seed=2)
         a, v, _ = P.get_state()
@@ -247,11 +276,12 @@ def test_P8_orthogonal_svm_one_epoch_on_gpu(D):
     assert g < 1e-12
 
 
-def test_zero_columns(D):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_zero_columns(D, kernel):
     d, n = 64, 40
     A, y = synth.svm_dense(d, n, seed=8)
     A[[3, 17, 39]] = 0
-    with D.create(A, y, 0.01, D.SVM_DUAL) as P:
+    with D.create(A, y, 0.01, D.SVM_DUAL, scd_kernel=kernel) as P:
         P.select(D.SEL_GAP, m=n)
         P.scd_epoch(passes=1, seed=0)
         a, _, _ = P.get_state()

@@ -21,6 +21,7 @@ ap.add_argument("--W", type=int, default=0)
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--lasso", action="store_true")
 ap.add_argument("--fast", action="store_true")
+ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 warp-specialised, 2 pipelined")
 a = ap.parse_args()
 if a.lasso:
     A = np.empty((a.n, a.d), dtype=np.float32)
@@ -32,7 +33,7 @@ else:
     lab = synth.svm_fill(A, a.d, a.n, 5)
     model, lam = D.SVM_DUAL, 1.0 / 40000
 P = D.create(A, lab, lam, model, profile=True, scd_block=a.W, scd_ctas=a.ctas, borrow_host=True,
-             scd_exact=not a.fast)
+             scd_exact=not a.fast, scd_kernel=a.kernel)
 P.select(D.SEL_GAP, m=a.n)
 t0 = time.perf_counter()
 P.scd_epoch(passes=a.passes, seed=1)
