@@ -307,7 +307,8 @@ def run_duhl(args, cfg, rank, world, local):
         obj = [D.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    policy = {"gap": D.SEL_GAP, "sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM}[args.policy]
+    policy = {"gap": D.SEL_GAP, "sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM,
+              "importance": D.SEL_IMPORTANCE}[args.policy]
 
     # ---------------- device-timed steady-state rounds
     t_create = time.perf_counter()
@@ -414,12 +415,12 @@ def run_duhl(args, cfg, rank, world, local):
                        "non-resident columns"}
 
     # ---------------- baselines: same library, budget and kernels, batch selection
-    # sequential blocks [Yu 2012] / uniform instead of gap top-m
+    # sequential blocks [Yu 2012] / uniform / importance sampling instead of gap top-m
     baselines = None
     if args.baselines:
         baselines = {}
-        for pol_name in ("sequential", "uniform"):
-            pol = {"sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM}[pol_name]
+        for pol_name in ("sequential", "uniform", "importance"):
+            pol = {"sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM, "importance": D.SEL_IMPORTANCE}[pol_name]
             t0 = time.perf_counter()
             cb = dict(common, refresh_fraction=0.0)  # batch baselines do not read z
             P3 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
@@ -489,7 +490,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--passes", type=int, default=1)
     ap.add_argument("--refresh", type=float, default=0.10)
-    ap.add_argument("--policy", default="gap", choices=["gap", "sequential", "uniform"])
+    ap.add_argument("--policy", default="gap", choices=["gap", "sequential", "uniform", "importance"])
     ap.add_argument("--eps", type=float, default=1e-5)
     ap.add_argument("--max-rounds", type=int, default=2000)
     ap.add_argument("--cert-every", type=int, default=50)
@@ -498,7 +499,7 @@ def main():
     ap.add_argument("--exact", action="store_true", help="fp64 Gram products in the SCD kernel")
     ap.add_argument("--linesearch", action="store_true", help="gamma line search also at N=1")
     ap.add_argument("--baselines", action="store_true",
-                    help="also time the sequential / uniform batch baselines to eps (capped rounds)")
+                    help="also time the sequential / uniform / importance batch baselines to eps (capped rounds)")
     ap.add_argument("--baseline-rounds", type=int, default=600)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unit-a-ctas", type=int, default=0,

@@ -46,7 +46,7 @@ typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1 } duhl_model;
 
 /* Block selection policies: Eq. 11 gap memory, and the paper's
  * reference schemes: sequential blocks [Yu 2012], uniform. */
-typedef enum { DUHL_SEL_GAP = 0, DUHL_SEL_SEQUENTIAL = 1, DUHL_SEL_UNIFORM = 2 } duhl_policy;
+typedef enum { DUHL_SEL_GAP = 0, DUHL_SEL_SEQUENTIAL = 1, DUHL_SEL_UNIFORM = 2, DUHL_SEL_IMPORTANCE = 3 } duhl_policy;
 
 typedef enum {
     DUHL_OK = 0,
@@ -159,7 +159,12 @@ duhl_status duhl_destroy(duhl_ctx* ctx);
 duhl_status duhl_gaps(duhl_ctx* ctx, const int64_t* idx, int64_t k, double* z_out, double* s_out);
 
 /* Working-set selection (Eq. 11 for DUHL_SEL_GAP: the m largest z, ties to the
- * lowest index, reading R7) for round `round`, then stages A_[P] into the HBM
+ * lowest index, reading R7; the baselines of P:400-404: DUHL_SEL_SEQUENTIAL blocks
+ * [k m, (k+1) m), k = round mod ceil(n/m); DUHL_SEL_UNIFORM the m smallest counter
+ * keys key(seed, round, -1, j); DUHL_SEL_IMPORTANCE m draws without replacement with
+ * probability proportional to ||a_j||^2, i.e. the m smallest exponential clocks
+ * -ln(u_j)/||a_j||^2, u_j = ((key(seed, round, -2, j) >> 11) + 1/2) 2^-53, zero columns
+ * last) for round `round`, then stages A_[P] into the HBM
  * slot pool (Alg. 2 l.4).  m = 0 uses cfg.m.  P_out (host int64[m], may be NULL)
  * receives P in ascending index order; *n_swaps_out (may be NULL) the number of
  * columns copied host -> HBM.  Errors: DUHL_E_INVALID (m > n or > pool), DUHL_E_CUDA. */

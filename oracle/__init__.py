@@ -24,7 +24,7 @@ _SRC = os.path.join(_HERE, "duhl_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 LASSO, SVM = 0, 1
-SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM = 0, 1, 2
+SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE = 0, 1, 2, 3
 OK, E_INVALID, E_NUMERIC, E_NOT_CONVERGED = 0, 2, 4, 9
 
 
@@ -164,6 +164,7 @@ def select_topm(z, m):
 
 
 def select_policy(policy, n, m, rnd, seed, z=None):
+    """z: the gap memory (SEL_GAP) or ||a_j||^2 (SEL_IMPORTANCE); unused otherwise."""
     zz = _f64(z) if z is not None else np.zeros(n)
     out = np.empty(m, dtype=np.int64)
     k = lib().or_select_policy(policy, n, m, rnd, seed, _p(zz), _p(out))

@@ -157,10 +157,41 @@ void or_select_topm(const double* z, i64 n, i64 m, i64* P_out) {
     free(idx);
 }
 
-/* Baseline selection policies (P:401 sequential blocks [Yu 2012]; P:434 uniform):
+/* Baseline selection policies (P:401 sequential blocks [Yu 2012]; P:434 uniform;
+ * P:403-404 importance sampling [Zhao 2015]):
  *   sequential: block k = round mod ceil(n/m), indices [k m, min((k+1) m, n))
  *   uniform   : the m indices with the smallest (key(seed, round, -1, j), j)
+ *   importance: m draws without replacement, each next draw with probability
+ *               proportional to ||a_j||^2 among the remaining columns (static
+ *               probabilities): the m smallest (e_j, j) with
+ *               e_j = -ln(u_j) / ||a_j||^2, u_j = (key(seed, round, -2, j) >> 11 + 1/2) 2^-53
+ *               (exponential clocks; zero columns never ahead of a nonzero one).
+ *               z holds ||a_j||^2 for this policy.
  * Returns the number of indices written (sequential's last block may be short). */
+static double or_is_clock(u64 seed, i64 round, i64 j, double w) {
+    double u = ((double)(or_perm_key(seed, round, -2, j) >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    return w > 0.0 ? -log(u) / w : INFINITY;
+}
+static void or_sort_by_dkey(double* key, i64* idx, i64 len) { /* merge sort on (key, idx) */
+    if (len < 2) return;
+    i64 h = len / 2;
+    or_sort_by_dkey(key, idx, h);
+    or_sort_by_dkey(key + h, idx + h, len - h);
+    double* tk = (double*)malloc(sizeof(double) * (size_t)len);
+    i64* ti = (i64*)malloc(sizeof(i64) * (size_t)len);
+    i64 p = 0, q = h, o = 0;
+    while (p < h && q < len) {
+        int take_q = (key[q] < key[p]) || (key[q] == key[p] && idx[q] < idx[p]);
+        if (take_q) { tk[o] = key[q]; ti[o++] = idx[q++]; }
+        else { tk[o] = key[p]; ti[o++] = idx[p++]; }
+    }
+    while (p < h) { tk[o] = key[p]; ti[o++] = idx[p++]; }
+    while (q < len) { tk[o] = key[q]; ti[o++] = idx[q++]; }
+    memcpy(key, tk, sizeof(double) * (size_t)len);
+    memcpy(idx, ti, sizeof(i64) * (size_t)len);
+    free(tk);
+    free(ti);
+}
 static void or_sort_by_key(u64* key, i64* idx, i64 len) { /* insertion-free merge sort */
     if (len < 2) return;
     i64 h = len / 2;
@@ -187,6 +218,16 @@ i64 or_select_policy(int policy, i64 n, i64 m, i64 round, u64 seed, const double
         i64 nblk = (n + m - 1) / m, k = round % nblk, lo = k * m, hi = lo + m < n ? lo + m : n;
         for (i64 i = lo; i < hi; ++i) P_out[i - lo] = i;
         return hi - lo;
+    }
+    if (policy == 3) {
+        double* e = (double*)malloc(sizeof(double) * (size_t)n);
+        i64* ix = (i64*)malloc(sizeof(i64) * (size_t)n);
+        for (i64 j = 0; j < n; ++j) { e[j] = or_is_clock(seed, round, j, z[j]); ix[j] = j; }
+        or_sort_by_dkey(e, ix, n);
+        for (i64 t = 0; t < m; ++t) P_out[t] = ix[t];
+        free(e);
+        free(ix);
+        return m;
     }
     u64* key = (u64*)malloc(sizeof(u64) * (size_t)n);
     i64* idx = (i64*)malloc(sizeof(i64) * (size_t)n);
@@ -397,7 +438,7 @@ static int or_cmp_i64(const void* a, const void* b) {
 
 typedef struct {
     int model;
-    int policy;           /* 0 gap top-m, 1 sequential, 2 uniform */
+    int policy;           /* 0 gap top-m, 1 sequential, 2 uniform, 3 importance (norm-proportional) */
     i64 m;
     int passes;
     i64 refresh_count;    /* unit-A refreshes per round (rotating cursor) */
@@ -440,7 +481,7 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
     i64 cursor = 0, t = 0;
     for (t = 0; t < cfg->max_rounds && s0 == OR_OK; ++t) {
         /* 1. selection */
-        i64 mt = or_select_policy(cfg->policy, n, m, t, cfg->seed, z, P);
+        i64 mt = or_select_policy(cfg->policy, n, m, t, cfg->seed, cfg->policy == 3 ? norms : z, P);
         qsort(P, (size_t)mt, sizeof(i64), or_cmp_i64); /* P as an ascending index set */
         /* 2. swap accounting */
         i64 swaps = 0;
@@ -604,7 +645,7 @@ int or_duhl_solve_cocoa(const or_duhl_cfg* cfg, int K, int linesearch, const flo
         i64 nP = 0;
         for (int k = 0; k < K; ++k) {
             i64 lo = (i64)k * n / K, hi = (i64)(k + 1) * n / K, nk = hi - lo;
-            for (i64 i = 0; i < nk; ++i) zloc[i] = z[lo + i];
+            for (i64 i = 0; i < nk; ++i) zloc[i] = cfg->policy == 3 ? norms[lo + i] : z[lo + i];
             i64 mt = or_select_policy(cfg->policy, nk, m, t, cfg->seed, zloc, P + nP);
             qsort(P + nP, (size_t)mt, sizeof(i64), or_cmp_i64);
             for (i64 q = 0; q < mt; ++q) P[nP + q] += lo;

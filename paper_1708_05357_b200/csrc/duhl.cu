@@ -931,11 +931,13 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
         int64_t nblk = (ctx->n + m - 1) / m, kb = round % nblk;
         int64_t lo = kb * m, hi = std::min(ctx->n, lo + m);
         for (int64_t i = lo; i < hi; ++i) P.push_back(i);
-    } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM) {
+    } else if (policy == DUHL_SEL_GAP || policy == DUHL_SEL_UNIFORM || policy == DUHL_SEL_IMPORTANCE) {
         {
             ProfScope ps(ctx, ctx->st, 2, 8.0 * ctx->n * 7);
-            CK(launch_topm(ctx->d_z, ctx->n, m, policy == DUHL_SEL_GAP ? 0 : 1, ctx->cfg.seed, round,
-                           ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches, ctx->d_topm_work));
+            const int keymode = policy == DUHL_SEL_GAP ? 0 : (policy == DUHL_SEL_UNIFORM ? 1 : 2);
+            CK(launch_topm(policy == DUHL_SEL_IMPORTANCE ? ctx->d_norms : ctx->d_z, ctx->n, m, keymode,
+                           ctx->cfg.seed, round, ctx->d_P, ctx->d_flag, ctx->st, &ctx->launches,
+                           ctx->d_topm_work));
         }
         if (ctx->cfg.hbm_budget_bytes == 0) {  // resident: P stays on the device
             TRY(finalize_staging(ctx));

@@ -222,7 +222,8 @@ cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* n
 // Top-m selection (Eq. 9 / Eq. 11): radix select of the m-th largest key, then
 // a stable compaction that keeps every key above the threshold and the
 // lowest-index keys equal to it (reading R7).  Keys: keymode 0 = IEEE bits of
-// z_i >= +0 (nonnegative doubles order as uint64); keymode 1 = ~key(seed,
+// z_i >= +0 (nonnegative doubles order as uint64); keymode 2 = importance clocks
+// (see select_key); keymode 1 = ~key(seed,
 // round, -1, i) (uniform baseline: the m smallest counter keys).
 // One CTA of 1024 threads; 11-bit digits, 6 passes.  P_out ascending.
 // =====================================================================================
@@ -234,6 +235,15 @@ constexpr int64_t kTopmSmallN = 1 << 17;  // one CTA up to here, the multi-CTA f
 __device__ __forceinline__ uint64_t select_key(const double* z, int64_t i, int keymode,
                                                uint64_t seed, int64_t round, int* bad) {
     if (keymode == 1) return ~perm_key(seed, round, -1, i);
+    if (keymode == 2) {
+        // importance sampling: m draws without replacement with probability
+        // proportional to ||a_i||^2 = the m smallest exponential clocks -ln(u_i)/||a_i||^2
+        // (z = norms); nonnegative doubles order as their bits, ~ turns smallest into largest
+        const double w = z[i];
+        const double u = ((double)(perm_key(seed, round, -2, i) >> 11) + 0.5) * 0x1p-53;
+        const double e = w > 0.0 ? -log(u) / w : __longlong_as_double(0x7ff0000000000000ll);
+        return ~(uint64_t)__double_as_longlong(e);
+    }
     double v = z[i];
     if (!(v >= 0.0)) { *bad = 1; v = 0.0; }  // NaN or negative: flagged, treated as 0
     return (uint64_t)__double_as_longlong(v + 0.0);  // +0.0 canonicalises -0.0

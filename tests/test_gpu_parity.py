@@ -169,6 +169,21 @@ def test_select_uniform_and_sequential_match_oracle(D):
             assert sel.tolist() == O.select_policy(O.SEL_SEQUENTIAL, 3000, 300, rnd, 0).tolist()
 
 
+@pytest.mark.parametrize("n,m", [(3000, 300), (300_001, 20_000)])   # one-CTA and multi-CTA top-m
+def test_select_importance_matches_oracle(D, n, m):
+    """IS baseline: the same m exponential clocks -ln(u)/||a||^2 on both sides."""
+    A, b = synth.lasso_dense(16, n, seed=4)
+    A[::97] *= 3.0                      # a spread of column norms
+    A[5] = 0.0                          # a zero column: never ahead of a nonzero one
+    norms = O.col_norms(A)
+    with D.create(A, b, 0.05, D.LASSO, seed=21) as P:
+        for rnd in (0, 1, 7):
+            sel, _ = P.select(D.SEL_IMPORTANCE, m=m, round=rnd)
+            ref = O.select_policy(O.SEL_IMPORTANCE, n, m, rnd, 21, norms)
+            assert sel.tolist() == sorted(ref.tolist())
+            assert 5 not in sel.tolist()
+
+
 # ------------------------------------------------------------------------- SCD epoch (a5)
 @pytest.mark.parametrize("kernel", [1, 2])   # warp-specialised / pipelined (control CTA)
 @pytest.mark.parametrize("model,d,n,m,W", [
@@ -292,6 +307,7 @@ def test_zero_columns(D, kernel):
 @pytest.mark.parametrize("model,policy,budget_cols", [
     (O.LASSO, O.SEL_GAP, 0), (O.SVM, O.SEL_GAP, 0),
     (O.LASSO, O.SEL_GAP, 300), (O.SVM, O.SEL_SEQUENTIAL, 260), (O.LASSO, O.SEL_UNIFORM, 250),
+    (O.SVM, O.SEL_IMPORTANCE, 250),
 ])
 def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     d, n = (400, 1000) if model == O.LASSO else (120, 1000)
@@ -327,8 +343,8 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     assert abs(r["rounds"] - ref["rounds"]) <= max(3, 0.3 * ref["rounds"])
     sw = [t.swaps for t in r["trace"]]
     assert sw[0] == m
-    if policy == O.SEL_SEQUENTIAL:
-        assert sw == ref["swaps"].tolist()
+    if policy in (O.SEL_SEQUENTIAL, O.SEL_IMPORTANCE):   # gap-independent: same sets every round
+        assert sw == ref["swaps"].tolist()[:len(sw)]
 
 
 def test_budget_smaller_than_data_swaps(D):

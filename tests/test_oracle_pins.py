@@ -316,6 +316,39 @@ def test_baseline_policies():
     assert abs(counts.mean() - 200) < 1e-9 and counts.std() < 3 * math.sqrt(200)
 
 
+def test_importance_sampling_policy():
+    """IS baseline: m draws without replacement, the next one with
+    probability proportional to ||a_j||^2 among the remaining columns.  Pinned by exact
+    successive-sampling inclusion probabilities (enumerated here) against frequencies over
+    many rounds, a single nonzero column, and equal norms == uniform inclusion m/n."""
+    # one nonzero column is always in the set; zero columns follow by index
+    w = np.zeros(10)
+    w[5] = 2.0
+    for r in range(5):
+        assert O.select_policy(O.SEL_IMPORTANCE, 10, 1, r, 3, w).tolist() == [5]
+        assert sorted(O.select_policy(O.SEL_IMPORTANCE, 10, 3, r, 3, w).tolist()) == [0, 1, 5]
+    # exact inclusion probabilities of successive sampling (m = 1 and m = 2)
+    w = np.array([1.0, 2.0, 3.0, 4.0, 10.0])
+    Wt = w.sum()
+    p1 = w / Wt
+    p2 = p1 + np.array([sum(w[k] / Wt * w[i] / (Wt - w[k]) for k in range(5) if k != i) for i in range(5)])
+    R = 20000
+    for m, p in ((1, p1), (2, p2)):
+        cnt = np.zeros(5)
+        for r in range(R):
+            cnt[O.select_policy(O.SEL_IMPORTANCE, 5, m, r, 11, w)] += 1
+        f = cnt / R
+        sd = np.sqrt(p * (1 - p) / R)
+        assert np.all(np.abs(f - p) < 5 * sd + 1e-12), (m, f, p)
+    # a plausible mistake (probabilities proportional to ||a||, or top-m of u * w) fails this:
+    assert np.abs(p2 - 2 * np.sqrt(w) / np.sqrt(w).sum()).max() > 0.02
+    # equal norms: uniform inclusion m / n
+    cnt = np.zeros(40)
+    for r in range(2000):
+        cnt[O.select_policy(O.SEL_IMPORTANCE, 40, 8, r, 4, np.full(40, 0.7))] += 1
+    assert abs(cnt.mean() - 400) < 1e-9 and cnt.std() < 4 * math.sqrt(400 * 0.8)
+
+
 # ----------------------------------------------------------------------------- generator
 def test_counter_generator_is_splitmix64():
     """or_mix64(x) is one splitmix64 step from state x; splitmix64(seed=0) first output."""
