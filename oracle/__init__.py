@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "duhl_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-LASSO, SVM = 0, 1
+LASSO, SVM, RIDGE = 0, 1, 2
 SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE = 0, 1, 2, 3
 OK, E_INVALID, E_NUMERIC, E_NOT_CONVERGED = 0, 2, 4, 9
 

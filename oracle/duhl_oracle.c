@@ -30,6 +30,8 @@ typedef uint64_t u64;
 
 #define OR_LASSO 0
 #define OR_SVM 1
+#define OR_RIDGE 2   /* ridge regression: f as Lasso, g_i = (lambda/2) alpha_i^2 */
+#define OR_HAS_B(model) ((model) != OR_SVM)   /* regression models: labels b, v~ = A alpha - b */
 
 #define OR_OK 0
 #define OR_E_INVALID 2
@@ -86,11 +88,12 @@ void or_matvec(const float* A, i64 d, i64 n, i64 ld, const double* alpha, double
 void or_primal_dual_w(int model, const double* v, const double* b, i64 d, i64 n, double lambda,
                       double* w) {
     for (i64 k = 0; k < d; ++k)
-        w[k] = (model == OR_LASSO) ? (v[k] - b[k]) : (v[k] / (lambda * (double)n));
+        w[k] = OR_HAS_B(model) ? (v[k] - b[k]) : (v[k] / (lambda * (double)n));
 }
 
 /* Per-coordinate duality gap, Eq. 4 in the closed forms of App. E:
  *   Lasso: gap_i = (1/d) [ a_i s_i + B [|s_i| - lambda d]_+ + lambda d |a_i| ]
+ *   Ridge: gap_i = (1/d) [ a_i s_i + s_i^2/(2 lambda d) + (lambda d/2) a_i^2 ]
  *   SVM: gap_i = (1/n) [ a_i s_i + max(0, 1 - y_i s_i) - y_i a_i ]
  * with s_i = a_i^T w.  gap_out[i] = gap, or +0.0 when gap <= 1e-12 x the
  * magnitude of its terms (rounding noise, reading R17); returns
@@ -110,6 +113,12 @@ int or_coord_gaps(int model, const float* A, i64 d, i64 n, i64 ld, const double*
             double lam_d = lambda * (double)d;
             double thr = fabs(s) - lam_d;
             double t1 = alpha[i] * s, t2 = B * (thr > 0.0 ? thr : 0.0), t3 = lam_d * fabs(alpha[i]);
+            g = (t1 + t2 + t3) / (double)d;
+            scale = (fabs(t1) + t2 + t3) / (double)d;
+        } else if (model == OR_RIDGE) {
+            /* gap_i = (1/d) [ a_i s_i + s_i^2/(2 lambda d) + (lambda d/2) a_i^2 ] */
+            double lam_d = lambda * (double)d;
+            double t1 = alpha[i] * s, t2 = s * s / (2.0 * lam_d), t3 = 0.5 * lam_d * alpha[i] * alpha[i];
             g = (t1 + t2 + t3) / (double)d;
             scale = (fabs(t1) + t2 + t3) / (double)d;
         } else {
@@ -266,15 +275,19 @@ void or_make_perm(const i64* P, i64 m, u64 seed, i64 round, i64 pass, i64* out) 
     for (i64 t = 0; t < m; ++t) out[t] = P[or_perm_index(seed, round, pass, m, t)];
 }
 
-/* One exact coordinate step (App. D, eta = 0 for Lasso):
+/* One exact coordinate step (App. D, eta = 0 for Lasso, eta = 1 for ridge):
  *   Lasso: gamma = (alpha_j ||a_j||^2 - a_j^T v~) / ||a_j||^2,
  *                      tau = lambda d / ||a_j||^2,  alpha' = sign(gamma) [|gamma| - tau]_+
+ *   Ridge (eta = 1): alpha' = (alpha_j ||a_j||^2 - a_j^T v~) / (||a_j||^2 + lambda d)
  *   SVM: Delta = (y_j - a_j^T v^ /(lambda n)) / (||a_j||^2 /(lambda n)),
  *                      alpha' = y_j max(0, min(1, y_j (alpha_j + Delta)))
  * s = a_j^T v~ (Lasso, v~ = A alpha - b) or a_j^T v^ (SVM, v^ = A alpha).
  * Zero column (reading R5): the exact 1-D minimiser, Lasso 0, SVM y_j. */
 double or_coord_update(int model, double alpha_j, double s, double norm, double y_j,
                        double lambda, i64 d, i64 n) {
+    if (model == OR_RIDGE) {  /* P:808-813 with eta = 1: tau = 0, denominator ||a||^2 + lambda d */
+        return (alpha_j * norm - s) / (norm + lambda * (double)d);
+    }
     if (model == OR_LASSO) {
         if (norm == 0.0) return 0.0;
         double gamma = (alpha_j * norm - s) / norm;
@@ -317,6 +330,8 @@ void or_scd_pass(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
  * Recomputes v = A alpha from scratch.  Returns gap = sum_i gap_i and
  *   Lasso: primal O = (1/2d)||w||^2 + lambda ||alpha||_1 (w = v - b),
  *          dual  D = -(u^T b + (d/2)||u||^2) - sum_i B [|a_i^T u| - lambda]_+,  u = w/d
+ *   Ridge: primal O = (1/2d)||w||^2 + (lambda/2)||alpha||^2,
+ *          dual  D = -(u^T b + (d/2)||u||^2) - sum_i (a_i^T u)^2 / (2 lambda)
  *   SVM:   primal O = -(1/n) sum y_i alpha_i + ||v||^2/(2 lambda n^2)
  *          dual  D = -P(w) = -[(1/n) sum_i max(0, 1 - y_i a_i^T w) + (lambda/2)||w||^2]
  * so that gap == O - D in exact arithmetic.  b_or_y = b (Lasso) / y (SVM). */
@@ -328,7 +343,7 @@ int or_duality_gap(int model, const float* A, i64 d, i64 n, i64 ld, const double
     double* s = (double*)malloc(sizeof(double) * (size_t)n);
     double* g = (double*)malloc(sizeof(double) * (size_t)n);
     or_matvec(A, d, n, ld, alpha, v);
-    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    const double* b = OR_HAS_B(model) ? b_or_y : NULL;
     const double* y = (model == OR_SVM) ? b_or_y : NULL;
     or_primal_dual_w(model, v, b, d, n, lambda, w);
     int st = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, s, g);
@@ -348,6 +363,23 @@ int or_duality_gap(int model, const float* A, i64 d, i64 n, i64 ld, const double
         for (i64 i = 0; i < n; ++i) {
             double x = fabs(s[i] / (double)d) - lambda;
             conj += B * (x > 0.0 ? x : 0.0);
+        }
+        D = -(ub + 0.5 * (double)d * uu) - conj;
+    } else if (model == OR_RIDGE) {
+        /* O = (1/2d)||w||^2 + (lambda/2)||alpha||^2;  g* of (lambda/2) x^2 is x^2/(2 lambda), so
+         * D = -(u^T b + (d/2)||u||^2) - sum_i (a_i^T u)^2/(2 lambda),  u = w/d */
+        double ww = 0.0, aa = 0.0, ub = 0.0, uu = 0.0, conj = 0.0;
+        for (i64 k = 0; k < d; ++k) ww += w[k] * w[k];
+        for (i64 i = 0; i < n; ++i) aa += alpha[i] * alpha[i];
+        O = ww / (2.0 * (double)d) + 0.5 * lambda * aa;
+        for (i64 k = 0; k < d; ++k) {
+            double u = w[k] / (double)d;
+            ub += u * b[k];
+            uu += u * u;
+        }
+        for (i64 i = 0; i < n; ++i) {
+            double x = s[i] / (double)d;
+            conj += x * x / (2.0 * lambda);
         }
         D = -(ub + 0.5 * (double)d * uu) - conj;
     } else {
@@ -387,7 +419,7 @@ int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
     double B = (model == OR_LASSO) ? or_lasso_B(b_or_y, d, lambda) : 0.0;
     const double* y = (model == OR_SVM) ? b_or_y : NULL;
     or_matvec(A, d, n, ld, alpha, vt);
-    if (model == OR_LASSO)
+    if (OR_HAS_B(model))
         for (i64 k = 0; k < d; ++k) vt[k] -= b_or_y[k];
     for (i64 i = 0; i < n; ++i) all[i] = i;
     int st = OR_E_NOT_CONVERGED;
@@ -428,7 +460,7 @@ int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
 /* w from the shared vector: Lasso w = v~ (P:855 with v~ = A alpha - b),
  * SVM w = v^/(lambda n). */
 static void or_shadow_w(int model, const double* vt, i64 d, i64 n, double lambda, double* w) {
-    for (i64 k = 0; k < d; ++k) w[k] = (model == OR_LASSO) ? vt[k] : vt[k] / (lambda * (double)n);
+    for (i64 k = 0; k < d; ++k) w[k] = OR_HAS_B(model) ? vt[k] : vt[k] / (lambda * (double)n);
 }
 
 static int or_cmp_i64(const void* a, const void* b) {
@@ -465,7 +497,7 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
     char* in_prev = (char*)calloc((size_t)n, 1);
     char* in_cur = (char*)calloc((size_t)n, 1);
     const double* y = (model == OR_SVM) ? b_or_y : NULL;
-    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    const double* b = OR_HAS_B(model) ? b_or_y : NULL;
     or_col_norms(A, d, n, ld, norms);
     double B = (model == OR_LASSO) ? or_lasso_B(b, d, lambda) : 0.0;
     int st = OR_E_NOT_CONVERGED;
@@ -474,7 +506,7 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
     /* state: the shared vector of App. D, v~ = A alpha - b (Lasso) or
      * v^ = A alpha (SVM); w follows from it (App. E). */
     or_matvec(A, d, n, ld, alpha, v);
-    for (i64 r = 0; r < d; ++r) vt[r] = (model == OR_LASSO) ? v[r] - b[r] : v[r];
+    for (i64 r = 0; r < d; ++r) vt[r] = OR_HAS_B(model) ? v[r] - b[r] : v[r];
     or_shadow_w(model, vt, d, n, lambda, w);
     int s0 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
     if (s0 != OR_OK) st = s0;
@@ -532,6 +564,8 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
  * global objective along alpha_old + gamma dalpha (v = v0 + gamma dv):
  *   SVM: O(g) = -(S + g sum_i y_i da_i)/n + ||v0 + g dv||^2/(2 lambda n^2)
  *                 -> g* = clip((sum y da / n - v0^T dv/(lambda n^2)) / (||dv||^2/(lambda n^2)), 0, 1)
+ *   Ridge: O(g) = ||vt0 + g dv||^2/(2d) + (lambda/2) sum_i (a_i + g da_i)^2: quadratic,
+ *                 g* = clip(-(vt0^T dv/d + lambda a.da) / (||dv||^2/d + lambda da.da), 0, 1)
  *   Lasso: O(g) = ||vt0 + g dv||^2/(2d) + lambda sum_i |a_i + g da_i|  (vt0 = A a - b)
  *                 convex piecewise quadratic: its right derivative
  *                 D(g) = (vt0^T dv + g ||dv||^2)/d + lambda sum_i da_i sgn+(a_i + g da_i)
@@ -563,6 +597,14 @@ double or_linesearch(int model, const double* v0, const double* dv, i64 d, const
         for (i64 i = 0; i < k; ++i) yda += y[i] * da[i];
         if (!(dvdv > 0.0)) return 1.0;
         double g = (yda / (double)n - vdv / ln2) / (dvdv / ln2);
+        return g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g);
+    }
+    if (model == OR_RIDGE) {  /* quadratic in g: O'(g) = (vdv + g dvdv)/d + lambda (a.da + g da.da) */
+        double ada = 0.0, dada = 0.0;
+        for (i64 i = 0; i < k; ++i) { ada += a_old[i] * da[i]; dada += da[i] * da[i]; }
+        double den = dvdv / (double)d + lambda * dada;
+        if (!(den > 0.0)) return 1.0;
+        double g = -(vdv / (double)d + lambda * ada) / den;
         return g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g);
     }
     if (or_lasso_rderiv(0.0, a_old, da, k, vdv, dvdv, lambda, d) >= 0.0) return 0.0;
@@ -613,7 +655,7 @@ int or_duhl_solve_cocoa(const or_duhl_cfg* cfg, int K, int linesearch, const flo
     i64 m = cfg->m;
     if (K < 1 || m < 1 || m * K > n) return OR_E_INVALID;
     const double* y = (model == OR_SVM) ? b_or_y : NULL;
-    const double* b = (model == OR_LASSO) ? b_or_y : NULL;
+    const double* b = OR_HAS_B(model) ? b_or_y : NULL;
     double* norms = (double*)malloc(sizeof(double) * (size_t)n);
     double* v = (double*)malloc(sizeof(double) * (size_t)d);
     double* vt = (double*)malloc(sizeof(double) * (size_t)d);
@@ -635,7 +677,7 @@ int or_duhl_solve_cocoa(const or_duhl_cfg* cfg, int K, int linesearch, const flo
     int st = OR_E_NOT_CONVERGED;
     double gap = INFINITY;
     or_matvec(A, d, n, ld, alpha, v);
-    for (i64 r = 0; r < d; ++r) vt[r] = (model == OR_LASSO) ? v[r] - b[r] : v[r];
+    for (i64 r = 0; r < d; ++r) vt[r] = OR_HAS_B(model) ? v[r] - b[r] : v[r];
     or_shadow_w(model, vt, d, n, lambda, w);
     int s0 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
     if (s0 != OR_OK) st = s0;

@@ -23,14 +23,16 @@ def _objective(model, A, lab, lam, alpha):
     v = A64.T @ alpha
     if model == O.LASSO:
         return ((v - lab) @ (v - lab)) / (2 * d) + lam * np.abs(alpha).sum()
+    if model == O.RIDGE:
+        return ((v - lab) @ (v - lab)) / (2 * d) + 0.5 * lam * (alpha @ alpha)
     return -(lab @ alpha) / n + (v @ v) / (2 * lam * n * n)
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
 def test_linesearch_is_the_exact_minimiser(model):
     rng = np.random.default_rng(5)
     for trial in range(20):
-        if model == O.LASSO:
+        if model in (O.LASSO, O.RIDGE):
             A, lab = synth.lasso_dense(40, 30, seed=trial)
             lam = 0.05
             a0 = rng.standard_normal(30) * (rng.random(30) < 0.5) * 0.2
@@ -41,7 +43,7 @@ def test_linesearch_is_the_exact_minimiser(model):
             a0 = lab * rng.random(30)
             a1 = lab * rng.random(30)
         A64 = A.astype(np.float64)
-        v0 = A64.T @ a0 - (lab if model == O.LASSO else 0)
+        v0 = A64.T @ a0 - (lab if model != O.SVM else 0)
         dv = A64.T @ (a1 - a0)
         idx = np.arange(30)
         g = O.linesearch(model, v0, dv, a0[idx], (a1 - a0)[idx],

@@ -177,6 +177,82 @@ def test_P5_P6_steps_minimise_1d_objective():
         assert psi(x) <= psi(cand) + 1e-12 * max(1, abs(psi(cand)))
 
 
+# ----------------------------------------------------------------------------- ridge (NEXT-2)
+def test_R1_ridge_worked_example():
+    """A = I_2, b = (1, 1), lambda = 1/4, d = 2 (P:746, P:841).  alpha* = b/(1 + lambda d) = 2/3;
+    at alpha = 0: s = a_i^T (A 0 - b) = -1, gap_i = (1/d)(s^2/(2 lambda d)) = 1/2, O = 1/2;
+    at alpha*: O* = (1/4)(2/9) + (1/8)(8/9) = 1/6 and every gap vanishes (s = -lambda d alpha)."""
+    A = np.eye(2, dtype=np.float32)
+    b = np.array([1.0, 1.0])
+    lam = 0.25
+    w0 = -b
+    g0 = O.coord_gaps(O.RIDGE, A, np.zeros(2), None, w0, lam)[2]
+    np.testing.assert_allclose(g0, [0.5, 0.5], rtol=0, atol=1e-15)
+    st, G, Ob, Db = O.duality_gap(O.RIDGE, A, np.zeros(2), b, lam)
+    assert st == O.OK and abs(G - 1.0) < 1e-15 and abs(Ob - 0.5) < 1e-15 and abs(G - (Ob - Db)) < 1e-15
+    astar = np.full(2, 2.0 / 3.0)
+    st, G, Ob, Db = O.duality_gap(O.RIDGE, A, astar, b, lam)
+    assert abs(Ob - 1.0 / 6.0) < 1e-15 and G < 1e-15
+    # one exact step from 0 reaches the minimiser (orthonormal design)
+    assert abs(O.coord_update(O.RIDGE, 0.0, -1.0, 1.0, 0.0, lam, 2, 2) - 2.0 / 3.0) < 1e-16
+
+
+def test_R2_ridge_closed_form_optimum_and_gap_identity():
+    """Textbook normal equations (A^T A + lambda d I) alpha* = A^T b; plain SCD reaches the
+    certified gap and alpha* (strongly convex: unique); sum gap_i = O - D and gap_i >= 0 at
+    random states; sklearn Ridge(alpha = lambda d) minimises the same objective."""
+    from sklearn.linear_model import Ridge
+    d, n, lam = 120, 80, 0.03
+    A, b = synth.lasso_dense(d, n, seed=17)
+    A64 = A.astype(np.float64).T                     # d x n
+    astar = np.linalg.solve(A64.T @ A64 + lam * d * np.eye(n), A64.T @ b)
+    st, alpha, gap, ep = O.solve_scd(O.RIDGE, A, b, lam, 1e-13, 5000, seed=2)
+    assert st == O.OK and gap <= 1e-13
+    np.testing.assert_allclose(alpha, astar, atol=1e-6 * np.abs(astar).max())
+    st, G, Ob, Db = O.duality_gap(O.RIDGE, A, astar, b, lam)
+    assert G < 1e-12
+    sk = Ridge(alpha=lam * d, fit_intercept=False, tol=1e-14, solver="cholesky").fit(A64, b).coef_
+    r = A64 @ sk - b
+    O_sk = r @ r / (2 * d) + 0.5 * lam * sk @ sk
+    assert abs(O_sk - Ob) <= 1e-12 * abs(Ob)
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        a = rng.standard_normal(n) * 0.3
+        st, G, Ob, Db = O.duality_gap(O.RIDGE, A, a, b, lam)
+        w = A64 @ a - b
+        g = O.coord_gaps(O.RIDGE, A, a, None, w, lam)[2]
+        assert np.all(g >= 0) and abs(g.sum() - G) <= 1e-12 * G
+        assert abs(G - (Ob - Db)) <= 1e-10 * max(1.0, abs(Ob))
+        # closed form of P:841: gap_i = (s_i + lambda d a_i)^2 / (2 lambda d^2)
+        s_ = A64.T @ w
+        np.testing.assert_allclose(g, (s_ + lam * d * a) ** 2 / (2 * lam * d * d), rtol=1e-9, atol=1e-300)
+
+
+def test_R3_ridge_step_minimises_1d_objective():
+    from scipy.optimize import minimize_scalar
+    rng = np.random.default_rng(8)
+    for _ in range(100):
+        d, n = int(rng.integers(2, 50)), int(rng.integers(2, 50))
+        nrm, aj, s_ = float(rng.uniform(0.0, 5)), float(rng.normal()), float(rng.normal() * 3)
+        lam = float(rng.uniform(0.001, 0.5))
+        phi = lambda x: (2 * s_ * (x - aj) + nrm * (x - aj) ** 2) / (2 * d) + 0.5 * lam * x * x
+        x = O.coord_update(O.RIDGE, aj, s_, nrm, 0.0, lam, d, n)
+        r = minimize_scalar(phi, bounds=(-100, 100), method="bounded", options={"xatol": 1e-10})
+        assert phi(x) <= r.fun + 1e-12 and abs(x - r.x) < 1e-6
+
+
+@pytest.mark.parametrize("policy", [O.SEL_GAP, O.SEL_UNIFORM])
+def test_R4_ridge_duhl_reaches_the_normal_equations(policy):
+    d, n, lam = 200, 400, 0.02
+    A, b = synth.lasso_dense(d, n, seed=23)
+    A64 = A.astype(np.float64).T
+    astar = np.linalg.solve(A64.T @ A64 + lam * d * np.eye(n), A64.T @ b)
+    r = O.duhl_solve(O.RIDGE, A, b, lam, m=100, passes=2, policy=policy, refresh_count=40,
+                     eps=1e-10, max_rounds=3000, cert_every=1, seed=4)
+    assert r["status"] == O.OK and r["gap"] <= 1e-10
+    np.testing.assert_allclose(r["alpha"], astar, atol=1e-4 * np.abs(astar).max())
+
+
 # ----------------------------------------------------------------------------- P7 / P8
 def test_P7_hadamard_lasso_closed_form_one_epoch():
     """Orthogonal design A^T A = d I: alpha* = soft(A^T b, lam d)/d (north_star pin).
