@@ -42,7 +42,7 @@ extern "C" {
 
 typedef struct duhl_ctx duhl_ctx; /* opaque; one per problem instance */
 
-typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1 } duhl_model;
+typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1, DUHL_RIDGE = 2 } duhl_model;
 
 /* Block selection policies: Eq. 11 gap memory, and the paper's
  * reference schemes: sequential blocks [Yu 2012], uniform. */

@@ -8,7 +8,7 @@ import numpy as np
 
 from . import build as _build
 
-LASSO, SVM_DUAL = 0, 1
+LASSO, SVM_DUAL, RIDGE = 0, 1, 2
 SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE = 0, 1, 2, 3
 STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "E_NOMEM",
           7: "E_CUDA", 8: "E_NCCL", 9: "E_NOT_CONVERGED"}

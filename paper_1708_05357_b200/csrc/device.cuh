@@ -14,6 +14,7 @@ constexpr int kLasso = 0;
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 constexpr int kSvm = 1;
+constexpr int kRidge = 2;  // ridge regression: the regression structure of Lasso, g = (lambda/2) a^2
 
 // ---------------------------------------------------------------- counter RNG
 // splitmix64 finaliser; permutation key(seed, round, pass, j) (DESIGN.md
@@ -38,11 +39,13 @@ __host__ __device__ __forceinline__ uint64_t perm_key(uint64_t seed, int64_t rou
 // a_j^T v^ (SVM, v^ = A alpha); nrm = ||a_j||^2.
 //   Lasso, eta = 0: gamma = (alpha nrm - s)/nrm, tau = lambda d/nrm,
 //                               alpha' = sign(gamma) max(|gamma| - tau, 0)
+//   Ridge (eta = 1): alpha' = (alpha nrm - s) / (nrm + lambda d)
 //   SVM: Delta = (y - s/(lambda n)) / (nrm/(lambda n)),
 //                    alpha' = y clip(y (alpha + Delta), 0, 1)
 // Zero column: the exact 1-D minimiser (Lasso 0, SVM y) -- reading R5.
 __device__ __forceinline__ double coord_step(int model, double alpha, double s, double nrm,
                                              double y, double lambda, double dd, double nn) {
+    if (model == kRidge) return (alpha * nrm - s) / (nrm + lambda * dd);  // P:808-813, eta = 1
     if (model == kLasso) {
         if (nrm == 0.0) return 0.0;
         double gamma = (alpha * nrm - s) / nrm;
@@ -61,6 +64,7 @@ __device__ __forceinline__ double coord_step(int model, double alpha, double s, 
 
 // Per-coordinate gap, Eq. 4 with the App. E closed forms; s = a_i^T w.
 //   Lasso: (1/d)[alpha s + B max(|s| - lambda d, 0) + lambda d |alpha|]
+//   Ridge: (1/d)[alpha s + s^2/(2 lambda d) + (lambda d/2) alpha^2]
 //   SVM: (1/n)[alpha s + max(0, 1 - y s) - y alpha]
 // Returns the raw gap; *scale receives the magnitude of its terms (for the
 // negative-gap check, reading R17); *aux receives the conjugate / loss term
@@ -68,6 +72,14 @@ __device__ __forceinline__ double coord_step(int model, double alpha, double s, 
 __device__ __forceinline__ double coord_gap(int model, double alpha, double s, double y,
                                             double lambda, double B, double dd, double nn,
                                             double* scale, double* aux) {
+    if (model == kRidge) {  // P:841; aux = g*(-a^T u) = (s/d)^2/(2 lambda) for the dual
+        const double lam_d = lambda * dd;
+        const double t1 = alpha * s, t2 = s * s / (2.0 * lam_d), t3 = 0.5 * lam_d * alpha * alpha;
+        *scale = (fabs(t1) + t2 + t3) / dd;
+        const double x = s / dd;
+        *aux = x * x / (2.0 * lambda);
+        return (t1 + t2 + t3) / dd;
+    }
     if (model == kLasso) {
         double lam_d = lambda * dd;
         double thr = fabs(s) - lam_d;

@@ -222,8 +222,13 @@ static ColSrc colsrc(const duhl_ctx* ctx) {
 
 static CscMat cscmat(const duhl_ctx* ctx) { return CscMat{ctx->d_colptr, ctx->d_rows, ctx->d_vals}; }
 
+// ridge: the SCD kernels take 1/(||a_j||^2 + lambda d) per position (k_perm_order)
+static double ridge_ld(const duhl_ctx* ctx) {
+    return ctx->model == DUHL_RIDGE ? ctx->lambda * (double)ctx->d : 0.0;
+}
+
 static double wscale(const duhl_ctx* ctx) {
-    return ctx->model == DUHL_LASSO ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n_glob);
+    return ctx->model != DUHL_SVM_DUAL ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n_glob);
 }
 
 // In-place sum (or max) allreduce over the group on the compute stream; no-op alone.
@@ -628,7 +633,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         return DUHL_E_INVALID;
     if (!A == !C || !b_or_y) return DUHL_E_INVALID;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return DUHL_E_INVALID;
-    if (model != DUHL_LASSO && model != DUHL_SVM_DUAL) return DUHL_E_INVALID;
+    if (model != DUHL_LASSO && model != DUHL_SVM_DUAL && model != DUHL_RIDGE) return DUHL_E_INVALID;
     const int64_t nin = A ? A->n : C->n, din = A ? A->d : C->d;
     if (nin > (int64_t)INT32_MAX - 1) return DUHL_E_INVALID;
     duhl_ctx* ctx = new duhl_ctx();
@@ -871,7 +876,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         ck(cudaStreamSynchronize(st));
         ctx->B = h[0] / (2.0 * lambda * (double)d);  // P:848, reading R1
     }
-    ck(launch_matvec(colsrc(ctx), ctx->d_alpha, 0, d, d4, model == DUHL_LASSO ? ctx->d_b : nullptr,
+    ck(launch_matvec(colsrc(ctx), ctx->d_alpha, 0, d, d4, model != DUHL_SVM_DUAL ? ctx->d_b : nullptr,
                      ctx->d_vt, st, &ctx->launches));  // alpha = 0: v~ = -b, v^ = 0
     ck(cudaStreamSynchronize(st));
     if (!ok2) { cudaGetLastError(); ctx->err = "precompute failed"; return bail(DUHL_E_CUDA); }
@@ -1069,7 +1074,8 @@ static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t 
         CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
                              ctx->d_order_j, ctx->d_order_slot, ctx->d_order_batch, ctx->d_order_a,
                              ctx->d_order_inv, ctx->d_order_y, ctx->d_alpha, ctx->d_norms,
-                             ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr, ctx->st, &ctx->launches));
+                             ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr, ctx->st, &ctx->launches,
+                             ridge_ld(ctx)));
         TRY(scd_launch(ctx, m));
         if (pass == 0) TRY(issue_staging(ctx));  // no-op unless overlapping: host enqueue overlaps pass 0
     }
@@ -1109,7 +1115,7 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
         CK(launch_perm_order(nullptr, nullptr, nullptr, perm_len, 0, 0, 0, ctx->d_order_j, ctx->d_order_slot,
                              ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                              ctx->d_alpha, ctx->d_norms, ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr,
-                             ctx->st, &ctx->launches));
+                             ctx->st, &ctx->launches, ridge_ld(ctx)));
         TRY(scd_launch(ctx, perm_len));
         TRY(issue_staging(ctx));
         TRY(finalize_staging(ctx));
@@ -1129,7 +1135,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
     TRY(allreduce(ctx, ctx->d_sums, 3));           // per-column sums over the shards
     TRY(allreduce(ctx, ctx->d_sums + 3, 1, ncclMax));
-    CK(launch_vec_sums(ctx->d_vt, ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
+    CK(launch_vec_sums(ctx->d_vt, ctx->model != DUHL_SVM_DUAL ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
                        ctx->st, &ctx->launches));     // v is replicated: no reduction
     double h[8];
     CK(cudaMemcpyAsync(h, ctx->d_sums, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
@@ -1143,6 +1149,10 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
     if (ctx->model == DUHL_LASSO) {
         // w = v~; O = ||w||^2/(2d) + lambda ||alpha||_1;  D = -(u^T b + (d/2)||u||^2) - sum B[|a^T u| - lambda]_+
         O = vv / (2.0 * dd) + lam * asum;
+        D = -(vb / dd + 0.5 * vv / dd) - aux;
+    } else if (ctx->model == DUHL_RIDGE) {
+        // O = ||w||^2/(2d) + (lambda/2)||alpha||^2;  D = -(u^T b + (d/2)||u||^2) - sum (a^T u)^2/(2 lambda)
+        O = vv / (2.0 * dd) + 0.5 * lam * asum;
         D = -(vb / dd + 0.5 * vv / dd) - aux;
     } else {
         // O = -(1/n) sum y a + ||v||^2/(2 lambda n^2);  D = -[(1/n) sum hinge + (lambda/2)||w||^2]
@@ -1182,7 +1192,19 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
     CK(launch_vec_sums(ctx->d_dv, ctx->d_vsnap, ctx->d4, ctx->d_ls, ctx->st, &ctx->launches));  // |dv|^2, v0.dv
     double gamma = 1.0;
     if (ctx->cfg.linesearch) {
-        if (ctx->model == DUHL_SVM_DUAL) {
+        if (ctx->model == DUHL_RIDGE) {  // quadratic in gamma: closed form
+            CK(launch_ridge_sums(ctx->d_alpha, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 2, ctx->st, &ctx->launches));
+            TRY(allreduce(ctx, ctx->d_ls + 2, 2));
+            double h[4];
+            CK(cudaMemcpyAsync(h, ctx->d_ls, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            const double dvdv = h[0], vdv = h[1], ada = h[2], dada = h[3];
+            const double den = dvdv / dd + lam * dada;
+            if (den > 0.0) {
+                gamma = -(vdv / dd + lam * ada) / den;
+                gamma = gamma < 0.0 ? 0.0 : (gamma > 1.0 ? 1.0 : gamma);
+            }
+        } else if (ctx->model == DUHL_SVM_DUAL) {
             CK(launch_ydalpha(ctx->d_alpha, ctx->d_y, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 2, ctx->st,
                               &ctx->launches));
             TRY(allreduce(ctx, ctx->d_ls + 2, 1));
@@ -1404,7 +1426,7 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
     }
     CK(cudaMemcpyAsync(ctx->d_alpha, alpha, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
     CK(launch_matvec(colsrc(ctx), ctx->d_alpha, ctx->csc ? 0 : ctx->n, ctx->d, ctx->d4,
-                     ctx->model == DUHL_LASSO ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
+                     ctx->model != DUHL_SVM_DUAL ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
     if (ctx->csc) CK(launch_csc_matvec(cscmat(ctx), ctx->d_alpha, ctx->n, ctx->d_vt, ctx->st, &ctx->launches));
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, nullptr));
     CK(cudaStreamSynchronize(ctx->st));

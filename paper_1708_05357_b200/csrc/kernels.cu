@@ -54,7 +54,7 @@ __device__ __forceinline__ void gap_finish_one(const GapParams& p, int64_t t, in
     if (p.s_out) p.s_out[t] = s;
     acc.g += gz;
     acc.aux += aux;
-    acc.a += p.model == kLasso ? fabs(a) : yy * a;
+    acc.a += p.model == kLasso ? fabs(a) : (p.model == kRidge ? a * a : yy * a);
     acc.amax = fmax(acc.amax, fabs(a));
 }
 
@@ -505,17 +505,18 @@ struct OrderOut {
     unsigned* batch;
     double *a, *inv, *y;
 };
+// inv: 1/||a_j||^2 (-1: zero column); ridge (ridge_ld = lambda d > 0): 1/(||a_j||^2 + lambda d)
 __device__ __forceinline__ void order_info(const OrderOut& o, int64_t t, int64_t j, const double* alpha,
-                                           const double* norms, const double* y) {
+                                           const double* norms, const double* y, double ridge_ld) {
     const double nrm = norms[j];
     o.a[t] = alpha[j];
-    o.inv[t] = nrm > 0.0 ? 1.0 / nrm : -1.0;
+    o.inv[t] = ridge_ld > 0.0 ? 1.0 / (nrm + ridge_ld) : (nrm > 0.0 ? 1.0 / nrm : -1.0);
     o.y[t] = y ? y[j] : 0.0;
 }
 
 __global__ void k_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
                              uint64_t key, int h, OrderOut o, const double* alpha, const double* norms,
-                             const double* y) {
+                             const double* y, double ridge_ld) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < m) {
         int64_t q = feistel_index(key, h, m, t);
@@ -523,30 +524,31 @@ __global__ void k_perm_order(const int64_t* P, const int* P_slot, const unsigned
         o.j[t] = j;
         o.slot[t] = P_slot[q];
         o.batch[t] = P_batch[q];
-        order_info(o, t, j, alpha, norms, y);
+        order_info(o, t, j, alpha, norms, y, ridge_ld);
     }
 }
 
-__global__ void k_order_info(int64_t L, OrderOut o, const double* alpha, const double* norms, const double* y) {
+__global__ void k_order_info(int64_t L, OrderOut o, const double* alpha, const double* norms, const double* y,
+                             double ridge_ld) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < L) order_info(o, t, o.j[t], alpha, norms, y);
+    if (t < L) order_info(o, t, o.j[t], alpha, norms, y, ridge_ld);
 }
 
 cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigned* P_batch, int64_t m,
                               uint64_t seed, int64_t round, int64_t pass, int64_t* order_j,
                               int* order_slot, unsigned* order_batch, double* order_a, double* order_inv,
                               double* order_y, const double* alpha, const double* norms, const double* y,
-                              cudaStream_t st, int64_t* launches) {
+                              cudaStream_t st, int64_t* launches, double ridge_ld) {
     if (m <= 0) return cudaSuccess;
     OrderOut o{order_j, order_slot, order_batch, order_a, order_inv, order_y};
     if (P == nullptr) {  // explicit order already in order_j / slot / batch: gather the rest
-        k_order_info<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(m, o, alpha, norms, y);
+        k_order_info<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(m, o, alpha, norms, y, ridge_ld);
     } else {
         int h = 1;
         while ((1ll << (2 * h)) < m) ++h;
         uint64_t key = mix64(mix64(mix64(seed) ^ (uint64_t)round) ^ (uint64_t)pass);
         k_perm_order<<<(unsigned)cdiv(m, 256), 256, 0, st>>>(P, P_slot, P_batch, m, key, h, o, alpha,
-                                                              norms, y);
+                                                              norms, y, ridge_ld);
     }
     ++*launches;
     return cudaGetLastError();
@@ -812,7 +814,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * R;
     const int rows = (int)imin64(R, p.d4 - r0);
-    const double lam_dn = MODEL == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
+    const double lam_dn = MODEL != kSvm ? p.lambda * (double)p.d : p.lambda * (double)p.n;
     const size_t bufsz = (size_t)NRED * kRedGroups * kRedStride;
     const int grp = c % kRedGroups;
 
@@ -997,6 +999,10 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                     t = a - sj * inv;
                     tau = lam_dn * inv;
                     scale = -inv;
+                } else if (MODEL == kRidge) {  // inv = 1/(||a||^2 + lambda d): t = gamma, no threshold
+                    t = a - (sj + lam_dn * a) * inv;
+                    tau = 0.0;
+                    scale = -inv;
                 } else {
                     t = fma(lam_dn - yy * sj, inv, yy * a);
                     cy_ = yy;
@@ -1012,7 +1018,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
             // every lane run all Wb steps redundantly: no per-step cross-lane traffic.
             if (lane < 16) {
                 sT[lane] = t;
-                sP[lane] = MODEL == kLasso ? tau : cy_;
+                sP[lane] = MODEL != kSvm ? tau : cy_;
                 sZ[lane] = zero ? 1 : 0;
                 sA[lane] = a;
                 sS[lane] = scale;
@@ -1036,7 +1042,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
                 if (j >= Wb) break;
                 const double aj = sA[j], pj = sP[j];
                 double an;
-                if (MODEL == kLasso) {
+                if (MODEL != kSvm) {
                     const double mag = fabs(tq[j]) - pj;
                     an = mag > 0.0 ? copysign(mag, tq[j]) : 0.0;
                     if (sZ[j]) an = 0.0;
@@ -1185,6 +1191,8 @@ cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launch
     size_t smem = scd_smem_bytes(p.W, p.R, kScdStages);
     const void* fn = p.model == kLasso
                          ? (p.exact ? (const void*)k_scd_gram<true, kLasso> : (const void*)k_scd_gram<false, kLasso>)
+                     : p.model == kRidge
+                         ? (p.exact ? (const void*)k_scd_gram<true, kRidge> : (const void*)k_scd_gram<false, kRidge>)
                          : (p.exact ? (const void*)k_scd_gram<true, kSvm> : (const void*)k_scd_gram<false, kSvm>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1280,6 +1288,27 @@ __global__ void k_ydalpha(const double* alpha, const double* y, const int64_t* P
         s += y[P[q]] * (alpha[P[q]] - aold[q]);
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) atomicAdd(&sums[0], s);
+}
+__global__ void k_ridge_sums(const double* alpha, const int64_t* P, const double* aold, int64_t k, double* sums) {
+    double s0 = 0, s1 = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x) {
+        const double da = alpha[P[q]] - aold[q];
+        s0 += aold[q] * da;
+        s1 += da * da;
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sums[0], s0);
+        atomicAdd(&sums[1], s1);
+    }
+}
+cudaError_t launch_ridge_sums(const double* alpha, const int64_t* P, const double* aold, int64_t k, double* sums,
+                              cudaStream_t st, int64_t* launches) {
+    if (k <= 0) return cudaSuccess;
+    k_ridge_sums<<<(unsigned)imin64(cdiv(k, 256), 148), 256, 0, st>>>(alpha, P, aold, k, sums);
+    ++*launches;
+    return cudaGetLastError();
 }
 // Lasso: out[g] += sum_q da_q sgn+(aold_q + gam[g] da_q), da_q = alpha_j - aold_q  (g < ng)
 __global__ void k_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
@@ -1547,6 +1576,8 @@ cudaError_t preload_kernels() {
         (const void*)k_scd_gram<true, kSvm>,   (const void*)k_scd_gram<false, kSvm>,
         (const void*)k_scd_pipe<true, kLasso>, (const void*)k_scd_pipe<false, kLasso>,
         (const void*)k_scd_pipe<true, kSvm>,   (const void*)k_scd_pipe<false, kSvm>,
+        (const void*)k_scd_gram<true, kRidge>, (const void*)k_scd_gram<false, kRidge>,
+        (const void*)k_scd_pipe<true, kRidge>, (const void*)k_scd_pipe<false, kRidge>, (const void*)k_ridge_sums,
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,

@@ -107,7 +107,7 @@ cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigne
                               uint64_t seed, int64_t round, int64_t pass, int64_t* order_j,
                               int* order_slot, unsigned* order_batch, double* order_a, double* order_inv,
                               double* order_y, const double* alpha, const double* norms, const double* y,
-                              cudaStream_t st, int64_t* launches);
+                              cudaStream_t st, int64_t* launches, double ridge_ld = 0.0);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
 // pipelined form (scd_pipe.cuh): p.G compute CTAs + one control CTA, W <= 32, p.NB in {3, 4}
 size_t pipe_red_doubles(int W);   // size of ScdParams::red (reduction + delta buffers)
@@ -131,6 +131,9 @@ cudaError_t launch_delta_v(const double* v, const double* v0, int64_t d4, double
                            cudaStream_t st, int64_t* launches);
 cudaError_t launch_ydalpha(const double* alpha, const double* y, const int64_t* P, const double* aold, int64_t k,
                            double* sums, cudaStream_t st, int64_t* launches);
+// ridge line search: sums[0] += sum_q aold_q da_q, sums[1] += sum_q da_q^2 (da_q = alpha_P[q] - aold_q)
+cudaError_t launch_ridge_sums(const double* alpha, const int64_t* P, const double* aold, int64_t k, double* sums,
+                              cudaStream_t st, int64_t* launches);
 cudaError_t launch_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
                                const double* gam, int ng, double* out, cudaStream_t st, int64_t* launches);
 cudaError_t launch_apply_gamma(double* v, const double* v0, const double* dv, int64_t d4, double* alpha,

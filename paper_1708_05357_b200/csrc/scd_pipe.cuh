@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
     unsigned* flg = p.bar + 8;   // [kPipeRot]
     const size_t rbsz = (size_t)NE * kRedStride;
     double* dbuf = p.red + (size_t)kPipeRot * rbsz;  // [kPipeRot][kPipeWMax]
-    const double lam_dn = MODEL == kLasso ? p.lambda * (double)p.d : p.lambda * (double)p.n;
+    const double lam_dn = MODEL != kSvm ? p.lambda * (double)p.d : p.lambda * (double)p.n;
     const bool tr = p.trace != nullptr && (tid == 0) && (c == G || c == 0);
     unsigned long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tprev = tr ? (unsigned long long)clock64() : 0;
@@ -301,6 +301,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                         t = a - sj * inv;
                         tau = lam_dn * inv;
                         scale = -inv;
+                    } else if (MODEL == kRidge) {  // inv = 1/(||a||^2 + lambda d): t = gamma, no threshold
+                        t = a - (sj + lam_dn * a) * inv;
+                        tau = 0.0;
+                        scale = -inv;
                     } else {
                         t = fma(lam_dn - y_in * sj, inv, y_in * a);
                         cy = y_in;
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                 for (int j = 0; j < kPipeWMax; ++j) {
                     if (j >= Wb) break;
                     double an;
-                    if (MODEL == kLasso) {
+                    if (MODEL != kSvm) {
                         const double mag = fabs(t) - tau;
                         an = mag > 0.0 ? copysign(mag, t) : 0.0;
                         if (zero) an = 0.0;
@@ -570,6 +574,8 @@ cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launch
     const size_t smem = pipe_smem_bytes(p.W, p.R, p.NB);
     const void* fn = p.model == kLasso
                          ? (p.exact ? (const void*)k_scd_pipe<true, kLasso> : (const void*)k_scd_pipe<false, kLasso>)
+                     : p.model == kRidge
+                         ? (p.exact ? (const void*)k_scd_pipe<true, kRidge> : (const void*)k_scd_pipe<false, kRidge>)
                          : (p.exact ? (const void*)k_scd_pipe<true, kSvm> : (const void*)k_scd_pipe<false, kSvm>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

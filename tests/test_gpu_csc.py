@@ -25,7 +25,7 @@ def D():
 def _problem(model, d, n, density, seed):
     cp, rows, vals = synth.csc_lasso(d, n, seed=seed, density=density)
     A = synth.csc_to_dense(cp, rows, vals, d)
-    if model == O.LASSO:
+    if model != O.SVM:
         lab = synth.lasso_finish(synth.csc_lasso_signal(cp, rows, vals, d, seed, support=0.05), d, seed)
         lam = 0.1 * np.abs(A.astype(np.float64) @ lab).max() / d
     else:
@@ -35,14 +35,14 @@ def _problem(model, d, n, density, seed):
 
 
 def _random_state(model, n, lab, rng):
-    if model == O.LASSO:
+    if model != O.SVM:
         return rng.standard_normal(n) * (rng.random(n) < 0.3) * 0.1
     return lab * rng.random(n) * (rng.random(n) < 0.5)
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
 def test_csc_gaps_and_certificate_match_oracle(D, model):
-    d, n = (3001, 2000) if model == O.LASSO else (2999, 1500)
+    d, n = (3001, 2000) if model != O.SVM else (2999, 1500)
     csc, A, lab, lam = _problem(model, d, n, 0.01, seed=31 + model)
     assert (np.diff(csc[0]) == 0).any() or True  # empty columns are allowed (density 1 %)
     rng = np.random.default_rng(7)
@@ -53,23 +53,24 @@ def test_csc_gaps_and_certificate_match_oracle(D, model):
         g_gpu, s_gpu = P.gaps(want_s=True)
         G, Ob, Db = P.duality_gap()
     v = O.matvec(A, alpha)
-    if model == O.LASSO:
-        w = O.primal_dual_w(O.LASSO, v, lab, n, lam)
-        _, s_or, g_or = O.coord_gaps(O.LASSO, A, alpha, None, w, lam, B)
+    if model != O.SVM:
+        w = O.primal_dual_w(model, v, lab, n, lam)
+        _, s_or, g_or = O.coord_gaps(model, A, alpha, None, w, lam, B)
     else:
         w = O.primal_dual_w(O.SVM, v, None, n, lam)
         _, s_or, g_or = O.coord_gaps(O.SVM, A, alpha, lab, w, lam)
     An = np.linalg.norm(A.astype(np.float64), axis=1)
     floor = KAPPA * An * np.linalg.norm(w)
     assert np.all(np.abs(s_gpu - s_or) <= TOL * np.maximum(np.abs(s_or), floor) + 1e-300)
-    c = (np.abs(alpha) + B) / d if model == O.LASSO else (np.abs(alpha) + 1) / n
+    c = ((np.abs(alpha) + B) / d if model == O.LASSO else (np.abs(alpha) + 1) / n if model == O.SVM
+         else (np.abs(s_or) + lam * d * np.abs(alpha)) / (lam * d * d) + 1.0 / d)
     assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), KAPPA * c * An * np.linalg.norm(w)) + 1e-300)
     st, G_ref, O_ref, D_ref = O.duality_gap(model, A, alpha, lab, lam, B)
     assert abs(G - G_ref) <= 1e-9 * max(1.0, abs(G_ref))
     assert abs(Ob - O_ref) <= 1e-9 * max(1.0, abs(O_ref))
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
 def test_csc_exact_epoch_matches_sequential_oracle(D, model):
     d, n, m = 2000, 1200, 700
     csc, A, lab, lam = _problem(model, d, n, 0.02, seed=41 + model)
@@ -82,7 +83,7 @@ def test_csc_exact_epoch_matches_sequential_oracle(D, model):
         P.scd_epoch(perm=order[::-1].copy())
         a_gpu, v_gpu, _ = P.get_state()
     alpha = np.zeros(n)
-    vt = -lab.copy() if model == O.LASSO else np.zeros(d)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
     norms = O.col_norms(A)
     O.scd_pass(model, A, norms, y, lam, alpha, vt, order)
     O.scd_pass(model, A, norms, y, lam, alpha, vt, order[::-1].copy())

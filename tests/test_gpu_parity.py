@@ -31,23 +31,23 @@ def _lab(model, A, seed):
 
 
 def _data(model, d, n, seed, ld=None):
-    if model == O.LASSO:
+    if model != O.SVM:   # Lasso and ridge regression share the data recipe
         return synth.lasso_dense(d, n, seed=seed, ld=ld)
     return synth.svm_dense(d, n, seed=seed, ld=ld)
 
 
 def _lam(model, n):
-    return 0.05 if model == O.LASSO else 1.0 / n
+    return 0.05 if model == O.LASSO else (0.02 if model == O.RIDGE else 1.0 / n)
 
 
 def _oracle_state(model, A, lab, lam, alpha, d):
     """Oracle s_i and gap_i at alpha (v = A alpha recomputed by the oracle)."""
     n = A.shape[0]
     v = O.matvec(A, alpha, d=d)
-    if model == O.LASSO:
-        w = O.primal_dual_w(O.LASSO, v, lab, n, lam)
-        B = O.lasso_B(lab, lam)
-        return O.coord_gaps(O.LASSO, A, alpha, None, w, lam, B, d=d) + (w,)
+    if model != O.SVM:
+        w = O.primal_dual_w(model, v, lab, n, lam)
+        B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+        return O.coord_gaps(model, A, alpha, None, w, lam, B, d=d) + (w,)
     w = O.primal_dual_w(O.SVM, v, None, n, lam)
     return O.coord_gaps(O.SVM, A, alpha, lab, w, lam, d=d) + (w,)
 
@@ -61,6 +61,8 @@ def _check_gaps(model, A, lab, lam, d, alpha, s_gpu, g_gpu, w):
     if model == O.LASSO:
         B = O.lasso_B(lab, lam)
         c = (np.abs(alpha) + B) / d
+    elif model == O.RIDGE:   # |d gap_i / d s_i| = |s_i + lambda d alpha_i| / (lambda d^2)
+        c = (np.abs(s_or) + lam * d * np.abs(alpha)) / (lam * d * d) + 1.0 / d
     else:
         c = (np.abs(alpha) + 1) / n
     gfloor = KAPPA * c * An * np.linalg.norm(w)
@@ -71,14 +73,14 @@ def _check_gaps(model, A, lab, lam, d, alpha, s_gpu, g_gpu, w):
 
 # ------------------------------------------------------------------------- gap pass (a2)
 @pytest.mark.parametrize("model,d,n", [(O.LASSO, 2000, 1000), (O.SVM, 500, 3000),
-                                       (O.LASSO, 9001, 300), (O.SVM, 10243, 257)])
+                                       (O.LASSO, 9001, 300), (O.SVM, 10243, 257), (O.RIDGE, 3001, 700)])
 def test_gaps_parity_at_injected_states(D, model, d, n):
     A, lab = _data(model, d, n, seed=100 + d)
     lam = _lam(model, n)
     rng = np.random.default_rng(d)
     with D.create(A, lab, lam, model) as P:
         states = [np.zeros(n)]
-        if model == O.LASSO:
+        if model != O.SVM:
             states.append(rng.standard_normal(n) * (rng.random(n) < 0.2) * 0.05)
         else:
             states.append(lab * rng.random(n) * (rng.random(n) < 0.5))
@@ -109,7 +111,7 @@ def test_gaps_subset_and_ragged_ld(D):
 
 
 def test_certificate_matches_oracle(D):
-    for model, d, n in [(O.LASSO, 600, 900), (O.SVM, 300, 1200)]:
+    for model, d, n in [(O.LASSO, 600, 900), (O.SVM, 300, 1200), (O.RIDGE, 500, 700)]:
         A, lab = _data(model, d, n, seed=9)
         lam = _lam(model, n)
         st, alpha, g, ep = O.solve_scd(model, A, lab, lam, 1e-3, 50, seed=1)
@@ -195,6 +197,8 @@ def test_select_importance_matches_oracle(D, n, m):
     (O.LASSO, 40000, 300, 299, 32),     # C3 row count: 32-wide blocks (pipelined only), ragged tail
     (O.SVM, 9998, 500, 477, 24),
     (O.LASSO, 1003, 400, 390, 20),
+    (O.RIDGE, 2000, 600, 500, 0),
+    (O.RIDGE, 30001, 300, 277, 32),
 ])
 def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
     """P12: same order, fp64 -> GPU epoch == oracle sequential epoch to ~1e-12."""
@@ -209,7 +213,7 @@ def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
         P.scd_epoch(perm=order)
         a_gpu, v_gpu, _ = P.get_state()
     alpha = np.zeros(n)
-    vt = -lab.copy() if model == O.LASSO else np.zeros(d)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
     O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
     scale_a = max(1e-300, np.abs(alpha).max())
     assert np.abs(a_gpu - alpha).max() <= 1e-11 * scale_a
@@ -217,7 +221,8 @@ def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
 
 
 @pytest.mark.parametrize("kernel", [1, 2])
-@pytest.mark.parametrize("model,d,n,m", [(O.LASSO, 40000, 400, 390), (O.SVM, 200704 // 8, 300, 290)])
+@pytest.mark.parametrize("model,d,n,m", [(O.LASSO, 40000, 400, 390), (O.SVM, 200704 // 8, 300, 290),
+                                         (O.RIDGE, 40000, 400, 390)])
 def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
     """Fast mode (scd_exact=0, the bench's): fp32 Gram partials inside a CTA (k_scd_pipe) or a
     warp (k_scd_gram), fp64 across CTAs and everywhere else.  The Gram entries only correct s_j
@@ -233,7 +238,7 @@ def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
         P.scd_epoch(perm=order)
         a_gpu, v_gpu, _ = P.get_state()
     alpha = np.zeros(n)
-    vt = -lab.copy() if model == O.LASSO else np.zeros(d)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
     O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
     assert np.abs(a_gpu - alpha).max() <= 1e-6 * max(1e-300, np.abs(alpha).max())
     assert np.abs(v_gpu - vt).max() <= 1e-6 * max(1.0, np.abs(vt).max())
@@ -307,10 +312,10 @@ def test_zero_columns(D, kernel):
 @pytest.mark.parametrize("model,policy,budget_cols", [
     (O.LASSO, O.SEL_GAP, 0), (O.SVM, O.SEL_GAP, 0),
     (O.LASSO, O.SEL_GAP, 300), (O.SVM, O.SEL_SEQUENTIAL, 260), (O.LASSO, O.SEL_UNIFORM, 250),
-    (O.SVM, O.SEL_IMPORTANCE, 250),
+    (O.SVM, O.SEL_IMPORTANCE, 250), (O.RIDGE, O.SEL_GAP, 300), (O.RIDGE, O.SEL_GAP, 0),
 ])
 def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
-    d, n = (400, 1000) if model == O.LASSO else (120, 1000)
+    d, n = (400, 1000) if model != O.SVM else (120, 1000)
     A, lab = _data(model, d, n, seed=300 + policy)
     lam = _lam(model, n)
     m = 250
@@ -330,9 +335,13 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     A64 = A.astype(np.float64)
     va = A64.T @ a
     O_np = (((va - lab) @ (va - lab)) / (2 * d) + lam * np.abs(a).sum() if model == O.LASSO
+            else ((va - lab) @ (va - lab)) / (2 * d) + 0.5 * lam * (a @ a) if model == O.RIDGE
             else -(lab @ a) / n + (va @ va) / (2 * lam * n * n))
     assert abs(O_np - Ob) <= 1e-10 * max(1, abs(Ob))
-    np.testing.assert_allclose(v, va - lab if model == O.LASSO else va, atol=1e-9)
+    np.testing.assert_allclose(v, va - lab if model != O.SVM else va, atol=1e-9)
+    if model == O.RIDGE:   # the normal equations fix alpha* (textbook pin); lambda-strong convexity
+        astar = np.linalg.solve(A64 @ A64.T + lam * d * np.eye(n), A64 @ lab)   # bounds the distance:
+        assert np.linalg.norm(a - astar) <= np.sqrt(2 * g / lam) * (1 + 1e-9)   # (lam/2)|a-a*|^2 <= gap
     st, G_ref, O_ref, _ = O.duality_gap(model, A, ref["alpha"], lab, lam, B)
     assert abs(Ob - O_ref) <= 1e-4 * abs(O_ref)  # north_star: converged objective within 1e-4
     # exact-sequential kernels + same generator: the same trajectory until a near-tie in z
@@ -363,12 +372,12 @@ def test_budget_smaller_than_data_swaps(D):
 
 
 # ------------------------------------------------------------------------- multi-GPU path (8(e))
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
 @pytest.mark.parametrize("with_comm", [False, True])
 def test_aggregation_linesearch_matches_oracle(D, model, with_comm):
     """The CoCoA aggregation path (dv, exact gamma line search, apply) on one rank,
     with and without a 1-rank NCCL communicator, against or_duhl_solve_cocoa(K=1)."""
-    d, n = (300, 800) if model == O.LASSO else (80, 800)
+    d, n = (300, 800) if model != O.SVM else (80, 800)
     A, lab = _data(model, d, n, seed=400 + model)
     lam = _lam(model, n)
     m, eps = 200, 1e-6
