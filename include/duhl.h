@@ -249,6 +249,12 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes,
                               int64_t* zc_bytes, int64_t* updates);
 
+/* Launch shape of the dense exact SCD epoch chosen at create (cfg.scd_kernel, shared
+ * memory): *kernel 1 = k_scd_gram (warp-specialised), 2 = k_scd_pipe (control CTA);
+ * W coordinates per Gram block, G (compute) CTAs of R rows each.  CSC problems report
+ * kernel 0 (k_csc_scd).  Any pointer may be NULL. */
+duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R);
+
 const char* duhl_last_error(const duhl_ctx* ctx);
 
 #ifdef __cplusplus

@@ -16,7 +16,7 @@ STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "
 FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_create_csc", "duhl_destroy", "duhl_gaps", "duhl_select",
              "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
              "duhl_set_state", "duhl_comm_unique_id", "duhl_comm_init", "duhl_get_stream",
-             "duhl_get_kernel_stats", "duhl_get_counters", "duhl_last_error"]
+             "duhl_get_kernel_stats", "duhl_get_counters", "duhl_get_scd_shape", "duhl_last_error"]
 KIND_SCD, KIND_GAP, KIND_TOPM, KIND_STAGE = 0, 1, 2, 3
 
 
@@ -86,6 +86,7 @@ def lib():
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
         L.duhl_get_counters.argtypes = [_P, _P, _P, _P, _P]
+        L.duhl_get_scd_shape.argtypes = [_P, _P, _P, _P, _P]
         L.duhl_last_error.argtypes = [_P]
         L.duhl_last_error.restype = C.c_char_p
         for f in FUNCTIONS:
@@ -212,6 +213,12 @@ class Problem:
         s = C.c_void_p()
         self._check(lib().duhl_get_stream(self._h, C.byref(s)))
         return s.value
+
+    def scd_shape(self):
+        """(kernel name, W, G, R) of the exact SCD epoch chosen at create."""
+        k, w, g, r = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        self._check(lib().duhl_get_scd_shape(self._h, C.byref(k), C.byref(w), C.byref(g), C.byref(r)))
+        return ["k_csc_scd", "k_scd_gram", "k_scd_pipe"][k.value], w.value, g.value, r.value
 
     def counters(self):
         a, b, z, c = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()

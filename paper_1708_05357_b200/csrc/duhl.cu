@@ -1481,6 +1481,15 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
     return DUHL_OK;
 }
 
+duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R) {
+    if (!ctx) return DUHL_E_INVALID;
+    if (kernel) *kernel = ctx->csc ? 0 : (ctx->pipe ? 2 : 1);
+    if (W) *W = ctx->W;
+    if (G) *G = ctx->G;
+    if (R) *R = ctx->R;
+    return DUHL_OK;
+}
+
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes, int64_t* zc_bytes,
                               int64_t* updates) {
     if (!ctx) return DUHL_E_INVALID;
