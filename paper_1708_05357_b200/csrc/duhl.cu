@@ -1372,23 +1372,32 @@ duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes
     duhl_status st = DUHL_E_NOT_CONVERGED;
     int64_t t = 0, last_cert = -1, backoff = 1;
     double zs = INFINITY;
+    // Adaptive certificates: the gap memory's sum z_s is a time-delayed estimate of the gap
+    // (P:307-313); a failed certificate calibrates it -- the next one waits until
+    // z_s * ratio <= eps, ratio = the largest certified gap / z_s seen (>= 1), and at least
+    // `backoff` rounds (doubling after each failure).
+    double ratio = 1.0;
+    auto want = [&](double z) { return ctx->cfg.cert_adaptive && z * ratio <= eps && (t - last_cert) >= backoff; };
+    auto failed = [&](double g, double z) {
+        if (z > 0.0 && g / z > ratio) ratio = g / z;
+        backoff *= 2;
+    };
     for (t = 0; t < max_rounds; ++t) {
-        // certify on the fixed schedule, or (adaptive) when the gap memory's own
-        // estimate says we may be done; failed adaptive checks back off 1, 2, 4, ... rounds
+        // certify on the fixed schedule, or (adaptive) when the calibrated estimate says we may be done
         bool sched = (t + 1) % ctx->cfg.cert_every == 0;
-        bool adapt = ctx->cfg.cert_adaptive && zs <= eps && (t - last_cert) >= backoff;
+        bool adapt = want(zs);
         duhl_round_record r{};
         TRY(round_impl(ctx, t, passes, policy, (sched || adapt) ? 1 : 0, &r));
         zs = r.z_sum;
         if (r.cert_gap >= 0.0) {
             gap = r.cert_gap;
-            if (adapt && !sched && gap > eps) backoff *= 2;
+            if (adapt && !sched && gap > eps) failed(gap, zs);  // both at the end of round t
             last_cert = t;
-        } else if (ctx->cfg.cert_adaptive && zs <= eps && (t - last_cert) >= backoff) {
+        } else if (want(zs)) {
             // the estimate crossed eps during this round: certify now rather than next round
             TRY(certificate(ctx, &gap, nullptr, nullptr));
             r.cert_gap = gap;
-            if (gap > eps) backoff *= 2;
+            if (gap > eps) failed(gap, zs);
             last_cert = t;
         }
         r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
