@@ -792,7 +792,7 @@ constexpr int kProdWarp = kScdWarps - 1;
 constexpr int kBarCompute = 1;  // named barrier id: compute warps only
 
 template <bool EXACT, int MODEL>
-__global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(ScdParams p) {
+__global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(const __grid_constant__ ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int W = p.W, R = p.R, T = W / 4;
     const int NRED = scd_nred(W);

@@ -63,7 +63,8 @@ size_t pipe_smem_bytes(int W, int R, int NS) {
     const size_t compute = 128 + align_up_dev((size_t)NS * W * pipe_stride(R) * sizeof(float)) +
                            align_up_dev((size_t)R * sizeof(double)) +
                            align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float)) +
-                           align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double));
+                           align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double)) +
+                           (R <= 512 ? align_up_dev((size_t)3 * R * sizeof(double)) : 0);
     const size_t control = 128 + align_up_dev((size_t)pipe_ne(W) * sizeof(double));
     return compute > control ? compute : control;
 }
@@ -207,7 +208,7 @@ __device__ __forceinline__ void pipe_issue(const ScdParams& p, float* Abuf, uint
 }
 
 template <bool EXACT, int MODEL>
-__global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
+__global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_constant__ ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int W = p.W, R = p.R, NS = p.NB, G = p.G;
     const int NE = pipe_ne(W);
@@ -311,11 +312,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                         scale = -y_in * inv;
                     }
                 }
-                // lane j's scaled Gram row: t_j += cg[k] delta_k for k < j (zero for k >= j)
-                double cg[kPipeWMax];
-#pragma unroll
-                for (int k = 0; k < kPipeWMax; ++k)
-                    cg[k] = (k < W && lane < Wb) ? scale * sRed[W + k * W + lane] : 0.0;
+                // lane j's scaled Gram row: t_j += scale_j G_jk delta_k for k < j (G_jk = 0 for k >= j;
+                // scale = 0 on lanes >= Wb), read from shared memory as the steps go (no register copy)
                 double afin = a;
                 double* dout = dbuf + (size_t)rb * kPipeWMax;
 #pragma unroll
@@ -333,7 +331,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                     double dl = an - a;
                     if (lane == j) afin = an;
                     dl = __shfl_sync(0xffffffffu, dl, j);
-                    t = fma(cg[j], dl, t);
+                    t = fma(scale * sRed[W + j * W + lane], dl, t);
                     if (lane == 0) {  // every lane has delta_j: lane 0 publishes (its own stores, then release)
                         __stcg(&dout[j], dl);
                         sDprev[j] = dl;
@@ -365,6 +363,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
         float* part = reinterpret_cast<float*>(smem + off);  // [kPipeCompute][2 W^2]
         off += align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float));
         double* upart = reinterpret_cast<double*>(smem + off);  // [kPipeCompute][32]
+        off += align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double));
+        double* vpart = reinterpret_cast<double*>(smem + off);  // [3][R] partial v updates
         __shared__ double sDelta[2][kPipeWMax];
         const int64_t r0 = (int64_t)c * R;
         const int rows = (int)imin64(R, p.d4 - r0);
@@ -441,31 +441,48 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
             };
             // u_blk = A_blk^T v over this warp's rows (lane j = column j), fp64; summed across warps
             auto u_block = [&](int64_t blk) {
-                // lane (jq, rs) = (lane & 3, lane >> 2): columns jq + 4a, rows r4 = rs mod 8 of the slice
                 const float* A1 = stage(blk);
-                const int jq = lane & 3, rs = lane >> 2, T = W >> 2;
                 const double2* v2 = reinterpret_cast<const double2*>(vs);
-                double acc[8];
-#pragma unroll
-                for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-                for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
-                    const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-#pragma unroll
-                    for (int a = 0; a < 8; ++a) {
-                        if (a >= T) break;
-                        const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
-                        acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
-                                     fma((double)x.w, v23.y, acc[a]))));
+                if (W > 16) {
+                    // lane j = column j over the warp's rows (no cross-lane reduction; two chains)
+                    if (lane < W) {
+                        const uint32_t ca = smem_addr(A1 + (size_t)lane * Rs);
+                        double acc0 = 0.0, acc1 = 0.0;
+                        for (int r4 = w4lo; r4 < w4hi; ++r4) {
+                            const float4 a4 = lds_f4(ca + 16u * r4);
+                            const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                            acc0 = fma((double)a4.x, v01.x, acc0);
+                            acc1 = fma((double)a4.y, v01.y, acc1);
+                            acc0 = fma((double)a4.z, v23.x, acc0);
+                            acc1 = fma((double)a4.w, v23.y, acc1);
+                        }
+                        upart[cw * kPipeWMax + lane] = acc0 + acc1;
                     }
-                }
+                } else {
+                    // lane (jq, rs) = (lane & 3, lane >> 2): columns jq + 4a, rows r4 = rs mod 8 of the slice
+                    const int jq = lane & 3, rs = lane >> 2, T = W >> 2;
+                    double acc[4];
 #pragma unroll
-                for (int a = 0; a < 8; ++a) {
-                    if (a >= T) break;
-                    double t = acc[a];
-                    t += __shfl_xor_sync(0xffffffffu, t, 4);
-                    t += __shfl_xor_sync(0xffffffffu, t, 8);
-                    t += __shfl_xor_sync(0xffffffffu, t, 16);
-                    if (rs == 0) upart[cw * kPipeWMax + jq + 4 * a] = t;
+                    for (int a = 0; a < 4; ++a) acc[a] = 0.0;
+                    for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
+                        const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            if (a >= T) break;
+                            const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
+                            acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
+                                         fma((double)x.w, v23.y, acc[a]))));
+                        }
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        if (a >= T) break;
+                        double t = acc[a];
+                        t += __shfl_xor_sync(0xffffffffu, t, 4);
+                        t += __shfl_xor_sync(0xffffffffu, t, 8);
+                        t += __shfl_xor_sync(0xffffffffu, t, 16);
+                        if (rs == 0) upart[cw * kPipeWMax + jq + 4 * a] = t;
+                    }
                 }
                 named_sync(kBarPipe, kPipeCompute * 32);
                 if (tid < W) {
@@ -493,14 +510,22 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                 }
                 named_sync(kBarPipe, kPipeCompute * 32);
             };
-            auto vupdate = [&](int64_t blk) {  // v slice += A_blk delta_blk (delta = 0 beyond the block)
+            // v slice += A_blk delta_blk (delta = 0 beyond the block).  Short slices (C3: 77 row
+            // groups for 224 threads): the columns are split over `vparts` thread groups, the
+            // partial sums of groups >= 1 go through shared memory (vpart) to group 0.
+            const int vq = n4 > 0 ? (kPipeCompute * 32) / n4 : 1;
+            const int vparts = vq < 1 ? 1 : (vq > 4 ? 4 : vq);
+            auto vupdate = [&](int64_t blk) {
                 const float* A = stage(blk);
                 const double* dl = sDelta[blk & 1];
                 double2* v2 = reinterpret_cast<double2*>(vs);
                 const uint32_t a0 = smem_addr(A);
-                for (int r4 = tid; r4 < n4; r4 += kPipeCompute * 32) {
+                const int span = n4 * vparts;
+                for (int it = tid; it < ((vparts > 1) ? span : n4); it += kPipeCompute * 32) {
+                    const int r4 = it % n4, part = it / n4;
+                    const int jlo = (W / 4 * part) / vparts * 4, jhi = (W / 4 * (part + 1)) / vparts * 4;
                     double2 p01 = make_double2(0.0, 0.0), p23 = p01, q01 = p01, q23 = p01;
-                    for (int j = 0; j < W; j += 4) {  // W % 4 == 0: two independent chains
+                    for (int j = jlo; j < jhi; j += 4) {  // W % 4 == 0: two independent chains
 #pragma unroll
                         for (int u = 0; u < 4; u += 2) {
                             const float4 x = lds_f4(a0 + 4u * (uint32_t)((j + u) * Rs) + 16u * r4);
@@ -516,27 +541,39 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                             q23.y = fma(dy, (double)y.w, q23.y);
                         }
                     }
-                    double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-                    v01.x += p01.x + q01.x;
-                    v01.y += p01.y + q01.y;
-                    v23.x += p23.x + q23.x;
-                    v23.y += p23.y + q23.y;
-                    v2[2 * r4] = v01;
-                    v2[2 * r4 + 1] = v23;
+                    p01.x += q01.x; p01.y += q01.y; p23.x += q23.x; p23.y += q23.y;
+                    if (part == 0) {
+                        double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                        v01.x += p01.x; v01.y += p01.y; v23.x += p23.x; v23.y += p23.y;
+                        v2[2 * r4] = v01;
+                        v2[2 * r4 + 1] = v23;
+                    } else {
+                        double2* vp = reinterpret_cast<double2*>(vpart) + 2 * ((size_t)(part - 1) * n4 + r4);
+                        vp[0] = p01;
+                        vp[1] = p23;
+                    }
+                }
+                if (vparts > 1) {
+                    named_sync(kBarPipe, kPipeCompute * 32);
+                    for (int r4 = tid; r4 < n4; r4 += kPipeCompute * 32) {
+                        double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                        for (int part = 1; part < vparts; ++part) {
+                            const double2* vp = reinterpret_cast<const double2*>(vpart) + 2 * ((size_t)(part - 1) * n4 + r4);
+                            v01.x += vp[0].x; v01.y += vp[0].y; v23.x += vp[1].x; v23.y += vp[1].y;
+                        }
+                        v2[2 * r4] = v01;
+                        v2[2 * r4 + 1] = v23;
+                    }
                 }
             };
-            if (nblk > 0) {
-                wait_data(0);
-                gc_block(0, false);
-                u_block(0);
-                arrive(0);
-            }
-            for (int64_t b = 0; b < nblk; ++b) {
+            // b = -1 is the prologue (block 0's partials, no cross Gram), b = nblk the epilogue
+            // (the last v update); one call site per phase keeps every lambda inlined
+            for (int64_t b = -1; b <= nblk; ++b) {
                 stamp(7);
                 if (b + 1 < nblk) {
                     wait_data(b + 1);
                     stamp(0);
-                    gc_block(b + 1, true);
+                    gc_block(b + 1, b >= 0);
                     stamp(1);
                 }
                 if (b >= 1) {
@@ -554,10 +591,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(ScdParams p) {
                     arrive(b + 1);
                     stamp(5);
                 }
-            }
-            if (nblk > 0) {
-                wait_delta(nblk - 1);
-                vupdate(nblk - 1);
             }
             named_sync(kBarPipe, kPipeCompute * 32);
         }
