@@ -98,7 +98,7 @@ typedef struct {
     int linesearch;           /* 1: exact line search on the aggregation weight gamma in [0,1] after each
                                  round's epoch; 0: gamma = 1 (Alg. 2 l.11) */
     int unit_a_ctas;          /* unit-A refresh beside the epoch: CTAs of its persistent gap kernel; the
-                                 SCD grid leaves them their SMs.  0 = auto (16 when the data exceeds the
+                                 SCD grid leaves them their SMs.  0 = auto (8 when the data exceeds the
                                  budget and refresh_fraction > 0), -1 = off (the refresh runs on the
                                  whole GPU before the epoch) */
     int scd_kernel;           /* dense exact SCD kernel: 1 = warp-specialised (a control warp in every CTA,

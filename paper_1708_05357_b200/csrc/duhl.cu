@@ -816,7 +816,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
     ctx->unit_a_ctas = ctx->cfg.unit_a_ctas > 0 ? std::min(ctx->cfg.unit_a_ctas, ctx->nsm / 2)
                        : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 &&
-                          ctx->cfg.refresh_fraction > 0.0) ? 16 : 0;
+                          ctx->cfg.refresh_fraction > 0.0) ? 8 : 0;  // 8 CTAs keep PCIe busy (measured:
+                                                                      // C4 step 85 vs 90 ms with 16)
     choose_scd_shape(ctx);
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)))

@@ -1,1 +1,3 @@
-for f in 0.1 0.06 0.15; do REFRESH=$f PASSES=2 timeout 600 python tools/solve_trace.py > gpurun_out/strace_c4_r$f.log 2>&1; done
+timeout 900 python bench.py --no-cpu --unit-a-ctas 8 > gpurun_out/ua8_c4.log 2>&1
+timeout 900 python bench.py --no-cpu --config c3 --unit-a-ctas 8 > gpurun_out/ua8_c3.log 2>&1
+timeout 900 python bench.py --no-cpu --config c3 > gpurun_out/ua16_c3.log 2>&1
