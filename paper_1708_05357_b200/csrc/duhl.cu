@@ -1051,8 +1051,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         const char* nm0[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
                               "cmp:vupdate", "cmp:tiles"};
         const char* nm1[8] = {"ctl:poll", "ctl:read", "ctl:steps", "ctl:other", "ctl:publish", "-", "-", "-"};
-        const char* nm1c[8] = {"cmp:wait-data", "cmp:GC", "cmp:wait-delta", "cmp:vupd", "cmp:u", "cmp:arrive",
-                               "-", "cmp:other"};
+        const char* nm1c[8] = {"gram:wait-data", "gram:tiles", "gram:sum+arrive", "v:wait-delta", "v:vupd",
+                               "v:u+arrive", "v:other", "gram:other"};
         const bool pipe = ctx->pipe;
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", pipe ? (c2 ? " | cta0: " : "control: ") : (c2 ? " | last: " : "cta0: "));

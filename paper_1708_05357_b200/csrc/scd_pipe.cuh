@@ -44,11 +44,13 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
 
 static_assert(kRedGroups == 1, "the pipelined kernel assumes one reduction group");
 constexpr int kPipeWMax = 32;
-constexpr int kPipeRot = 4;
+constexpr int kPipeRot = 6;
 constexpr int kPipeThreads = 256;
 constexpr int kPipeCompute = 7;   // compute warps 0..6 of a compute CTA
 constexpr int kPipeProd = 7;      // producer warp (TMA)
-constexpr int kBarPipe = 2;       // named barrier: the compute warps of a compute CTA
+constexpr int kGcWarps = 4;       // Gram group: warps 0..3 (FFMA2)
+constexpr int kVWarps = kPipeCompute - kGcWarps;  // v group: warps 4..6 (fp64 update and u)
+constexpr int kBarGc = 1, kBarV = 2;              // named barriers of the two groups
 
 // Reduction entries of one block (expanded layout, see tile4<..., XL>):
 //   u_j [0, W),  G_jk (k < j) at W + k W + j,  C_jk at W + W^2 + k W + j.
@@ -62,7 +64,7 @@ __host__ __device__ __forceinline__ int pipe_stride(int R) { return ((R >> 2) & 
 size_t pipe_smem_bytes(int W, int R, int NS) {
     const size_t compute = 128 + align_up_dev((size_t)NS * W * pipe_stride(R) * sizeof(float)) +
                            align_up_dev((size_t)R * sizeof(double)) +
-                           align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float)) +
+                           align_up_dev((size_t)kGcWarps * 2 * W * W * sizeof(float)) +
                            align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double)) +
                            (R <= 512 ? align_up_dev((size_t)3 * R * sizeof(double)) : 0);
     const size_t control = 128 + align_up_dev((size_t)pipe_ne(W) * sizeof(double));
@@ -167,15 +169,16 @@ __device__ __forceinline__ void gc_warp(const float* A1, const float* A0, int Rs
 
 // Cross-warp sum of the fast-mode partials (fp32 within the CTA, fp64 REDs across CTAs).
 template <int T>
-__device__ __forceinline__ void gc_sum(const float* __restrict__ part, int W, int tid, const RedOut& out) {
+__device__ __forceinline__ void gc_sum(const float* __restrict__ part, int W, int tid, int nwarps,
+                                       const RedOut& out) {
     constexpr int nslot = 32 * T * T;
-    for (int sl = tid; sl < nslot; sl += kPipeCompute * 32) {
+    for (int sl = tid; sl < nslot; sl += nwarps * 32) {
         const int ln = sl & 31, e = sl >> 5, a = e / T, bb = e - a * T;
         const int j = (ln & 3) + 4 * a, k = (ln >> 2) + 8 * bb;
         if (k >= W || k < j) {
             float sum = 0.f;
 #pragma unroll
-            for (int w = 0; w < kPipeCompute; ++w) sum += part[w * 2 * 16 * T * T + sl];
+            for (int w = 0; w < nwarps; ++w) sum += part[w * 2 * 16 * T * T + sl];
             out.add(W + k * W + j, (double)sum);
         }
     }
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
             stamp(3);
             if (tid == 0) {
                 const unsigned long long t0 = gtimer();
-                while (ld_acquire_u32(&cnt[rb]) < (unsigned)G) {
+                while (ld_acquire_u32(&cnt[rb]) < (unsigned)(2 * G)) {  // both groups of every CTA
                     if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 2); break; }
                 }
             }
@@ -360,8 +363,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
         size_t off = 128 + align_up_dev((size_t)NS * W * Rs * sizeof(float));
         double* vs = reinterpret_cast<double*>(smem + off);
         off += align_up_dev((size_t)R * sizeof(double));
-        float* part = reinterpret_cast<float*>(smem + off);  // [kPipeCompute][2 W^2]
-        off += align_up_dev((size_t)kPipeCompute * 2 * W * W * sizeof(float));
+        float* part = reinterpret_cast<float*>(smem + off);  // [kGcWarps][2 W^2]
+        off += align_up_dev((size_t)kGcWarps * 2 * W * W * sizeof(float));
         double* upart = reinterpret_cast<double*>(smem + off);  // [kPipeCompute][32]
         off += align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double));
         double* vpart = reinterpret_cast<double*>(smem + off);  // [3][R] partial v updates
@@ -400,199 +403,223 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                 pipe_issue(p, Abuf, full, q, r0, rows, lane, slot, need, seen, Rs);
             }
         } else {
-            const int cw = warp;
+            // Two warp groups on different pipes, each with its own named barrier and arrival:
+            //   Gram group (warps 0 .. kGcWarps-1, FFMA2): G_{b+1}, C_{b+1,b} as soon as block b+1
+            //     has landed -- needs no delta;
+            //   v group (the other compute warps, fp64): wait delta_{b-1}, v += A_{b-1} delta_{b-1},
+            //     u_{b+1} = A_{b+1}^T v_b.
+            // Each group REDs its entries, fences and adds 1 to cnt[(b+1) % K] (the control CTA
+            // waits for 2 G arrivals).  A stage is released when every compute warp is done with
+            // it: the Gram warps after G/C of the next block (its last read, as the C partner),
+            // the v warps after the v update.
             const int n4 = rows >> 2;
-            const int w4lo = (cw * n4) / kPipeCompute, w4hi = ((cw + 1) * n4) / kPipeCompute;  // this warp's rows
             auto stage = [&](int64_t blk) { return Abuf + (size_t)(blk % NS) * W * Rs; };
             auto wait_data = [&](int64_t blk) {
                 mbar_wait_bounded(&full[blk % NS], (unsigned)((blk / NS) & 1), p.err, 8, kSpinTimeoutNs);
             };
             auto out_of = [&](int64_t blk) { return RedOut{p.red + (size_t)(blk % kPipeRot) * rbsz, 0}; };
-            // G_{blk} (lower) and C_{blk,blk-1}: every warp takes the whole W x 2W block over its
-            // own rows (no cross-lane reduction); fp32 partials are summed across warps in fp64.
-            auto gc_block = [&](int64_t blk, bool with_c) {
-                const float* A1 = stage(blk);
-                const float* A0 = with_c ? stage(blk - 1) : A1;  // block 0: C is never read
-                const RedOut out = out_of(blk);
-                float* mypart = part + (size_t)cw * 2 * W * W;
-                switch (W >> 2) {
-                    case 1: gc_warp<EXACT, 1>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 2: gc_warp<EXACT, 2>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 3: gc_warp<EXACT, 3>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 4: gc_warp<EXACT, 4>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 5: gc_warp<EXACT, 5>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 6: gc_warp<EXACT, 6>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    case 7: gc_warp<EXACT, 7>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                    default: gc_warp<EXACT, 8>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
-                }
-                if (!EXACT) {  // sum the warps' partials and add one (fp64) RED per entry
-                    named_sync(kBarPipe, kPipeCompute * 32);
-                    switch (W >> 2) {
-                        case 1: gc_sum<1>(part, W, tid, out); break;
-                        case 2: gc_sum<2>(part, W, tid, out); break;
-                        case 3: gc_sum<3>(part, W, tid, out); break;
-                        case 4: gc_sum<4>(part, W, tid, out); break;
-                        case 5: gc_sum<5>(part, W, tid, out); break;
-                        case 6: gc_sum<6>(part, W, tid, out); break;
-                        case 7: gc_sum<7>(part, W, tid, out); break;
-                        default: gc_sum<8>(part, W, tid, out); break;
-                    }
-                }
+            auto arrive_cnt = [&](int64_t blk) {  // after the group's named barrier
+                __threadfence();
+                atomicAdd(&cnt[blk % kPipeRot], 1u);
             };
-            // u_blk = A_blk^T v over this warp's rows (lane j = column j), fp64; summed across warps
-            auto u_block = [&](int64_t blk) {
-                const float* A1 = stage(blk);
-                const double2* v2 = reinterpret_cast<const double2*>(vs);
-                if (W > 16) {
-                    // lane j = column j over the warp's rows (no cross-lane reduction; two chains)
-                    if (lane < W) {
-                        const uint32_t ca = smem_addr(A1 + (size_t)lane * Rs);
-                        double acc0 = 0.0, acc1 = 0.0;
-                        for (int r4 = w4lo; r4 < w4hi; ++r4) {
-                            const float4 a4 = lds_f4(ca + 16u * r4);
-                            const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-                            acc0 = fma((double)a4.x, v01.x, acc0);
-                            acc1 = fma((double)a4.y, v01.y, acc1);
-                            acc0 = fma((double)a4.z, v23.x, acc0);
-                            acc1 = fma((double)a4.w, v23.y, acc1);
-                        }
-                        upart[cw * kPipeWMax + lane] = acc0 + acc1;
+            if (warp < kGcWarps) {
+                // ---------------------------------------------------------- Gram group
+                const int gw = warp, gtid = tid;
+                const int w4lo = (gw * n4) / kGcWarps, w4hi = ((gw + 1) * n4) / kGcWarps;
+                float* mypart = part + (size_t)gw * 2 * W * W;
+                for (int64_t b = -1; b + 1 < nblk; ++b) {
+                    stamp(7);
+                    wait_data(b + 1);
+                    stamp(0);
+                    const float* A1 = stage(b + 1);
+                    const float* A0 = b >= 0 ? stage(b) : A1;  // block 0: C is never read
+                    const RedOut out = out_of(b + 1);
+                    switch (W >> 2) {
+                        case 1: gc_warp<EXACT, 1>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 2: gc_warp<EXACT, 2>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 3: gc_warp<EXACT, 3>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 4: gc_warp<EXACT, 4>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 5: gc_warp<EXACT, 5>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 6: gc_warp<EXACT, 6>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        case 7: gc_warp<EXACT, 7>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
+                        default: gc_warp<EXACT, 8>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
                     }
-                } else {
-                    // lane (jq, rs) = (lane & 3, lane >> 2): columns jq + 4a, rows r4 = rs mod 8 of the slice
-                    const int jq = lane & 3, rs = lane >> 2, T = W >> 2;
-                    double acc[4];
+                    __syncwarp();
+                    if (b >= 0 && lane == 0) mbar_arrive(&empty[b % NS]);  // last Gram read of block b
+                    stamp(1);
+                    if (!EXACT) {  // sum the warps' partials and add one (fp64) RED per entry
+                        named_sync(kBarGc, kGcWarps * 32);
+                        switch (W >> 2) {
+                            case 1: gc_sum<1>(part, W, gtid, kGcWarps, out); break;
+                            case 2: gc_sum<2>(part, W, gtid, kGcWarps, out); break;
+                            case 3: gc_sum<3>(part, W, gtid, kGcWarps, out); break;
+                            case 4: gc_sum<4>(part, W, gtid, kGcWarps, out); break;
+                            case 5: gc_sum<5>(part, W, gtid, kGcWarps, out); break;
+                            case 6: gc_sum<6>(part, W, gtid, kGcWarps, out); break;
+                            case 7: gc_sum<7>(part, W, gtid, kGcWarps, out); break;
+                            default: gc_sum<8>(part, W, gtid, kGcWarps, out); break;
+                        }
+                    }
+                    named_sync(kBarGc, kGcWarps * 32);  // partials consumed, every RED issued
+                    if (gtid == 0) arrive_cnt(b + 1);
+                    stamp(2);
+                }
+            } else {
+                // ---------------------------------------------------------- v group
+                const int vw = warp - kGcWarps, vtid = tid - kGcWarps * 32;
+                constexpr int kVThreads = kVWarps * 32;
+                const int w4lo = (vw * n4) / kVWarps, w4hi = ((vw + 1) * n4) / kVWarps;
+                const int vq = n4 > 0 ? kVThreads / n4 : 1;
+                const int vparts = vq < 1 ? 1 : (vq > 4 ? 4 : vq);
+                auto wait_delta = [&](int64_t blk) {  // delta_blk -> sDelta[blk & 1]
+                    if (vw == 0) {
+                        const unsigned* f = &flg[blk % kPipeRot];
+                        const unsigned long long t0 = gtimer();
+                        while (ld_acquire_u32(f) < (unsigned)(blk + 1)) {
+                            if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 16); break; }
+                        }
+                        if (lane < W) sDelta[blk & 1][lane] = ld_cg_f64(&dbuf[(size_t)(blk % kPipeRot) * kPipeWMax + lane]);
+                    }
+                    named_sync(kBarV, kVThreads);
+                };
+                // v slice += A_blk delta_blk (delta = 0 beyond the block); short slices split the
+                // columns over `vparts` thread groups, partials of groups >= 1 via shared memory
+                auto vupdate = [&](int64_t blk) {
+                    const double* dl = sDelta[blk & 1];
+                    double2* v2 = reinterpret_cast<double2*>(vs);
+                    const uint32_t a0 = smem_addr(stage(blk));
+                    const int span = n4 * vparts;
+                    for (int it = vtid; it < span; it += kVThreads) {
+                        const int r4 = it % n4, part_ = it / n4;
+                        const int jlo = (W / 4 * part_) / vparts * 4, jhi = (W / 4 * (part_ + 1)) / vparts * 4;
+                        double2 p01 = make_double2(0.0, 0.0), p23 = p01, q01 = p01, q23 = p01;
+                        for (int j = jlo; j < jhi; j += 4) {  // W % 4 == 0: two independent chains
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) acc[a] = 0.0;
-                    for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
-                        const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                            for (int u = 0; u < 4; u += 2) {
+                                const float4 x = lds_f4(a0 + 4u * (uint32_t)((j + u) * Rs) + 16u * r4);
+                                const float4 y = lds_f4(a0 + 4u * (uint32_t)((j + u + 1) * Rs) + 16u * r4);
+                                const double dx = dl[j + u], dy = dl[j + u + 1];
+                                p01.x = fma(dx, (double)x.x, p01.x);
+                                p01.y = fma(dx, (double)x.y, p01.y);
+                                p23.x = fma(dx, (double)x.z, p23.x);
+                                p23.y = fma(dx, (double)x.w, p23.y);
+                                q01.x = fma(dy, (double)y.x, q01.x);
+                                q01.y = fma(dy, (double)y.y, q01.y);
+                                q23.x = fma(dy, (double)y.z, q23.x);
+                                q23.y = fma(dy, (double)y.w, q23.y);
+                            }
+                        }
+                        p01.x += q01.x; p01.y += q01.y; p23.x += q23.x; p23.y += q23.y;
+                        if (part_ == 0) {
+                            double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                            v01.x += p01.x; v01.y += p01.y; v23.x += p23.x; v23.y += p23.y;
+                            v2[2 * r4] = v01;
+                            v2[2 * r4 + 1] = v23;
+                        } else {
+                            double2* vp = reinterpret_cast<double2*>(vpart) + 2 * ((size_t)(part_ - 1) * n4 + r4);
+                            vp[0] = p01;
+                            vp[1] = p23;
+                        }
+                    }
+                    if (vparts > 1) {
+                        named_sync(kBarV, kVThreads);
+                        for (int r4 = vtid; r4 < n4; r4 += kVThreads) {
+                            double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                            for (int q = 1; q < vparts; ++q) {
+                                const double2* vp = reinterpret_cast<const double2*>(vpart) + 2 * ((size_t)(q - 1) * n4 + r4);
+                                v01.x += vp[0].x; v01.y += vp[0].y; v23.x += vp[1].x; v23.y += vp[1].y;
+                            }
+                            v2[2 * r4] = v01;
+                            v2[2 * r4 + 1] = v23;
+                        }
+                    }
+                };
+                // u_blk = A_blk^T v (v = v_{blk-1}) over this warp's rows, fp64, summed across the group
+                auto u_block = [&](int64_t blk) {
+                    const float* A1 = stage(blk);
+                    const double2* v2 = reinterpret_cast<const double2*>(vs);
+                    if (W > 16) {  // lane j = column j (no cross-lane reduction; two chains)
+                        if (lane < W) {
+                            const uint32_t ca = smem_addr(A1 + (size_t)lane * Rs);
+                            double acc0 = 0.0, acc1 = 0.0;
+                            for (int r4 = w4lo; r4 < w4hi; ++r4) {
+                                const float4 a4 = lds_f4(ca + 16u * r4);
+                                const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+                                acc0 = fma((double)a4.x, v01.x, acc0);
+                                acc1 = fma((double)a4.y, v01.y, acc1);
+                                acc0 = fma((double)a4.z, v23.x, acc0);
+                                acc1 = fma((double)a4.w, v23.y, acc1);
+                            }
+                            upart[vw * kPipeWMax + lane] = acc0 + acc1;
+                        }
+                    } else {  // lane (jq, rs) = (lane & 3, lane >> 2): columns jq + 4a, rows rs mod 8
+                        const int jq = lane & 3, rs = lane >> 2, T = W >> 2;
+                        double acc[4];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) acc[a] = 0.0;
+                        for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
+                            const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
+#pragma unroll
+                            for (int a = 0; a < 4; ++a) {
+                                if (a >= T) break;
+                                const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
+                                acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
+                                             fma((double)x.w, v23.y, acc[a]))));
+                            }
+                        }
 #pragma unroll
                         for (int a = 0; a < 4; ++a) {
                             if (a >= T) break;
-                            const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
-                            acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
-                                         fma((double)x.w, v23.y, acc[a]))));
+                            double t = acc[a];
+                            t += __shfl_xor_sync(0xffffffffu, t, 4);
+                            t += __shfl_xor_sync(0xffffffffu, t, 8);
+                            t += __shfl_xor_sync(0xffffffffu, t, 16);
+                            if (rs == 0) upart[vw * kPipeWMax + jq + 4 * a] = t;
                         }
                     }
+                    named_sync(kBarV, kVThreads);
+                    if (vtid < W) {
+                        double sum = 0.0;
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        if (a >= T) break;
-                        double t = acc[a];
-                        t += __shfl_xor_sync(0xffffffffu, t, 4);
-                        t += __shfl_xor_sync(0xffffffffu, t, 8);
-                        t += __shfl_xor_sync(0xffffffffu, t, 16);
-                        if (rs == 0) upart[cw * kPipeWMax + jq + 4 * a] = t;
+                        for (int w = 0; w < kVWarps; ++w) sum += upart[w * kPipeWMax + vtid];
+                        out_of(blk).add(vtid, sum);
                     }
-                }
-                named_sync(kBarPipe, kPipeCompute * 32);
-                if (tid < W) {
-                    double sum = 0.0;
+                };
+                // b = -1: u_0 against the initial v; b = nblk: the last v update
+                const bool trv = p.trace != nullptr && c == 0 && vtid == 0;
+                unsigned long long tv = trv ? (unsigned long long)clock64() : 0;
+                auto vstamp = [&](int k) {
+                    if (trv) {
+                        const unsigned long long t = (unsigned long long)clock64();
 #pragma unroll
-                    for (int w = 0; w < kPipeCompute; ++w) sum += upart[w * kPipeWMax + tid];
-                    out_of(blk).add(tid, sum);
-                }
-            };
-            auto arrive = [&](int64_t blk) {  // this CTA's partials of block blk are complete
-                named_sync(kBarPipe, kPipeCompute * 32);
-                if (tid == 0) {
-                    __threadfence();
-                    atomicAdd(&cnt[blk % kPipeRot], 1u);
-                }
-            };
-            auto wait_delta = [&](int64_t blk) {  // delta_blk -> sDelta[blk & 1]
-                if (cw == 0) {
-                    const unsigned* f = &flg[blk % kPipeRot];
-                    const unsigned long long t0 = gtimer();
-                    while (ld_acquire_u32(f) < (unsigned)(blk + 1)) {
-                        if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 16); break; }
+                        for (int q = 3; q < 7; ++q)
+                            if (q == k) trc[q] += t - tv;
+                        tv = t;
                     }
-                    if (lane < W) sDelta[blk & 1][lane] = ld_cg_f64(&dbuf[(size_t)(blk % kPipeRot) * kPipeWMax + lane]);
-                }
-                named_sync(kBarPipe, kPipeCompute * 32);
-            };
-            // v slice += A_blk delta_blk (delta = 0 beyond the block).  Short slices (C3: 77 row
-            // groups for 224 threads): the columns are split over `vparts` thread groups, the
-            // partial sums of groups >= 1 go through shared memory (vpart) to group 0.
-            const int vq = n4 > 0 ? (kPipeCompute * 32) / n4 : 1;
-            const int vparts = vq < 1 ? 1 : (vq > 4 ? 4 : vq);
-            auto vupdate = [&](int64_t blk) {
-                const float* A = stage(blk);
-                const double* dl = sDelta[blk & 1];
-                double2* v2 = reinterpret_cast<double2*>(vs);
-                const uint32_t a0 = smem_addr(A);
-                const int span = n4 * vparts;
-                for (int it = tid; it < ((vparts > 1) ? span : n4); it += kPipeCompute * 32) {
-                    const int r4 = it % n4, part = it / n4;
-                    const int jlo = (W / 4 * part) / vparts * 4, jhi = (W / 4 * (part + 1)) / vparts * 4;
-                    double2 p01 = make_double2(0.0, 0.0), p23 = p01, q01 = p01, q23 = p01;
-                    for (int j = jlo; j < jhi; j += 4) {  // W % 4 == 0: two independent chains
-#pragma unroll
-                        for (int u = 0; u < 4; u += 2) {
-                            const float4 x = lds_f4(a0 + 4u * (uint32_t)((j + u) * Rs) + 16u * r4);
-                            const float4 y = lds_f4(a0 + 4u * (uint32_t)((j + u + 1) * Rs) + 16u * r4);
-                            const double dx = dl[j + u], dy = dl[j + u + 1];
-                            p01.x = fma(dx, (double)x.x, p01.x);
-                            p01.y = fma(dx, (double)x.y, p01.y);
-                            p23.x = fma(dx, (double)x.z, p23.x);
-                            p23.y = fma(dx, (double)x.w, p23.y);
-                            q01.x = fma(dy, (double)y.x, q01.x);
-                            q01.y = fma(dy, (double)y.y, q01.y);
-                            q23.x = fma(dy, (double)y.z, q23.x);
-                            q23.y = fma(dy, (double)y.w, q23.y);
-                        }
+                };
+                for (int64_t b = -1; b <= nblk; ++b) {
+                    vstamp(6);
+                    if (b >= 1) {
+                        wait_delta(b - 1);
+                        vstamp(3);
+                        vupdate(b - 1);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[(b - 1) % NS]);
+                        named_sync(kBarV, kVThreads);  // v_b complete before the u tiles read it
+                        vstamp(4);
                     }
-                    p01.x += q01.x; p01.y += q01.y; p23.x += q23.x; p23.y += q23.y;
-                    if (part == 0) {
-                        double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-                        v01.x += p01.x; v01.y += p01.y; v23.x += p23.x; v23.y += p23.y;
-                        v2[2 * r4] = v01;
-                        v2[2 * r4 + 1] = v23;
-                    } else {
-                        double2* vp = reinterpret_cast<double2*>(vpart) + 2 * ((size_t)(part - 1) * n4 + r4);
-                        vp[0] = p01;
-                        vp[1] = p23;
+                    if (b + 1 < nblk) {
+                        wait_data(b + 1);
+                        u_block(b + 1);
+                        named_sync(kBarV, kVThreads);
+                        if (vtid == 0) arrive_cnt(b + 1);
+                        vstamp(5);
                     }
                 }
-                if (vparts > 1) {
-                    named_sync(kBarPipe, kPipeCompute * 32);
-                    for (int r4 = tid; r4 < n4; r4 += kPipeCompute * 32) {
-                        double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
-                        for (int part = 1; part < vparts; ++part) {
-                            const double2* vp = reinterpret_cast<const double2*>(vpart) + 2 * ((size_t)(part - 1) * n4 + r4);
-                            v01.x += vp[0].x; v01.y += vp[0].y; v23.x += vp[1].x; v23.y += vp[1].y;
-                        }
-                        v2[2 * r4] = v01;
-                        v2[2 * r4 + 1] = v23;
-                    }
-                }
-            };
-            // b = -1 is the prologue (block 0's partials, no cross Gram), b = nblk the epilogue
-            // (the last v update); one call site per phase keeps every lambda inlined
-            for (int64_t b = -1; b <= nblk; ++b) {
-                stamp(7);
-                if (b + 1 < nblk) {
-                    wait_data(b + 1);
-                    stamp(0);
-                    gc_block(b + 1, b >= 0);
-                    stamp(1);
-                }
-                if (b >= 1) {
-                    wait_delta(b - 1);
-                    stamp(2);
-                    vupdate(b - 1);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[(b - 1) % NS]);
-                    named_sync(kBarPipe, kPipeCompute * 32);  // v_b complete before the u tiles read it
-                    stamp(3);
-                }
-                if (b + 1 < nblk) {
-                    u_block(b + 1);
-                    stamp(4);
-                    arrive(b + 1);
-                    stamp(5);
-                }
+                if (trv)
+                    for (int q = 3; q < 7; ++q)
+                        if (trc[q]) atomicAdd(&p.trace[8 + q], trc[q]);
             }
-            named_sync(kBarPipe, kPipeCompute * 32);
         }
         __syncthreads();
         for (int r = tid; r < rows; r += kPipeThreads) p.vt[r0 + r] = vs[r];
