@@ -48,7 +48,7 @@ struct ScdParams {
     double* alpha;             // [n]
     double* vt;                // [d4] shared vector
     int W, R, G, NB;           // block size (% 4 == 0; <= 16 legacy, <= 32 pipe), rows per CTA, (compute) CTAs, TMA stages
-    // pipe kernel: bar = cnt[4] (arrivals per reduction buffer) + flg[4] at bar + 8 (delta tags)
+    // pipe kernel: bar = cnt[6] (arrivals per reduction buffer) + flg[6] at bar + 8 (delta tags)
     int exact;                 // 1: fp64 Gram products (bit-level parity mode); 0: fp32 Gram within a warp
     double* red;               // [scd_red_doubles(W)] zero on entry
     unsigned* bar;             // [2] grid-barrier counters (per block parity), zero on entry

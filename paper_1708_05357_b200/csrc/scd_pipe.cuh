@@ -48,8 +48,10 @@ constexpr int kPipeRot = 6;
 constexpr int kPipeThreads = 256;
 constexpr int kPipeCompute = 7;   // compute warps 0..6 of a compute CTA
 constexpr int kPipeProd = 7;      // producer warp (TMA)
-constexpr int kGcWarps = 4;       // Gram group: warps 0..3 (FFMA2)
-constexpr int kVWarps = kPipeCompute - kGcWarps;  // v group: warps 4..6 (fp64 update and u)
+constexpr int kGcWarps = 4;       // Gram group: warps 0..3 (FFMA2); v group: warps 4..6 (fp64)
+constexpr int kGcWarpsMax = kGcWarps;
+// (3 Gram warps: C4 W = 12 6.97 vs 7.59 ms; 4: C3 W = 32 12.0 vs 16.2 ms -- C3 is the shape that
+// runs this kernel by default)
 constexpr int kBarGc = 1, kBarV = 2;              // named barriers of the two groups
 
 // Reduction entries of one block (expanded layout, see tile4<..., XL>):
@@ -64,7 +66,7 @@ __host__ __device__ __forceinline__ int pipe_stride(int R) { return ((R >> 2) & 
 size_t pipe_smem_bytes(int W, int R, int NS) {
     const size_t compute = 128 + align_up_dev((size_t)NS * W * pipe_stride(R) * sizeof(float)) +
                            align_up_dev((size_t)R * sizeof(double)) +
-                           align_up_dev((size_t)kGcWarps * 2 * W * W * sizeof(float)) +
+                           align_up_dev((size_t)kGcWarpsMax * 2 * W * W * sizeof(float)) +
                            align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double)) +
                            (R <= 512 ? align_up_dev((size_t)3 * R * sizeof(double)) : 0);
     const size_t control = 128 + align_up_dev((size_t)pipe_ne(W) * sizeof(double));
@@ -128,6 +130,43 @@ __device__ __forceinline__ void gc_warp_part(const float* __restrict__ A1, const
                 const int j = jg + 4 * a, k = kg + 8 * (B0 + b);
                 if (k >= W || k < j) out.add(W + k * W + j, acc[a][b]);
             }
+    } else if (T + NBK <= 8) {
+        // small tiles (W <= 16): loads of row group r4 + 1 in flight while r4's FMAs issue
+        float2 acc[T][NBK];
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) acc[a][b] = make_float2(0.f, 0.f);
+        float4 xn[T], yn[NBK];
+        const int r4c = r4lo < r4hi ? r4lo : 0;
+#pragma unroll
+        for (int a = 0; a < T; ++a) xn[a] = lds_f4(xa[a] + 16u * r4c);
+#pragma unroll
+        for (int b = 0; b < NBK; ++b) yn[b] = lds_f4(ya[b] + 16u * r4c);
+        for (int r4 = r4lo; r4 < r4hi; ++r4) {
+            float4 x[T], y[NBK];
+#pragma unroll
+            for (int a = 0; a < T; ++a) x[a] = xn[a];
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) y[b] = yn[b];
+            const uint32_t nx = 16u * (uint32_t)(r4 + 1 < r4hi ? r4 + 1 : r4);
+#pragma unroll
+            for (int a = 0; a < T; ++a) xn[a] = lds_f4(xa[a] + nx);
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) yn[b] = lds_f4(ya[b] + nx);
+#pragma unroll
+            for (int b = 0; b < NBK; ++b)
+#pragma unroll
+                for (int a = 0; a < T; ++a) {
+                    if (upper(a, B0 + b)) continue;
+                    ffma2(acc[a][b], x[a].x, x[a].y, y[b].x, y[b].y);
+                    ffma2(acc[a][b], x[a].z, x[a].w, y[b].z, y[b].w);
+                }
+        }
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) part[(a * T + B0 + b) * 32 + lane] = acc[a][b].x + acc[a][b].y;
     } else {
         float2 acc[T][NBK];
 #pragma unroll
@@ -178,7 +217,8 @@ __device__ __forceinline__ void gc_sum(const float* __restrict__ part, int W, in
         if (k >= W || k < j) {
             float sum = 0.f;
 #pragma unroll
-            for (int w = 0; w < nwarps; ++w) sum += part[w * 2 * 16 * T * T + sl];
+            for (int w = 0; w < kGcWarpsMax; ++w)
+                if (w < nwarps) sum += part[w * 2 * 16 * T * T + sl];
             out.add(W + k * W + j, (double)sum);
         }
     }
@@ -363,8 +403,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
         size_t off = 128 + align_up_dev((size_t)NS * W * Rs * sizeof(float));
         double* vs = reinterpret_cast<double*>(smem + off);
         off += align_up_dev((size_t)R * sizeof(double));
-        float* part = reinterpret_cast<float*>(smem + off);  // [kGcWarps][2 W^2]
-        off += align_up_dev((size_t)kGcWarps * 2 * W * W * sizeof(float));
+        float* part = reinterpret_cast<float*>(smem + off);  // [ngc][2 W^2]
+        off += align_up_dev((size_t)kGcWarpsMax * 2 * W * W * sizeof(float));
         double* upart = reinterpret_cast<double*>(smem + off);  // [kPipeCompute][32]
         off += align_up_dev((size_t)kPipeCompute * kPipeWMax * sizeof(double));
         double* vpart = reinterpret_cast<double*>(smem + off);  // [3][R] partial v updates
@@ -404,7 +444,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
             }
         } else {
             // Two warp groups on different pipes, each with its own named barrier and arrival:
-            //   Gram group (warps 0 .. kGcWarps-1, FFMA2): G_{b+1}, C_{b+1,b} as soon as block b+1
+            //   Gram group (warps 0 .. ngc-1, FFMA2): G_{b+1}, C_{b+1,b} as soon as block b+1
             //     has landed -- needs no delta;
             //   v group (the other compute warps, fp64): wait delta_{b-1}, v += A_{b-1} delta_{b-1},
             //     u_{b+1} = A_{b+1}^T v_b.
@@ -419,13 +459,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
             };
             auto out_of = [&](int64_t blk) { return RedOut{p.red + (size_t)(blk % kPipeRot) * rbsz, 0}; };
             auto arrive_cnt = [&](int64_t blk) {  // after the group's named barrier
+#ifndef DUHL_EXP_NOFENCE
                 __threadfence();
+#endif
                 atomicAdd(&cnt[blk % kPipeRot], 1u);
             };
-            if (warp < kGcWarps) {
+            constexpr int ngc = kGcWarps, nvw = kPipeCompute - kGcWarps;
+            if (warp < ngc) {
                 // ---------------------------------------------------------- Gram group
                 const int gw = warp, gtid = tid;
-                const int w4lo = (gw * n4) / kGcWarps, w4hi = ((gw + 1) * n4) / kGcWarps;
+                const int w4lo = (gw * n4) / ngc, w4hi = ((gw + 1) * n4) / ngc;
                 float* mypart = part + (size_t)gw * 2 * W * W;
                 for (int64_t b = -1; b + 1 < nblk; ++b) {
                     stamp(7);
@@ -448,27 +491,27 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                     if (b >= 0 && lane == 0) mbar_arrive(&empty[b % NS]);  // last Gram read of block b
                     stamp(1);
                     if (!EXACT) {  // sum the warps' partials and add one (fp64) RED per entry
-                        named_sync(kBarGc, kGcWarps * 32);
+                        named_sync(kBarGc, ngc * 32);
                         switch (W >> 2) {
-                            case 1: gc_sum<1>(part, W, gtid, kGcWarps, out); break;
-                            case 2: gc_sum<2>(part, W, gtid, kGcWarps, out); break;
-                            case 3: gc_sum<3>(part, W, gtid, kGcWarps, out); break;
-                            case 4: gc_sum<4>(part, W, gtid, kGcWarps, out); break;
-                            case 5: gc_sum<5>(part, W, gtid, kGcWarps, out); break;
-                            case 6: gc_sum<6>(part, W, gtid, kGcWarps, out); break;
-                            case 7: gc_sum<7>(part, W, gtid, kGcWarps, out); break;
-                            default: gc_sum<8>(part, W, gtid, kGcWarps, out); break;
+                            case 1: gc_sum<1>(part, W, gtid, ngc, out); break;
+                            case 2: gc_sum<2>(part, W, gtid, ngc, out); break;
+                            case 3: gc_sum<3>(part, W, gtid, ngc, out); break;
+                            case 4: gc_sum<4>(part, W, gtid, ngc, out); break;
+                            case 5: gc_sum<5>(part, W, gtid, ngc, out); break;
+                            case 6: gc_sum<6>(part, W, gtid, ngc, out); break;
+                            case 7: gc_sum<7>(part, W, gtid, ngc, out); break;
+                            default: gc_sum<8>(part, W, gtid, ngc, out); break;
                         }
                     }
-                    named_sync(kBarGc, kGcWarps * 32);  // partials consumed, every RED issued
+                    named_sync(kBarGc, ngc * 32);  // partials consumed, every RED issued
                     if (gtid == 0) arrive_cnt(b + 1);
                     stamp(2);
                 }
             } else {
                 // ---------------------------------------------------------- v group
-                const int vw = warp - kGcWarps, vtid = tid - kGcWarps * 32;
-                constexpr int kVThreads = kVWarps * 32;
-                const int w4lo = (vw * n4) / kVWarps, w4hi = ((vw + 1) * n4) / kVWarps;
+                const int vw = warp - ngc, vtid = tid - ngc * 32;
+                constexpr int kVThreads = nvw * 32;
+                const int w4lo = (vw * n4) / nvw, w4hi = ((vw + 1) * n4) / nvw;
                 const int vq = n4 > 0 ? kVThreads / n4 : 1;
                 const int vparts = vq < 1 ? 1 : (vq > 4 ? 4 : vq);
                 auto wait_delta = [&](int64_t blk) {  // delta_blk -> sDelta[blk & 1]
@@ -557,16 +600,23 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                         double acc[4];
 #pragma unroll
                         for (int a = 0; a < 4; ++a) acc[a] = 0.0;
+                        double acc2[4];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) acc2[a] = 0.0;
                         for (int r4 = w4lo + rs; r4 < w4hi; r4 += 8) {
                             const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
 #pragma unroll
                             for (int a = 0; a < 4; ++a) {
                                 if (a >= T) break;
                                 const float4 x = lds_f4(smem_addr(A1 + (size_t)(jq + 4 * a) * Rs) + 16u * r4);
-                                acc[a] = fma((double)x.x, v01.x, fma((double)x.y, v01.y, fma((double)x.z, v23.x,
-                                             fma((double)x.w, v23.y, acc[a]))));
+                                acc[a] = fma((double)x.x, v01.x, acc[a]);   // two chains per column
+                                acc2[a] = fma((double)x.y, v01.y, acc2[a]);
+                                acc[a] = fma((double)x.z, v23.x, acc[a]);
+                                acc2[a] = fma((double)x.w, v23.y, acc2[a]);
                             }
                         }
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) acc[a] += acc2[a];
 #pragma unroll
                         for (int a = 0; a < 4; ++a) {
                             if (a >= T) break;
@@ -581,7 +631,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                     if (vtid < W) {
                         double sum = 0.0;
 #pragma unroll
-                        for (int w = 0; w < kVWarps; ++w) sum += upart[w * kPipeWMax + vtid];
+                        for (int w = 0; w < kPipeCompute; ++w)
+                            if (w < nvw) sum += upart[w * kPipeWMax + vtid];
                         out_of(blk).add(vtid, sum);
                     }
                 };
