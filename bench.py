@@ -390,35 +390,41 @@ def run_duhl(args, cfg, rank, world, local):
     # ---------------- end to end: create from host buffers + solve to certified eps
     e2e = None
     if not args.no_e2e:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        P2 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
-                      **common)
-        if uid is not None:
-            P2.comm_init(uid, world, rank)
-        t_c2 = time.perf_counter() - t0
-        t1 = time.perf_counter()
-        r = P2.solve(args.eps, args.max_rounds, passes=args.passes, policy=policy)
-        t_solve = time.perf_counter() - t1
-        wall = time.perf_counter() - t0
-        c2 = P2.counters()
-        g_final = r["gap"]
-        P2.close()
-        wall = max_over_ranks(wall, world)
-        c2["updates"] = int(max_over_ranks(c2["updates"], world)) * world
+        runs = []  # fresh create + solve each: time-to-eps is the median of --e2e-runs
+        for rep in range(max(1, args.e2e_runs)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P2 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact,
+                        **common)
+            if uid is not None:
+                P2.comm_init(uid, world, rank)
+            t_c2 = time.perf_counter() - t0
+            t1 = time.perf_counter()
+            r = P2.solve(args.eps, args.max_rounds, passes=args.passes, policy=policy)
+            t_solve = time.perf_counter() - t1
+            wall = time.perf_counter() - t0
+            c2 = P2.counters()
+            P2.close()
+            c2["updates"] = int(max_over_ranks(c2["updates"], world)) * world
+            runs.append(dict(r=r, c=c2, t_create=t_c2, t_solve=max_over_ranks(t_solve, world),
+                             wall=max_over_ranks(wall, world)))
+        order = sorted(range(len(runs)), key=lambda q: runs[q]["t_solve"])
+        med = runs[order[len(runs) // 2]]
+        r, c2, wall = med["r"], med["c"], med["wall"]
         rounds = max(1, r["rounds"])
         e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
                "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
                "zero_copy_bytes_per_step": int(c2["zc_bytes"] / rounds),
                "d2h_bytes_per_step": int(m * 8 + 64),
-               "time_to_eps_s": max_over_ranks(t_solve, world), "eps": args.eps,
-               "certified_gap": g_final, "create_plus_solve_s": wall,
-               "converged": r["status"] == 0, "rounds": r["rounds"], "create_s": t_c2,
-               "note": "value = updates / (duhl_create from host buffers (pin in place, norms, z at "
-                       "alpha=0 over PCIe) + duhl_solve to the certified gap); time_to_eps_s = "
-                       "duhl_solve alone (data resident in pinned host memory, cold HBM fill "
-                       "included); h2d = cold fill + swaps (memcpy); zero-copy = refresh + certificate reads of "
-                       "non-resident columns"}
+               "time_to_eps_s": med["t_solve"], "time_to_eps_runs_s": [q["t_solve"] for q in runs],
+               "eps": args.eps, "certified_gap": r["gap"], "create_plus_solve_s": wall,
+               "converged": all(q["r"]["status"] == 0 for q in runs), "rounds": r["rounds"],
+               "create_s": med["t_create"],
+               "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
+                       "from host buffers (pin in place, norms, z at alpha=0 over PCIe) + duhl_solve to the "
+                       "certified gap); time_to_eps_s = duhl_solve alone (data resident in pinned host "
+                       "memory, cold HBM fill included); h2d = cold fill + swaps (memcpy); zero-copy = "
+                       "refresh + certificate reads of non-resident columns"}
 
     # ---------------- baselines: same library, budget and kernels, batch selection
     # sequential blocks [Yu 2012] / uniform / importance sampling instead of gap top-m
@@ -504,6 +510,7 @@ def main():
                     help="scheduled certificates every R rounds (default: adaptive ones only)")
     ap.add_argument("--ref-cols", type=int, default=2000)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-runs", type=int, default=3, help="fresh create + solve runs; the median is reported")
     ap.add_argument("--exact", action="store_true", help="fp64 Gram products in the SCD kernel")
     ap.add_argument("--linesearch", action="store_true", help="gamma line search also at N=1")
     ap.add_argument("--baselines", action="store_true",

@@ -356,6 +356,23 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
         assert sw == ref["swaps"].tolist()[:len(sw)]
 
 
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_adaptive_certificates_only(D, model):
+    """duhl_solve with no certificate schedule: the gap memory's estimate (calibrated by failed
+    certificates) decides when to certify; the result is still certified <= eps, with few passes."""
+    d, n = (400, 2000) if model == O.LASSO else (150, 2000)
+    A, lab = _data(model, d, n, seed=77)
+    lam = _lam(model, n)
+    eps = 1e-6
+    with D.create(A, lab, lam, model, hbm_budget_bytes=500 * d * 4, m=400, refresh_fraction=0.1,
+                  cert_every=1 << 30, seed=3) as P:
+        r = P.solve(eps, 5000, passes=2)
+        g, _, _ = P.duality_gap()
+    assert r["status"] == 0 and r["gap"] <= eps and g <= eps
+    ncert = sum(1 for t in r["trace"] if t.cert_gap >= 0)
+    assert 1 <= ncert <= 6, ncert
+
+
 def test_budget_smaller_than_data_swaps(D):
     """Data 4x the HBM budget: the pool holds only m columns; swaps fall over rounds (Fig. 4b)."""
     d, n = 256, 2000
