@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "duhl_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-LASSO, SVM, RIDGE = 0, 1, 2
+LASSO, SVM, RIDGE, ELASTIC = 0, 1, 2, 3
 SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE = 0, 1, 2, 3
 OK, E_INVALID, E_NUMERIC, E_NOT_CONVERGED = 0, 2, 4, 9
 
@@ -54,6 +54,8 @@ def lib():
         L.or_col_norms.argtypes = [_P, _I, _I, _I, _P]
         L.or_lasso_B.restype = C.c_double
         L.or_lasso_B.argtypes = [_P, _I, C.c_double]
+        L.or_set_eta.restype = None
+        L.or_set_eta.argtypes = [C.c_double]
         L.or_matvec.argtypes = [_P, _I, _I, _I, _P, _P]
         L.or_primal_dual_w.argtypes = [C.c_int, _P, _P, _I, _I, C.c_double, _P]
         L.or_coord_gaps.restype = C.c_int
@@ -114,6 +116,11 @@ def col_norms(A, d=None):
     out = np.empty(n)
     lib().or_col_norms(_p(A), d, n, ld, _p(out))
     return out
+
+
+def set_eta(eta):
+    """eta of the elastic-net model (OR_ELASTIC), global in the oracle library."""
+    lib().or_set_eta(float(eta))
 
 
 def lasso_B(b, lam):

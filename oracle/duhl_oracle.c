@@ -31,6 +31,11 @@ typedef uint64_t u64;
 #define OR_LASSO 0
 #define OR_SVM 1
 #define OR_RIDGE 2   /* ridge regression: f as Lasso, g_i = (lambda/2) alpha_i^2 */
+#define OR_ELASTIC 3 /* elastic net: g_i = lambda (eta/2 alpha_i^2 + (1-eta)|alpha_i|), 0 < eta < 1 */
+
+/* eta of the elastic-net model (or_set_eta; test infrastructure, one value at a time). */
+static double or_eta = 0.5;
+void or_set_eta(double eta) { or_eta = eta; }
 #define OR_HAS_B(model) ((model) != OR_SVM)   /* regression models: labels b, v~ = A alpha - b */
 
 #define OR_OK 0
@@ -115,6 +120,16 @@ int or_coord_gaps(int model, const float* A, i64 d, i64 n, i64 ld, const double*
             double t1 = alpha[i] * s, t2 = B * (thr > 0.0 ? thr : 0.0), t3 = lam_d * fabs(alpha[i]);
             g = (t1 + t2 + t3) / (double)d;
             scale = (fabs(t1) + t2 + t3) / (double)d;
+        } else if (model == OR_ELASTIC) {
+            /* Eq. 4 with g_i(a) = lambda (eta/2 a^2 + (1-eta)|a|) and its conjugate
+             * g*(x) = [|x| - lambda (1-eta)]_+^2 / (2 lambda eta):
+             * gap_i = g_i(a_i) + g*(-s_i/d) + a_i s_i/d  (reading R20; eta = 1 gives P:841) */
+            double e = or_eta, x = fabs(s) / (double)d - lambda * (1.0 - e);
+            double t1 = alpha[i] * s / (double)d;
+            double t2 = lambda * (0.5 * e * alpha[i] * alpha[i] + (1.0 - e) * fabs(alpha[i]));
+            double t3 = x > 0.0 ? x * x / (2.0 * lambda * e) : 0.0;
+            g = t1 + t2 + t3;
+            scale = fabs(t1) + t2 + t3;
         } else if (model == OR_RIDGE) {
             /* gap_i = (1/d) [ a_i s_i + s_i^2/(2 lambda d) + (lambda d/2) a_i^2 ] */
             double lam_d = lambda * (double)d;
@@ -288,6 +303,14 @@ double or_coord_update(int model, double alpha_j, double s, double norm, double 
     if (model == OR_RIDGE) {  /* P:808-813 with eta = 1: tau = 0, denominator ||a||^2 + lambda d */
         return (alpha_j * norm - s) / (norm + lambda * (double)d);
     }
+    if (model == OR_ELASTIC) {  /* gamma, tau over ||a||^2 + lambda eta d; soft threshold */
+        double den = norm + lambda * or_eta * (double)d;
+        double gamma = (alpha_j * norm - s) / den;
+        double tau = lambda * (double)d * (1.0 - or_eta) / den;
+        double mag = fabs(gamma) - tau;
+        if (mag <= 0.0) return 0.0;
+        return gamma > 0.0 ? mag : -mag;
+    }
     if (model == OR_LASSO) {
         if (norm == 0.0) return 0.0;
         double gamma = (alpha_j * norm - s) / norm;
@@ -363,6 +386,23 @@ int or_duality_gap(int model, const float* A, i64 d, i64 n, i64 ld, const double
         for (i64 i = 0; i < n; ++i) {
             double x = fabs(s[i] / (double)d) - lambda;
             conj += B * (x > 0.0 ? x : 0.0);
+        }
+        D = -(ub + 0.5 * (double)d * uu) - conj;
+    } else if (model == OR_ELASTIC) {
+        /* O = (1/2d)||w||^2 + lambda sum (eta/2 a^2 + (1-eta)|a|);
+         * D = -(u^T b + (d/2)||u||^2) - sum_i g*(a_i^T u),  u = w/d */
+        double ww = 0.0, pen = 0.0, ub = 0.0, uu = 0.0, conj = 0.0, e = or_eta;
+        for (i64 k = 0; k < d; ++k) ww += w[k] * w[k];
+        for (i64 i = 0; i < n; ++i) pen += 0.5 * e * alpha[i] * alpha[i] + (1.0 - e) * fabs(alpha[i]);
+        O = ww / (2.0 * (double)d) + lambda * pen;
+        for (i64 k = 0; k < d; ++k) {
+            double u = w[k] / (double)d;
+            ub += u * b[k];
+            uu += u * u;
+        }
+        for (i64 i = 0; i < n; ++i) {
+            double x = fabs(s[i]) / (double)d - lambda * (1.0 - e);
+            if (x > 0.0) conj += x * x / (2.0 * lambda * e);
         }
         D = -(ub + 0.5 * (double)d * uu) - conj;
     } else if (model == OR_RIDGE) {
@@ -582,11 +622,13 @@ static double or_sgnp(double x, double da) {
     if (x < 0.0) return -1.0;
     return da > 0.0 ? 1.0 : (da < 0.0 ? -1.0 : 0.0);
 }
+/* right derivative along gamma; l1 = weight of the |.| part (1 Lasso, 1-eta elastic net), l2 = weight
+ * of the quadratic part (0 Lasso, eta elastic net) with ada = a.da, dada = da.da */
 static double or_lasso_rderiv(double g, const double* a_old, const double* da, i64 k, double vdv,
-                              double dvdv, double lambda, i64 d) {
+                              double dvdv, double lambda, i64 d, double l1, double l2, double ada, double dada) {
     double s = 0.0;
     for (i64 i = 0; i < k; ++i) s += da[i] * or_sgnp(a_old[i] + g * da[i], da[i]);
-    return (vdv + g * dvdv) / (double)d + lambda * s;
+    return (vdv + g * dvdv) / (double)d + lambda * (l1 * s + l2 * (ada + g * dada));
 }
 double or_linesearch(int model, const double* v0, const double* dv, i64 d, const double* a_old,
                      const double* da, const double* y, i64 k, double lambda, i64 n) {
@@ -607,8 +649,14 @@ double or_linesearch(int model, const double* v0, const double* dv, i64 d, const
         double g = -(vdv / (double)d + lambda * ada) / den;
         return g < 0.0 ? 0.0 : (g > 1.0 ? 1.0 : g);
     }
-    if (or_lasso_rderiv(0.0, a_old, da, k, vdv, dvdv, lambda, d) >= 0.0) return 0.0;
-    if (or_lasso_rderiv(1.0, a_old, da, k, vdv, dvdv, lambda, d) < 0.0) return 1.0;
+    double l1 = 1.0, l2 = 0.0, ada = 0.0, dada = 0.0;
+    if (model == OR_ELASTIC) {  /* elastic net: the Lasso walk plus the eta-weighted quadratic */
+        l1 = 1.0 - or_eta;
+        l2 = or_eta;
+        for (i64 i = 0; i < k; ++i) { ada += a_old[i] * da[i]; dada += da[i] * da[i]; }
+    }
+    if (or_lasso_rderiv(0.0, a_old, da, k, vdv, dvdv, lambda, d, l1, l2, ada, dada) >= 0.0) return 0.0;
+    if (or_lasso_rderiv(1.0, a_old, da, k, vdv, dvdv, lambda, d, l1, l2, ada, dada) < 0.0) return 1.0;
     /* breakpoints strictly inside (0, 1) */
     double* bp = (double*)malloc(sizeof(double) * (size_t)(k + 2));
     i64 nb = 0;
@@ -625,11 +673,13 @@ double or_linesearch(int model, const double* v0, const double* dv, i64 d, const
         double lo = bp[q], hi = bp[q + 1];
         if (!(hi > lo)) continue;
         double mid = 0.5 * (lo + hi);
-        /* on (lo, hi) the sign pattern is constant: D(x) = (vdv + x dvdv)/d + lambda S */
+        /* on (lo, hi) the sign pattern is constant:
+         * D(x) = (vdv + x dvdv)/d + lambda (l1 S + l2 (ada + x dada)) */
         double S = 0.0;
         for (i64 i = 0; i < k; ++i) S += da[i] * or_sgnp(a_old[i] + mid * da[i], da[i]);
-        if (or_lasso_rderiv(lo, a_old, da, k, vdv, dvdv, lambda, d) >= 0.0) { g = lo; break; }
-        double x = dvdv > 0.0 ? (-(double)d * lambda * S - vdv) / dvdv : hi;
+        if (or_lasso_rderiv(lo, a_old, da, k, vdv, dvdv, lambda, d, l1, l2, ada, dada) >= 0.0) { g = lo; break; }
+        double den = dvdv / (double)d + lambda * l2 * dada;
+        double x = den > 0.0 ? -(vdv / (double)d + lambda * (l1 * S + l2 * ada)) / den : hi;
         if (x < hi) { g = x > lo ? x : lo; break; }
     }
     free(bp);

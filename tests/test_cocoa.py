@@ -25,14 +25,17 @@ def _objective(model, A, lab, lam, alpha):
         return ((v - lab) @ (v - lab)) / (2 * d) + lam * np.abs(alpha).sum()
     if model == O.RIDGE:
         return ((v - lab) @ (v - lab)) / (2 * d) + 0.5 * lam * (alpha @ alpha)
+    if model == O.ELASTIC:  # P:796-800 with eta = 0.5 (O.set_eta)
+        return ((v - lab) @ (v - lab)) / (2 * d) + lam * (0.25 * (alpha @ alpha) + 0.5 * np.abs(alpha).sum())
     return -(lab @ alpha) / n + (v @ v) / (2 * lam * n * n)
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 def test_linesearch_is_the_exact_minimiser(model):
+    O.set_eta(0.5)
     rng = np.random.default_rng(5)
     for trial in range(20):
-        if model in (O.LASSO, O.RIDGE):
+        if model in (O.LASSO, O.RIDGE, O.ELASTIC):
             A, lab = synth.lasso_dense(40, 30, seed=trial)
             lam = 0.05
             a0 = rng.standard_normal(30) * (rng.random(30) < 0.5) * 0.2

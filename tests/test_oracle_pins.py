@@ -253,6 +253,74 @@ def test_R4_ridge_duhl_reaches_the_normal_equations(policy):
     np.testing.assert_allclose(r["alpha"], astar, atol=1e-4 * np.abs(astar).max())
 
 
+# ----------------------------------------------------------------------------- elastic net
+def test_E1_elastic_net_worked_example_and_limits():
+    """A = I_2, b = (1, 1), lambda = 1/4, eta = 1/2: per coordinate
+    (1/4)(a - 1)^2 + lambda (eta/2 a^2 + (1 - eta)|a|) is minimised at
+    a* = (1 - 2 lambda (1 - eta)) / (1 + 2 lambda eta) = 0.6, where every gap vanishes; one step from
+    0 reaches it.  eta = 1 reproduces the ridge gaps exactly."""
+    A = np.eye(2, dtype=np.float32)
+    b = np.array([1.0, 1.0])
+    lam = 0.25
+    O.set_eta(0.5)
+    assert abs(O.coord_update(O.ELASTIC, 0.0, -1.0, 1.0, 0.0, lam, 2, 2) - 0.6) < 1e-15
+    st, G, Ob, Db = O.duality_gap(O.ELASTIC, A, np.full(2, 0.6), b, lam)
+    assert st == O.OK and G < 1e-15 and abs(G - (Ob - Db)) < 1e-15
+    # O* = (1/4)(2 * 0.16) + 0.25 (0.25 * 0.72 + 0.5 * 1.2) = 0.08 + 0.195 = 0.275
+    assert abs(Ob - 0.275) < 1e-15
+    rng = np.random.default_rng(4)
+    A2, b2 = synth.lasso_dense(60, 40, seed=8)
+    a = rng.standard_normal(40) * 0.2
+    w = A2.astype(np.float64).T @ a - b2
+    O.set_eta(1.0)
+    ge = O.coord_gaps(O.ELASTIC, A2, a, None, w, 0.03)[2]
+    gr = O.coord_gaps(O.RIDGE, A2, a, None, w, 0.03)[2]
+    np.testing.assert_allclose(ge, gr, rtol=1e-12, atol=1e-300)
+    O.set_eta(0.5)
+
+
+@pytest.mark.parametrize("eta", [0.2, 0.7])
+def test_E2_elastic_net_matches_sklearn_and_gap_identity(eta):
+    """sklearn ElasticNet(alpha = lambda, l1_ratio = 1 - eta, fit_intercept = False) minimises the
+    same objective (its 1/(2 n_samples) is our 1/(2d)); plain SCD reaches a certified gap and the
+    same objective; sum gap_i = O - D with gap_i >= 0 at random states."""
+    from sklearn.linear_model import ElasticNet
+    O.set_eta(eta)
+    d, n, lam = 150, 90, 0.02
+    A, b = synth.lasso_dense(d, n, seed=29)
+    A64 = A.astype(np.float64).T
+    st, alpha, gap, ep = O.solve_scd(O.ELASTIC, A, b, lam, 1e-12, 20000, seed=1)
+    assert st == O.OK and gap <= 1e-12
+    sk = ElasticNet(alpha=lam, l1_ratio=1 - eta, fit_intercept=False, tol=1e-14, max_iter=200000).fit(A64, b).coef_
+    r = A64 @ sk - b
+    O_sk = r @ r / (2 * d) + lam * (0.5 * eta * sk @ sk + (1 - eta) * np.abs(sk).sum())
+    st, G, Ob, Db = O.duality_gap(O.ELASTIC, A, alpha, b, lam)
+    assert Ob <= O_sk + 1e-12 and O_sk - Ob <= 1e-9 * abs(Ob)
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        a = rng.standard_normal(n) * (rng.random(n) < 0.5) * 0.3
+        st, G, Ob, Db = O.duality_gap(O.ELASTIC, A, a, b, lam)
+        g = O.coord_gaps(O.ELASTIC, A, a, None, A64 @ a - b, lam)[2]
+        assert np.all(g >= 0) and abs(g.sum() - G) <= 1e-12 * G and abs(G - (Ob - Db)) <= 1e-10 * max(1, abs(Ob))
+    O.set_eta(0.5)
+
+
+def test_E3_elastic_step_minimises_1d_objective():
+    from scipy.optimize import minimize_scalar
+    rng = np.random.default_rng(9)
+    for _ in range(100):
+        eta = float(rng.uniform(0.05, 0.95))
+        O.set_eta(eta)
+        d, n = int(rng.integers(2, 50)), int(rng.integers(2, 50))
+        nrm, aj, s_ = float(rng.uniform(0.0, 5)), float(rng.normal()), float(rng.normal() * 3)
+        lam = float(rng.uniform(0.001, 0.5))
+        phi = lambda x: (2 * s_ * (x - aj) + nrm * (x - aj) ** 2) / (2 * d) + lam * (0.5 * eta * x * x + (1 - eta) * abs(x))
+        x = O.coord_update(O.ELASTIC, aj, s_, nrm, 0.0, lam, d, n)
+        r = minimize_scalar(phi, bounds=(-100, 100), method="bounded", options={"xatol": 1e-10})
+        assert phi(x) <= r.fun + 1e-12 and abs(x - r.x) < 1e-6
+    O.set_eta(0.5)
+
+
 # ----------------------------------------------------------------------------- P7 / P8
 def test_P7_hadamard_lasso_closed_form_one_epoch():
     """Orthogonal design A^T A = d I: alpha* = soft(A^T b, lam d)/d (north_star pin).
