@@ -42,7 +42,7 @@ extern "C" {
 
 typedef struct duhl_ctx duhl_ctx; /* opaque; one per problem instance */
 
-typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1, DUHL_RIDGE = 2 } duhl_model;
+typedef enum { DUHL_LASSO = 0, DUHL_SVM_DUAL = 1, DUHL_RIDGE = 2, DUHL_ELASTIC_NET = 3 } duhl_model;
 
 /* Block selection policies: Eq. 11 gap memory, and the paper's
  * reference schemes: sequential blocks [Yu 2012], uniform. */
@@ -106,6 +106,8 @@ typedef struct {
                                  tiles of block b+1 run before delta_{b-1} is known; W <= 32); 0 = auto
                                  (pipelined where shared memory holds W >= 24).  Both execute the same
                                  sequential order (App. D), up to summation order. */
+    double eta;               /* DUHL_ELASTIC_NET only: g_i = lambda (eta/2 alpha_i^2 + (1-eta)|alpha_i|)
+                                 (P:796-800), 0 < eta < 1; eta = 0 is DUHL_LASSO, eta = 1 DUHL_RIDGE */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */

@@ -8,7 +8,7 @@ import numpy as np
 
 from . import build as _build
 
-LASSO, SVM_DUAL, RIDGE = 0, 1, 2
+LASSO, SVM_DUAL, RIDGE, ELASTIC_NET = 0, 1, 2, 3
 SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE = 0, 1, 2, 3
 STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "E_NOMEM",
           7: "E_CUDA", 8: "E_NCCL", 9: "E_NOT_CONVERGED"}
@@ -41,7 +41,7 @@ class Config(C.Structure):
                 ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
                 ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
                 ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int),
-                ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int)]
+                ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int), ("eta", C.c_double)]
 
 
 class RoundRecord(C.Structure):
@@ -229,8 +229,8 @@ class Problem:
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
            cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
-           linesearch=False, unit_a_ctas=0, scd_kernel=0):
-    """duhl_create.  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
+           linesearch=False, unit_a_ctas=0, scd_kernel=0, eta=0.0):
+    """duhl_create.  eta: the elastic-net mix (model ELASTIC_NET only).  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
         raise ValueError("A must be a C-contiguous (n, ld) float32 array")
@@ -244,7 +244,7 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
                          profile=int(bool(profile)), scd_exact=int(bool(scd_exact)),
                          n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)),
-                         unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel)
+                         unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel, eta=float(eta))
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:
@@ -257,7 +257,7 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
 
 def create_csc(col_ptr, row_idx, values, d, b_or_y, lam, model, m=0, device=0, refresh_fraction=0.05,
                cert_every=10, seed=170805357, cert_adaptive=True, profile=False, scd_exact=True,
-               n_global=0, col_offset=0, linesearch=False, scd_ctas=0):
+               n_global=0, col_offset=0, linesearch=False, scd_ctas=0, eta=0.0):
     """duhl_create_csc.  CSC arrays: col_ptr int64 [n+1], row_idx int32 [nnz] (ascending per
     column), values float32 [nnz]; the matrix is copied to HBM."""
     cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
@@ -269,7 +269,7 @@ def create_csc(col_ptr, row_idx, values, d, b_or_y, lam, model, m=0, device=0, r
     cfg = default_config(m=m, device=device, refresh_fraction=refresh_fraction, cert_every=cert_every,
                          seed=seed, cert_adaptive=int(bool(cert_adaptive)), profile=int(bool(profile)),
                          scd_exact=int(bool(scd_exact)), n_global=n_global, col_offset=col_offset,
-                         linesearch=int(bool(linesearch)), scd_ctas=scd_ctas)
+                         linesearch=int(bool(linesearch)), scd_ctas=scd_ctas, eta=float(eta))
     h = C.c_void_p()
     st = lib().duhl_create_csc(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

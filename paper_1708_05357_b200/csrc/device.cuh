@@ -15,6 +15,7 @@ constexpr int kLasso = 0;
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 constexpr int kSvm = 1;
 constexpr int kRidge = 2;  // ridge regression: the regression structure of Lasso, g = (lambda/2) a^2
+constexpr int kElastic = 3;  // elastic net: g = lambda (eta/2 a^2 + (1-eta)|a|), 0 < eta < 1
 
 // ---------------------------------------------------------------- counter RNG
 // splitmix64 finaliser; permutation key(seed, round, pass, j) (DESIGN.md
@@ -44,8 +45,14 @@ __host__ __device__ __forceinline__ uint64_t perm_key(uint64_t seed, int64_t rou
 //                    alpha' = y clip(y (alpha + Delta), 0, 1)
 // Zero column: the exact 1-D minimiser (Lasso 0, SVM y) -- reading R5.
 __device__ __forceinline__ double coord_step(int model, double alpha, double s, double nrm,
-                                             double y, double lambda, double dd, double nn) {
+                                             double y, double lambda, double dd, double nn, double eta = 0.0) {
     if (model == kRidge) return (alpha * nrm - s) / (nrm + lambda * dd);  // P:808-813, eta = 1
+    if (model == kElastic) {  // gamma and tau over ||a||^2 + lambda eta d
+        const double den = nrm + lambda * eta * dd;
+        const double gamma = (alpha * nrm - s) / den, tau = lambda * dd * (1.0 - eta) / den;
+        const double mag = fabs(gamma) - tau;
+        return mag > 0.0 ? copysign(mag, gamma) : 0.0;
+    }
     if (model == kLasso) {
         if (nrm == 0.0) return 0.0;
         double gamma = (alpha * nrm - s) / nrm;
@@ -71,7 +78,16 @@ __device__ __forceinline__ double coord_step(int model, double alpha, double s, 
 // used by the certificate: Lasso B max(|s|/d - lambda, 0), SVM max(0, 1 - y s).
 __device__ __forceinline__ double coord_gap(int model, double alpha, double s, double y,
                                             double lambda, double B, double dd, double nn,
-                                            double* scale, double* aux) {
+                                            double* scale, double* aux, double eta = 0.0) {
+    if (model == kElastic) {  // Eq. 4 with the conjugate g*(x) = [|x| - lambda(1-eta)]_+^2/(2 lambda eta)
+        const double x = fabs(s) / dd - lambda * (1.0 - eta);
+        const double t1 = alpha * s / dd;
+        const double t2 = lambda * (0.5 * eta * alpha * alpha + (1.0 - eta) * fabs(alpha));
+        const double t3 = x > 0.0 ? x * x / (2.0 * lambda * eta) : 0.0;
+        *scale = fabs(t1) + t2 + t3;
+        *aux = t3;  // g*(a^T u), u = w/d: the dual's penalty term
+        return t1 + t2 + t3;
+    }
     if (model == kRidge) {  // P:841; aux = g*(-a^T u) = (s/d)^2/(2 lambda) for the dual
         const double lam_d = lambda * dd;
         const double t1 = alpha * s, t2 = s * s / (2.0 * lam_d), t3 = 0.5 * lam_d * alpha * alpha;

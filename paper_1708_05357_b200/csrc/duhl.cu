@@ -223,8 +223,10 @@ static ColSrc colsrc(const duhl_ctx* ctx) {
 static CscMat cscmat(const duhl_ctx* ctx) { return CscMat{ctx->d_colptr, ctx->d_rows, ctx->d_vals}; }
 
 // ridge: the SCD kernels take 1/(||a_j||^2 + lambda d) per position (k_perm_order)
+// (elastic net: 1/(||a_j||^2 + lambda eta d))
 static double ridge_ld(const duhl_ctx* ctx) {
-    return ctx->model == DUHL_RIDGE ? ctx->lambda * (double)ctx->d : 0.0;
+    return ctx->model == DUHL_RIDGE ? ctx->lambda * (double)ctx->d
+         : ctx->model == DUHL_ELASTIC_NET ? ctx->lambda * ctx->cfg.eta * (double)ctx->d : 0.0;
 }
 
 static double wscale(const duhl_ctx* ctx) {
@@ -254,6 +256,7 @@ static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
     p.y = ctx->d_y;
     p.lambda = ctx->lambda;
     p.B = ctx->B;
+    p.eta = ctx->cfg.eta;
     p.s_acc = ctx->d_s_acc;
     p.z = ctx->d_z;
     p.flag = ctx->d_flag;
@@ -641,7 +644,9 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         return DUHL_E_INVALID;
     if (!A == !C || !b_or_y) return DUHL_E_INVALID;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return DUHL_E_INVALID;
-    if (model != DUHL_LASSO && model != DUHL_SVM_DUAL && model != DUHL_RIDGE) return DUHL_E_INVALID;
+    if (model != DUHL_LASSO && model != DUHL_SVM_DUAL && model != DUHL_RIDGE && model != DUHL_ELASTIC_NET)
+        return DUHL_E_INVALID;
+    if (model == DUHL_ELASTIC_NET && !(cfg_in && cfg_in->eta > 0.0 && cfg_in->eta < 1.0)) return DUHL_E_INVALID;
     const int64_t nin = A ? A->n : C->n, din = A ? A->d : C->d;
     if (nin > (int64_t)INT32_MAX - 1) return DUHL_E_INVALID;
     duhl_ctx* ctx = new duhl_ctx();
@@ -997,6 +1002,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
         q.y = ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr;
         q.alpha = ctx->d_alpha;
         q.vt = ctx->d_vt;
+        q.eta = ctx->cfg.eta;
         ProfScope ps(ctx, ctx->st, 0, ctx->csc_pass_bytes);
         CK(launch_csc_scd(q, ctx->cfg.scd_exact ? 1 : ctx->csc_warps, ctx->st, &ctx->launches));
         ctx->updates += L;
@@ -1022,6 +1028,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.G = ctx->G;
     p.NB = ctx->NB;
     p.exact = ctx->cfg.scd_exact;
+    p.lam_q = ridge_ld(ctx);
+    p.lam_l1 = ctx->model == DUHL_ELASTIC_NET ? ctx->lambda * (double)ctx->d * (1.0 - ctx->cfg.eta) : 0.0;
     p.red = ctx->d_red;
     p.order_batch = ctx->overlap ? ctx->d_order_batch : nullptr;
     p.err = ctx->d_flag + 1;
@@ -1159,6 +1167,10 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
         // w = v~; O = ||w||^2/(2d) + lambda ||alpha||_1;  D = -(u^T b + (d/2)||u||^2) - sum B[|a^T u| - lambda]_+
         O = vv / (2.0 * dd) + lam * asum;
         D = -(vb / dd + 0.5 * vv / dd) - aux;
+    } else if (ctx->model == DUHL_ELASTIC_NET) {
+        // O = ||w||^2/(2d) + lambda sum (eta/2 a^2 + (1-eta)|a|);  D = -(u^T b + (d/2)||u||^2) - sum g*(a^T u)
+        O = vv / (2.0 * dd) + lam * asum;
+        D = -(vb / dd + 0.5 * vv / dd) - aux;
     } else if (ctx->model == DUHL_RIDGE) {
         // O = ||w||^2/(2d) + (lambda/2)||alpha||^2;  D = -(u^T b + (d/2)||u||^2) - sum (a^T u)^2/(2 lambda)
         O = vv / (2.0 * dd) + 0.5 * lam * asum;
@@ -1225,12 +1237,18 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
                 gamma = (yda / nn - vdv / ln2) / (dvdv / ln2);
                 gamma = gamma < 0.0 ? 0.0 : (gamma > 1.0 ? 1.0 : gamma);
             }
-        } else {
-            double h[2];
-            CK(cudaMemcpyAsync(h, ctx->d_ls, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+        } else {  // Lasso (l1 = 1, l2 = 0) and elastic net (l1 = 1 - eta, l2 = eta): walk the breakpoints
+            const bool en = ctx->model == DUHL_ELASTIC_NET;
+            const double l1 = en ? 1.0 - ctx->cfg.eta : 1.0, l2 = en ? ctx->cfg.eta : 0.0;
+            if (en) {
+                CK(launch_ridge_sums(ctx->d_alpha, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 2, ctx->st, &ctx->launches));
+                TRY(allreduce(ctx, ctx->d_ls + 2, 2));
+            }
+            double h[4];
+            CK(cudaMemcpyAsync(h, ctx->d_ls, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
-            const double dvdv = h[0], vdv = h[1];
-            auto Dfun = [&](double g, double S) { return (vdv + g * dvdv) / dd + lam * S; };
+            const double dvdv = h[0], vdv = h[1], ada = en ? h[2] : 0.0, dada = en ? h[3] : 0.0;
+            auto Dfun = [&](double g, double S) { return (vdv + g * dvdv) / dd + lam * (l1 * S + l2 * (ada + g * dada)); };
             double lo = 0.0, hi = 1.0, gam[64], S[64];
             bool done = false;
             for (int it = 0; it < 5 && !done; ++it) {
@@ -1258,7 +1276,8 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
                     if (q > 0) lo = gam[q - 1];
                     hi = gam[q < ng ? q : ng - 1];
                 } else {
-                    const double x = dvdv > 0.0 ? (-dd * lam * S[0] - vdv) / dvdv : hi;
+                    const double den = dvdv / dd + lam * l2 * dada;
+                    const double x = den > 0.0 ? -(vdv / dd + lam * (l1 * S[0] + l2 * ada)) / den : hi;
                     gamma = x < lo ? lo : (x > hi ? hi : x);
                     done = true;
                 }

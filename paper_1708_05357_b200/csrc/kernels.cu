@@ -45,7 +45,7 @@ __device__ __forceinline__ void gap_finish_one(const GapParams& p, int64_t t, in
     double a = p.alpha[i];
     double yy = p.model == kSvm ? p.y[i] : 0.0;
     double scale, aux;
-    double g = coord_gap(p.model, a, s, yy, p.lambda, p.B, (double)p.d, (double)p.n, &scale, &aux);
+    double g = coord_gap(p.model, a, s, yy, p.lambda, p.B, (double)p.d, (double)p.n, &scale, &aux, p.eta);
     if (!isfinite(g)) flag |= 2;
     else if (g < -1e-12 * (scale > 1.0 ? scale : 1.0)) flag |= 1;
     double gz = g > 1e-12 * scale ? g : 0.0;  // rounding noise reads as +0.0 (reading R17)
@@ -54,7 +54,9 @@ __device__ __forceinline__ void gap_finish_one(const GapParams& p, int64_t t, in
     if (p.s_out) p.s_out[t] = s;
     acc.g += gz;
     acc.aux += aux;
-    acc.a += p.model == kLasso ? fabs(a) : (p.model == kRidge ? a * a : yy * a);
+    acc.a += p.model == kLasso ? fabs(a)
+             : p.model == kRidge ? a * a
+             : p.model == kElastic ? 0.5 * p.eta * a * a + (1.0 - p.eta) * fabs(a) : yy * a;
     acc.amax = fmax(acc.amax, fabs(a));
 }
 
@@ -999,9 +1001,9 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(const __grid_consta
                     t = a - sj * inv;
                     tau = lam_dn * inv;
                     scale = -inv;
-                } else if (MODEL == kRidge) {  // inv = 1/(||a||^2 + lambda d): t = gamma, no threshold
-                    t = a - (sj + lam_dn * a) * inv;
-                    tau = 0.0;
+                } else if (MODEL == kRidge) {  // ridge / elastic net: inv = 1/(||a||^2 + lambda eta d)
+                    t = a - (sj + p.lam_q * a) * inv;
+                    tau = p.lam_l1 * inv;
                     scale = -inv;
                 } else {
                     t = fma(lam_dn - yy * sj, inv, yy * a);
@@ -1191,7 +1193,7 @@ cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launch
     size_t smem = scd_smem_bytes(p.W, p.R, kScdStages);
     const void* fn = p.model == kLasso
                          ? (p.exact ? (const void*)k_scd_gram<true, kLasso> : (const void*)k_scd_gram<false, kLasso>)
-                     : p.model == kRidge
+                     : (p.model == kRidge || p.model == kElastic)
                          ? (p.exact ? (const void*)k_scd_gram<true, kRidge> : (const void*)k_scd_gram<false, kRidge>)
                          : (p.exact ? (const void*)k_scd_gram<true, kSvm> : (const void*)k_scd_gram<false, kSvm>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1468,7 +1470,7 @@ __global__ void __launch_bounds__(256) k_csc_scd(CscScdParams p) {
             s = fma((double)p.A.vals[k], __ldcg(p.vt + p.A.rows[k]), s);
         s = warp_sum(s);
         const double a = p.alpha[j];
-        const double an = coord_step(p.model, a, s, p.norms[j], p.y ? p.y[j] : 0.0, p.lambda, dd, nn);
+        const double an = coord_step(p.model, a, s, p.norms[j], p.y ? p.y[j] : 0.0, p.lambda, dd, nn, p.eta);
         const double dl = an - a;
         if (dl != 0.0)
             for (int64_t k = k0 + lane; k < k1; k += 32) atomicAdd(p.vt + p.A.rows[k], dl * (double)p.A.vals[k]);

@@ -26,6 +26,7 @@ struct GapParams {
     const double* alpha;       // [n]
     const double* y;           // [n] SVM labels (nullptr for Lasso)
     double lambda, B;
+    double eta;                // elastic net only
     double* s_acc;             // [k] partial-dot accumulator (multi-tile passes), zero on entry
     double* z;                 // [n] gap memory or nullptr
     double* gap_out;           // [k] or nullptr
@@ -50,6 +51,7 @@ struct ScdParams {
     int W, R, G, NB;           // block size (% 4 == 0; <= 16 legacy, <= 32 pipe), rows per CTA, (compute) CTAs, TMA stages
     // pipe kernel: bar = cnt[6] (arrivals per reduction buffer) + flg[6] at bar + 8 (delta tags)
     int exact;                 // 1: fp64 Gram products (bit-level parity mode); 0: fp32 Gram within a warp
+    double lam_q, lam_l1;      // ridge / elastic-net kernels: lambda eta d (quadratic), lambda (1-eta) d (l1)
     double* red;               // [scd_red_doubles(W)] zero on entry
     unsigned* bar;             // [2] grid-barrier counters (per block parity), zero on entry
     unsigned long long* trace; // developer phase timer [16] or nullptr
@@ -82,6 +84,7 @@ struct CscScdParams {
     const double* y;         // [n] (SVM) or nullptr
     double* alpha;           // [n]
     double* vt;              // [d4]
+    double eta;              // elastic net only
 };
 
 __host__ __device__ int scd_nred(int W);

@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                         t = a - sj * inv;
                         tau = lam_dn * inv;
                         scale = -inv;
-                    } else if (MODEL == kRidge) {  // inv = 1/(||a||^2 + lambda d): t = gamma, no threshold
-                        t = a - (sj + lam_dn * a) * inv;
-                        tau = 0.0;
+                    } else if (MODEL == kRidge) {  // ridge / elastic net: inv = 1/(||a||^2 + lambda eta d)
+                        t = a - (sj + p.lam_q * a) * inv;
+                        tau = p.lam_l1 * inv;
                         scale = -inv;
                     } else {
                         t = fma(lam_dn - y_in * sj, inv, y_in * a);
@@ -685,7 +685,7 @@ cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launch
     const size_t smem = pipe_smem_bytes(p.W, p.R, p.NB);
     const void* fn = p.model == kLasso
                          ? (p.exact ? (const void*)k_scd_pipe<true, kLasso> : (const void*)k_scd_pipe<false, kLasso>)
-                     : p.model == kRidge
+                     : (p.model == kRidge || p.model == kElastic)
                          ? (p.exact ? (const void*)k_scd_pipe<true, kRidge> : (const void*)k_scd_pipe<false, kRidge>)
                          : (p.exact ? (const void*)k_scd_pipe<true, kSvm> : (const void*)k_scd_pipe<false, kSvm>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

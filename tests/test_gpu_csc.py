@@ -11,7 +11,7 @@ import pytest
 
 import oracle as O
 import synth
-from test_gpu_parity import KAPPA, TOL
+from test_gpu_parity import ETA, KAPPA, TOL
 
 pytestmark = pytest.mark.gpu
 
@@ -19,6 +19,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def D():
     import paper_1708_05357_b200 as D
+    O.set_eta(ETA)
     return D
 
 
@@ -40,7 +41,7 @@ def _random_state(model, n, lab, rng):
     return lab * rng.random(n) * (rng.random(n) < 0.5)
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 def test_csc_gaps_and_certificate_match_oracle(D, model):
     d, n = (3001, 2000) if model != O.SVM else (2999, 1500)
     csc, A, lab, lam = _problem(model, d, n, 0.01, seed=31 + model)
@@ -48,7 +49,7 @@ def test_csc_gaps_and_certificate_match_oracle(D, model):
     rng = np.random.default_rng(7)
     alpha = _random_state(model, n, lab, rng)
     B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
-    with D.create_csc(*csc, d, lab, lam, model) as P:
+    with D.create_csc(*csc, d, lab, lam, model, eta=ETA if model == O.ELASTIC else 0.0) as P:
         P.set_state(alpha)
         g_gpu, s_gpu = P.gaps(want_s=True)
         G, Ob, Db = P.duality_gap()
@@ -63,20 +64,21 @@ def test_csc_gaps_and_certificate_match_oracle(D, model):
     floor = KAPPA * An * np.linalg.norm(w)
     assert np.all(np.abs(s_gpu - s_or) <= TOL * np.maximum(np.abs(s_or), floor) + 1e-300)
     c = ((np.abs(alpha) + B) / d if model == O.LASSO else (np.abs(alpha) + 1) / n if model == O.SVM
-         else (np.abs(s_or) + lam * d * np.abs(alpha)) / (lam * d * d) + 1.0 / d)
+         else (np.abs(s_or) + lam * d * np.abs(alpha)) / (lam * d * d) + 1.0 / d if model == O.RIDGE
+         else np.abs(alpha) / d + np.abs(s_or) / (lam * ETA * d * d) + 1.0 / d)
     assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), KAPPA * c * An * np.linalg.norm(w)) + 1e-300)
     st, G_ref, O_ref, D_ref = O.duality_gap(model, A, alpha, lab, lam, B)
     assert abs(G - G_ref) <= 1e-9 * max(1.0, abs(G_ref))
     assert abs(Ob - O_ref) <= 1e-9 * max(1.0, abs(O_ref))
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 def test_csc_exact_epoch_matches_sequential_oracle(D, model):
     d, n, m = 2000, 1200, 700
     csc, A, lab, lam = _problem(model, d, n, 0.02, seed=41 + model)
     y = lab if model == O.SVM else None
     order = synth.permutation(np.arange(m), 3)
-    with D.create_csc(*csc, d, lab, lam, model, m=m, scd_exact=True) as P:
+    with D.create_csc(*csc, d, lab, lam, model, m=m, scd_exact=True, eta=ETA if model == O.ELASTIC else 0.0) as P:
         sel, _ = P.select(D.SEL_SEQUENTIAL, m=m, round=0)
         assert sel.tolist() == list(range(m))
         P.scd_epoch(perm=order)

@@ -17,10 +17,29 @@ TOL = 1e-6        # north_star: fp64-accumulated mode, relative
 KAPPA = 1e-3      # SURVEY 8(c) conditioning floor
 
 
+ETA = 0.5         # elastic-net mix of the ELASTIC cases (the oracle's or_set_eta, the GPU's cfg.eta)
+
+
+class _WithEta:
+    """The binding, with eta = ETA filled in for elastic-net problems."""
+
+    def __init__(self, mod):
+        self._m = mod
+
+    def __getattr__(self, k):
+        return getattr(self._m, k)
+
+    def create(self, A, lab, lam, model, **kw):
+        if model == O.ELASTIC:
+            kw.setdefault("eta", ETA)
+        return self._m.create(A, lab, lam, model, **kw)
+
+
 @pytest.fixture(scope="module")
 def D():
     import paper_1708_05357_b200 as D
-    return D
+    O.set_eta(ETA)
+    return _WithEta(D)
 
 
 def _lab(model, A, seed):
@@ -37,7 +56,7 @@ def _data(model, d, n, seed, ld=None):
 
 
 def _lam(model, n):
-    return 0.05 if model == O.LASSO else (0.02 if model == O.RIDGE else 1.0 / n)
+    return 0.05 if model == O.LASSO else (0.02 if model == O.RIDGE else (0.03 if model == O.ELASTIC else 1.0 / n))
 
 
 def _oracle_state(model, A, lab, lam, alpha, d):
@@ -63,6 +82,8 @@ def _check_gaps(model, A, lab, lam, d, alpha, s_gpu, g_gpu, w):
         c = (np.abs(alpha) + B) / d
     elif model == O.RIDGE:   # |d gap_i / d s_i| = |s_i + lambda d alpha_i| / (lambda d^2)
         c = (np.abs(s_or) + lam * d * np.abs(alpha)) / (lam * d * d) + 1.0 / d
+    elif model == O.ELASTIC:  # |alpha_i|/d + (|s_i|/d) / (lambda eta d)
+        c = np.abs(alpha) / d + np.abs(s_or) / (lam * ETA * d * d) + 1.0 / d
     else:
         c = (np.abs(alpha) + 1) / n
     gfloor = KAPPA * c * An * np.linalg.norm(w)
@@ -73,7 +94,8 @@ def _check_gaps(model, A, lab, lam, d, alpha, s_gpu, g_gpu, w):
 
 # ------------------------------------------------------------------------- gap pass (a2)
 @pytest.mark.parametrize("model,d,n", [(O.LASSO, 2000, 1000), (O.SVM, 500, 3000),
-                                       (O.LASSO, 9001, 300), (O.SVM, 10243, 257), (O.RIDGE, 3001, 700)])
+                                       (O.LASSO, 9001, 300), (O.SVM, 10243, 257), (O.RIDGE, 3001, 700),
+                                       (O.ELASTIC, 2003, 900)])
 def test_gaps_parity_at_injected_states(D, model, d, n):
     A, lab = _data(model, d, n, seed=100 + d)
     lam = _lam(model, n)
@@ -111,7 +133,7 @@ def test_gaps_subset_and_ragged_ld(D):
 
 
 def test_certificate_matches_oracle(D):
-    for model, d, n in [(O.LASSO, 600, 900), (O.SVM, 300, 1200), (O.RIDGE, 500, 700)]:
+    for model, d, n in [(O.LASSO, 600, 900), (O.SVM, 300, 1200), (O.RIDGE, 500, 700), (O.ELASTIC, 500, 800)]:
         A, lab = _data(model, d, n, seed=9)
         lam = _lam(model, n)
         st, alpha, g, ep = O.solve_scd(model, A, lab, lam, 1e-3, 50, seed=1)
@@ -199,6 +221,8 @@ def test_select_importance_matches_oracle(D, n, m):
     (O.LASSO, 1003, 400, 390, 20),
     (O.RIDGE, 2000, 600, 500, 0),
     (O.RIDGE, 30001, 300, 277, 32),
+    (O.ELASTIC, 2000, 600, 500, 0),
+    (O.ELASTIC, 30001, 300, 290, 32),
 ])
 def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
     """P12: same order, fp64 -> GPU epoch == oracle sequential epoch to ~1e-12."""
@@ -313,6 +337,7 @@ def test_zero_columns(D, kernel):
     (O.LASSO, O.SEL_GAP, 0), (O.SVM, O.SEL_GAP, 0),
     (O.LASSO, O.SEL_GAP, 300), (O.SVM, O.SEL_SEQUENTIAL, 260), (O.LASSO, O.SEL_UNIFORM, 250),
     (O.SVM, O.SEL_IMPORTANCE, 250), (O.RIDGE, O.SEL_GAP, 300), (O.RIDGE, O.SEL_GAP, 0),
+    (O.ELASTIC, O.SEL_GAP, 300),
 ])
 def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     d, n = (400, 1000) if model != O.SVM else (120, 1000)
@@ -336,6 +361,8 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     va = A64.T @ a
     O_np = (((va - lab) @ (va - lab)) / (2 * d) + lam * np.abs(a).sum() if model == O.LASSO
             else ((va - lab) @ (va - lab)) / (2 * d) + 0.5 * lam * (a @ a) if model == O.RIDGE
+            else ((va - lab) @ (va - lab)) / (2 * d) + lam * (0.5 * ETA * (a @ a) + (1 - ETA) * np.abs(a).sum())
+            if model == O.ELASTIC
             else -(lab @ a) / n + (va @ va) / (2 * lam * n * n))
     assert abs(O_np - Ob) <= 1e-10 * max(1, abs(Ob))
     np.testing.assert_allclose(v, va - lab if model != O.SVM else va, atol=1e-9)
@@ -389,7 +416,7 @@ def test_budget_smaller_than_data_swaps(D):
 
 
 # ------------------------------------------------------------------------- multi-GPU path (8(e))
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 @pytest.mark.parametrize("with_comm", [False, True])
 def test_aggregation_linesearch_matches_oracle(D, model, with_comm):
     """The CoCoA aggregation path (dv, exact gamma line search, apply) on one rank,
