@@ -5,7 +5,7 @@ One step = one DuHL round (Algorithm 2) over the configured workload:
 gap-memory top-m selection (Eq. 11) -> staging of A_[P] host -> HBM under the
 budget -> unit-A refresh of a rotating fraction of the gaps (zero-copy from
 pinned host memory) -> `passes` exact SCD passes over the working set (App. D;
-per-config default: C4 2, C3 4 -- they run in the shadow of the PCIe-bound
+per-config default: C4 2, C3 5 -- they run in the shadow of the PCIe-bound
 refresh) -> refresh of z_P.  The metric is BASELINE.json's: coordinate updates/s (plus
 time-to-certified-gap and gap-pass GB/s as extra keys).
 
@@ -40,8 +40,8 @@ CONFIGS = {
     # passes: SCD passes per round (tuned per scheme): the epoch runs in the shadow of the
     # PCIe-bound unit-A refresh, so extra passes are free until they outlast it (measured sweep:
     # C4 time-to-eps 5.5 / 4.8 / 6.2 s at 1 / 2 / 4 passes; C3 14.2 / 8.1 / 6.6 s at 1 / 2 / 3, and
-    # with adaptive-only certificates (tools/c3_sweep.py) 6.1 / 5.6 s at 3 / 4)
-    "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=4,
+    # with adaptive-only certificates (tools/c3_sweep.py) 6.1 / 5.2 / 4.9 / 5.2 s at 3 / 4 / 5 / 6)
+    "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=5,
                label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "
                      "(32.1 GB pinned host), HBM budget 25% (8.03 GB), m=50176, lambda=0.07 lambda_max"),
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None, passes=2,

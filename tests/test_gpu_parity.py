@@ -245,6 +245,25 @@ def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
 
 
 @pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("m", [1, 3, 33])
+def test_scd_epoch_tiny_working_sets(D, kernel, m):
+    """Edge cases of the block pipeline: one coordinate, one partial block, W + 1."""
+    d, n = 1500, 60
+    A, lab = _data(O.SVM, d, n, seed=500 + m)
+    lam = _lam(O.SVM, n)
+    order = synth.permutation(np.arange(m), 2)
+    with D.create(A, lab, lam, O.SVM, m=m, scd_kernel=kernel, scd_block=32) as P:
+        P.select(D.SEL_SEQUENTIAL, m=m, round=0)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = np.zeros(d)
+    O.scd_pass(O.SVM, A, O.col_norms(A), lab, lam, alpha, vt, order)
+    assert np.abs(a_gpu - alpha).max() <= 1e-11 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("model,d,n,m", [(O.LASSO, 40000, 400, 390), (O.SVM, 200704 // 8, 300, 290),
                                          (O.RIDGE, 40000, 400, 390)])
 def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
