@@ -119,6 +119,8 @@ typedef struct {
     double z_sum;             /* sum_i z_i after the round: the (time-delayed) gap estimate of the gap memory */
     double gamma;             /* aggregation weight applied this round (1 without line search) */
     double time_s;            /* wall seconds since duhl_solve entry (duhl_round: duration of the round) */
+    double rho;               /* rho_{t,P} (Eq. 6) on the gap memory at selection time:
+                                 (mean of z over P) / (mean of z over this rank's columns); 1 if z = 0 */
 } duhl_round_record;
 
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,

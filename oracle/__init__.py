@@ -62,6 +62,8 @@ def lib():
         L.or_coord_gaps.argtypes = [C.c_int, _P, _I, _I, _I, _P, _P, _P, C.c_double, C.c_double,
                                     _P, _I, _P, _P]
         L.or_select_topm.argtypes = [_P, _I, _I, _P]
+        L.or_rho.restype = C.c_double
+        L.or_rho.argtypes = [_P, _I, _P, _I]
         L.or_select_policy.restype = _I
         L.or_select_policy.argtypes = [C.c_int, _I, _I, _I, C.c_uint64, _P, _P]
         L.or_make_perm.argtypes = [_P, _I, C.c_uint64, _I, _I, _P]
@@ -168,6 +170,13 @@ def select_topm(z, m):
     out = np.empty(m, dtype=np.int64)
     lib().or_select_topm(_p(z), z.size, m, _p(out))
     return out
+
+
+def rho(z, P):
+    """rho_{t,P} (Eq. 6) of the index set P on the gap vector z."""
+    z = _f64(z)
+    PP = np.ascontiguousarray(P, dtype=np.int64)
+    return lib().or_rho(_p(z), z.size, _p(PP), PP.size)
 
 
 def select_policy(policy, n, m, rnd, seed, z=None):

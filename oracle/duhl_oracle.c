@@ -181,6 +181,17 @@ void or_select_topm(const double* z, i64 n, i64 m, i64* P_out) {
     free(idx);
 }
 
+/* rho_{t,P} of Eq. 6 (Sec. 3.2): (1/m sum_{j in P} gap_j) / (1/n sum_j gap_j),
+ * written out on the gap vector z it is given (DuHL's gap memory, reading R21).
+ * Returns 1 when sum_j z_j = 0 (every block is equally (un)important). */
+double or_rho(const double* z, i64 n, const i64* P, i64 m) {
+    double sp = 0.0, sa = 0.0;
+    for (i64 t = 0; t < m; ++t) sp += z[P[t]];
+    for (i64 j = 0; j < n; ++j) sa += z[j];
+    if (!(sa > 0.0) || m <= 0) return 1.0;
+    return (sp / (double)m) / (sa / (double)n);
+}
+
 /* Baseline selection policies (P:401 sequential blocks [Yu 2012]; P:434 uniform;
  * P:403-404 importance sampling [Zhao 2015]):
  *   sequential: block k = round mod ceil(n/m), indices [k m, min((k+1) m, n))

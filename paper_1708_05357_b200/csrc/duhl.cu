@@ -91,6 +91,7 @@ struct duhl_ctx {
     // refreshed only when an ABI call needs them
     int* d_stamp = nullptr;         // [n] id of the select that last took column j
     unsigned long long* d_rsel = nullptr;  // [2] swaps, nnz over P
+    double* d_rho = nullptr;               // [2] sum of z over P, over all columns (round record rho)
     int sel_id = 0;
     int64_t m_cur = 0;              // |P|
     bool P_host_valid = true;
@@ -552,7 +553,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
-                        ctx->d_stamp, ctx->d_rsel};
+                        ctx->d_stamp, ctx->d_rsel, ctx->d_rho};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -833,7 +834,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
                                                                       // C4 step 85 vs 90 ms with 16)
     choose_scd_shape(ctx);
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
-        !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)))
+        !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)))
         return bail(DUHL_E_NOMEM);
     if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
     if (!dmal((void**)&ctx->d_red, scd_red_bytes(ctx)) ||
@@ -1321,6 +1322,12 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     TRY(finalize_staging(ctx));
     ctx->overlap = ctx->write_value != nullptr && kref == 0;
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
+    {   // rho_{t,P} (Eq. 6) on the gap memory the selection used
+        CK(cudaMemsetAsync(ctx->d_rho, 0, 2 * sizeof(double), ctx->st));
+        CK(launch_gather_f64(ctx->d_z, ctx->d_P, ctx->m_cur, ctx->d_gap_out, ctx->st, &ctx->launches));
+        CK(launch_sum(ctx->d_gap_out, ctx->m_cur, ctx->d_rho, ctx->st, &ctx->launches));
+        CK(launch_sum(ctx->d_z, n, ctx->d_rho + 1, ctx->st, &ctx->launches));
+    }
     auto tstaged = now();
     std::vector<int64_t> idx(kref);
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
@@ -1368,8 +1375,9 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     CK(cudaMemsetAsync(ctx->d_sums + 6, 0, sizeof(double), ctx->st));
     CK(launch_sum(ctx->d_z, n, ctx->d_sums + 6, ctx->st, &ctx->launches));
     TRY(allreduce(ctx, ctx->d_sums + 6, 1));
-    double zs = 0.0;
+    double zs = 0.0, rs[2] = {0.0, 0.0};
     CK(cudaMemcpyAsync(&zs, ctx->d_sums + 6, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaMemcpyAsync(rs, ctx->d_rho, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     TRY(check_flag(ctx, "duhl_round"));
     harvest(ctx);
@@ -1388,6 +1396,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->z_sum = zs;
         rec->gamma = gamma;
         rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        rec->rho = (rs[1] > 0.0 && m > 0) ? (rs[0] / (double)m) / (rs[1] / (double)n) : 1.0;
     }
     return DUHL_OK;
 }

@@ -434,6 +434,29 @@ def test_budget_smaller_than_data_swaps(D):
     assert c["h2d_bytes"] >= sw.sum() * d * 4
 
 
+
+@pytest.mark.parametrize("model,policy", [(O.LASSO, O.SEL_GAP), (O.SVM, O.SEL_GAP),
+                                          (O.LASSO, O.SEL_SEQUENTIAL)])
+def test_round_record_rho(D, model, policy):
+    """duhl_round_record.rho = Eq. 6 on the gap memory at selection time (reading R21):
+    the oracle's or_rho of the set the oracle selects from the same z, round by round, on a
+    budgeted problem (the z the selection saw is read back with duhl_get_state)."""
+    d, n, m = (300, 1500, 300) if model == O.LASSO else (120, 1500, 300)
+    A, lab = _data(model, d, n, seed=91)
+    lam = _lam(model, n)
+    with D.create(A, lab, lam, model, hbm_budget_bytes=400 * d * 4, m=m, refresh_fraction=0.1,
+                  cert_every=1 << 30, seed=4) as P:
+        seen = []
+        for t in range(12):
+            z = P.get_state()[2]
+            rec = P.round(t, passes=1, policy=policy)
+            sel = O.select_policy(policy, n, m, t, 4, z=z)
+            want = O.rho(z, sel)
+            assert abs(rec.rho - want) <= 1e-12 * max(1.0, want), (t, rec.rho, want)
+            seen.append(rec.rho)
+    if policy == O.SEL_GAP:   # top-m maximises Eq. 6 (Eq. 9): never below the average block
+        assert min(seen) >= 1.0 - 1e-12 and max(seen) > 1.0
+
 # ------------------------------------------------------------------------- multi-GPU path (8(e))
 @pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 @pytest.mark.parametrize("with_comm", [False, True])

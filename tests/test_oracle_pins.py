@@ -552,3 +552,22 @@ def test_duhl_converges_to_certified_optimum(model):
     assert max(obs) - min(obs) <= 2e-6
     # gap-based selection needs fewer rounds than the sequential scheme (P:433-435 shape)
     assert res[O.SEL_GAP][0] < res[O.SEL_SEQUENTIAL][0]
+
+
+def test_rho_definition_pins():
+    """rho_{t,P} (Eq. 6): the whole index set gives 1; a uniform gap vector gives 1 for
+    every P; averaged over all m-subsets rho is exactly 1 (each j lies in C(n-1,m-1) of the
+    C(n,m) subsets); top-m maximises it (Eq. 9) and the complement of top-m minimises it."""
+    z = np.array([4.0, 0.0, 1.0, 3.0, 2.0])
+    assert O.rho(z, np.arange(5)) == 1.0
+    assert abs(O.rho(z, [0]) - 4.0 / 2.0) < 1e-15          # worked: (4/1) / (10/5)
+    assert abs(O.rho(z, [0, 3]) - 3.5 / 2.0) < 1e-15
+    assert O.rho(np.full(7, 0.3), [2, 5]) == 1.0
+    assert O.rho(np.zeros(4), [1]) == 1.0                    # zero gap: no block is preferred
+    rng = np.random.default_rng(11)
+    for n, m in [(6, 2), (7, 3), (5, 5)]:
+        g = rng.random(n)
+        vals = [O.rho(g, list(c)) for c in itertools.combinations(range(n), m)]
+        assert abs(np.mean(vals) - 1.0) < 1e-13
+        assert abs(max(vals) - O.rho(g, O.select_topm(g, m))) < 1e-15
+        assert max(vals) >= 1.0 >= min(vals)
