@@ -192,6 +192,19 @@ class Sparse:
         return np.where(np.diff(self.cp) > 0, out, 0.0)
 
 
+def rho_mean(trace):
+    """Mean rho_{t,P} (Eq. 6) over a solve's rounds (on the gap memory, DESIGN R21)."""
+    return float(np.mean([t.rho for t in trace])) if trace else None
+
+
+def swaps_trend(trace):
+    """Mean swaps per round over the first and the last quarter of a solve (Fig. 4b)."""
+    if not trace:
+        return None
+    q = max(1, len(trace) // 4)
+    return [float(np.mean([t.swaps for t in trace[:q]])), float(np.mean([t.swaps for t in trace[-q:]]))]
+
+
 def create(D, A, lab, lam, model, **kw):
     """duhl_create (dense) or duhl_create_csc (sparse) with the bench's options."""
     if isinstance(A, Sparse):
@@ -305,7 +318,8 @@ def run_duhl(args, cfg, rank, world, local):
     m = cfg["m"] // world
     common = dict(hbm_budget_bytes=budget, m=m, device=local, refresh_fraction=args.refresh,
                   seed=seed, borrow_host=True, n_global=n, col_offset=lo,
-                  linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas)
+                  linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas,
+                  unit_a_host_threads=args.unit_a_host, unit_a_host_share=args.host_share)
     uid = None
     if world > 1:  # NCCL group for the dv allreduce: id from rank 0, broadcast by torch.distributed
         import torch.distributed as dist
@@ -361,6 +375,7 @@ def run_duhl(args, cfg, rank, world, local):
     k2 = P.kernel_stats(0)
     ko_ms = (k2[1] - k1[0][1]) / max(1, k2[0] - k1[0][0])
     ko_bytes = (k2[2] - k1[0][2]) / max(1, k2[0] - k1[0][0])
+    hua = P.unit_a_host()
     P.close()
     updates = args.steps * m * args.passes * world
     value = updates / elapsed
@@ -419,6 +434,8 @@ def run_duhl(args, cfg, rank, world, local):
                "time_to_eps_s": med["t_solve"], "time_to_eps_runs_s": [q["t_solve"] for q in runs],
                "eps": args.eps, "certified_gap": r["gap"], "create_plus_solve_s": wall,
                "converged": all(q["r"]["status"] == 0 for q in runs), "rounds": r["rounds"],
+               "rho_mean": rho_mean(r["trace"]),
+               "swaps_per_round_first_last": swaps_trend(r["trace"]),
                "create_s": med["t_create"],
                "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
                        "from host buffers (pin in place, norms, z at alpha=0 over PCIe) + duhl_solve to the "
@@ -448,6 +465,7 @@ def run_duhl(args, cfg, rank, world, local):
             P3.close()
             baselines[pol_name] = {"time_s": wall, "rounds": r["rounds"], "converged": r["status"] == 0,
                                    "certified_gap": g3, "h2d_GB": c3["h2d_bytes"] / 1e9,
+                                   "rho_mean": rho_mean(r["trace"]),
                                    "time_to_eps_s": wall if r["status"] == 0 else None}
 
     # ---------------- CPU oracle on a bounded sample of the same workload
@@ -472,7 +490,10 @@ def run_duhl(args, cfg, rank, world, local):
                               if cfg.get("sparse") else
                               "inputs larger than L2 (working set 8 GB >> 126 MB L2)" if budget
                               else "working set may be L2-resident (small config)"),
-                       "parallelism": f"cocoa{world}"},
+                       "parallelism": f"cocoa{world}",
+                       "unit_a_host": ({"threads": args.unit_a_host,
+                                        "share": hua[1], "cols_total": hua[0]}
+                                       if args.unit_a_host > 0 else None)},
             "roofline": roofline,
             "pcie": pcie,
             "roofline_scd_kernel_only": {"bound": "hbm", "kernel": scd_name, "unit": "GB/s",
@@ -519,6 +540,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unit-a-ctas", type=int, default=0,
                     help="CTAs of the unit-A refresh beside the epoch (0 auto, -1 off)")
+    ap.add_argument("--unit-a-host", type=int, default=0,
+                    help="host threads that take part of the unit-A refresh (paper's CPU unit A; 0 off)")
+    ap.add_argument("--host-share", type=float, default=-1.0,
+                    help="their share of the refresh's non-resident columns (<0: balanced per round)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     cfg = CONFIGS[args.config]

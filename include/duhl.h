@@ -108,6 +108,12 @@ typedef struct {
                                  sequential order (App. D), up to summation order. */
     double eta;               /* DUHL_ELASTIC_NET only: g_i = lambda (eta/2 alpha_i^2 + (1-eta)|alpha_i|)
                                  (P:796-800), 0 < eta < 1; eta = 0 is DUHL_LASSO, eta = 1 DUHL_RIDGE */
+    int unit_a_host_threads;  /* unit A on the host (Alg. 2 l.7-10 as the paper's CPU unit):
+                                 host threads that compute a_i^T v~ for part of the refresh's non-resident
+                                 columns from the pinned store (DRAM, not PCIe); the device finishes their
+                                 gaps.  0 = off (the whole refresh runs on the GPU) */
+    double unit_a_host_share; /* share of the refresh's non-resident columns given to those threads, in
+                                 [0, 1]; < 0 = balanced each round from the measured host and PCIe rates */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -252,6 +258,11 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
  * columns, 4 d4 per column), SCD coordinate updates.  Any may be NULL. */
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes,
                               int64_t* zc_bytes, int64_t* updates);
+
+/* Host-thread unit A (cfg.unit_a_host_threads): columns whose refresh dots the host
+ * threads computed (all rounds so far) and the current share of the refresh's
+ * non-resident columns they take.  0 / 0 when off.  Either pointer may be NULL. */
+duhl_status duhl_get_unit_a_host(duhl_ctx* ctx, int64_t* cols, double* share);
 
 /* Launch shape of the dense exact SCD epoch chosen at create (cfg.scd_kernel, shared
  * memory): *kernel 1 = k_scd_gram (warp-specialised), 2 = k_scd_pipe (control CTA);

@@ -16,7 +16,8 @@ STATUS = {0: "OK", 2: "E_INVALID", 3: "E_IO", 4: "E_NUMERIC", 5: "E_BOUND", 6: "
 FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_create_csc", "duhl_destroy", "duhl_gaps", "duhl_select",
              "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
              "duhl_set_state", "duhl_comm_unique_id", "duhl_comm_init", "duhl_get_stream",
-             "duhl_get_kernel_stats", "duhl_get_counters", "duhl_get_scd_shape", "duhl_last_error"]
+             "duhl_get_kernel_stats", "duhl_get_counters", "duhl_get_scd_shape", "duhl_get_unit_a_host",
+             "duhl_last_error"]
 KIND_SCD, KIND_GAP, KIND_TOPM, KIND_STAGE = 0, 1, 2, 3
 
 
@@ -41,7 +42,8 @@ class Config(C.Structure):
                 ("cert_every", C.c_int64), ("seed", C.c_uint64), ("borrow_host", C.c_int),
                 ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
                 ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int),
-                ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int), ("eta", C.c_double)]
+                ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int), ("eta", C.c_double),
+                ("unit_a_host_threads", C.c_int), ("unit_a_host_share", C.c_double)]
 
 
 class RoundRecord(C.Structure):
@@ -86,6 +88,7 @@ def lib():
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
         L.duhl_get_counters.argtypes = [_P, _P, _P, _P, _P]
+        L.duhl_get_unit_a_host.argtypes = [_P, _P, _P]
         L.duhl_get_scd_shape.argtypes = [_P, _P, _P, _P, _P]
         L.duhl_last_error.argtypes = [_P]
         L.duhl_last_error.restype = C.c_char_p
@@ -214,6 +217,12 @@ class Problem:
         self._check(lib().duhl_get_stream(self._h, C.byref(s)))
         return s.value
 
+    def unit_a_host(self):
+        """duhl_get_unit_a_host: (host-refreshed columns so far, current host share)."""
+        c, sh = C.c_int64(), C.c_double()
+        self._check(lib().duhl_get_unit_a_host(self._h, C.byref(c), C.byref(sh)))
+        return c.value, sh.value
+
     def scd_shape(self):
         """(kernel name, W, G, R) of the exact SCD epoch chosen at create."""
         k, w, g, r = C.c_int(), C.c_int(), C.c_int(), C.c_int()
@@ -229,7 +238,8 @@ class Problem:
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
            cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
-           linesearch=False, unit_a_ctas=0, scd_kernel=0, eta=0.0):
+           linesearch=False, unit_a_ctas=0, scd_kernel=0, eta=0.0, unit_a_host_threads=0,
+           unit_a_host_share=-1.0):
     """duhl_create.  eta: the elastic-net mix (model ELASTIC_NET only).  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -244,7 +254,9 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          borrow_host=int(bool(borrow_host)), cert_adaptive=int(bool(cert_adaptive)),
                          profile=int(bool(profile)), scd_exact=int(bool(scd_exact)),
                          n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)),
-                         unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel, eta=float(eta))
+                         unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel, eta=float(eta),
+                         unit_a_host_threads=int(unit_a_host_threads),
+                         unit_a_host_share=float(unit_a_host_share))
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

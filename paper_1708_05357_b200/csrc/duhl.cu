@@ -21,6 +21,7 @@
 
 #include "../../include/duhl.h"
 #include "device.cuh"
+#include "unit_a_host.h"
 #include "kernels.h"
 
 using namespace duhl;
@@ -127,6 +128,16 @@ struct duhl_ctx {
     int64_t st_launch[5] = {0, 0, 0, 0, 0};
     double st_ms[5] = {0, 0, 0, 0, 0}, st_bytes[5] = {0, 0, 0, 0, 0};
     double* d_s_acc2 = nullptr;  // partial-dot accumulator of the concurrent refresh pass
+    // ---- unit A on host threads (cfg.unit_a_host_threads): a_i^T v~ for part of the refresh
+    HostUnitA* hua = nullptr;
+    double* h_vt = nullptr;        // pinned [d4]: round-start v~ for the host threads
+    double* h_hs = nullptr;        // pinned [n]: their dots
+    int64_t* h_hcols = nullptr;    // pinned [n]: their columns
+    double* d_hs = nullptr;        // [n] dots uploaded for k_gap_finalize
+    int64_t* d_hcols = nullptr;    // [n]
+    cudaEvent_t ev_hvt = nullptr, ev_g0 = nullptr, ev_g1 = nullptr;  // v~ on the host; GPU refresh span
+    double hua_share = 0.5;        // current share of the non-resident refresh columns on the host
+    int64_t hua_cols = 0;          // host-refreshed columns (all rounds)
     // ---- staging overlapped with the SCD epoch
     typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
     WriteValue32 write_value = nullptr;  // cuStreamWriteValue32 via cudaGetDriverEntryPoint
@@ -553,10 +564,16 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
-                        ctx->d_stamp, ctx->d_rsel, ctx->d_rho};
+                        ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
+    hua_destroy(ctx->hua);
+    ctx->hua = nullptr;
+    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hcols})
+        if (p) cudaFreeHost(p);
+    for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1})
+        if (e) cudaEventDestroy(e);
     if (ctx->registered) cudaHostUnregister(ctx->h_store);
     if (ctx->own_store && ctx->h_store) cudaFreeHost(ctx->h_store);
     for (auto& t : ctx->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -631,6 +648,7 @@ void duhl_default_config(duhl_config* cfg) {
     cfg->seed = 170805357ull;
     cfg->cert_adaptive = 1;
     cfg->scd_exact = 1;
+    cfg->unit_a_host_share = -1.0;
 }
 
 const char* duhl_last_error(const duhl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -837,6 +855,20 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)))
         return bail(DUHL_E_NOMEM);
     if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
+    if (!ctx->csc && ctx->cfg.unit_a_host_threads > 0) {  // unit A on host threads (duhl.h)
+        if (ctx->cfg.unit_a_host_threads > 1024 || ctx->cfg.unit_a_host_share > 1.0) return bail(DUHL_E_INVALID);
+        if (!dmal((void**)&ctx->d_hs, n * sizeof(double)) || !dmal((void**)&ctx->d_hcols, n * sizeof(int64_t)) ||
+            cudaMemset(ctx->d_hs, 0, n * sizeof(double)) != cudaSuccess)
+            return bail(DUHL_E_NOMEM);
+        if (cudaHostAlloc((void**)&ctx->h_vt, ctx->d4 * sizeof(double), 0) != cudaSuccess ||
+            cudaHostAlloc((void**)&ctx->h_hs, n * sizeof(double), 0) != cudaSuccess ||
+            cudaHostAlloc((void**)&ctx->h_hcols, n * sizeof(int64_t), 0) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_hvt, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreate(&ctx->ev_g0) != cudaSuccess || cudaEventCreate(&ctx->ev_g1) != cudaSuccess)
+            return bail(DUHL_E_NOMEM);
+        if (ctx->cfg.unit_a_host_share >= 0.0) ctx->hua_share = ctx->cfg.unit_a_host_share;
+        ctx->hua = hua_create(ctx->cfg.unit_a_host_threads, ctx->dev);
+    }
     if (!dmal((void**)&ctx->d_red, scd_red_bytes(ctx)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
@@ -1330,6 +1362,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     }
     auto tstaged = now();
     std::vector<int64_t> idx(kref);
+    int64_t kg = kref, kh = 0, nonres = 0;  // refresh columns on the GPU / host threads; non-resident
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
     if (agg) {  // round-start state for the aggregation: v0 and alpha_P
         CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
@@ -1345,14 +1378,39 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
             idx[q] = (ctx->cursor + q) % n;
             host_cols += ctx->col_slot[idx[q]] < 0;
         }
-        ctx->zc_bytes += host_cols * ctx->ld_dev * (int64_t)sizeof(float);
         ctx->cursor = (ctx->cursor + kref) % n;
-        CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kref * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        nonres = host_cols;
+        // the host threads take the last kh of the non-resident columns; the GPU the rest
+        kh = ctx->hua ? (int64_t)std::llround(ctx->hua_share * (double)host_cols) : 0;
+        if (kh > 0) {
+            int64_t g = 0, hcount = 0, seen = 0;
+            for (int64_t q = 0; q < kref; ++q) {
+                const bool nr = ctx->col_slot[idx[q]] < 0;
+                if (nr && seen++ >= host_cols - kh) ctx->h_hcols[hcount++] = idx[q];
+                else idx[g++] = idx[q];
+            }
+            kg = g;
+        }
+        ctx->zc_bytes += (host_cols - kh) * ctx->ld_dev * (int64_t)sizeof(float);
+        if (kg > 0)
+            CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kg * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         if (!agg)
             CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
-        TRY(refresh_launch(ctx, kref));
-        if (ctx->unit_a_ctas <= 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));
+        if (kh > 0) {  // v~ snapshot to the host threads; their columns to the device for the finalize
+            CK(cudaMemcpyAsync(ctx->h_vt, ctx->d_vsnap, ctx->d4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaEventRecord(ctx->ev_hvt, ctx->st));
+            CK(cudaMemcpyAsync(ctx->d_hcols, ctx->h_hcols, kh * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+            hua_post(ctx->hua, ctx->h_store, ctx->ld_host, ctx->d4, ctx->h_hcols, kh, ctx->h_vt, wscale(ctx),
+                     ctx->ev_hvt, ctx->h_hs);
+            CK(cudaEventRecord(ctx->ev_g0, ctx->st));
+        }
+        TRY(refresh_launch(ctx, kg));
+        if (kh > 0) {
+            if (kg > 0) CK(cudaEventRecord(ctx->ev_g1, ctx->rst));
+            else CK(cudaEventRecord(ctx->ev_g1, ctx->st));
+        }
+        if (ctx->unit_a_ctas <= 0 && kg > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));
     }
     auto tlaunch = now();
     TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
@@ -1365,7 +1423,17 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         CK(cudaStreamSynchronize(ctx->rst));
         tref = now();
     }
-    if (kref > 0 && ctx->unit_a_ctas > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));  // join unit A
+    if (kg > 0 && ctx->unit_a_ctas > 0) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_ref, 0));  // join unit A
+    double host_s = 0.0;
+    if (kh > 0) {  // join the host threads: their dots -> gap_i at the round-start alpha of columns
+                   // outside P (columns of P are refreshed after the epoch below, R9)
+        host_s = hua_wait(ctx->hua);
+        CK(cudaMemcpyAsync(ctx->d_hs, ctx->h_hs, kh * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+        GapParams hp = gap_params(ctx, ctx->d_hcols, kh);
+        hp.s_acc = ctx->d_hs;
+        CK(launch_gap_finalize(hp, ctx->st, &ctx->launches));
+        ctx->hua_cols += kh;
+    }
     double gamma = 1.0;
     if (agg) TRY(aggregate(ctx, &gamma));                                   // l.11 across ranks
     const int64_t m = ctx->m_cur;                                          // z_P at alpha^(t+1) (R9)
@@ -1397,6 +1465,18 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->gamma = gamma;
         rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         rec->rho = (rs[1] > 0.0 && m > 0) ? (rs[0] / (double)m) / (rs[1] / (double)n) : 1.0;
+    }
+    if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0) {  // balance: both units end their share together
+        float gms = 0.0f;
+        const int64_t kgn = nonres - kh;  // non-resident columns the GPU read over PCIe
+        if (host_s > 0.0 && kgn > 0 && cudaEventElapsedTime(&gms, ctx->ev_g0, ctx->ev_g1) == cudaSuccess &&
+            gms > 0.0f) {
+            const double rh = (double)kh / host_s, rg = (double)kgn / (1e-3 * gms);
+            const double target = rh / (rh + rg);
+            ctx->hua_share = std::min(0.95, std::max(0.05, 0.5 * ctx->hua_share + 0.5 * target));
+        } else if (kgn == 0) {
+            ctx->hua_share = std::max(0.05, ctx->hua_share - 0.05);
+        }
     }
     return DUHL_OK;
 }
@@ -1553,6 +1633,13 @@ duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_byt
     if (h2d_bytes) *h2d_bytes = ctx->h2d_bytes;
     if (zc_bytes) *zc_bytes = ctx->zc_bytes;
     if (updates) *updates = ctx->updates;
+    return DUHL_OK;
+}
+
+duhl_status duhl_get_unit_a_host(duhl_ctx* ctx, int64_t* cols, double* share) {
+    if (!ctx) return DUHL_E_INVALID;
+    if (cols) *cols = ctx->hua ? ctx->hua_cols : 0;
+    if (share) *share = ctx->hua ? ctx->hua_share : 0.0;
     return DUHL_OK;
 }
 

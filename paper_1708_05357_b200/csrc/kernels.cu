@@ -193,6 +193,13 @@ cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, 
     return cudaGetLastError();
 }
 
+cudaError_t launch_gap_finalize(const GapParams& p, cudaStream_t st, int64_t* launches) {
+    if (p.k <= 0) return cudaSuccess;
+    k_gap_finalize<<<(unsigned)cdiv(p.k, kGapThreads), kGapThreads, 0, st>>>(p);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // =====================================================================================
 // Column norms ||a_i||^2: warp per column, fp64 accumulation.
 // =====================================================================================

@@ -93,6 +93,8 @@ size_t scd_smem_bytes(int W, int R, int NB);
 
 cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, int64_t* launches,
                             int max_ctas = 0);
+// k_gap_finalize alone: gap_i from the complete dots p.s_acc[t] of columns p.cols[t] (s_acc is zeroed).
+cudaError_t launch_gap_finalize(const GapParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t launch_col_norms(const ColSrc& src, int64_t d4, int64_t n, double* norms,
                              cudaStream_t st, int64_t* launches);
 // work: device scratch of launch_topm_work_bytes() (multi-CTA form for large n; nullptr = one CTA)

@@ -1,0 +1,81 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+C4 (hinge-SVM dual, 200,704 x 40,000 fp32 = 32.1 GB in pinned host memory) and C3 (Lasso,
+40,000 x 200,704) under the 8.03 GB HBM budget, m, passes, refresh and SCD mode of the bench
+(fast mode: fp32 Gram products inside a warp).  After a few DuHL rounds (Alg. 2)
+the device state is checked against the oracle on what it can compute at this size:
+
+* v = A alpha (- b): the oracle's matvec over the columns alpha touches (exact definition);
+* a2 gap pass: gap_i and s_i = a_i^T w of sampled columns (ragged tail included) against the
+  oracle's coord_gaps at the same alpha (Eq. 4, P:852 / P:867), north_star tolerance;
+* a7 certificate: the total duality gap and the objective against the oracle's;
+* properties that hold at any size: SVM box y_i alpha_i in [0, 1], z >= 0, rho >= 1 for the
+  gap-selected sets (Eq. 9), swaps(first round) = m, the objective decreases from alpha = 0.
+"""
+import gc
+
+import numpy as np
+import pytest
+
+import bench
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def D():
+    import paper_1708_05357_b200 as D
+    return D
+
+
+@pytest.mark.parametrize("name", ["c4", "c3"])
+def test_full_size_rounds_against_oracle(D, name):
+    cfg = bench.CONFIGS[name]
+    d, n, model = cfg["d"], cfg["n"], cfg["model"]
+    A, lab = bench.make_data(cfg, 170805357 + 3)
+    lam = bench.lam_of(cfg, A, lab)
+    col_bytes = ((d + 3) // 4) * 16
+    budget = int(cfg["budget_frac"] * n * col_bytes)
+    m = cfg["m"]
+    with D.create(A, lab, lam, model, hbm_budget_bytes=budget, m=m, refresh_fraction=0.10,
+                  seed=170805357 + 3, borrow_host=True, cert_every=1 << 40, scd_exact=False) as P:
+        recs = [P.round(t, passes=cfg["passes"]) for t in range(3)]
+        a, v, z = P.get_state()
+        rng = np.random.default_rng(5)
+        idx = np.unique(np.concatenate([rng.choice(n, 62, replace=False), [0, n - 1]]))
+        g_gpu, s_gpu = P.gaps(idx, want_s=True)
+        G, Ob, Db = P.duality_gap()
+    assert recs[0].swaps == m and all(r.rho >= 1.0 - 1e-12 for r in recs)
+    assert np.all(z >= 0) and np.all(np.isfinite(a))
+    if model == O.SVM:
+        ya = lab * a
+        assert ya.min() >= 0.0 and ya.max() <= 1.0
+    assert np.count_nonzero(a) > 0
+    # v = A alpha (- b): the oracle's matvec (skips alpha_i = 0)
+    v_or = O.matvec(A, a)
+    if model == O.LASSO:
+        v_or = v_or - lab
+    scale = np.abs(A[np.flatnonzero(a)]).max() * np.abs(a).sum()
+    assert np.max(np.abs(v - v_or)) <= 1e-9 * scale
+    # sampled gap pass
+    w = O.primal_dual_w(model, v_or + (lab if model == O.LASSO else 0.0),
+                        lab if model == O.LASSO else None, n, lam)
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    st, s_or, g_or = O.coord_gaps(model, A, a, lab if model == O.SVM else None, w, lam, B, idx=idx)
+    An = np.linalg.norm(A[idx].astype(np.float64), axis=1)
+    floor = 1e-3 * An * np.linalg.norm(w)
+    assert np.all(np.abs(s_gpu - s_or) <= TOL * np.maximum(np.abs(s_or), floor))
+    c = (np.abs(a[idx]) + B) / d if model == O.LASSO else (np.abs(a[idx]) + 1) / n
+    assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), 1e-3 * c * An * np.linalg.norm(w)))
+    # certificate (a7) against the oracle's full pass
+    st, G_or, O_or, D_or = O.duality_gap(model, A, a, lab, lam, B)
+    assert st == O.OK
+    assert abs(Ob - O_or) <= 1e-9 * max(1.0, abs(O_or))
+    assert abs(G - G_or) <= TOL * max(G_or, 1e-12)
+    O0 = 0.0 if model == O.SVM else float(lab @ lab) / (2 * d)   # objective at alpha = 0
+    assert Ob < O0
+    del A
+    gc.collect()

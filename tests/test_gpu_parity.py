@@ -457,6 +457,55 @@ def test_round_record_rho(D, model, policy):
     if policy == O.SEL_GAP:   # top-m maximises Eq. 6 (Eq. 9): never below the average block
         assert min(seen) >= 1.0 - 1e-12 and max(seen) > 1.0
 
+
+@pytest.mark.parametrize("model,share", [(O.LASSO, 1.0), (O.SVM, 0.5), (O.RIDGE, -1.0), (O.ELASTIC, 1.0)])
+def test_unit_a_host_threads_refresh(D, model, share):
+    """Host-thread unit A (cfg.unit_a_host_threads, NEXT-1): the refreshed columns outside the
+    working set carry the oracle's gap at the round-start state (reading R8), whichever unit
+    computed their dot; P is the oracle's top-m of the gap memory the round started from."""
+    d, n, m = (400, 1000, 250) if model != O.SVM else (120, 1000, 250)
+    A, lab = _data(model, d, n, seed=41)
+    lam = _lam(model, n)
+    kref = 300
+    with D.create(A, lab, lam, model, hbm_budget_bytes=300 * d * 4, m=m, refresh_fraction=kref / n,
+                  cert_every=1 << 30, seed=8, unit_a_host_threads=3, unit_a_host_share=share) as P:
+        for t in range(6):
+            a0, _, z0 = P.get_state()
+            P.round(t, passes=1)
+            a1, _, z1 = P.get_state()
+            sel = set(O.select_topm(z0, m).tolist())
+            R = [(t * kref + q) % n for q in range(kref)]
+            out = np.array([i for i in R if i not in sel])
+            assert np.array_equal(a1[out], a0[out])
+            g_or = _oracle_state(model, A, lab, lam, a0, d)[2]
+            tol = 1e-9 * max(1e-300, np.abs(g_or).max())
+            assert np.all(np.abs(z1[out] - g_or[out]) <= 1e-7 * np.abs(g_or[out]) + tol), t
+        cols, sh = P.unit_a_host()
+    assert cols > 0 and 0.0 < sh <= 1.0
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_unit_a_host_threads_solve(D, model):
+    """Alg. 2 with unit A shared by host threads (balanced share) reaches a certified gap and
+    the oracle's optimum (objective within 1e-4, the north_star bound)."""
+    d, n = (400, 1500) if model == O.LASSO else (120, 1500)
+    A, lab = _data(model, d, n, seed=55)
+    lam = _lam(model, n)
+    eps = 1e-6
+    ref = O.duhl_solve(model, A, lab, lam, m=300, passes=2, refresh_count=150, eps=eps,
+                       max_rounds=3000, cert_every=1, seed=5)
+    assert ref["status"] == O.OK
+    with D.create(A, lab, lam, model, hbm_budget_bytes=350 * d * 4, m=300, refresh_fraction=0.1,
+                  cert_every=1, seed=5, unit_a_host_threads=4) as P:
+        r = P.solve(eps, 3000, passes=2)
+        g, Ob, _ = P.duality_gap()
+        cols, _ = P.unit_a_host()
+    assert r["status"] == 0 and r["gap"] <= eps and g <= eps and cols > 0
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    _, _, O_ref, _ = O.duality_gap(model, A, ref["alpha"], lab, lam, B)
+    assert abs(Ob - O_ref) <= 1e-4 * abs(O_ref)
+    assert abs(r["rounds"] - ref["rounds"]) <= max(3, 0.3 * ref["rounds"])
+
 # ------------------------------------------------------------------------- multi-GPU path (8(e))
 @pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
 @pytest.mark.parametrize("with_comm", [False, True])
