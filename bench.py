@@ -41,7 +41,10 @@ CONFIGS = {
     # PCIe-bound unit-A refresh, so extra passes are free until they outlast it (measured sweep:
     # C4 time-to-eps 5.5 / 4.8 / 6.2 s at 1 / 2 / 4 passes; C3 14.2 / 8.1 / 6.6 s at 1 / 2 / 3, and
     # with adaptive-only certificates (tools/c3_sweep.py) 6.1 / 5.2 / 4.9 / 5.2 s at 3 / 4 / 5 / 6)
+    # with host threads in unit A (--unit-a-host) the refresh no longer hides the epoch: C3 4.3 s at
+    # 2 and 3 passes, 5.1 s at 4 (passes_host)
     "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=5,
+               passes_host=3,
                label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "
                      "(32.1 GB pinned host), HBM budget 25% (8.03 GB), m=50176, lambda=0.07 lambda_max"),
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None, passes=2,
@@ -208,7 +211,7 @@ def swaps_trend(trace):
 def create(D, A, lab, lam, model, **kw):
     """duhl_create (dense) or duhl_create_csc (sparse) with the bench's options."""
     if isinstance(A, Sparse):
-        for k in ("hbm_budget_bytes", "borrow_host", "unit_a_ctas"):
+        for k in ("hbm_budget_bytes", "borrow_host", "unit_a_ctas", "unit_a_host_threads", "unit_a_host_share"):
             kw.pop(k, None)
         return D.create_csc(A.cp, A.rows, A.vals, A.d, lab, lam, model, **kw)
     return D.create(A, lab, lam, model, **kw)
@@ -540,15 +543,20 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unit-a-ctas", type=int, default=0,
                     help="CTAs of the unit-A refresh beside the epoch (0 auto, -1 off)")
-    ap.add_argument("--unit-a-host", type=int, default=0,
-                    help="host threads that take part of the unit-A refresh (paper's CPU unit A; 0 off)")
+    ap.add_argument("--unit-a-host", type=int, default=-1,
+                    help="host threads that take part of the unit-A refresh (the paper's CPU unit A, P:332); "
+                         "0 off (GPU-only refresh); -1 auto: min(14, cores - 2) on the out-of-core dense configs")
     ap.add_argument("--host-share", type=float, default=-1.0,
                     help="their share of the refresh's non-resident columns (<0: balanced per round)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     cfg = CONFIGS[args.config]
+    if args.unit_a_host < 0:  # out-of-core dense configs only: the refresh reads host columns there
+        cores = os.cpu_count() or 1
+        args.unit_a_host = (min(14, cores - 2) if cfg["budget_frac"] > 0 and not cfg.get("sparse")
+                            and cores >= 4 else 0)
     if args.passes <= 0:
-        args.passes = cfg.get("passes", 1)
+        args.passes = cfg.get("passes_host", cfg.get("passes", 1)) if args.unit_a_host > 0 else cfg.get("passes", 1)
     if args.impl == "reference":  # the CPU oracle: rank 0 alone, no process group needed
         run_reference(args, cfg, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return

@@ -4,6 +4,7 @@
 #include <immintrin.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
@@ -32,6 +33,30 @@ __attribute__((target("avx2,fma"))) double dot_avx2(const float* a, const double
     return r;
 }
 
+// Four columns against one v: each 8-element slice of v is loaded once (a zmm) and used by
+// four columns, so v (1.6 MB at C4) streams from L2 a quarter as often; 8 FMA chains.
+__attribute__((target("avx512f"))) void dot4_avx512(const float* const* a, const double* v, int64_t n,
+                                                    double* out) {
+    __m512d s[4][2];
+    for (int c = 0; c < 4; ++c) s[c][0] = s[c][1] = _mm512_setzero_pd();
+    int64_t i = 0;
+    for (; i + 16 <= n; i += 16) {
+        const __m512d v0 = _mm512_loadu_pd(v + i), v1 = _mm512_loadu_pd(v + i + 8);
+#pragma GCC unroll 4
+        for (int c = 0; c < 4; ++c) {
+            const __m512 f = _mm512_loadu_ps(a[c] + i);
+            s[c][0] = _mm512_fmadd_pd(_mm512_cvtps_pd(_mm512_castps512_ps256(f)), v0, s[c][0]);
+            s[c][1] = _mm512_fmadd_pd(
+                _mm512_cvtps_pd(_mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castps_pd(f), 1))), v1, s[c][1]);
+        }
+    }
+    for (int c = 0; c < 4; ++c) {
+        double r = _mm512_reduce_add_pd(_mm512_add_pd(s[c][0], s[c][1]));
+        for (int64_t k = i; k < n; ++k) r += (double)a[c][k] * v[k];
+        out[c] = r;
+    }
+}
+
 double dot_scalar(const float* a, const double* v, int64_t n) {
     double r0 = 0, r1 = 0;
     int64_t i = 0;
@@ -47,7 +72,7 @@ double dot_scalar(const float* a, const double* v, int64_t n) {
 
 struct HostUnitA {
     int dev = 0;
-    bool avx2 = false;
+    bool avx2 = false, avx512 = false;
     std::vector<std::thread> workers;
     std::mutex mu;
     std::condition_variable cv_job, cv_done;
@@ -82,10 +107,20 @@ struct HostUnitA {
             const int64_t now = std::chrono::steady_clock::now().time_since_epoch().count();
             t_ready_ns.compare_exchange_strong(expect, now);
             for (;;) {
-                const int64_t t = next.fetch_add(1, std::memory_order_relaxed);
+                const int64_t t = next.fetch_add(4, std::memory_order_relaxed);
                 if (t >= k) break;
-                const float* a = store + cols[t] * ld;
-                s_out[t] = scale * (avx2 ? dot_avx2(a, vt, d4) : dot_scalar(a, vt, d4));
+                if (avx512 && t + 4 <= k) {
+                    const float* a4[4];
+                    double r[4];
+                    for (int c = 0; c < 4; ++c) a4[c] = store + cols[t + c] * ld;
+                    dot4_avx512(a4, vt, d4, r);
+                    for (int c = 0; c < 4; ++c) s_out[t + c] = scale * r[c];
+                    continue;
+                }
+                for (int64_t u = t; u < t + 4 && u < k; ++u) {
+                    const float* a = store + cols[u] * ld;
+                    s_out[u] = scale * (avx2 ? dot_avx2(a, vt, d4) : dot_scalar(a, vt, d4));
+                }
             }
             std::lock_guard<std::mutex> lk(mu);
             if (--active == 0) {
@@ -102,6 +137,7 @@ HostUnitA* hua_create(int threads, int dev) {
     h->dev = dev;
     __builtin_cpu_init();
     h->avx2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+    h->avx512 = __builtin_cpu_supports("avx512f") && std::getenv("DUHL_HOST_NO_AVX512") == nullptr;
     for (int i = 0; i < threads; ++i) h->workers.emplace_back([h] { h->run_worker(); });
     return h;
 }
