@@ -109,9 +109,9 @@ typedef struct {
     double eta;               /* DUHL_ELASTIC_NET only: g_i = lambda (eta/2 alpha_i^2 + (1-eta)|alpha_i|)
                                  (P:796-800), 0 < eta < 1; eta = 0 is DUHL_LASSO, eta = 1 DUHL_RIDGE */
     int unit_a_host_threads;  /* unit A on the host (Alg. 2 l.7-10 as the paper's CPU unit):
-                                 host threads that compute a_i^T v~ for part of the refresh's non-resident
-                                 columns from the pinned store (DRAM, not PCIe); the device finishes their
-                                 gaps.  0 = off (the whole refresh runs on the GPU) */
+                                 host threads that compute a_i^T v~ for part of the refresh's (and of every
+                                 certificate's) non-resident columns from the pinned store (DRAM, not PCIe);
+                                 the device finishes their gaps.  0 = off (the GPU reads them over PCIe) */
     double unit_a_host_share; /* share of the refresh's non-resident columns given to those threads, in
                                  [0, 1]; < 0 = balanced each round from the measured host and PCIe rates */
 } duhl_config;

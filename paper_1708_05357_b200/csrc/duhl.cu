@@ -135,8 +135,10 @@ struct duhl_ctx {
     int64_t* h_hcols = nullptr;    // pinned [n]: their columns
     double* d_hs = nullptr;        // [n] dots uploaded for k_gap_finalize
     int64_t* d_hcols = nullptr;    // [n]
-    cudaEvent_t ev_hvt = nullptr, ev_g0 = nullptr, ev_g1 = nullptr;  // v~ on the host; GPU refresh span
-    double hua_share = 0.5;        // current share of the non-resident refresh columns on the host
+    cudaEvent_t ev_hvt = nullptr, ev_g0 = nullptr, ev_g1 = nullptr, ev_c1 = nullptr;  // v~ on the host;
+                                   // GPU refresh span; end of the round's staging copies
+    double cert_share = 0.4;       // share of a certificate's non-resident columns on the host
+    double hua_share = 0.7;        // current share of the non-resident refresh columns on the host
     int64_t hua_cols = 0;          // host-refreshed columns (all rounds)
     // ---- staging overlapped with the SCD epoch
     typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
@@ -572,7 +574,7 @@ static void free_all(duhl_ctx* ctx) {
     ctx->hua = nullptr;
     for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hcols})
         if (p) cudaFreeHost(p);
-    for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1})
+    for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1, ctx->ev_c1})
         if (e) cudaEventDestroy(e);
     if (ctx->registered) cudaHostUnregister(ctx->h_store);
     if (ctx->own_store && ctx->h_store) cudaFreeHost(ctx->h_store);
@@ -864,7 +866,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
             cudaHostAlloc((void**)&ctx->h_hs, n * sizeof(double), 0) != cudaSuccess ||
             cudaHostAlloc((void**)&ctx->h_hcols, n * sizeof(int64_t), 0) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_hvt, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreate(&ctx->ev_g0) != cudaSuccess || cudaEventCreate(&ctx->ev_g1) != cudaSuccess)
+            cudaEventCreate(&ctx->ev_g0) != cudaSuccess || cudaEventCreate(&ctx->ev_g1) != cudaSuccess ||
+            cudaEventCreate(&ctx->ev_c1) != cudaSuccess)
             return bail(DUHL_E_NOMEM);
         if (ctx->cfg.unit_a_host_share >= 0.0) ctx->hua_share = ctx->cfg.unit_a_host_share;
         ctx->hua = hua_create(ctx->cfg.unit_a_host_threads, ctx->dev);
@@ -1181,8 +1184,47 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
     CK(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), ctx->st));
     int64_t resident = 0;
     for (int64_t s = 0; s < ctx->S; ++s) resident += ctx->slot_col[s] >= 0;
-    ctx->zc_bytes += (ctx->n - resident) * ctx->ld_dev * (int64_t)sizeof(float);
-    TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+    const int64_t nonres = ctx->csc ? 0 : ctx->n - resident;
+    const int64_t kh = ctx->hua ? (int64_t)std::llround(ctx->cert_share * (double)nonres) : 0;
+    ctx->zc_bytes += (nonres - kh) * ctx->ld_dev * (int64_t)sizeof(float);
+    if (kh > 0) {  // host threads take the last kh non-resident columns (unit A on the host, duhl.h)
+        std::vector<int64_t> gcols;
+        gcols.reserve(ctx->n - kh);
+        int64_t seen = 0, hc = 0;
+        for (int64_t i = 0; i < ctx->n; ++i) {
+            if (ctx->col_slot[i] < 0 && seen++ >= nonres - kh) ctx->h_hcols[hc++] = i;
+            else gcols.push_back(i);
+        }
+        const int64_t kg = (int64_t)gcols.size();
+        CK(cudaMemcpyAsync(ctx->h_vt, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaEventRecord(ctx->ev_hvt, ctx->st));
+        hua_post(ctx->hua, ctx->h_store, ctx->ld_host, ctx->d4, ctx->h_hcols, kh, ctx->h_vt, wscale(ctx),
+                 ctx->ev_hvt, ctx->h_hs);
+        CK(cudaMemcpyAsync(ctx->d_hcols, ctx->h_hcols, kh * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        if (kg > 0) {
+            CK(cudaMemcpyAsync(ctx->d_cols, gcols.data(), kg * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+            CK(cudaEventRecord(ctx->ev_g0, ctx->st));
+            TRY(run_gaps(ctx, ctx->d_cols, kg, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+            CK(cudaEventRecord(ctx->ev_g1, ctx->st));
+        }
+        const double host_s = hua_wait(ctx->hua);
+        CK(cudaMemcpyAsync(ctx->d_hs, ctx->h_hs, kh * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+        GapParams hp = gap_params(ctx, ctx->d_hcols, kh);
+        hp.s_acc = ctx->d_hs;
+        hp.sums = ctx->d_sums;
+        hp.z = nullptr;
+        CK(launch_gap_finalize(hp, ctx->st, &ctx->launches));
+        CK(cudaStreamSynchronize(ctx->st));  // gcols is pageable and local
+        float gms = 0.0f;  // balance the next certificate: both units end together
+        if (kg > 0 && host_s > 0.0 && cudaEventElapsedTime(&gms, ctx->ev_g0, ctx->ev_g1) == cudaSuccess &&
+            gms > 0.0f && nonres > kh) {
+            const double rh = (double)kh / host_s, rg = (double)(nonres - kh) / (1e-3 * gms);
+            ctx->cert_share = std::min(0.95, std::max(0.05, 0.5 * ctx->cert_share + 0.5 * rh / (rh + rg)));
+        }
+        ctx->hua_cols += kh;
+    } else {
+        TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+    }
     TRY(allreduce(ctx, ctx->d_sums, 3));           // per-column sums over the shards
     TRY(allreduce(ctx, ctx->d_sums + 3, 1, ncclMax));
     CK(launch_vec_sums(ctx->d_vt, ctx->model != DUHL_SVM_DUAL ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
@@ -1352,7 +1394,8 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     // shared by the staging copies and the zero-copy refresh reads, so both run
     // first, side by side, and the epoch follows at full HBM rate.
     TRY(finalize_staging(ctx));
-    ctx->overlap = ctx->write_value != nullptr && kref == 0;
+    static const bool host_overlap = std::getenv("DUHL_HOST_OVERLAP") != nullptr;  // experiment
+    ctx->overlap = ctx->write_value != nullptr && (kref == 0 || (host_overlap && ctx->hua && ctx->hua_share >= 0.5));
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
     {   // rho_{t,P} (Eq. 6) on the gap memory the selection used
         CK(cudaMemsetAsync(ctx->d_rho, 0, 2 * sizeof(double), ctx->st));
@@ -1414,6 +1457,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     }
     auto tlaunch = now();
     TRY(scd_passes(ctx, passes, ctx->cfg.seed, t));                        // l.6, l.11
+    if (kh > 0) CK(cudaEventRecord(ctx->ev_c1, ctx->cst));  // the staging copies are all enqueued
     TRY(finalize_staging(ctx));                                            // staged columns -> table
     auto tscd = now();
     auto tref = tscd;
@@ -1466,16 +1510,18 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         rec->rho = (rs[1] > 0.0 && m > 0) ? (rs[0] / (double)m) / (rs[1] / (double)n) : 1.0;
     }
-    if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0) {  // balance: both units end their share together
-        float gms = 0.0f;
+    if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0) {
+        // balance: the host's columns take as long as what PCIe carries this round (staging
+        // copies + the GPU's zero-copy columns): kh = (swaps + nonres) r_h / (r_h + r_p)
+        float gms = 0.0f, cms = 0.0f;
         const int64_t kgn = nonres - kh;  // non-resident columns the GPU read over PCIe
-        if (host_s > 0.0 && kgn > 0 && cudaEventElapsedTime(&gms, ctx->ev_g0, ctx->ev_g1) == cudaSuccess &&
-            gms > 0.0f) {
-            const double rh = (double)kh / host_s, rg = (double)kgn / (1e-3 * gms);
-            const double target = rh / (rh + rg);
-            ctx->hua_share = std::min(0.95, std::max(0.05, 0.5 * ctx->hua_share + 0.5 * target));
-        } else if (kgn == 0) {
-            ctx->hua_share = std::max(0.05, ctx->hua_share - 0.05);
+        if (kgn == 0 || cudaEventElapsedTime(&gms, ctx->ev_g0, ctx->ev_g1) != cudaSuccess) gms = 0.0f;
+        if (swaps == 0 || cudaEventElapsedTime(&cms, ctx->ev_g0, ctx->ev_c1) != cudaSuccess) cms = 0.0f;
+        const double tp = 1e-3 * std::max(gms, cms);
+        if (host_s > 0.0 && tp > 0.0 && swaps + kgn > 0) {
+            const double rh = (double)kh / host_s, rp = (double)(swaps + kgn) / tp;
+            const double target = std::min(1.0, (double)(swaps + nonres) * rh / (rh + rp) / (double)nonres);
+            ctx->hua_share = std::min(1.0, std::max(0.05, 0.75 * ctx->hua_share + 0.25 * target));
         }
     }
     return DUHL_OK;

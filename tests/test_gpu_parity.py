@@ -480,6 +480,11 @@ def test_unit_a_host_threads_refresh(D, model, share):
             g_or = _oracle_state(model, A, lab, lam, a0, d)[2]
             tol = 1e-9 * max(1e-300, np.abs(g_or).max())
             assert np.all(np.abs(z1[out] - g_or[out]) <= 1e-7 * np.abs(g_or[out]) + tol), t
+        G, Ob, Db = P.duality_gap()   # certificate split between the host threads and the GPU
+        B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+        st, G_or, O_or, D_or = O.duality_gap(model, A, a1, lab, lam, B)
+        assert abs(G - G_or) <= 1e-7 * G_or and abs(Ob - O_or) <= 1e-9 * max(1.0, abs(O_or))
+        assert abs(Db - D_or) <= 1e-9 * max(1.0, abs(D_or))
         cols, sh = P.unit_a_host()
     assert cols > 0 and 0.0 < sh <= 1.0
 
