@@ -1064,6 +1064,10 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.G = ctx->G;
     p.NB = ctx->NB;
     p.exact = ctx->cfg.scd_exact;
+    {   // DUHL_GRAM_TC=0/1 overrides the default (tensor-core Gram tiles where they apply)
+        static const int tc = std::getenv("DUHL_GRAM_TC") ? std::atoi(std::getenv("DUHL_GRAM_TC")) : 1;
+        p.gram_tc = tc;
+    }
     p.lam_q = ridge_ld(ctx);
     p.lam_l1 = ctx->model == DUHL_ELASTIC_NET ? ctx->lambda * (double)ctx->d * (1.0 - ctx->cfg.eta) : 0.0;
     p.red = ctx->d_red;

@@ -59,6 +59,7 @@ struct ScdParams {
     const double *order_a, *order_inv, *order_y;  // [L] alpha at pass start, 1/||a||^2 (-1: zero column), y
     const unsigned* progress;     // last landed staging copy, written by the copy stream; or nullptr
     int* err;                     // set (bit 0: staging wait, bit 1: grid barrier) on a wait timeout
+    int gram_tc;                  // pipe kernel, fast mode, W = 32: Gram tiles on the tensor cores (3xTF32; default 1)
 };
 
 // Sparse matrix, compressed sparse columns, resident in HBM:

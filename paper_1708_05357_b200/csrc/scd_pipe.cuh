@@ -206,6 +206,91 @@ __device__ __forceinline__ void gc_warp(const float* A1, const float* A0, int Rs
     }
 }
 
+// Tensor-core form of gc_warp for W = 32 in fast mode (p.gram_tc): the warp's 32 x 64 block
+// M = A1^T [A1 | A0] over its rows [4 r4lo, 4 r4hi) as 2 x 8 tiles of mma.sync m16n8k8 TF32
+// (M index j = column of A1, N index k = column of [A1 | A0], K index = row).  Each fp32
+// operand x is split x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and every tile takes
+// hi*lo + lo*hi + hi*hi (3xTF32: the product error of plain TF32 would be ~1e-3, the split
+// keeps it near fp32's), accumulated in fp32 like the FFMA2 path.  Fragments are single
+// 32-bit shared loads at (column g, row t) -- lane = 4 g + t, the column stride Rs = 4 x odd,
+// so the 32 lanes of a load hit 32 distinct banks.  The two all-upper tiles of G (j < 16,
+// 16 <= k < 32) are skipped; results go to the same `part` slots as gc_warp_part's
+// (slot ((j/4) 8 + k/8) 32 + (j%4) + 4 (k%8)) for gc_sum<8>.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void gc_warp_tc32(const float* __restrict__ A1, const float* __restrict__ A0, int Rs,
+                                             int r4lo, int r4hi, int lane, float* __restrict__ part) {
+    const int g = lane >> 2, t = lane & 3;
+    float acc[2][8][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+    // lane's base addresses: A rows j = 16 mt + g (+ 8), B columns k = 8 nt + g
+    const uint32_t a_base = smem_addr(A1 + (size_t)g * Rs + t);
+    const uint32_t b1_base = smem_addr(A1 + (size_t)g * Rs + t);  // k < 32: columns of A1
+    const uint32_t b0_base = smem_addr(A0 + (size_t)g * Rs + t);  // k >= 32: columns of A0
+    const uint32_t cs = 4u * (uint32_t)Rs;                         // one column, bytes
+    const int r_lo = 4 * r4lo, r_hi = 4 * r4hi;
+    for (int r = r_lo; r < r_hi; r += 8) {
+        const bool full = r + 8 <= r_hi;   // else rows r .. r + 3 only (4-row tail)
+        const uint32_t ro = 4u * (uint32_t)r;
+        uint32_t ah[2][4], al[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t o = a_base + ro + (uint32_t)(16 * mt) * cs;
+            const float x0 = lds_f32(o), x1 = lds_f32(o + 8u * cs);
+            const float x2 = full ? lds_f32(o + 16u) : 0.f, x3 = full ? lds_f32(o + 8u * cs + 16u) : 0.f;
+            tf32_split(x0, ah[mt][0], al[mt][0]);
+            tf32_split(x1, ah[mt][1], al[mt][1]);
+            tf32_split(x2, ah[mt][2], al[mt][2]);
+            tf32_split(x3, ah[mt][3], al[mt][3]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            const uint32_t o = (nt < 4 ? b1_base + (uint32_t)(8 * nt) * cs : b0_base + (uint32_t)(8 * (nt - 4)) * cs) + ro;
+            const float y0 = lds_f32(o), y1 = full ? lds_f32(o + 16u) : 0.f;
+            uint32_t bh0, bl0, bh1, bl1;
+            tf32_split(y0, bh0, bl0);
+            tf32_split(y1, bh1, bl1);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                if (mt == 0 && (nt == 2 || nt == 3)) continue;  // all-upper G tiles
+                mma_tf32(acc[mt][nt], al[mt], bh0, bh1);
+                mma_tf32(acc[mt][nt], ah[mt], bl0, bl1);
+                mma_tf32(acc[mt][nt], ah[mt], bh0, bh1);
+            }
+        }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            if (mt == 0 && (nt == 2 || nt == 3)) continue;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 16 * mt + g + 8 * (q >> 1), k = 8 * nt + 2 * t + (q & 1);
+                part[(((j >> 2) * 8 + (k >> 3)) << 5) + (j & 3) + 4 * (k & 7)] = acc[mt][nt][q];
+            }
+        }
+}
+
 // Cross-warp sum of the fast-mode partials (fp32 within the CTA, fp64 REDs across CTAs).
 template <int T>
 __device__ __forceinline__ void gc_sum(const float* __restrict__ part, int W, int tid, int nwarps,
@@ -477,7 +562,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                     const float* A1 = stage(b + 1);
                     const float* A0 = b >= 0 ? stage(b) : A1;  // block 0: C is never read
                     const RedOut out = out_of(b + 1);
-                    switch (W >> 2) {
+                    if (!EXACT && W == 32 && p.gram_tc) {
+                        gc_warp_tc32(A1, A0, Rs, w4lo, w4hi, lane, mypart);
+                    } else switch (W >> 2) {
                         case 1: gc_warp<EXACT, 1>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
                         case 2: gc_warp<EXACT, 2>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
                         case 3: gc_warp<EXACT, 3>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
