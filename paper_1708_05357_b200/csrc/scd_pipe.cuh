@@ -232,46 +232,64 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
                  : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void gc_warp_tc32(const float* __restrict__ A1, const float* __restrict__ A0, int Rs,
-                                             int r4lo, int r4hi, int lane, float* __restrict__ part) {
+// General W = 4 T (T <= 8): MT = ceil(W / 16) row tiles (rows j >= W load zeros), NT = T column
+// tiles of 8 over [A1 | A0] (lane g's column k = 8 nt + g is in A1 for k < W, else A0 at k - W,
+// so a tile may straddle the two blocks when W % 8 = 4).  A tile is skipped when every entry
+// of it is an upper-G entry (16 mt + 15 < 8 nt <= k < W).
+template <int T>
+__device__ __forceinline__ void gc_warp_tc(const float* __restrict__ A1, const float* __restrict__ A0, int Rs,
+                                           int r4lo, int r4hi, int lane, float* __restrict__ part) {
+    constexpr int W = 4 * T, MT = (W + 15) / 16, NT = T;
     const int g = lane >> 2, t = lane & 3;
-    float acc[2][8][4];
+    auto skip = [](int mt, int nt) { return 8 * nt + 7 < W && 16 * mt + 15 < 8 * nt; };
+    float acc[MT][NT][4];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
-    // lane's base addresses: A rows j = 16 mt + g (+ 8), B columns k = 8 nt + g
-    const uint32_t a_base = smem_addr(A1 + (size_t)g * Rs + t);
-    const uint32_t b1_base = smem_addr(A1 + (size_t)g * Rs + t);  // k < 32: columns of A1
-    const uint32_t b0_base = smem_addr(A0 + (size_t)g * Rs + t);  // k >= 32: columns of A0
-    const uint32_t cs = 4u * (uint32_t)Rs;                         // one column, bytes
+    uint32_t aa[MT][2];   // lane's A rows j = 16 mt + g (+ 8); valid flags
+    bool av[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = 16 * mt + g + 8 * h;
+            av[mt][h] = j < W;
+            aa[mt][h] = smem_addr(A1 + (size_t)(j < W ? j : 0) * Rs + t);
+        }
+    uint32_t ba[NT];      // lane's B column k = 8 nt + g of [A1 | A0]
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int k = 8 * nt + g;
+        ba[nt] = smem_addr((k < W ? A1 + (size_t)k * Rs : A0 + (size_t)(k - W) * Rs) + t);
+    }
     const int r_lo = 4 * r4lo, r_hi = 4 * r4hi;
     for (int r = r_lo; r < r_hi; r += 8) {
         const bool full = r + 8 <= r_hi;   // else rows r .. r + 3 only (4-row tail)
         const uint32_t ro = 4u * (uint32_t)r;
-        uint32_t ah[2][4], al[2][4];
+        uint32_t ah[MT][4], al[MT][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const uint32_t o = a_base + ro + (uint32_t)(16 * mt) * cs;
-            const float x0 = lds_f32(o), x1 = lds_f32(o + 8u * cs);
-            const float x2 = full ? lds_f32(o + 16u) : 0.f, x3 = full ? lds_f32(o + 8u * cs + 16u) : 0.f;
+        for (int mt = 0; mt < MT; ++mt) {
+            const float x0 = av[mt][0] ? lds_f32(aa[mt][0] + ro) : 0.f;
+            const float x1 = av[mt][1] ? lds_f32(aa[mt][1] + ro) : 0.f;
+            const float x2 = (av[mt][0] && full) ? lds_f32(aa[mt][0] + ro + 16u) : 0.f;
+            const float x3 = (av[mt][1] && full) ? lds_f32(aa[mt][1] + ro + 16u) : 0.f;
             tf32_split(x0, ah[mt][0], al[mt][0]);
             tf32_split(x1, ah[mt][1], al[mt][1]);
             tf32_split(x2, ah[mt][2], al[mt][2]);
             tf32_split(x3, ah[mt][3], al[mt][3]);
         }
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-            const uint32_t o = (nt < 4 ? b1_base + (uint32_t)(8 * nt) * cs : b0_base + (uint32_t)(8 * (nt - 4)) * cs) + ro;
-            const float y0 = lds_f32(o), y1 = full ? lds_f32(o + 16u) : 0.f;
+        for (int nt = 0; nt < NT; ++nt) {
+            const float y0 = lds_f32(ba[nt] + ro), y1 = full ? lds_f32(ba[nt] + ro + 16u) : 0.f;
             uint32_t bh0, bl0, bh1, bl1;
             tf32_split(y0, bh0, bl0);
             tf32_split(y1, bh1, bl1);
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                if (mt == 0 && (nt == 2 || nt == 3)) continue;  // all-upper G tiles
+            for (int mt = 0; mt < MT; ++mt) {
+                if (skip(mt, nt)) continue;
                 mma_tf32(acc[mt][nt], al[mt], bh0, bh1);
                 mma_tf32(acc[mt][nt], ah[mt], bl0, bl1);
                 mma_tf32(acc[mt][nt], ah[mt], bh0, bh1);
@@ -279,14 +297,14 @@ __device__ __forceinline__ void gc_warp_tc32(const float* __restrict__ A1, const
         }
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-            if (mt == 0 && (nt == 2 || nt == 3)) continue;
+        for (int nt = 0; nt < NT; ++nt) {
+            if (skip(mt, nt)) continue;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = 16 * mt + g + 8 * (q >> 1), k = 8 * nt + 2 * t + (q & 1);
-                part[(((j >> 2) * 8 + (k >> 3)) << 5) + (j & 3) + 4 * (k & 7)] = acc[mt][nt][q];
+                if (j < W) part[(((j >> 2) * T + (k >> 3)) << 5) + (j & 3) + 4 * (k & 7)] = acc[mt][nt][q];
             }
         }
 }
@@ -562,8 +580,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_scd_pipe(const __grid_const
                     const float* A1 = stage(b + 1);
                     const float* A0 = b >= 0 ? stage(b) : A1;  // block 0: C is never read
                     const RedOut out = out_of(b + 1);
-                    if (!EXACT && W == 32 && p.gram_tc) {
-                        gc_warp_tc32(A1, A0, Rs, w4lo, w4hi, lane, mypart);
+                    if (!EXACT && p.gram_tc && (W == 32 || (p.gram_tc > 1 && (W == 12 || W == 16 || W == 24)))) {
+                        switch (W >> 2) {
+                            case 3: gc_warp_tc<3>(A1, A0, Rs, w4lo, w4hi, lane, mypart); break;
+                            case 4: gc_warp_tc<4>(A1, A0, Rs, w4lo, w4hi, lane, mypart); break;
+                            case 6: gc_warp_tc<6>(A1, A0, Rs, w4lo, w4hi, lane, mypart); break;
+                            default: gc_warp_tc<8>(A1, A0, Rs, w4lo, w4hi, lane, mypart); break;
+                        }
                     } else switch (W >> 2) {
                         case 1: gc_warp<EXACT, 1>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;
                         case 2: gc_warp<EXACT, 2>(A1, A0, Rs, W, w4lo, w4hi, lane, mypart, out); break;

@@ -287,6 +287,28 @@ def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
     assert np.abs(v_gpu - vt).max() <= 1e-6 * max(1.0, np.abs(vt).max())
 
 
+@pytest.mark.parametrize("W", [12, 16, 24])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_scd_epoch_fast_mode_block_sizes(D, model, W):
+    """Fast mode of the pipelined kernel at W < 32 (FFMA2 Gram tiles; tensor-core tiles under
+    DUHL_GRAM_TC=2), long row slices and a ragged last block: within ~1e-6 of the oracle."""
+    d, n, m = 60001, 200, 190
+    A, lab = _data(model, d, n, seed=400 + W)
+    lam = _lam(model, n)
+    y = lab if model == O.SVM else None
+    order = synth.permutation(np.arange(m), 9)
+    with D.create(A, lab, lam, model, m=m, scd_kernel=2, scd_block=W, scd_exact=False) as P:
+        assert P.scd_shape()[:2] == ("k_scd_pipe", W)
+        P.select(D.SEL_SEQUENTIAL, m=m, round=0)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
+    O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
+    assert np.abs(a_gpu - alpha).max() <= 1e-6 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-6 * max(1.0, np.abs(vt).max())
+
+
 def test_scd_internal_permutation_generator_matches_oracle(D):
     """The device counter-based permutation equals the oracle's."""
     A, b = synth.lasso_dense(1000, 800, seed=3)
