@@ -206,7 +206,8 @@ __device__ __forceinline__ void gc_warp(const float* A1, const float* A0, int Rs
     }
 }
 
-// Tensor-core form of gc_warp for W = 32 in fast mode (p.gram_tc): the warp's 32 x 64 block
+// Tensor-core form of gc_warp in fast mode (p.gram_tc; default at W = 32, the case described
+// here -- gc_warp_tc<T> below generalises it to W = 4 T): the warp's 32 x 64 block
 // M = A1^T [A1 | A0] over its rows [4 r4lo, 4 r4hi) as 2 x 8 tiles of mma.sync m16n8k8 TF32
 // (M index j = column of A1, N index k = column of [A1 | A0], K index = row).  Each fp32
 // operand x is split x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and every tile takes
