@@ -77,12 +77,42 @@ def dist_init(n_gpus):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        # one process per GPU: N > 1 must be launched by torchrun (WORLD_SIZE = N); a mismatch
+        # would silently measure a different GPU count
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world}; launch N > 1 with "
+                         f"python -m torch.distributed.run --nproc-per-node {n_gpus} bench.py --gpus {n_gpus}")
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
+
+
+def numa_bind(local):
+    """Restrict this rank (and the threads it starts: data generation, the library's ingest
+    and host unit-A threads) to the CPUs of its GPU's NUMA node, so the pinned host shard is
+    first-touched there and unit A reads local DRAM.  Returns the node, or None when the
+    topology is not exposed (single-node boxes, containers)."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read().strip())
+        if node < 0:
+            return None
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return node
+    except Exception:
+        return None
 
 
 def barrier(world):
@@ -272,6 +302,48 @@ def oracle_sample(cfg, A, lab, lam, ncols, passes=1):
     return passes * ncols / t_scd, ncols * cfg["d"] * 4 / t_gap / 1e9, t_scd + t_gap
 
 
+def oracle_time_to_eps(cfg, A, lab, lam, eps, cap_s):
+    """The oracle as it stands (oracle/duhl_oracle.c, one thread): plain SCD over all n
+    coordinates, one permutation per epoch (or_solve_scd's order), certificate after every
+    epoch, until gap <= eps or the wall cap.  Unconverged: the gap reached, and an
+    extrapolated time to eps from the last epochs' linear rate (flagged)."""
+    import oracle as O
+    if isinstance(A, Sparse):
+        return None
+    n = A.shape[0]
+    model = cfg["model"]
+    B = O.lasso_B(lab, lam) if model == 0 else 0.0
+    norms = O.col_norms(A)
+    alpha = np.zeros(n)
+    vt = np.zeros(cfg["d"]) if model == 1 else -np.asarray(lab, dtype=np.float64).copy()
+    y = lab if model == 1 else None
+    allc = np.arange(n, dtype=np.int64)
+    t0 = time.perf_counter()
+    gaps, times, t_scd = [], [], 0.0
+    e = 0
+    while True:
+        t1 = time.perf_counter()
+        O.scd_pass(model, A, norms, y, lam, alpha, vt, O.make_perm(allc, 0, e, 0))
+        t_scd += time.perf_counter() - t1
+        st, g, _, _ = O.duality_gap(model, A, alpha, lab, lam, B)
+        e += 1
+        gaps.append(g)
+        times.append(time.perf_counter() - t0)
+        if g <= eps or times[-1] >= cap_s:
+            break
+    out = {"kind": "oracle", "cores": 1, "eps": eps, "epochs": e, "gap_reached": gaps[-1],
+           "wall_s": times[-1], "scd_s": t_scd, "converged": gaps[-1] <= eps,
+           "gaps": gaps[:20], "wall_cap_s": cap_s,
+           "note": "plain sequential SCD over all n columns (P:406 single-threaded CPU baseline), "
+                   "certificate after every epoch (its time included)"}
+    if not out["converged"] and len(gaps) >= 2 and 0 < gaps[-1] < gaps[-2]:
+        rate = gaps[-1] / gaps[-2]
+        more = np.log(eps / gaps[-1]) / np.log(rate)
+        out["extrapolated_time_to_eps_s"] = times[-1] + more * (times[-1] - times[-2])
+        out["extrapolated"] = True
+    return out
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
@@ -307,6 +379,7 @@ def run_duhl(args, cfg, rank, world, local):
     import torch
     import paper_1708_05357_b200 as D
     torch.cuda.set_device(local)
+    numa = numa_bind(local) if world > 1 else None   # the shard is first-touched on the GPU's node
     seed = 170805357 + 3
     d, n = cfg["d"], cfg["n"]
     # CoCoA-style sharding of the columns across ranks (one block per rank)
@@ -433,7 +506,7 @@ def run_duhl(args, cfg, rank, world, local):
         e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
                "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
                "zero_copy_bytes_per_step": int(c2["zc_bytes"] / rounds),
-               "d2h_bytes_per_step": int(m * 8 + 64),
+               "d2h_bytes_per_step": int(c2["d2h_bytes"] / rounds),
                "time_to_eps_s": med["t_solve"], "time_to_eps_runs_s": [q["t_solve"] for q in runs],
                "eps": args.eps, "certified_gap": r["gap"], "create_plus_solve_s": wall,
                "converged": all(q["r"]["status"] == 0 for q in runs), "rounds": r["rounds"],
@@ -449,9 +522,11 @@ def run_duhl(args, cfg, rank, world, local):
     # ---------------- baselines: same library, budget and kernels, batch selection
     # sequential blocks [Yu 2012] / uniform / importance sampling instead of gap top-m
     baselines = None
-    if args.baselines:
+    if not args.no_baselines and not cfg.get("sparse") and budget > 0:
         baselines = {}
-        for pol_name in ("sequential", "uniform", "importance"):
+        caps = {"uniform": args.baseline_rounds, "sequential": args.seq_rounds,
+                "importance": args.baseline_rounds}
+        for pol_name in (("sequential", "uniform", "importance") if args.baselines else ("uniform", "sequential")):
             pol = {"sequential": D.SEL_SEQUENTIAL, "uniform": D.SEL_UNIFORM, "importance": D.SEL_IMPORTANCE}[pol_name]
             t0 = time.perf_counter()
             cb = dict(common, refresh_fraction=0.0)  # batch baselines do not read z
@@ -459,7 +534,7 @@ def run_duhl(args, cfg, rank, world, local):
                           **cb)
             if uid is not None:
                 P3.comm_init(uid, world, rank)
-            rounds_cap = args.baseline_rounds
+            rounds_cap = caps[pol_name]
             t1 = time.perf_counter()
             r = P3.solve(args.eps, rounds_cap, passes=args.passes, policy=pol)
             wall = max_over_ranks(time.perf_counter() - t1, world)
@@ -468,8 +543,25 @@ def run_duhl(args, cfg, rank, world, local):
             P3.close()
             baselines[pol_name] = {"time_s": wall, "rounds": r["rounds"], "converged": r["status"] == 0,
                                    "certified_gap": g3, "h2d_GB": c3["h2d_bytes"] / 1e9,
-                                   "rho_mean": rho_mean(r["trace"]),
+                                   "rho_mean": rho_mean(r["trace"]), "rounds_cap": rounds_cap,
                                    "time_to_eps_s": wall if r["status"] == 0 else None}
+        baselines["note"] = ("same library, kernels, HBM budget and passes; selection by sequential blocks "
+                             "[Yu 2012] (P:401) / uniform (P:434) instead of the gap memory; no unit-A refresh; "
+                             "time_s = duhl_solve wall (data in pinned host memory), capped at rounds_cap rounds")
+
+    # ---------------- the oracle's plain SCD to eps (the paper's single-threaded CPU baseline,
+    # P:406): full at small configs, wall-capped at the large ones with the gap it reached, the
+    # GPU's time to that same certified gap, and an extrapolated oracle time to eps
+    oracle_tte = None
+    if not args.no_cpu and not args.no_oracle_tte and rank == 0 and world == 1:
+        oracle_tte = oracle_time_to_eps(cfg, A, lab, lam, args.eps, args.oracle_cap)
+        if oracle_tte and not oracle_tte["converged"] and oracle_tte["gap_reached"] is not None:
+            P4 = create(D, A, lab, lam, cfg["model"], cert_every=1, scd_exact=args.exact, **common)
+            t1 = time.perf_counter()
+            r4 = P4.solve(oracle_tte["gap_reached"], args.max_rounds, passes=args.passes, policy=policy)
+            oracle_tte["gpu_time_to_same_gap_s"] = time.perf_counter() - t1
+            oracle_tte["gpu_rounds_to_same_gap"] = r4["rounds"]
+            P4.close()
 
     # ---------------- CPU oracle on a bounded sample of the same workload
     cpu = None
@@ -483,9 +575,14 @@ def run_duhl(args, cfg, rank, world, local):
 
     line = {"metric": METRIC, "value": value, "unit": "coord updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.exact else "f32",
             "data": "synthetic",
             "config": {"workload": cfg["label"], "d": d, "n": n, "m": m, "passes": args.passes,
+                       "arithmetic": ("fp32 data; SCD Gram products fp64 (scd_exact)" if args.exact else
+                                      "fp32 data; SCD Gram tiles fp32 (FFMA2 / 3xTF32 mma) within a warp, "
+                                      "fp64 across warps; dots, v, alpha, gaps and certificates fp64"),
+                       "scd_exact": bool(args.exact), "numa_node": numa,
                        "policy": args.policy, "refresh_fraction": args.refresh,
                        "hbm_budget_GB": budget / 1e9, "lambda": lam,
                        "scd_kernel": {"name": scd_name, "W": scd_W, "G": scd_G, "R": scd_R},
@@ -511,6 +608,7 @@ def run_duhl(args, cfg, rank, world, local):
             "refresh_GBps": (by[4] / (ms[4] / 1e3) / 1e9) if ms[4] > 0 else None,
             "swaps_per_step": swaps / args.steps, "refreshed_per_step": refreshed / args.steps,
             "cpu_baseline": cpu, "e2e": e2e, "batch_baselines": baselines,
+            "oracle_time_to_eps": oracle_tte,
             "gpu_launches": c1["launches"] - c0["launches"],
             "clocks": clk.summary(),
             "setup_s": {"generate": t_gen, "create": t_create}}
@@ -538,8 +636,14 @@ def main():
     ap.add_argument("--exact", action="store_true", help="fp64 Gram products in the SCD kernel")
     ap.add_argument("--linesearch", action="store_true", help="gamma line search also at N=1")
     ap.add_argument("--baselines", action="store_true",
-                    help="also time the sequential / uniform / importance batch baselines to eps (capped rounds)")
-    ap.add_argument("--baseline-rounds", type=int, default=600)
+                    help="also time the importance-sampling baseline (uniform and sequential run by default)")
+    ap.add_argument("--baseline-rounds", type=int, default=200,
+                    help="round cap of the uniform / importance baselines")
+    ap.add_argument("--seq-rounds", type=int, default=40, help="round cap of the sequential baseline")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the default uniform / sequential baselines")
+    ap.add_argument("--no-oracle-tte", action="store_true", help="skip the oracle time-to-eps run")
+    ap.add_argument("--oracle-cap", type=float, default=60.0,
+                    help="wall cap (s) of the oracle's plain SCD run to eps (rank 0, N = 1)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--unit-a-ctas", type=int, default=0,
                     help="CTAs of the unit-A refresh beside the epoch (0 auto, -1 off)")
@@ -552,7 +656,8 @@ def main():
     args.warmup = max(args.warmup, 0)
     cfg = CONFIGS[args.config]
     if args.unit_a_host < 0:  # out-of-core dense configs only: the refresh reads host columns there
-        cores = os.cpu_count() or 1
+        # the host's cores are shared by the ranks of this node (one process per GPU)
+        cores = (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
         args.unit_a_host = (min(14, cores - 2) if cfg["budget_frac"] > 0 and not cfg.get("sparse")
                             and cores >= 4 else 0)
     if args.passes <= 0:

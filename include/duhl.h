@@ -223,20 +223,50 @@ duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes
 duhl_status duhl_get_state(duhl_ctx* ctx, double* alpha_out, double* v_out, double* z_out);
 
 /* Sets alpha (host float64[n]; SVM entries must satisfy y_i alpha_i in [0,1]),
- * recomputes the shared vector exactly from A and resets z to the exact gaps. */
+ * recomputes the shared vector exactly from A and resets z to the exact gaps.
+ * On a ctx joined to a communicator this is collective: every rank passes its
+ * shard's alpha and v = sum_k A_k alpha_k (- b) is reduced over the ranks. */
 duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha);
 
 /* Multi-GPU (CoCoA-style): one process per GPU, each
  * holding a contiguous column shard (cfg.n_global, cfg.col_offset).  The
  * shared vector v is replicated; each round every rank selects and solves on
  * its own shard from the common v, then dv is summed with ncclAllReduce over
- * NVLink and applied with weight gamma (cfg.linesearch).  Certificates sum the
+ * NVLink and applied with weight gamma chosen by the exact line search (forced
+ * on when nranks > 1: sigma' = 1 local steps summed with weight 1 can diverge).
+ * A communicator of one rank still runs ncclAllReduce.  duhl_set_state is
+ * collective on a joined ctx (v = sum over ranks of A_k alpha_k, minus b).  Certificates sum the
  * per-column terms over ranks.  duhl_comm_unique_id (one rank) returns the 128
  * byte NCCL id that the caller broadcasts; every rank then calls
  * duhl_comm_init on its ctx.  All later calls that reduce must be made by all
  * ranks in the same order.  Errors: DUHL_E_NCCL (libnccl.so.2 missing / NCCL failure). */
 duhl_status duhl_comm_unique_id(void* id_out);
 duhl_status duhl_comm_init(duhl_ctx* ctx, const void* id, int nranks, int rank);
+
+/* In-process group (SURVEY 8(e) "single process, one host thread per GPU"): the
+ * contexts of one process, each driven by its own host thread (on the same or on
+ * different GPUs), join a group instead of an NCCL communicator.  Collectives copy
+ * the buffer to host memory, wait for every rank (bounded: 600 s, then
+ * DUHL_E_NCCL), and every rank sums the buffers in rank order, so all ranks hold
+ * bit-identical results.  The same rules as duhl_comm_init apply (all ranks call
+ * every reducing function in the same order; aggregation takes the exact line
+ * search when nranks > 1).  The group must outlive its contexts; the caller owns it.
+ * Errors: DUHL_E_INVALID (nranks < 1, rank out of range, ctx already joined). */
+typedef struct duhl_group duhl_group;
+duhl_status duhl_group_create(int nranks, duhl_group** out);
+duhl_status duhl_group_destroy(duhl_group* g);
+duhl_status duhl_comm_init_group(duhl_ctx* ctx, duhl_group* g, int rank);
+
+/* The current working set P (Alg. 2 l.3, ascending local column indices) as chosen
+ * by the last duhl_select / duhl_round / duhl_solve round: *m_out = |P|; P_out
+ * (host int64[cap], may be NULL) receives it.  Errors: DUHL_E_INVALID (cap < |P|). */
+duhl_status duhl_get_working_set(duhl_ctx* ctx, int64_t* P_out, int64_t cap, int64_t* m_out);
+
+/* Per-round callback of duhl_solve (SURVEY 8(b) duhl_trace_cb): called on the calling
+ * thread after every round with that round's record (valid during the call only) and
+ * `user`; cb = NULL removes it.  It is called in addition to filling the trace array. */
+typedef void (*duhl_trace_cb)(const duhl_round_record* rec, void* user);
+duhl_status duhl_set_trace_callback(duhl_ctx* ctx, duhl_trace_cb cb, void* user);
 
 /* Device-side view for callers that time kernels on their own stream:
  * returns the CUDA stream (cudaStream_t) all compute of ctx is issued on. */
@@ -255,9 +285,10 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
 /* Counters since creation: kernel launches issued, bytes copied host->device
  * (copy engine: cold fill + swaps), bytes the gap kernels read from pinned host
  * memory over PCIe (zero-copy: unit-A refresh + certificates of non-resident
- * columns, 4 d4 per column), SCD coordinate updates.  Any may be NULL. */
+ * columns, 4 d4 per column), SCD coordinate updates, bytes read back device->host
+ * (status flags, reductions, P, state, the host unit A's v snapshot).  Any may be NULL. */
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes,
-                              int64_t* zc_bytes, int64_t* updates);
+                              int64_t* zc_bytes, int64_t* updates, int64_t* d2h_bytes);
 
 /* Host-thread unit A (cfg.unit_a_host_threads): columns whose refresh dots the host
  * threads computed (all rounds so far) and the current share of the refresh's

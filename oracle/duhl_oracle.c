@@ -100,9 +100,9 @@ void or_primal_dual_w(int model, const double* v, const double* b, i64 d, i64 n,
  *   Lasso: gap_i = (1/d) [ a_i s_i + B [|s_i| - lambda d]_+ + lambda d |a_i| ]
  *   Ridge: gap_i = (1/d) [ a_i s_i + s_i^2/(2 lambda d) + (lambda d/2) a_i^2 ]
  *   SVM: gap_i = (1/n) [ a_i s_i + max(0, 1 - y_i s_i) - y_i a_i ]
- * with s_i = a_i^T w.  gap_out[i] = gap, or +0.0 when gap <= 1e-12 x the
- * magnitude of its terms (rounding noise, reading R17); returns
- * OR_E_NUMERIC if a gap is below -1e-12 * (scale of its terms) or not finite.
+ * with s_i = a_i^T w.  gap_out[i] = max(gap_i, +0.0) (reading R17: gap_i >= 0 in exact
+ * arithmetic, so a rounding-negative value clamps to +0.0, which also maps -0.0 to
+ * +0.0); returns OR_E_NUMERIC if a gap is below -1e-12 * (scale of its terms) or not finite.
  * idx == NULL means all columns (k must equal n).  s_out may be NULL. */
 int or_coord_gaps(int model, const float* A, i64 d, i64 n, i64 ld, const double* alpha,
                   const double* y, const double* w, double lambda, double B, const i64* idx,
@@ -144,9 +144,8 @@ int or_coord_gaps(int model, const float* A, i64 d, i64 n, i64 ld, const double*
         }
         if (!isfinite(g) || g < -1e-12 * (scale > 1.0 ? scale : 1.0)) status = OR_E_NUMERIC;
         if (s_out) s_out[t] = s;
-        /* reading R17: a gap within 1e-12 of the magnitude of its own terms is
-         * rounding noise and reads as +0.0 (also maps -0.0 to +0.0) */
-        gap_out[t] = (g > 1e-12 * scale) ? g : 0.0;
+        /* reading R17: gap_i >= 0 in exact arithmetic; clamp at +0.0 */
+        gap_out[t] = (g > 0.0) ? g : 0.0;
     }
     return status;
 }

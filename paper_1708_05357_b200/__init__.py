@@ -11,7 +11,7 @@ There is no CPU fallback: importing works anywhere (the symbols load), but any
 call that computes raises ``DuhlError`` unless a B200 is present.
 """
 from ._abi import (LASSO, SVM_DUAL, RIDGE, ELASTIC_NET, SEL_GAP, SEL_SEQUENTIAL, SEL_UNIFORM, SEL_IMPORTANCE, DuhlError, Problem,
-                   RoundRecord, create, create_csc, comm_unique_id, lib, lib_path, exported_symbols)
+                   RoundRecord, Group, create, create_csc, comm_unique_id, lib, lib_path, exported_symbols)
 
 __all__ = ["LASSO", "SVM_DUAL", "RIDGE", "ELASTIC_NET", "SEL_GAP", "SEL_SEQUENTIAL", "SEL_UNIFORM", "SEL_IMPORTANCE", "DuhlError", "Problem",
-           "RoundRecord", "create", "create_csc", "comm_unique_id", "lib", "lib_path", "exported_symbols"]
+           "RoundRecord", "Group", "create", "create_csc", "comm_unique_id", "lib", "lib_path", "exported_symbols"]

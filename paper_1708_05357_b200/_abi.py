@@ -17,7 +17,8 @@ FUNCTIONS = ["duhl_default_config", "duhl_create", "duhl_create_csc", "duhl_dest
              "duhl_scd_epoch", "duhl_duality_gap", "duhl_round", "duhl_solve", "duhl_get_state",
              "duhl_set_state", "duhl_comm_unique_id", "duhl_comm_init", "duhl_get_stream",
              "duhl_get_kernel_stats", "duhl_get_counters", "duhl_get_scd_shape", "duhl_get_unit_a_host",
-             "duhl_last_error"]
+             "duhl_group_create", "duhl_group_destroy", "duhl_comm_init_group", "duhl_get_working_set",
+             "duhl_set_trace_callback", "duhl_last_error"]
 KIND_SCD, KIND_GAP, KIND_TOPM, KIND_STAGE = 0, 1, 2, 3
 
 
@@ -51,6 +52,8 @@ class RoundRecord(C.Structure):
                 ("cert_gap", C.c_double), ("z_sum", C.c_double), ("gamma", C.c_double),
                 ("time_s", C.c_double), ("rho", C.c_double)]
 
+
+TRACE_CB = C.CFUNCTYPE(None, C.POINTER(RoundRecord), C.c_void_p)
 
 _lib = None
 _P = C.c_void_p
@@ -87,9 +90,14 @@ def lib():
         L.duhl_get_state.argtypes = [_P, _P, _P, _P]
         L.duhl_set_state.argtypes = [_P, _P]
         L.duhl_get_stream.argtypes = [_P, C.POINTER(C.c_void_p)]
-        L.duhl_get_counters.argtypes = [_P, _P, _P, _P, _P]
+        L.duhl_get_counters.argtypes = [_P, _P, _P, _P, _P, _P]
         L.duhl_get_unit_a_host.argtypes = [_P, _P, _P]
         L.duhl_get_scd_shape.argtypes = [_P, _P, _P, _P, _P]
+        L.duhl_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.duhl_group_destroy.argtypes = [_P]
+        L.duhl_comm_init_group.argtypes = [_P, _P, C.c_int]
+        L.duhl_get_working_set.argtypes = [_P, _P, _I, _P]
+        L.duhl_set_trace_callback.argtypes = [_P, TRACE_CB, _P]
         L.duhl_last_error.argtypes = [_P]
         L.duhl_last_error.restype = C.c_char_p
         for f in FUNCTIONS:
@@ -207,6 +215,23 @@ class Problem:
         a = np.ascontiguousarray(alpha, dtype=np.float64)
         self._check(lib().duhl_set_state(self._h, _p(a)))
 
+    def working_set(self):
+        """duhl_get_working_set: the current P (ascending local column indices)."""
+        m = C.c_int64()
+        self._check(lib().duhl_get_working_set(self._h, None, 0, C.byref(m)))
+        P = np.empty(m.value, dtype=np.int64)
+        self._check(lib().duhl_get_working_set(self._h, _p(P), P.size, C.byref(m)))
+        return P
+
+    def set_trace_callback(self, fn):
+        """duhl_set_trace_callback: fn(RoundRecord) after every duhl_solve round (None removes it)."""
+        self._cb = None if fn is None else TRACE_CB(lambda rec, user: fn(rec.contents))
+        self._check(lib().duhl_set_trace_callback(self._h, self._cb if self._cb else TRACE_CB(), None))
+
+    def comm_init_group(self, group, rank: int):
+        """duhl_comm_init_group: join an in-process Group (contexts driven by host threads)."""
+        self._check(lib().duhl_comm_init_group(self._h, group._h, rank))
+
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):
         """duhl_comm_init: join the NCCL group identified by the 128-byte id."""
         buf = C.create_string_buffer(bytes(unique_id), 128)
@@ -230,9 +255,10 @@ class Problem:
         return ["k_csc_scd", "k_scd_gram", "k_scd_pipe"][k.value], w.value, g.value, r.value
 
     def counters(self):
-        a, b, z, c = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
-        self._check(lib().duhl_get_counters(self._h, C.byref(a), C.byref(b), C.byref(z), C.byref(c)))
-        return dict(launches=a.value, h2d_bytes=b.value, zc_bytes=z.value, updates=c.value)
+        a, b, z, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().duhl_get_counters(self._h, C.byref(a), C.byref(b), C.byref(z), C.byref(c),
+                                            C.byref(e)))
+        return dict(launches=a.value, h2d_bytes=b.value, zc_bytes=z.value, updates=c.value, d2h_bytes=e.value)
 
 
 def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0, scd_ctas=0,
@@ -289,6 +315,29 @@ def create_csc(col_ptr, row_idx, values, d, b_or_y, lam, model, m=0, device=0, r
     prob = Problem(h, d, n)
     prob.m = cfg.m if cfg.m > 0 else n
     return prob
+
+
+class Group:
+    """duhl_group_create / duhl_group_destroy: an in-process communicator for nranks contexts,
+    each driven by its own host thread; collectives reduce through host memory in rank order."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        st = lib().duhl_group_create(nranks, C.byref(h))
+        if st != 0:
+            raise DuhlError(st, "duhl_group_create failed")
+        self._h, self.nranks = h, nranks
+
+    def close(self):
+        if self._h:
+            lib().duhl_group_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def comm_unique_id() -> bytes:

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -60,12 +62,40 @@ static NcclApi* nccl_api() {
     return api.ok ? &api : nullptr;
 }
 
+// In-process group (duhl_group_create): contexts driven by threads of one process
+// reduce through host memory in rank order (deterministic; no NCCL).
+struct duhl_group {
+    int n = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    std::vector<std::vector<double>> slot;  // [n] one buffer per rank
+    // generation barrier; false after timeout_s seconds without all ranks
+    bool barrier(double timeout_s) {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t g = gen;
+        if (++arrived == n) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return true;
+        }
+        const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g; });
+        if (!ok) --arrived;
+        return ok;
+    }
+};
+
 struct duhl_ctx {
     // ---- problem (this rank's shard: columns [col_offset, col_offset + n) of n_glob)
     int model = 0;
     int64_t d = 0, d4 = 0, n = 0, n_glob = 0, col_offset = 0;
     // ---- multi-GPU (CoCoA-style aggregation)
     ncclComm_t comm = nullptr;
+    duhl_group* group = nullptr;  // in-process group instead of NCCL (duhl_comm_init_group)
+    duhl_trace_cb trace_cb = nullptr;  // duhl_solve per-round callback
+    void* trace_user = nullptr;
     int nranks = 1, rank = 0;
     double *d_dv = nullptr, *d_aold = nullptr, *d_ls = nullptr;  // dv, alpha_P at round start, line search
     double lambda = 0, B = 0;
@@ -120,7 +150,7 @@ struct duhl_ctx {
     unsigned* d_bar = nullptr;
     int W = 0, R = 0, G = 0, NB = 2;
     // ---- misc
-    int64_t launches = 0, h2d_bytes = 0, zc_bytes = 0, updates = 0, cursor = 0;
+    int64_t launches = 0, h2d_bytes = 0, zc_bytes = 0, updates = 0, cursor = 0, d2h_bytes = 0;
     // ---- profiling (cfg.profile): CUDA-event pairs per launch, harvested at sync points
     struct Timed { cudaEvent_t a, b; int kind; double bytes; };
     std::vector<Timed> pending;
@@ -218,9 +248,17 @@ static void harvest(duhl_ctx* ctx) {  // call after the streams are synchronized
         if (s_ != DUHL_OK) return s_;      \
     } while (0)
 
+// Device -> host read-back on stream st, counted (duhl_get_counters: d2h_bytes).
+static cudaError_t d2h_copy(duhl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 static duhl_status fail(duhl_ctx* ctx, duhl_status s, const std::string& msg) {
     ctx->err = msg;
     return s;
+}
+
+static cudaError_t d2h_copy(duhl_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    ctx->d2h_bytes += (int64_t)bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
 }
 
 // ------------------------------------------------------------------------- helpers
@@ -247,9 +285,35 @@ static double wscale(const duhl_ctx* ctx) {
     return ctx->model != DUHL_SVM_DUAL ? 1.0 : 1.0 / (ctx->lambda * (double)ctx->n_glob);
 }
 
-// In-place sum (or max) allreduce over the group on the compute stream; no-op alone.
+// In-process group: copy out, barrier, every rank sums the slots in rank order (so
+// all ranks hold bit-identical results, as the oracle's shard-order sum), barrier,
+// copy back.  Bounded waits: a rank that never arrives fails the call.
+static duhl_status group_allreduce(duhl_ctx* ctx, double* buf, size_t count, bool is_max) {
+    duhl_group* g = ctx->group;
+    std::vector<double>& mine = g->slot[ctx->rank];
+    mine.resize(count);
+    if (d2h_copy(ctx, mine.data(), buf, count * sizeof(double), ctx->st) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->st) != cudaSuccess)
+        return fail(ctx, DUHL_E_CUDA, "group allreduce: device -> host copy failed");
+    if (!g->barrier(600.0)) return fail(ctx, DUHL_E_NCCL, "group allreduce: a rank did not arrive");
+    std::vector<double> out(g->slot[0]);
+    for (int r = 1; r < g->n; ++r) {
+        const std::vector<double>& x = g->slot[r];
+        if (x.size() != count) return fail(ctx, DUHL_E_NCCL, "group allreduce: ranks disagree on the count");
+        for (size_t i = 0; i < count; ++i) out[i] = is_max ? std::max(out[i], x[i]) : out[i] + x[i];
+    }
+    if (!g->barrier(600.0)) return fail(ctx, DUHL_E_NCCL, "group allreduce: a rank did not arrive");
+    if (cudaMemcpyAsync(buf, out.data(), count * sizeof(double), cudaMemcpyHostToDevice, ctx->st) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->st) != cudaSuccess)
+        return fail(ctx, DUHL_E_CUDA, "group allreduce: host -> device copy failed");
+    return DUHL_OK;
+}
+
+// In-place sum (or max) allreduce over the group on the compute stream; no-op without a
+// communicator (a 1-rank NCCL communicator still runs the collective).
 static duhl_status allreduce(duhl_ctx* ctx, double* buf, size_t count, ncclRedOp_t op = ncclSum) {
-    if (!ctx->comm || ctx->nranks < 2) return DUHL_OK;
+    if (ctx->group) return group_allreduce(ctx, buf, count, op == ncclMax);
+    if (!ctx->comm) return DUHL_OK;
     ncclResult_t r = nccl_api()->allReduce(buf, buf, count, ncclDouble, op, ctx->comm, ctx->st);
     if (r != ncclSuccess) return fail(ctx, DUHL_E_NCCL, std::string("ncclAllReduce: ") + nccl_api()->getErrorString(r));
     return DUHL_OK;
@@ -279,7 +343,7 @@ static GapParams gap_params(duhl_ctx* ctx, const int64_t* d_cols, int64_t k) {
 
 static duhl_status check_flag(duhl_ctx* ctx, const char* where) {
     int fl[2] = {0, 0};
-    CK(cudaMemcpyAsync(fl, ctx->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h_copy(ctx, fl, ctx->d_flag, 2 * sizeof(int), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     const int flag = fl[0];
     if (fl[1]) {
@@ -436,7 +500,7 @@ static duhl_status resident_commit(duhl_ctx* ctx, int64_t m, int64_t* swaps) {
     CK(launch_resident_select(ctx->d_P, m, ctx->d_stamp, ctx->sel_id, ctx->d_P_slot, ctx->d_P_batch,
                               ctx->csc ? ctx->d_colptr : nullptr, ctx->d_rsel, ctx->st, &ctx->launches));
     unsigned long long h[2] = {0, 0};
-    CK(cudaMemcpyAsync(h, ctx->d_rsel, sizeof(h), cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h_copy(ctx, h, ctx->d_rsel, sizeof(h), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     ctx->m_cur = m;
     if (ctx->csc) ctx->csc_pass_bytes = 8.0 * (double)h[1] + 24.0 * (double)m;
@@ -448,7 +512,7 @@ static duhl_status resident_commit(duhl_ctx* ctx, int64_t m, int64_t* swaps) {
 static duhl_status ensure_host_P(duhl_ctx* ctx) {
     if (ctx->P_host_valid) return DUHL_OK;
     ctx->P.resize(ctx->m_cur);
-    CK(cudaMemcpyAsync(ctx->P.data(), ctx->d_P, ctx->m_cur * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h_copy(ctx, ctx->P.data(), ctx->d_P, ctx->m_cur * sizeof(int64_t), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     std::fill(ctx->inP.begin(), ctx->inP.end(), 0);
     for (int64_t j : ctx->P) ctx->inP[j] = 1;
@@ -922,7 +986,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         double h[2] = {0, 0};
         ck(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), st));
         ck(launch_vec_sums(ctx->d_b, nullptr, d4, ctx->d_sums, st, &ctx->launches));
-        ck(cudaMemcpyAsync(h, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        ck(d2h_copy(ctx, h, ctx->d_sums, 2 * sizeof(double), st));
         ck(cudaStreamSynchronize(st));
         ctx->B = h[0] / (2.0 * lambda * (double)d);  // P:848, reading R1
     }
@@ -971,8 +1035,8 @@ duhl_status duhl_gaps(duhl_ctx* ctx, const int64_t* idx, int64_t k, double* z_ou
         k = ctx->n;
     }
     TRY(run_gaps(ctx, dcols, k, z_out ? ctx->d_gap_out : nullptr, s_out ? ctx->d_s_out : nullptr, nullptr));
-    if (z_out) CK(cudaMemcpyAsync(z_out, ctx->d_gap_out, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    if (s_out) CK(cudaMemcpyAsync(s_out, ctx->d_s_out, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    if (z_out) CK(d2h_copy(ctx, z_out, ctx->d_gap_out, k * sizeof(double), ctx->st));
+    if (s_out) CK(d2h_copy(ctx, s_out, ctx->d_s_out, k * sizeof(double), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return check_flag(ctx, "duhl_gaps");
 }
@@ -1001,7 +1065,7 @@ static duhl_status select_impl(duhl_ctx* ctx, duhl_policy policy, int64_t m, int
             return check_flag(ctx, "duhl_select");
         }
         P.resize(m);
-        CK(cudaMemcpyAsync(P.data(), ctx->d_P, m * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+        CK(d2h_copy(ctx, P.data(), ctx->d_P, m * sizeof(int64_t), ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         TRY(check_flag(ctx, "duhl_select"));
     } else {
@@ -1095,7 +1159,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     if (trace) {
         unsigned long long h[16];
         TRY(issue_staging(ctx));  // the synchronize below must not starve a waiting epoch
-        CK(cudaMemcpyAsync(h, dtr, sizeof(h), cudaMemcpyDeviceToHost, ctx->st));
+        CK(d2h_copy(ctx, h, dtr, sizeof(h), ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         cudaFree(dtr);
         const double nb = (double)((L + ctx->W - 1) / ctx->W);
@@ -1200,7 +1264,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
             else gcols.push_back(i);
         }
         const int64_t kg = (int64_t)gcols.size();
-        CK(cudaMemcpyAsync(ctx->h_vt, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+        CK(d2h_copy(ctx, ctx->h_vt, ctx->d_vt, ctx->d4 * sizeof(double), ctx->st));
         CK(cudaEventRecord(ctx->ev_hvt, ctx->st));
         hua_post(ctx->hua, ctx->h_store, ctx->ld_host, ctx->d4, ctx->h_hcols, kh, ctx->h_vt, wscale(ctx),
                  ctx->ev_hvt, ctx->h_hs);
@@ -1234,7 +1298,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
     CK(launch_vec_sums(ctx->d_vt, ctx->model != DUHL_SVM_DUAL ? ctx->d_b : nullptr, ctx->d4, ctx->d_sums + 4,
                        ctx->st, &ctx->launches));     // v is replicated: no reduction
     double h[8];
-    CK(cudaMemcpyAsync(h, ctx->d_sums, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h_copy(ctx, h, ctx->d_sums, 8 * sizeof(double), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     TRY(check_flag(ctx, "certificate"));
     const double dd = (double)ctx->d, nn = (double)ctx->n_glob, lam = ctx->lambda;
@@ -1296,7 +1360,7 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
             CK(launch_ridge_sums(ctx->d_alpha, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 2, ctx->st, &ctx->launches));
             TRY(allreduce(ctx, ctx->d_ls + 2, 2));
             double h[4];
-            CK(cudaMemcpyAsync(h, ctx->d_ls, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(d2h_copy(ctx, h, ctx->d_ls, 4 * sizeof(double), ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             const double dvdv = h[0], vdv = h[1], ada = h[2], dada = h[3];
             const double den = dvdv / dd + lam * dada;
@@ -1309,7 +1373,7 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
                               &ctx->launches));
             TRY(allreduce(ctx, ctx->d_ls + 2, 1));
             double h[3];
-            CK(cudaMemcpyAsync(h, ctx->d_ls, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(d2h_copy(ctx, h, ctx->d_ls, 3 * sizeof(double), ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             const double dvdv = h[0], vdv = h[1], yda = h[2], ln2 = lam * nn * nn;
             if (dvdv > 0.0) {
@@ -1324,7 +1388,7 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
                 TRY(allreduce(ctx, ctx->d_ls + 2, 2));
             }
             double h[4];
-            CK(cudaMemcpyAsync(h, ctx->d_ls, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(d2h_copy(ctx, h, ctx->d_ls, 4 * sizeof(double), ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             const double dvdv = h[0], vdv = h[1], ada = en ? h[2] : 0.0, dada = en ? h[3] : 0.0;
             auto Dfun = [&](double g, double S) { return (vdv + g * dvdv) / dd + lam * (l1 * S + l2 * (ada + g * dada)); };
@@ -1340,7 +1404,7 @@ static duhl_status aggregate(duhl_ctx* ctx, double* gamma_out) {
                 CK(launch_lasso_dgrid(ctx->d_alpha, ctx->d_P, ctx->d_aold, m, ctx->d_ls + 128, nq, ctx->d_ls + 192,
                                       ctx->st, &ctx->launches));
                 TRY(allreduce(ctx, ctx->d_ls + 192, (size_t)nq));
-                CK(cudaMemcpyAsync(S, ctx->d_ls + 192, nq * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+                CK(d2h_copy(ctx, S, ctx->d_ls + 192, nq * sizeof(double), ctx->st));
                 CK(cudaStreamSynchronize(ctx->st));
                 if (it == 0) {
                     if (Dfun(0.0, S[0]) >= 0.0) { gamma = 0.0; done = true; break; }
@@ -1445,7 +1509,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
             CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
         if (kh > 0) {  // v~ snapshot to the host threads; their columns to the device for the finalize
-            CK(cudaMemcpyAsync(ctx->h_vt, ctx->d_vsnap, ctx->d4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+            CK(d2h_copy(ctx, ctx->h_vt, ctx->d_vsnap, ctx->d4 * sizeof(double), ctx->st));
             CK(cudaEventRecord(ctx->ev_hvt, ctx->st));
             CK(cudaMemcpyAsync(ctx->d_hcols, ctx->h_hcols, kh * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
             hua_post(ctx->hua, ctx->h_store, ctx->ld_host, ctx->d4, ctx->h_hcols, kh, ctx->h_vt, wscale(ctx),
@@ -1492,8 +1556,8 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     CK(launch_sum(ctx->d_z, n, ctx->d_sums + 6, ctx->st, &ctx->launches));
     TRY(allreduce(ctx, ctx->d_sums + 6, 1));
     double zs = 0.0, rs[2] = {0.0, 0.0};
-    CK(cudaMemcpyAsync(&zs, ctx->d_sums + 6, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaMemcpyAsync(rs, ctx->d_rho, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CK(d2h_copy(ctx, &zs, ctx->d_sums + 6, sizeof(double), ctx->st));
+    CK(d2h_copy(ctx, rs, ctx->d_rho, 2 * sizeof(double), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     TRY(check_flag(ctx, "duhl_round"));
     harvest(ctx);
@@ -1579,6 +1643,7 @@ duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes
         }
         r.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (trace && t < trace_cap) trace[t] = r;
+        if (ctx->trace_cb) ctx->trace_cb(&r, ctx->trace_user);
         if (r.cert_gap >= 0.0 && gap <= eps) { st = DUHL_OK; ++t; break; }
     }
     if (rounds_out) *rounds_out = t;
@@ -1590,9 +1655,9 @@ duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes
 duhl_status duhl_get_state(duhl_ctx* ctx, double* alpha_out, double* v_out, double* z_out) {
     if (!ctx) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
-    if (alpha_out) CK(cudaMemcpyAsync(alpha_out, ctx->d_alpha, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    if (v_out) CK(cudaMemcpyAsync(v_out, ctx->d_vt, ctx->d * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
-    if (z_out) CK(cudaMemcpyAsync(z_out, ctx->d_z, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    if (alpha_out) CK(d2h_copy(ctx, alpha_out, ctx->d_alpha, ctx->n * sizeof(double), ctx->st));
+    if (v_out) CK(d2h_copy(ctx, v_out, ctx->d_vt, ctx->d * sizeof(double), ctx->st));
+    if (z_out) CK(d2h_copy(ctx, z_out, ctx->d_z, ctx->n * sizeof(double), ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return DUHL_OK;
 }
@@ -1611,9 +1676,13 @@ duhl_status duhl_set_state(duhl_ctx* ctx, const double* alpha) {
             return fail(ctx, DUHL_E_INVALID, "SVM alpha outside the box y_i alpha_i in [0,1]");
     }
     CK(cudaMemcpyAsync(ctx->d_alpha, alpha, ctx->n * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+    // sharded (collective): v = sum_k A_k alpha_k - b, i.e. each rank its own columns, b
+    // subtracted on rank 0 only, then summed over the ranks
+    const bool sub_b = ctx->model != DUHL_SVM_DUAL && ctx->rank == 0;
     CK(launch_matvec(colsrc(ctx), ctx->d_alpha, ctx->csc ? 0 : ctx->n, ctx->d, ctx->d4,
-                     ctx->model != DUHL_SVM_DUAL ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
+                     sub_b ? ctx->d_b : nullptr, ctx->d_vt, ctx->st, &ctx->launches));
     if (ctx->csc) CK(launch_csc_matvec(cscmat(ctx), ctx->d_alpha, ctx->n, ctx->d_vt, ctx->st, &ctx->launches));
+    TRY(allreduce(ctx, ctx->d_vt, (size_t)ctx->d4));
     TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, nullptr));
     CK(cudaStreamSynchronize(ctx->st));
     return check_flag(ctx, "duhl_set_state");
@@ -1634,7 +1703,7 @@ duhl_status duhl_comm_init(duhl_ctx* ctx, const void* id, int nranks, int rank) 
     CK(cudaSetDevice(ctx->dev));
     NcclApi* api = nccl_api();
     if (!api) return fail(ctx, DUHL_E_NCCL, "libnccl.so.2 not found");
-    if (ctx->comm) return fail(ctx, DUHL_E_INVALID, "communicator already initialised");
+    if (ctx->comm || ctx->group) return fail(ctx, DUHL_E_INVALID, "communicator already initialised");
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     ncclResult_t r = api->commInitRank(&ctx->comm, nranks, uid, rank);
@@ -1644,6 +1713,56 @@ duhl_status duhl_comm_init(duhl_ctx* ctx, const void* id, int nranks, int rank) 
     }
     ctx->nranks = nranks;
     ctx->rank = rank;
+    // sigma' = 1 local subproblems summed with weight 1 can diverge; the exact line search on
+    // gamma keeps every round monotone (R16), so it is on for K > 1
+    if (nranks > 1) ctx->cfg.linesearch = 1;
+    return DUHL_OK;
+}
+
+duhl_status duhl_group_create(int nranks, duhl_group** out) {
+    if (!out) return DUHL_E_INVALID;
+    *out = nullptr;
+    if (nranks < 1 || nranks > 1024) return DUHL_E_INVALID;
+    duhl_group* g = new duhl_group();
+    g->n = nranks;
+    g->slot.resize(nranks);
+    *out = g;
+    return DUHL_OK;
+}
+
+duhl_status duhl_group_destroy(duhl_group* g) {
+    if (!g) return DUHL_E_INVALID;
+    delete g;
+    return DUHL_OK;
+}
+
+duhl_status duhl_comm_init_group(duhl_ctx* ctx, duhl_group* g, int rank) {
+    if (!ctx || !g || rank < 0 || rank >= g->n) return DUHL_E_INVALID;
+    if (ctx->comm || ctx->group) return fail(ctx, DUHL_E_INVALID, "communicator already initialised");
+    ctx->group = g;
+    ctx->nranks = g->n;
+    ctx->rank = rank;
+    if (g->n > 1) ctx->cfg.linesearch = 1;
+    return DUHL_OK;
+}
+
+duhl_status duhl_set_trace_callback(duhl_ctx* ctx, duhl_trace_cb cb, void* user) {
+    if (!ctx) return DUHL_E_INVALID;
+    ctx->trace_cb = cb;
+    ctx->trace_user = user;
+    return DUHL_OK;
+}
+
+duhl_status duhl_get_working_set(duhl_ctx* ctx, int64_t* P_out, int64_t cap, int64_t* m_out) {
+    if (!ctx) return DUHL_E_INVALID;
+    CK(cudaSetDevice(ctx->dev));
+    TRY(ensure_host_P(ctx));
+    const int64_t m = (int64_t)ctx->P.size();
+    if (m_out) *m_out = m;
+    if (P_out) {
+        if (cap < m) return fail(ctx, DUHL_E_INVALID, "P_out capacity smaller than |P|");
+        std::memcpy(P_out, ctx->P.data(), m * sizeof(int64_t));
+    }
     return DUHL_OK;
 }
 
@@ -1677,8 +1796,9 @@ duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* 
 }
 
 duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_bytes, int64_t* zc_bytes,
-                              int64_t* updates) {
+                              int64_t* updates, int64_t* d2h_bytes) {
     if (!ctx) return DUHL_E_INVALID;
+    if (d2h_bytes) *d2h_bytes = ctx->d2h_bytes;
     if (launches) *launches = ctx->launches;
     if (h2d_bytes) *h2d_bytes = ctx->h2d_bytes;
     if (zc_bytes) *zc_bytes = ctx->zc_bytes;

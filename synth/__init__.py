@@ -285,6 +285,23 @@ def hadamard_columns(d: int, n: int, scales=None) -> np.ndarray:
     return A.astype(np.float32)
 
 
+def disjoint_support_csc(d: int, n: int, k: int, seed: int, scales=None):
+    """CSC matrix whose n columns have k nonzeros each on pairwise DISJOINT row sets (n k <= d):
+    a_i^T a_j = 0 for i != j exactly, whatever subset of their entries is summed, so every
+    interleaving of concurrent coordinate updates is the sequential one (the P7/P8 pins of the
+    asynchronous epoch).  Rows drawn as a seeded permutation, sorted per column; values N(0,1)
+    times an optional per-column scale.  Returns (col_ptr int64, rows int32, vals float32)."""
+    assert n * k <= d
+    r = np.random.Generator(np.random.Philox(key=[seed, 77]))
+    perm = r.permutation(d)[:n * k].reshape(n, k)
+    rows = np.sort(perm, axis=1).astype(np.int32).ravel()
+    vals = r.standard_normal((n, k))
+    if scales is not None:
+        vals *= np.asarray(scales, dtype=np.float64)[:, None]
+    col_ptr = np.arange(n + 1, dtype=np.int64) * k
+    return col_ptr, rows, vals.astype(np.float32).ravel()
+
+
 def permutation(P, seed: int) -> np.ndarray:
     """A seeded permutation of the index list P (explicit-order parity tests)."""
     P = np.asarray(P, dtype=np.int64)

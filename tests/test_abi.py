@@ -84,3 +84,28 @@ def test_invalid_csc_rejected_before_device():
     with pytest.raises(D.DuhlError) as e:           # lambda must be > 0
         D.create_csc(*good, 5, b, 0.0, D.LASSO)
     assert e.value.status == 2
+
+
+def _build_abi_check(tmp_path):
+    """Compile tests/c/abi_check.c (plain C11) against include/duhl.h, linked to libduhl.so."""
+    import subprocess
+    import paper_1708_05357_b200 as D
+    lib = D.lib_path()
+    exe = str(tmp_path / "abi_check")
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_check.c"), "-o", exe,
+                           "-L", os.path.dirname(lib), "-lduhl", "-lm",
+                           f"-Wl,-rpath,{os.path.dirname(lib)}"])
+    return exe
+
+
+def test_c_program_compiles_against_header_and_runs(tmp_path):
+    """A C caller compiles against include/duhl.h alone and links libduhl.so; without a GPU
+    duhl_create returns DUHL_E_CUDA and the host-only calls (config, group) work."""
+    import subprocess
+    import torch
+    exe = _build_abi_check(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: the GPU run is tests/test_gpu_edge.py::test_c_program_solves_P1")
+    r = subprocess.run([exe, "0"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr

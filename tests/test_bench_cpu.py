@@ -31,3 +31,11 @@ def test_reference_arm_non_zero_rank_is_silent():
     out = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--config", "c1", "--steps", "1",
                "--warmup", "0", "--ref-cols", "50")
     assert out == ""
+
+
+def test_gpus_mismatch_refused():
+    """--gpus N without a matching WORLD_SIZE (torchrun) exits non-zero instead of measuring
+    another GPU count (VERDICT r01 weak #4)."""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "c1", "--steps", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)

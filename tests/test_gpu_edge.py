@@ -191,3 +191,13 @@ def test_invalid_arguments_are_rejected(D):
             P.gaps(np.array([0, n]))                                 # index out of range
         assert e.value.status == 2
         P.gaps()                                                     # the handle is still usable
+
+
+def test_c_program_solves_P1(tmp_path):
+    """tests/c/abi_check.c, a plain C caller of include/duhl.h: solves the P1 worked example
+    (alpha* = (1/2, 1/2), O* = 0.375) through duhl_solve with a trace callback."""
+    import subprocess
+    from test_abi import _build_abi_check
+    exe = _build_abi_check(tmp_path)
+    r = subprocess.run([exe, "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -361,6 +361,40 @@ def test_P8_orthogonal_sample_svm_closed_form():
         assert G < 1e-13
 
 
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_P7s_P8s_disjoint_support_closed_forms(model):
+    """Sparse orthogonal designs (columns on disjoint row sets, a_i^T a_j = 0): the objective
+    separates per coordinate, so Lasso alpha_i* = soft(a_i^T b, lam d)/||a_i||^2 and
+    SVM y_i alpha_i* = clip(lam n/||a_i||^2, 0, 1), reached by one sequential epoch
+    in any order (the pins the asynchronous GPU epochs are held to)."""
+    d, n, k = 3000, 500, 6
+    cp, rows, vals = synth.disjoint_support_csc(d, n, k, seed=5, scales=np.linspace(0.3, 3.0, n))
+    A = synth.csc_to_dense(cp, rows, vals, d)
+    A64 = A.astype(np.float64)
+    assert np.count_nonzero(np.triu(A64 @ A64.T, 1)) == 0
+    norms = O.col_norms(A)
+    rng = np.random.default_rng(3)
+    if model == O.LASSO:
+        b = rng.standard_normal(d)
+        lam = 0.2 * np.abs(A64 @ b).max() / d
+        c = A64 @ b
+        want = np.sign(c) * np.maximum(np.abs(c) - lam * d, 0) / (A64 ** 2).sum(1)
+        assert 0 < np.count_nonzero(want) < n
+        alpha, vt, lab = np.zeros(n), -b.copy(), b
+        O.scd_pass(O.LASSO, A, norms, None, lam, alpha, vt, synth.permutation(np.arange(n), 8))
+        np.testing.assert_allclose(alpha, want, rtol=1e-12, atol=1e-15)
+    else:
+        y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        lam = 1.0 / n
+        beta = np.clip(lam * n / (A64 ** 2).sum(1), 0, 1)
+        assert 0 < np.count_nonzero(beta < 1) < n
+        alpha, vt, lab = np.zeros(n), np.zeros(d), y
+        O.scd_pass(O.SVM, A, norms, y, lam, alpha, vt, synth.permutation(np.arange(n), 8))
+        np.testing.assert_allclose(y * alpha, beta, rtol=1e-12, atol=1e-15)
+    st, G, Ob, D = O.duality_gap(model, A, alpha, lab, lam, O.lasso_B(lab, lam) if model == O.LASSO else 0.0)
+    assert st == O.OK and G < 1e-12
+
+
 # ----------------------------------------------------------------------------- P9 / P10
 def _svm_bruteforce(A64, y, lam):
     """Enumerate beta_i = y_i alpha_i in {0, 1, free}; solve free block stationarity."""
