@@ -388,14 +388,8 @@ def run_duhl(args, cfg, rank, world, local):
     A, lab = make_data(cfg, seed, lo, hi, world)
     lam = lam_of(cfg, A, lab, world)
     t_gen = time.perf_counter() - t_gen
-    col_bytes = ((d + 3) // 4) * 16
-    # strong scaling: the aggregate budget and working set stay those of the config
-    budget = int(cfg["budget_frac"] * n * col_bytes) // world if cfg["budget_frac"] > 0 else 0
-    m = cfg["m"] // world
-    common = dict(hbm_budget_bytes=budget, m=m, device=local, refresh_fraction=args.refresh,
-                  seed=seed, borrow_host=True, n_global=n, col_offset=lo,
-                  linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas,
-                  unit_a_host_threads=args.unit_a_host, unit_a_host_share=args.host_share)
+    common = launch_kwargs(args, cfg, rank, world, local)
+    budget, m = common["hbm_budget_bytes"], common["m"]
     uid = None
     if world > 1:  # NCCL group for the dv allreduce: id from rank 0, broadcast by torch.distributed
         import torch.distributed as dist
@@ -616,7 +610,20 @@ def run_duhl(args, cfg, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
-def main():
+def launch_kwargs(args, cfg, rank=0, world=1, local=0):
+    """duhl_create options of the bench's launch (also used by tests/test_gpu_fullsize.py so the
+    full-size parity runs the timed configuration).  Strong scaling: the aggregate budget and
+    working set stay those of the config; rank k owns columns [k n/N, (k+1) n/N)."""
+    d, n = cfg["d"], cfg["n"]
+    col_bytes = ((d + 3) // 4) * 16
+    budget = int(cfg["budget_frac"] * n * col_bytes) // world if cfg["budget_frac"] > 0 else 0
+    return dict(hbm_budget_bytes=budget, m=cfg["m"] // world, device=local, refresh_fraction=args.refresh,
+                seed=170805357 + 3, borrow_host=True, n_global=n, col_offset=rank * n // world,
+                linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas,
+                unit_a_host_threads=args.unit_a_host, unit_a_host_share=args.host_share)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -652,7 +659,7 @@ def main():
                          "0 off (GPU-only refresh); -1 auto: min(14, cores - 2) on the out-of-core dense configs")
     ap.add_argument("--host-share", type=float, default=-1.0,
                     help="their share of the refresh's non-resident columns (<0: balanced per round)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 0)
     cfg = CONFIGS[args.config]
     if args.unit_a_host < 0:  # out-of-core dense configs only: the refresh reads host columns there
@@ -662,6 +669,11 @@ def main():
                             and cores >= 4 else 0)
     if args.passes <= 0:
         args.passes = cfg.get("passes_host", cfg.get("passes", 1)) if args.unit_a_host > 0 else cfg.get("passes", 1)
+    return args, cfg
+
+
+def main():
+    args, cfg = parse_args()
     if args.impl == "reference":  # the CPU oracle: rank 0 alone, no process group needed
         run_reference(args, cfg, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return

@@ -59,7 +59,7 @@ class Alg2:
             return O.primal_dual_w(O.SVM, self.vt, None, self.n, self.lam)
         return self.vt.copy()
 
-    def _tau(self, idx, eta=0.5):
+    def _tau(self, idx, eta=0.5, tol=TOL):
         """Gap tolerance of SURVEY 8(c): tol * max(|z_i|, kappa c_i ||a_i|| ||w||), c_i a bound
         on |d gap_i / d s_i| at the current state."""
         a = np.abs(self.alpha[idx])
@@ -74,10 +74,11 @@ class Alg2:
             c = (an * wn + lam * d * a) / (lam * d * d) + 1.0 / d
         else:
             c = a / d + an * wn / (lam * eta * d * d) + 1.0 / d
-        return TOL * np.maximum(np.abs(self.z[idx]), KAPPA * c * an * wn)
+        return tol * np.maximum(np.abs(self.z[idx]), KAPPA * c * an * wn)
 
-    def check_selection(self, P_list, policy, t):
-        """P_list[k]: shard k's working set (global indices, ascending) from the device."""
+    def check_selection(self, P_list, policy, t, tol=TOL):
+        """P_list[k]: shard k's working set (global indices, ascending) from the device.
+        tol: the gap tolerance (north_star: 1e-6 fp64-accumulated, 1e-4 fp32 mode)."""
         for k, Pk in enumerate(P_list):
             lo, hi = self.shard(k)
             Pk = np.asarray(Pk, dtype=np.int64)
@@ -92,7 +93,7 @@ class Alg2:
             assert Pk.size == mk, (k, t, Pk.size, mk)
             zk = self.z[lo:hi]
             thr = np.sort(zk)[::-1][mk - 1]
-            tau = self._tau(np.arange(lo, hi))
+            tau = self._tau(np.arange(lo, hi), tol=tol)
             sel = np.zeros(nk, dtype=bool)
             sel[Pk - lo] = True
             must_in = zk > thr + tau

@@ -48,7 +48,7 @@ __device__ __forceinline__ void gap_finish_one(const GapParams& p, int64_t t, in
     double g = coord_gap(p.model, a, s, yy, p.lambda, p.B, (double)p.d, (double)p.n, &scale, &aux, p.eta);
     if (!isfinite(g)) flag |= 2;
     else if (g < -1e-12 * (scale > 1.0 ? scale : 1.0)) flag |= 1;
-    double gz = g > 1e-12 * scale ? g : 0.0;  // rounding noise reads as +0.0 (reading R17)
+    double gz = g > 0.0 ? g : 0.0;  // gap_i >= 0 in exact arithmetic: clamp at +0.0 (reading R17)
     if (p.z) p.z[i] = gz;
     if (p.gap_out) p.gap_out[t] = gz;
     if (p.s_out) p.s_out[t] = s;

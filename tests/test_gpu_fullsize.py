@@ -1,5 +1,11 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
+test_bench_launch_rounds_replay_oracle: the bench's own options (bench.parse_args +
+bench.launch_kwargs: fast-mode SCD, k_scd_gram W = 12 on 140 CTAs at C4 / k_scd_pipe W = 32
+with tensor-core Gram tiles at C3, 8 unit-A refresh CTAs, host unit-A threads, passes per
+round) for the first rounds from alpha = 0, each round replayed by the oracle on the device's
+(band-verified) working set (oracle/replay.py): alpha and v element-wise, the certificate.
+
 C4 (hinge-SVM dual, 200,704 x 40,000 fp32 = 32.1 GB in pinned host memory) and C3 (Lasso,
 40,000 x 200,704) under the 8.03 GB HBM budget, m, passes, refresh and SCD mode of the bench
 (fast mode: fp32 Gram products inside a warp).  After a few DuHL rounds (Alg. 2)
@@ -19,6 +25,7 @@ import pytest
 
 import bench
 import oracle as O
+from oracle.replay import Alg2
 
 pytestmark = pytest.mark.gpu
 
@@ -77,5 +84,35 @@ def test_full_size_rounds_against_oracle(D, name):
     assert abs(G - G_or) <= TOL * max(G_or, 1e-12)
     O0 = 0.0 if model == O.SVM else float(lab @ lab) / (2 * d)   # objective at alpha = 0
     assert Ob < O0
+    del A
+    gc.collect()
+
+
+@pytest.mark.parametrize("name,rounds", [("c4", 3), ("c3", 2)])
+def test_bench_launch_rounds_replay_oracle(D, name, rounds):
+    args, cfg = bench.parse_args(["--config", name])
+    kw = bench.launch_kwargs(args, cfg)
+    d, n, model = cfg["d"], cfg["n"], cfg["model"]
+    A, lab = bench.make_data(cfg, kw["seed"])
+    lam = bench.lam_of(cfg, A, lab)
+    m, passes = kw["m"], args.passes
+    R = Alg2(model, A, lab, lam, m, passes, int(np.ceil(args.refresh * n - 1e-9)), kw["seed"])
+    with D.create(A, lab, lam, model, cert_every=1 << 40, scd_exact=args.exact, **kw) as P:
+        shape = P.scd_shape()
+        assert shape[0] == ("k_scd_gram" if name == "c4" else "k_scd_pipe")
+        for t in range(rounds):
+            rec = P.round(t, passes=passes, certify=(t == rounds - 1))
+            Pd = P.working_set()
+            R.check_selection([Pd], O.SEL_GAP, t, tol=1e-4)   # fast mode: the fp32-mode tolerance
+            rr = R.round(t, [Pd], certify=(t == rounds - 1))
+            assert rec.swaps == rr["swaps"], (t, rec.swaps, rr["swaps"])
+        a, v, _ = P.get_state()
+        cols, share = P.unit_a_host()
+    if args.unit_a_host > 0:
+        assert cols > 0                                  # the host threads took part of unit A
+    sa = np.abs(R.alpha).max()
+    assert np.abs(a - R.alpha).max() <= 1e-6 * sa, np.abs(a - R.alpha).max() / sa
+    assert np.abs(v - R.vt).max() <= 1e-6 * max(1.0, np.abs(R.vt).max())
+    assert abs(rec.cert_gap - rr["gap"]) <= 1e-6 * rr["gap"], (rec.cert_gap, rr["gap"])
     del A
     gc.collect()
