@@ -225,6 +225,19 @@ class Sparse:
         return np.where(np.diff(self.cp) > 0, out, 0.0)
 
 
+def pin_host(A):
+    """Page-lock the host matrix once (cudaHostRegister, mapped), as a caller keeping its data in
+    pinned memory would; duhl_create(borrow_host=1) then uses it in place.  Returns bytes pinned."""
+    if isinstance(A, Sparse):
+        return 0
+    import torch
+    cr = torch.cuda.cudart()
+    for flags in (2 | 8, 2):   # cudaHostRegisterMapped | ReadOnly, else Mapped
+        if int(cr.cudaHostRegister(A.ctypes.data, A.nbytes, flags)) == 0:
+            return A.nbytes
+    return 0
+
+
 def rho_mean(trace):
     """Mean rho_{t,P} (Eq. 6) over a solve's rounds (on the gap memory, DESIGN R21)."""
     return float(np.mean([t.rho for t in trace])) if trace else None
@@ -336,11 +349,16 @@ def oracle_time_to_eps(cfg, A, lab, lam, eps, cap_s):
            "gaps": gaps[:20], "wall_cap_s": cap_s,
            "note": "plain sequential SCD over all n columns (P:406 single-threaded CPU baseline), "
                    "certificate after every epoch (its time included)"}
-    if not out["converged"] and len(gaps) >= 2 and 0 < gaps[-1] < gaps[-2]:
-        rate = gaps[-1] / gaps[-2]
-        more = np.log(eps / gaps[-1]) / np.log(rate)
-        out["extrapolated_time_to_eps_s"] = times[-1] + more * (times[-1] - times[-2])
-        out["extrapolated"] = True
+    out["gap_reached"] = min(gaps)   # the duality gap of an SCD epoch need not decrease monotonically
+    if not out["converged"] and len(gaps) >= 3:
+        # linear convergence fitted to log(gap) over the epochs run, extrapolated to eps (flagged)
+        e_idx = np.arange(1, len(gaps) + 1)
+        slope, icpt = np.polyfit(e_idx, np.log(np.maximum(gaps, 1e-300)), 1)
+        if slope < 0:
+            epochs_eps = (np.log(eps) - icpt) / slope
+            out["extrapolated_time_to_eps_s"] = float(epochs_eps * times[-1] / len(gaps))
+            out["extrapolated_epochs_to_eps"] = float(epochs_eps)
+            out["extrapolated"] = True
     return out
 
 
@@ -388,6 +406,9 @@ def run_duhl(args, cfg, rank, world, local):
     A, lab = make_data(cfg, seed, lo, hi, world)
     lam = lam_of(cfg, A, lab, world)
     t_gen = time.perf_counter() - t_gen
+    t_pin = time.perf_counter()
+    pinned = pin_host(A)   # the caller's data lives in pinned host memory (the e2e precondition)
+    t_pin = time.perf_counter() - t_pin
     common = launch_kwargs(args, cfg, rank, world, local)
     budget, m = common["hbm_budget_bytes"], common["m"]
     uid = None
@@ -413,7 +434,7 @@ def run_duhl(args, cfg, rank, world, local):
     barrier(world)
     torch.cuda.synchronize()
     c0 = P.counters()
-    k0 = {k: P.kernel_stats(k) for k in range(5)}
+    k0 = {k: P.kernel_stats(k) for k in range(6)}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     swaps = refreshed = 0
     with ClockSampler(local) as clk:
@@ -430,15 +451,12 @@ def run_duhl(args, cfg, rank, world, local):
     c1 = P.counters()
     pcie_peak = pcie_h2d_peak(local)
     pcie_bytes = (c1["h2d_bytes"] - c0["h2d_bytes"] + c1["zc_bytes"] - c0["zc_bytes"]) / args.steps
-    pcie = None if budget == 0 else {"bytes_per_step": pcie_bytes,
+    pcie_step = None if budget == 0 else {"bytes_per_step": pcie_bytes,
             "copy_bytes_per_step": (c1["h2d_bytes"] - c0["h2d_bytes"]) / args.steps,
             "zero_copy_bytes_per_step": (c1["zc_bytes"] - c0["zc_bytes"]) / args.steps,
             "achieved_GBps": pcie_bytes / (elapsed / args.steps) / 1e9,
-            "peak_GBps": pcie_peak, "frac": pcie_bytes / (elapsed / args.steps) / 1e9 / pcie_peak,
-            "note": "the step's binding resource when the working set changes: staging copies + "
-                    "unit-A zero-copy refresh reads over PCIe; peak = 1 GiB pinned H2D copy measured "
-                    "in this run"}
-    k1 = {k: P.kernel_stats(k) for k in range(5)}
+            "peak_GBps": pcie_peak, "frac": pcie_bytes / (elapsed / args.steps) / 1e9 / pcie_peak}
+    k1 = {k: P.kernel_stats(k) for k in range(6)}
     # kernel-only SCD roofline: extra passes over the working set now resident in HBM
     # (no staging waits inside the launch), outside the timed region
     P.scd_epoch(passes=3, seed=12345, round=10 ** 6)
@@ -449,12 +467,15 @@ def run_duhl(args, cfg, rank, world, local):
     P.close()
     updates = args.steps * m * args.passes * world
     value = updates / elapsed
-    ms = {k: k1[k][1] - k0[k][1] for k in range(5)}
-    nl = {k: k1[k][0] - k0[k][0] for k in range(5)}
-    by = {k: k1[k][2] - k0[k][2] for k in range(5)}
+    ms = {k: k1[k][1] - k0[k][1] for k in range(6)}
+    nl = {k: k1[k][0] - k0[k][0] for k in range(6)}
+    by = {k: k1[k][2] - k0[k][2] for k in range(6)}
     peak, peak_src = hbm_peak()
     scd_gbs = by[0] / (ms[0] / 1e3) / 1e9 if ms[0] > 0 else None
     gap_gbs = by[1] / (ms[1] / 1e3) / 1e9 if ms[1] > 0 else None
+    # the HBM roofline kernel: the SCD epoch launches that wait for nothing (kind 0: passes >= 1,
+    # and pass 0 of rounds without staging); pass-0 launches that consume staged columns as they
+    # land (kind 5) are bound by the staging and reported under "pcie"
     dom = 0 if ms[0] >= ms[1] else 1
     dom_gbs = scd_gbs if dom == 0 else gap_gbs
     traffic = None
@@ -470,7 +491,25 @@ def run_duhl(args, cfg, rank, world, local):
                 "peak_source": peak_src,
                 "share_of_step": (ms[dom] / 1e3) / elapsed,
                 "algorithmic_bytes_per_launch": by[dom] / max(1, nl[dom]),
-                "avg_launch_ms": ms[dom] / max(1, nl[dom])}
+                "avg_launch_ms": ms[dom] / max(1, nl[dom]),
+                "launches": nl[dom],
+                "note": ("SCD launches that wait for no staged column (passes >= 1; pass 0 overlapping the "
+                         "staging is under pcie.scd_overlapped)" if dom == 0 else "gap pass")}
+    pcie = None
+    if pcie_step is not None:
+        stage_gbs = by[3] / (ms[3] / 1e3) / 1e9 if ms[3] > 0 else None
+        pcie = dict(pcie_step,
+                    staging={"kernel": "k_stage_gather (light rounds) / copy engine (heavy rounds)",
+                             "achieved_GBps": stage_gbs, "peak_GBps": pcie_peak,
+                             "frac": stage_gbs / pcie_peak if stage_gbs else None,
+                             "ms_per_step": ms[3] / args.steps},
+                    scd_overlapped={"kernel": scd_name, "launches": nl[5],
+                                    "avg_launch_ms": ms[5] / max(1, nl[5]),
+                                    "share_of_step": (ms[5] / 1e3) / elapsed},
+                    note="the step's binding resource when the working set changes: staging (gather kernel "
+                         "zero-copy reads / copy-engine copies) + unit-A zero-copy refresh reads over PCIe; peak "
+                         "= 1 GiB pinned H2D copy measured in this run; pass 0 of the epoch consumes the staged "
+                         "columns as they land (scd_overlapped)")
 
     # ---------------- end to end: create from host buffers + solve to certified eps
     e2e = None
@@ -508,10 +547,11 @@ def run_duhl(args, cfg, rank, world, local):
                "swaps_per_round_first_last": swaps_trend(r["trace"]),
                "create_s": med["t_create"],
                "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
-                       "from host buffers (pin in place, norms, z at alpha=0 over PCIe) + duhl_solve to the "
-                       "certified gap); time_to_eps_s = duhl_solve alone (data resident in pinned host "
-                       "memory, cold HBM fill included); h2d = cold fill + swaps (memcpy); zero-copy = "
-                       "refresh + certificate reads of non-resident columns"}
+                       "from the caller's pinned host buffers (used in place; one device pass over A for "
+                       "norms + z at alpha=0) + duhl_solve to the certified gap); time_to_eps_s = "
+                       "duhl_solve alone (cold HBM fill included); h2d = cold fill + swaps (copy engine and "
+                       "staging gather); zero-copy = refresh + certificate reads of non-resident columns; "
+                       "d2h = the library's read-backs (counted)"}
 
     # ---------------- baselines: same library, budget and kernels, batch selection
     # sequential blocks [Yu 2012] / uniform / importance sampling instead of gap top-m
@@ -550,7 +590,7 @@ def run_duhl(args, cfg, rank, world, local):
     if not args.no_cpu and not args.no_oracle_tte and rank == 0 and world == 1:
         oracle_tte = oracle_time_to_eps(cfg, A, lab, lam, args.eps, args.oracle_cap)
         if oracle_tte and not oracle_tte["converged"] and oracle_tte["gap_reached"] is not None:
-            P4 = create(D, A, lab, lam, cfg["model"], cert_every=1, scd_exact=args.exact, **common)
+            P4 = create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact, **common)
             t1 = time.perf_counter()
             r4 = P4.solve(oracle_tte["gap_reached"], args.max_rounds, passes=args.passes, policy=policy)
             oracle_tte["gpu_time_to_same_gap_s"] = time.perf_counter() - t1
@@ -597,7 +637,8 @@ def run_duhl(args, cfg, rank, world, local):
                                          "note": "3 passes over the HBM-resident working set after the "
                                                  "timed rounds (no staging waits in the launch)"},
             "gap_pass_GBps": gap_gbs, "scd_GBps": scd_gbs,
-            "kernel_ms": {"scd": ms[0], "gap_zP": ms[1], "topm": ms[2], "stage_h2d": ms[3],
+            "kernel_ms": {"scd": ms[0], "scd_overlapped_staging": ms[5], "gap_zP": ms[1], "topm": ms[2],
+                          "stage_h2d": ms[3],
                           "refresh_unitA": ms[4]},
             "refresh_GBps": (by[4] / (ms[4] / 1e3) / 1e9) if ms[4] > 0 else None,
             "swaps_per_step": swaps / args.steps, "refreshed_per_step": refreshed / args.steps,
@@ -605,7 +646,7 @@ def run_duhl(args, cfg, rank, world, local):
             "oracle_time_to_eps": oracle_tte,
             "gpu_launches": c1["launches"] - c0["launches"],
             "clocks": clk.summary(),
-            "setup_s": {"generate": t_gen, "create": t_create}}
+            "setup_s": {"generate": t_gen, "pin_host": t_pin, "pinned_bytes": pinned, "create": t_create}}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -130,11 +130,50 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------- memory model
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// staging counter c of the gather lives at progress[c * kProgressStride] (own 128-byte line:
+// the polls of the SCD grid and the releases of the other gather CTAs do not share it)
+constexpr int kProgressStride = 32;
+
+// Wait until a staged column has landed in HBM (the SCD kernels' producer warps).
+// need = 0: resident.  stage_ctas = 0: copy-engine staging, one monotone sequence
+// counter progress[0] (need = the copy's sequence number; seen caches the last value
+// read).  stage_ctas = G > 0: the gather kernel k_stage_gather, plan entry q = need - 1
+// landed once progress[(q % G) * kProgressStride] > q / G.  After the acquire, a proxy fence orders the
+// generic-proxy stores of the gather before this thread's async-proxy (TMA) reads.
+// Bounded: after timeout_ns the wait gives up and sets *err (bit 0).
+__device__ __forceinline__ bool wait_staged(const unsigned* progress, int stage_ctas, unsigned need,
+                                            unsigned& seen, int* err, unsigned long long timeout_ns) {
+    if (!progress || need == 0) return true;
+    const unsigned* c = progress;
+    unsigned thr = need;
+    if (stage_ctas > 0) {
+        c = progress + (size_t)((need - 1) % (unsigned)stage_ctas) * kProgressStride;
+        thr = (need - 1) / (unsigned)stage_ctas + 1;
+    } else if (need <= seen) {
+        return true;
+    }
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned v;
+    while ((v = ld_acquire_u32(c)) < thr) {
+        __nanosleep(128);
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > timeout_ns) { atomicOr(err, 1); return false; }
+    }
+    if (stage_ctas == 0) seen = v;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    return true;
+}
+
 __device__ __forceinline__ double ld_cg_f64(const double* p) {
     double v;
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");

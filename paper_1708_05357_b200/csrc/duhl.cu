@@ -30,6 +30,8 @@ using namespace duhl;
 
 namespace {
 constexpr int kGapTileRows = 4096;
+constexpr int kStageCtas = 16;  // k_stage_gather CTAs (2 per SM the SCD grid leaves): 51.4 GB/s alone (stage2.cu)
+constexpr size_t kProgressBytes = 16 * 128;  // staging counters, one 128-byte line each (kProgressStride)
 inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
 }  // namespace
 
@@ -155,8 +157,8 @@ struct duhl_ctx {
     struct Timed { cudaEvent_t a, b; int kind; double bytes; };
     std::vector<Timed> pending;
     std::vector<cudaEvent_t> event_pool;
-    int64_t st_launch[5] = {0, 0, 0, 0, 0};
-    double st_ms[5] = {0, 0, 0, 0, 0}, st_bytes[5] = {0, 0, 0, 0, 0};
+    int64_t st_launch[6] = {0, 0, 0, 0, 0, 0};
+    double st_ms[6] = {0, 0, 0, 0, 0, 0}, st_bytes[6] = {0, 0, 0, 0, 0, 0};
     double* d_s_acc2 = nullptr;  // partial-dot accumulator of the concurrent refresh pass
     // ---- unit A on host threads (cfg.unit_a_host_threads): a_i^T v~ for part of the refresh
     HostUnitA* hua = nullptr;
@@ -174,6 +176,12 @@ struct duhl_ctx {
     typedef int (*WriteValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
     WriteValue32 write_value = nullptr;  // cuStreamWriteValue32 via cudaGetDriverEntryPoint
     bool overlap = false;  // this round's copies overlap the epoch (progress counter); else copies first
+    int stage_ctas = 0;    // > 0: this round's copies are a k_stage_gather launch of that many CTAs
+    int64_t* h_plan_cols = nullptr;  // pinned gather plan (columns, slots), uploaded on the copy stream
+    int* h_plan_slots = nullptr;
+    int64_t* d_plan_cols = nullptr;
+    int* d_plan_slots = nullptr;
+    cudaEvent_t ev_plan = nullptr;   // the last plan upload has read the pinned plan
     unsigned* d_progress = nullptr;      // last landed staging copy (sequence number)
     unsigned batch_seq = 0;
     std::vector<unsigned> slot_batch;    // [S] sequence number of the copy that filled a slot
@@ -444,6 +452,30 @@ static duhl_status finalize_staging(duhl_ctx* ctx) {
 static duhl_status issue_staging(duhl_ctx* ctx) {
     if (ctx->copy_plan.empty()) return DUHL_OK;
     duhl_status rc = DUHL_OK;
+    if (ctx->stage_ctas > 0) {  // light round: one gather launch (k_stage_gather), entries in plan order
+        const size_t np = ctx->copy_plan.size();
+        const size_t col_bytes = (size_t)ctx->ld_dev * sizeof(float);
+        ProfScope ps(ctx, ctx->cst, 3, (double)(np * col_bytes));
+        cudaEventSynchronize(ctx->ev_plan);  // the previous upload has read the pinned plan
+        for (size_t q = 0; q < np; ++q) {
+            ctx->h_plan_cols[q] = ctx->copy_plan[q].col;
+            ctx->h_plan_slots[q] = ctx->copy_plan[q].slot;
+        }
+        if (cudaMemcpyAsync(ctx->d_plan_cols, ctx->h_plan_cols, np * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            ctx->cst) != cudaSuccess ||
+            cudaMemcpyAsync(ctx->d_plan_slots, ctx->h_plan_slots, np * sizeof(int), cudaMemcpyHostToDevice,
+                            ctx->cst) != cudaSuccess ||
+            cudaEventRecord(ctx->ev_plan, ctx->cst) != cudaSuccess ||
+            launch_stage_gather(ctx->h_alias, ctx->ld_host, ctx->pool, ctx->ld_dev, ctx->ld_dev, ctx->d_plan_cols,
+                                ctx->d_plan_slots, (int64_t)np, ctx->d_progress, ctx->stage_ctas, ctx->cst,
+                                &ctx->launches) != cudaSuccess)
+            rc = fail(ctx, DUHL_E_CUDA, "staging gather launch failed");
+        ctx->h2d_bytes += (int64_t)(np * col_bytes);
+        ctx->copy_plan.clear();
+        cudaEventRecord(ctx->ev_copy, ctx->cst);
+        if (!ctx->overlap) cudaStreamWaitEvent(ctx->st, ctx->ev_copy, 0);
+        return rc;
+    }
     {
         ProfScope ps(ctx, ctx->cst, 3, 0.0);
         const size_t col_bytes = (size_t)ctx->ld_dev * sizeof(float);
@@ -569,6 +601,18 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // large copies at full PCIe rate, and one progress write at the end.
         const bool heavy = (int64_t)news.size() * 2 > m;
         if (heavy) std::sort(news.begin(), news.end());
+        // every earlier copy has landed before this round's epoch (the compute stream waited on
+        // ev_copy): kept slots need no wait
+        std::fill(ctx->slot_batch.begin(), ctx->slot_batch.end(), 0u);
+        // light rounds that overlap the epoch: zero-copy gather by kStageCtas CTAs on the SMs the
+        // SCD grid leaves to unit A (faster than per-column copies); entry q + 1 is the
+        // column's wait token.  The counters are zeroed on the compute stream before this round's
+        // epoch can poll them.
+        static const bool force_ce = std::getenv("DUHL_STAGE_CE") != nullptr;
+        static const int nstage = std::getenv("DUHL_STAGE_CTAS") ? std::max(1, std::min(16, std::atoi(std::getenv("DUHL_STAGE_CTAS"))))
+                                                               : kStageCtas;  // developer override (<= 16 counters)
+        ctx->stage_ctas = (ctx->overlap && !heavy && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
+        if (ctx->stage_ctas > 0) CK(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, ctx->st));
         size_t fi = 0;
         const unsigned heavy_seq = ctx->overlap && heavy ? ctx->batch_seq + 1 : 0u;
         for (size_t q = 0; q < news.size(); ++q) {
@@ -579,12 +623,13 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             ctx->pend_cols.push_back(j);
             ctx->pend_slots.push_back(s);
             unsigned seq = 0;
-            if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
+            if (ctx->stage_ctas > 0) seq = (unsigned)q + 1;
+            else if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
             ctx->slot_batch[s] = seq;
             ctx->copy_plan.push_back({j, s, seq});
             ++nsw;
         }
-        if (ctx->overlap && !news.empty())
+        if (ctx->overlap && ctx->stage_ctas == 0 && !news.empty())
             ctx->batch_seq = heavy ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
@@ -630,13 +675,15 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
-                        ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols};
+                        ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols,
+                        ctx->d_plan_cols, ctx->d_plan_slots};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
     hua_destroy(ctx->hua);
     ctx->hua = nullptr;
-    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hcols})
+    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hcols, (void*)ctx->h_plan_cols,
+                    (void*)ctx->h_plan_slots})
         if (p) cudaFreeHost(p);
     for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1, ctx->ev_c1})
         if (e) cudaEventDestroy(e);
@@ -647,6 +694,7 @@ static void free_all(duhl_ctx* ctx) {
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->ev_snap) cudaEventDestroy(ctx->ev_snap);
     if (ctx->ev_ref) cudaEventDestroy(ctx->ev_ref);
+    if (ctx->ev_plan) cudaEventDestroy(ctx->ev_plan);
     if (ctx->rst) cudaStreamDestroy(ctx->rst);
 
     if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -819,14 +867,22 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     if (can_borrow) {
         ctx->h_store = const_cast<float*>(A->values);
         ctx->ld_host = A->ld;
-        if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float),
-                             cudaHostRegisterMapped | cudaHostRegisterReadOnly) != cudaSuccess) {
-            cudaGetLastError();
-            if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float), cudaHostRegisterMapped) !=
-                cudaSuccess)
-                return bail(DUHL_E_CUDA);
+        // memory the caller already pinned (cudaHostAlloc / cudaHostRegister, e.g. a pinned
+        // torch tensor) is used as is -- pinning 32 GB costs ~3.3 s on this box (tools/micro/stage.cu)
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, ctx->h_store) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+        cudaGetLastError();
+        if (!pinned) {
+            if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float),
+                                 cudaHostRegisterMapped | cudaHostRegisterReadOnly) != cudaSuccess) {
+                cudaGetLastError();
+                if (cudaHostRegister(ctx->h_store, (size_t)n * A->ld * sizeof(float), cudaHostRegisterMapped) !=
+                    cudaSuccess)
+                    return bail(DUHL_E_CUDA);
+            }
+            ctx->registered = true;
         }
-        ctx->registered = true;
     } else {
         ctx->ld_host = d4;
         if (cudaHostAlloc((void**)&ctx->h_store, (size_t)n * d4 * sizeof(float), cudaHostAllocMapped) !=
@@ -847,23 +903,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
             });
         for (auto& x : th) x.join();
     }
-    // data validity: finite values (checked on the host copy once, cheap relative to ingest)
-    {
-        std::vector<char> badv(64, 0);
-        unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> th;
-        const float* hs = ctx->h_store;
-        const int64_t ldh = ctx->ld_host;
-        for (unsigned t = 0; t < nt; ++t)
-            th.emplace_back([=, &badv]() {
-                for (int64_t i = t; i < n; i += nt)
-                    for (int64_t k = 0; k < d; ++k)
-                        if (!std::isfinite(hs[i * ldh + k])) { badv[t] = 1; break; }
-            });
-        for (auto& x : th) x.join();
-        for (char c : badv)
-            if (c) return bail(DUHL_E_INVALID);
-    }
+    // data validity (finite values) is checked by the device ingest pass below: a non-finite
+    // element makes ||a_i||^2 non-finite
     void* alias = nullptr;
     if (cudaHostGetDevicePointer(&alias, ctx->h_store, 0) != cudaSuccess) return bail(DUHL_E_CUDA);
     ctx->h_alias = (const float*)alias;
@@ -900,7 +941,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
               dmal((void**)&ctx->d_aold, n * sizeof(double)) &&
               dmal((void**)&ctx->d_ls, 256 * sizeof(double)) &&
               dmal((void**)&ctx->d_s_acc2, n * sizeof(double)) &&
-              dmal((void**)&ctx->d_progress, 64) &&
+              dmal((void**)&ctx->d_progress, kProgressBytes) &&
               dmal((void**)&ctx->d_P_batch, n * sizeof(unsigned)) &&
               dmal((void**)&ctx->d_order_batch, n * sizeof(unsigned)) &&
               dmal((void**)&ctx->d_order_a, n * sizeof(double)) &&
@@ -910,12 +951,14 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
               dmal((void**)&ctx->d_gap_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_s_out, n * sizeof(double)) &&
               dmal((void**)&ctx->d_sums, 8 * sizeof(double)) &&
-              dmal((void**)&ctx->d_flag, 4 * sizeof(int));
+              dmal((void**)&ctx->d_flag, 4 * sizeof(int)) &&
+              dmal((void**)&ctx->d_plan_cols, n * sizeof(int64_t)) &&
+              dmal((void**)&ctx->d_plan_slots, n * sizeof(int));
     if (!ok) { cudaGetLastError(); ctx->err = "cudaMalloc failed"; return bail(DUHL_E_NOMEM); }
+    // SMs the SCD grid leaves to unit A's refresh and the staging gather of budgeted problems:
+    // 8 (measured: C4 step 85 vs 90 ms with 16 refresh CTAs)
     ctx->unit_a_ctas = ctx->cfg.unit_a_ctas > 0 ? std::min(ctx->cfg.unit_a_ctas, ctx->nsm / 2)
-                       : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 &&
-                          ctx->cfg.refresh_fraction > 0.0) ? 8 : 0;  // 8 CTAs keep PCIe busy (measured:
-                                                                      // C4 step 85 vs 90 ms with 16)
+                       : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 && !ctx->csc) ? 8 : 0;
     choose_scd_shape(ctx);
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)))
@@ -939,6 +982,11 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     if (!dmal((void**)&ctx->d_red, scd_red_bytes(ctx)) ||
         !dmal((void**)&ctx->d_bar, 64))
         return bail(DUHL_E_NOMEM);
+    if (!ctx->csc && ctx->cfg.hbm_budget_bytes != 0 &&
+        (cudaHostAlloc((void**)&ctx->h_plan_cols, n * sizeof(int64_t), 0) != cudaSuccess ||
+         cudaHostAlloc((void**)&ctx->h_plan_slots, n * sizeof(int), 0) != cudaSuccess ||
+         cudaEventCreateWithFlags(&ctx->ev_plan, cudaEventDisableTiming) != cudaSuccess))
+        return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
     ctx->slot_col.assign(ctx->S, -1);
     ctx->slot_batch.assign(ctx->S, 0u);
@@ -959,7 +1007,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     auto ck = [&](cudaError_t e) { if (e != cudaSuccess) ok2 = false; };
     ck(cudaMemsetAsync(ctx->d_s_acc, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_s_acc2, 0, n * sizeof(double), st));
-    ck(cudaMemsetAsync(ctx->d_progress, 0, 64, st));
+    ck(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, st));
     ck(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), st));
     ck(cudaMemsetAsync(ctx->d_alpha, 0, n * sizeof(double), st));
     ck(cudaMemsetAsync(ctx->d_b, 0, d4 * sizeof(double), st));
@@ -979,9 +1027,9 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         ck(cudaMemcpyAsync(ctx->d_b, b_or_y, d * sizeof(double), cudaMemcpyHostToDevice, st));
     ck(cudaStreamSynchronize(st));
     if (!ok2) { cudaGetLastError(); ctx->err = "device setup failed"; return bail(DUHL_E_CUDA); }
-    // ---- precompute (a1): norms, B, initial shared vector, z at alpha = 0
+    // ---- precompute (a1): B, initial shared vector, then ONE pass over A for ||a_i||^2 and
+    // z = the exact gaps at alpha = 0 (SVM: 1/n; regression: from a_i^T (-b))
     if (ctx->csc) ck(launch_csc_norms(cscmat(ctx), n, ctx->d_norms, st, &ctx->launches));
-    else ck(launch_col_norms(colsrc(ctx), d4, n, ctx->d_norms, st, &ctx->launches));
     if (model == DUHL_LASSO) {
         double h[2] = {0, 0};
         ck(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), st));
@@ -994,7 +1042,23 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
                      ctx->d_vt, st, &ctx->launches));  // alpha = 0: v~ = -b, v^ = 0
     ck(cudaStreamSynchronize(st));
     if (!ok2) { cudaGetLastError(); ctx->err = "precompute failed"; return bail(DUHL_E_CUDA); }
-    if (run_gaps(ctx, nullptr, n, nullptr, nullptr, nullptr) != DUHL_OK) return bail(DUHL_E_CUDA);
+    if (!ctx->csc) {  // ingest: norms + gaps at alpha = 0 in one pass (k_gap_tile<INGEST>)
+        ck(cudaMemsetAsync(ctx->d_norms, 0, n * sizeof(double), st));
+        GapParams p = gap_params(ctx, nullptr, n);
+        p.norms_out = ctx->d_norms;
+        ProfScope ps(ctx, st, 1, (double)n * (4.0 * ctx->d4 + 24.0));
+        ck(launch_gap_pass(p, kGapTileRows, st, &ctx->launches));
+        ps.end();
+        double h = 0.0;
+        ck(cudaMemsetAsync(ctx->d_sums + 7, 0, sizeof(double), st));
+        ck(launch_sum(ctx->d_norms, n, ctx->d_sums + 7, st, &ctx->launches));
+        ck(cudaMemcpyAsync(&h, ctx->d_sums + 7, sizeof(double), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        if (!ok2) { cudaGetLastError(); ctx->err = "ingest pass failed"; return bail(DUHL_E_CUDA); }
+        if (!std::isfinite(h)) { ctx->err = "non-finite matrix entries"; return bail(DUHL_E_INVALID); }
+    } else if (run_gaps(ctx, nullptr, n, nullptr, nullptr, nullptr) != DUHL_OK) {
+        return bail(DUHL_E_CUDA);
+    }
     if (check_flag(ctx, "initial gaps") != DUHL_OK) return bail(DUHL_E_NUMERIC);
     *out = ctx;
     return DUHL_OK;
@@ -1088,7 +1152,7 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
     return DUHL_OK;
 }
 
-static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
+static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = false) {
     if (ctx->csc) {  // asynchronous warp-per-coordinate epoch (exact mode: one warp, in order)
         CscScdParams q{};
         q.model = ctx->model;
@@ -1141,6 +1205,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     p.order_inv = ctx->d_order_inv;
     p.order_y = ctx->d_order_y;
     p.progress = ctx->overlap ? ctx->d_progress : nullptr;
+    p.stage_ctas = ctx->overlap ? ctx->stage_ctas : 0;
     p.bar = ctx->d_bar;
     CK(cudaMemsetAsync(ctx->d_red, 0, scd_red_bytes(ctx), ctx->st));
     CK(cudaMemsetAsync(ctx->d_bar, 0, 64, ctx->st));
@@ -1152,7 +1217,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
     }
     p.trace = dtr;
     {
-        ProfScope ps(ctx, ctx->st, 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
+        ProfScope ps(ctx, ctx->st, waits_on_staging ? 5 : 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
         CK(ctx->pipe ? launch_scd_pipe(p, ctx->st, &ctx->launches)
                                     : launch_scd_gram(p, ctx->st, &ctx->launches));
     }
@@ -1190,14 +1255,19 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L) {
 // progress counter per block), else before it (the compute stream waits).
 static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t round) {
     const int64_t m = ctx->m_cur;
+    // staging that overlaps the epoch is enqueued after the pass-0 launch: the host enqueue of
+    // per-column copies overlaps it, and a gather launch finds the cooperative SCD grid resident
+    // on its SMs (one CTA per SM, the whole register file), so its CTAs can only go to the SMs
+    // the grid leaves (unit_a_ctas) -- never in the way of the grid it feeds
     if (!ctx->overlap) TRY(issue_staging(ctx));
+    const bool staged = ctx->overlap && !ctx->copy_plan.empty();  // pass 0 consumes columns as they land
     for (int pass = 0; pass < passes; ++pass) {
         CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
                              ctx->d_order_j, ctx->d_order_slot, ctx->d_order_batch, ctx->d_order_a,
                              ctx->d_order_inv, ctx->d_order_y, ctx->d_alpha, ctx->d_norms,
                              ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr, ctx->st, &ctx->launches,
                              ridge_ld(ctx)));
-        TRY(scd_launch(ctx, m));
+        TRY(scd_launch(ctx, m, staged && pass == 0));
         if (pass == 0) TRY(issue_staging(ctx));  // no-op unless overlapping: host enqueue overlaps pass 0
     }
     return DUHL_OK;
@@ -1462,8 +1532,12 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     // shared by the staging copies and the zero-copy refresh reads, so both run
     // first, side by side, and the epoch follows at full HBM rate.
     TRY(finalize_staging(ctx));
-    static const bool host_overlap = std::getenv("DUHL_HOST_OVERLAP") != nullptr;  // experiment
-    ctx->overlap = ctx->write_value != nullptr && (kref == 0 || (host_overlap && ctx->hua && ctx->hua_share >= 0.5));
+    // With host threads in unit A, PCIe carries (almost) only the staging: the copies overlap the
+    // epoch and the threads take every non-resident refresh column.  DUHL_NO_HOST_OVERLAP=1
+    // restores copies-first.
+    static const bool no_host_overlap = std::getenv("DUHL_NO_HOST_OVERLAP") != nullptr;
+    const bool host_overlap = ctx->hua && !no_host_overlap;
+    ctx->overlap = ctx->write_value != nullptr && (kref == 0 || host_overlap);
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
     {   // rho_{t,P} (Eq. 6) on the gap memory the selection used
         CK(cudaMemsetAsync(ctx->d_rho, 0, 2 * sizeof(double), ctx->st));
@@ -1492,7 +1566,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         ctx->cursor = (ctx->cursor + kref) % n;
         nonres = host_cols;
         // the host threads take the last kh of the non-resident columns; the GPU the rest
-        kh = ctx->hua ? (int64_t)std::llround(ctx->hua_share * (double)host_cols) : 0;
+        kh = ctx->hua ? (ctx->overlap ? host_cols : (int64_t)std::llround(ctx->hua_share * (double)host_cols)) : 0;
         if (kh > 0) {
             int64_t g = 0, hcount = 0, seen = 0;
             for (int64_t q = 0; q < kref; ++q) {
@@ -1774,7 +1848,7 @@ duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {
 
 duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
                                   double* bytes) {
-    if (!ctx || kind < 0 || kind > 4) return DUHL_E_INVALID;
+    if (!ctx || kind < 0 || kind > 5) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
     CK(cudaStreamSynchronize(ctx->st));
     CK(cudaStreamSynchronize(ctx->cst));

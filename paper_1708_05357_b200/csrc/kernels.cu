@@ -102,6 +102,10 @@ __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
 
 // Work item vb = (column group vb % ngroups, row tile vb / ngroups); a grid
 // smaller than the item count loops (a persistent unit-A grid beside the SCD epoch).
+// INGEST (duhl_create's one pass over A): also ||a_i||^2 into
+// p.norms_out (fp64; added atomically across row tiles, zero on entry) -- a non-finite
+// element makes it non-finite, which is how create detects invalid data.
+template <bool INGEST>
 __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int tile_rows, int ntiles, int64_t ngroups) {
     extern __shared__ double ws[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -125,11 +129,18 @@ __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int ti
     for (int64_t t = t0 + warp; t < t1; t += nw) {
         const int64_t i = p.cols ? p.cols[t] : t;
         const float4* a = reinterpret_cast<const float4*>(col_ptr(p.src, i) + r0);
-        double s0 = 0.0, s1 = 0.0;
+        double s0 = 0.0, s1 = 0.0, n0 = 0.0, n1 = 0.0;
+        auto sq = [&](const float4& f) {
+            if (INGEST) {
+                n0 = fma((double)f.x, (double)f.x, n0); n1 = fma((double)f.y, (double)f.y, n1);
+                n0 = fma((double)f.z, (double)f.z, n0); n1 = fma((double)f.w, (double)f.w, n1);
+            }
+        };
         int q = lane;
         for (; q + 96 < nv; q += 128) {  // 4 independent 16-B loads in flight per lane
             float4 f0 = ld_stream_f4(a + q), f1 = ld_stream_f4(a + q + 32);
             float4 f2 = ld_stream_f4(a + q + 64), f3 = ld_stream_f4(a + q + 96);
+            sq(f0); sq(f1); sq(f2); sq(f3);
             double2 u, v;
             u = w2[2 * q]; v = w2[2 * q + 1];
             s0 = fma((double)f0.x, u.x, s0); s1 = fma((double)f0.y, u.y, s1);
@@ -146,11 +157,19 @@ __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int ti
         }
         for (; q < nv; q += 32) {
             float4 f = ld_stream_f4(a + q);
+            sq(f);
             double2 u = w2[2 * q], v = w2[2 * q + 1];
             s0 = fma((double)f.x, u.x, s0); s1 = fma((double)f.y, u.y, s1);
             s0 = fma((double)f.z, v.x, s0); s1 = fma((double)f.w, v.y, s1);
         }
         double s = warp_sum(s0 + s1);
+        if (INGEST) {
+            const double nr = warp_sum(n0 + n1);
+            if (lane == 0) {
+                if (ntiles == 1) p.norms_out[i] = nr;
+                else atomicAdd(&p.norms_out[i], nr);
+            }
+        }
         if (lane == 0) {
             if (ntiles == 1) gap_finish_one(p, t, i, s, acc, flag);
             else atomicAdd(&p.s_acc[t], s);
@@ -180,11 +199,13 @@ cudaError_t launch_gap_pass(const GapParams& p, int tile_rows, cudaStream_t st, 
     int64_t items = ngroups * ntiles;
     if (max_ctas > 0 && items > max_ctas) items = max_ctas;
     size_t smem = (size_t)tile_rows * sizeof(double);
+    const void* fn = p.norms_out ? (const void*)k_gap_tile<true> : (const void*)k_gap_tile<false>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_gap_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_gap_tile<<<(unsigned)items, kGapThreads, smem, st>>>(p, tile_rows, ntiles, ngroups);
+    if (p.norms_out) k_gap_tile<true><<<(unsigned)items, kGapThreads, smem, st>>>(p, tile_rows, ntiles, ngroups);
+    else k_gap_tile<false><<<(unsigned)items, kGapThreads, smem, st>>>(p, tile_rows, ntiles, ngroups);
     ++*launches;
     if (ntiles > 1) {
         k_gap_finalize<<<(unsigned)cdiv(p.k, kGapThreads), kGapThreads, 0, st>>>(p);
@@ -483,6 +504,50 @@ cudaError_t launch_topm(const double* z, int64_t n, int64_t m, int keymode, uint
 size_t launch_topm_work_bytes() { return 64 + kBins * sizeof(int) + 2 * kTopChunks * sizeof(int); }
 
 // =====================================================================================
+// Working-set staging host -> HBM by a zero-copy gather (light rounds, Alg. 2 l.4).
+// The copy engine moves one 803-KB C4 column per cudaMemcpyAsync at 42.7 GB/s on this
+// box (per-copy overhead; 1, 2, 4 or 8 streams alike), 16 CTAs of this kernel read
+// scattered pinned host columns at 51.5 GB/s (tools/micro/stage.cu).  CTA c copies plan
+// entries q = c, c + G, c + 2G, ... in order (4 x 16-byte loads in flight per thread)
+// and then publishes progress[c] = entries done (release); the SCD kernels wait for
+// entry q on progress[q % G] > q / G (wait_staged), so the epoch consumes columns as
+// they land.
+// =====================================================================================
+constexpr int kStageThreads = 256;
+constexpr int kStageUnroll = 8;  // 16-byte loads in flight per thread (32 KB per CTA)
+__global__ void __launch_bounds__(kStageThreads) k_stage_gather(const float* host, int64_t ld_host, float* pool,
+                                                                 int64_t ld_dev, int64_t d4, const int64_t* cols,
+                                                                 const int* slots, int64_t nplan, unsigned* progress) {
+    const int64_t n4 = d4 / 4;
+    unsigned done = 0;
+    for (int64_t q = blockIdx.x; q < nplan; q += gridDim.x) {
+        const float4* src = reinterpret_cast<const float4*>(host + cols[q] * ld_host);
+        float4* dst = reinterpret_cast<float4*>(pool + (int64_t)slots[q] * ld_dev);
+        int64_t i = threadIdx.x;
+        for (; i + (kStageUnroll - 1) * kStageThreads < n4; i += kStageUnroll * kStageThreads) {
+            float4 x[kStageUnroll];
+#pragma unroll
+            for (int u = 0; u < kStageUnroll; ++u) x[u] = ld_stream_f4(src + i + u * kStageThreads);
+#pragma unroll
+            for (int u = 0; u < kStageUnroll; ++u) dst[i + u * kStageThreads] = x[u];
+        }
+        for (; i < n4; i += kStageThreads) dst[i] = ld_stream_f4(src + i);
+        __threadfence();  // this thread's stores, device-wide, before the CTA's release below
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_gpu_u32(progress + (size_t)blockIdx.x * kProgressStride, ++done);
+    }
+}
+
+cudaError_t launch_stage_gather(const float* host, int64_t ld_host, float* pool, int64_t ld_dev, int64_t d4,
+                                const int64_t* cols, const int* slots, int64_t nplan, unsigned* progress,
+                                int ctas, cudaStream_t st, int64_t* launches) {
+    if (nplan <= 0) return cudaSuccess;
+    k_stage_gather<<<ctas, kStageThreads, 0, st>>>(host, ld_host, pool, ld_dev, d4, cols, slots, nplan, progress);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// =====================================================================================
 // Pass permutation: position t takes P[pi(t)], pi a
 // keyed 8-round Feistel bijection on [0, 4^h) >= m, restricted to [0, m) by
 // cycle walking.  One thread per position, no sort.
@@ -756,13 +821,7 @@ __device__ __forceinline__ void scd_issue(const ScdParams& p, float* Abuf, uint6
     const int st = (int)(blk % kScdStages);
     float* dst = Abuf + (size_t)st * W * p.R;
     const unsigned bytes = (unsigned)rows * 4u;
-    if (p.progress && lane < Wb && need > seen) {
-        const unsigned long long t0 = gtimer();
-        while ((seen = ld_acquire_u32(p.progress)) < need) {
-            __nanosleep(128);
-            if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 1); break; }  // never hang the GPU
-        }
-    }
+    if (lane < Wb) wait_staged(p.progress, p.stage_ctas, need, seen, p.err, kSpinTimeoutNs);  // never hangs
     // (the stage's last generic accesses are reads, completed before the CTA barrier
     // that precedes this refill: no proxy fence is needed for that order)
     if (lane == 0) mbar_arrive_expect_tx(&mbar[st], bytes * (unsigned)Wb);
@@ -1579,7 +1638,7 @@ cudaError_t launch_resident_select(const int64_t* P, int64_t m, int* stamp, int 
 // host has yet to enqueue (the refresh kernel is launched in between).
 cudaError_t preload_kernels() {
     const void* fns[] = {
-        (const void*)k_gap_tile,    (const void*)k_gap_finalize, (const void*)k_col_norms,
+        (const void*)k_gap_tile<false>, (const void*)k_gap_tile<true>, (const void*)k_gap_finalize, (const void*)k_col_norms,
         (const void*)k_topm,        (const void*)k_perm_order,   (const void*)k_order_info,
         (const void*)k_scd_gram<true, kLasso>, (const void*)k_scd_gram<false, kLasso>,
         (const void*)k_scd_gram<true, kSvm>,   (const void*)k_scd_gram<false, kSvm>,
@@ -1593,7 +1652,7 @@ cudaError_t preload_kernels() {
         (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
         (const void*)k_csc_matvec,  (const void*)k_topm_hist,    (const void*)k_topm_pick,
         (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write,
-        (const void*)k_resident_select};
+        (const void*)k_resident_select, (const void*)k_stage_gather};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -33,6 +33,7 @@ struct GapParams {
     double* s_out;             // [k] or nullptr
     double* sums;              // [4] certificate sums or nullptr: sum gap, sum aux, sum |a| / sum y a, max |a| (bits)
     int* flag;                 // bit0 negative gap, bit1 non-finite
+    double* norms_out;         // create's ingest pass: ||a_i||^2 by column index (zero on entry) or nullptr
 };
 
 struct ScdParams {
@@ -60,6 +61,8 @@ struct ScdParams {
     const unsigned* progress;     // last landed staging copy, written by the copy stream; or nullptr
     int* err;                     // set (bit 0: staging wait, bit 1: grid barrier) on a wait timeout
     int gram_tc;                  // pipe kernel, fast mode, W = 32: Gram tiles on the tensor cores (3xTF32; default 1)
+    int stage_ctas;               // > 0: order_batch holds gather-plan entries + 1 (k_stage_gather with this many
+                                  // CTAs, progress[q % stage_ctas]); 0: copy-engine sequence numbers (progress[0])
 };
 
 // Sparse matrix, compressed sparse columns, resident in HBM:
@@ -115,6 +118,11 @@ cudaError_t launch_perm_order(const int64_t* P, const int* P_slot, const unsigne
                               double* order_y, const double* alpha, const double* norms, const double* y,
                               cudaStream_t st, int64_t* launches, double ridge_ld = 0.0);
 cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launches);
+// light-round staging: plan entries (cols[q] -> slots[q]) gathered host -> HBM by `ctas` CTAs;
+// progress[c] = entries done by CTA c (zero on entry)
+cudaError_t launch_stage_gather(const float* host, int64_t ld_host, float* pool, int64_t ld_dev, int64_t d4,
+                                const int64_t* cols, const int* slots, int64_t nplan, unsigned* progress,
+                                int ctas, cudaStream_t st, int64_t* launches);
 // pipelined form (scd_pipe.cuh): p.G compute CTAs + one control CTA, W <= 32, p.NB in {3, 4}
 size_t pipe_red_doubles(int W);   // size of ScdParams::red (reduction + delta buffers)
 size_t pipe_smem_bytes(int W, int R, int NS);

@@ -342,13 +342,7 @@ __device__ __forceinline__ void pipe_issue(const ScdParams& p, float* Abuf, uint
     const int st = (int)(blk % p.NB);
     float* dst = Abuf + (size_t)st * W * Rs;
     const unsigned bytes = (unsigned)rows * 4u;
-    if (p.progress && lane < Wb && need > seen) {
-        const unsigned long long t0 = gtimer();
-        while ((seen = ld_acquire_u32(p.progress)) < need) {
-            __nanosleep(128);
-            if (gtimer() - t0 > kSpinTimeoutNs) { atomicOr(p.err, 1); break; }
-        }
-    }
+    if (lane < Wb) wait_staged(p.progress, p.stage_ctas, need, seen, p.err, kSpinTimeoutNs);
     if (lane == 0) mbar_arrive_expect_tx(&full[st], bytes * (unsigned)Wb);
     __syncwarp();
     if (lane < Wb) bulk_g2s(dst + (size_t)lane * Rs, p.pool + (int64_t)slot * p.ld_dev + r0, bytes, &full[st]);

@@ -375,13 +375,15 @@ def test_zero_columns(D, kernel):
 
 
 # ------------------------------------------------------------------------- DuHL loop
-@pytest.mark.parametrize("model,policy,budget_cols", [
-    (O.LASSO, O.SEL_GAP, 0), (O.SVM, O.SEL_GAP, 0),
-    (O.LASSO, O.SEL_GAP, 300), (O.SVM, O.SEL_SEQUENTIAL, 260), (O.LASSO, O.SEL_UNIFORM, 250),
-    (O.SVM, O.SEL_IMPORTANCE, 250), (O.RIDGE, O.SEL_GAP, 300), (O.RIDGE, O.SEL_GAP, 0),
-    (O.ELASTIC, O.SEL_GAP, 300),
+@pytest.mark.parametrize("model,policy,budget_cols,host", [
+    (O.LASSO, O.SEL_GAP, 0, 0), (O.SVM, O.SEL_GAP, 0, 0),
+    (O.LASSO, O.SEL_GAP, 300, 0), (O.SVM, O.SEL_SEQUENTIAL, 260, 0), (O.LASSO, O.SEL_UNIFORM, 250, 0),
+    (O.SVM, O.SEL_IMPORTANCE, 250, 0), (O.RIDGE, O.SEL_GAP, 300, 0), (O.RIDGE, O.SEL_GAP, 0, 0),
+    (O.ELASTIC, O.SEL_GAP, 300, 0),
+    # host unit-A threads: staging overlaps the epoch, light rounds staged by k_stage_gather
+    (O.LASSO, O.SEL_GAP, 300, 2), (O.SVM, O.SEL_GAP, 260, 2), (O.SVM, O.SEL_UNIFORM, 250, 3),
 ])
-def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
+def test_duhl_solve_matches_oracle(D, model, policy, budget_cols, host):
     d, n = (400, 1000) if model != O.SVM else (120, 1000)
     A, lab = _data(model, d, n, seed=300 + policy)
     lam = _lam(model, n)
@@ -392,7 +394,7 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
                        eps=eps, max_rounds=3000, cert_every=1, seed=5)
     assert ref["status"] == O.OK
     with D.create(A, lab, lam, model, hbm_budget_bytes=budget, m=m, refresh_fraction=0.05,
-                  cert_every=1, seed=5) as P:
+                  cert_every=1, seed=5, unit_a_host_threads=host) as P:
         r = P.solve(eps, 3000, passes=2, policy=policy)
         a, v, z = P.get_state()
         g, Ob, Db = P.duality_gap()
@@ -424,7 +426,7 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols):
     # (SURVEY 8(c) band), and the oracle's round on that set gives the device's certificate
     R = Alg2(model, A, lab, lam, m, 2, 50, 5)
     with D.create(A, lab, lam, model, hbm_budget_bytes=budget, m=m, refresh_fraction=0.05,
-                  cert_every=1, seed=5) as P:
+                  cert_every=1, seed=5, unit_a_host_threads=host) as P:
         for t in range(min(25, ref["rounds"])):
             rec = P.round(t, passes=2, policy=policy, certify=True)
             Pd = P.working_set()

@@ -1,22 +1,26 @@
-"""Time-to-eps sweep on C4 over refresh fraction and passes (gap policy)."""
+"""Time-to-eps sweep on C4 over refresh fraction and passes per round (gap policy), in the
+bench's launch configuration (bench.parse_args + launch_kwargs: host unit-A threads, fast-mode
+SCD, gather staging overlapping the epoch).  Usage: python tools/sweep_c4.py f:p [f:p ...]"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench, paper_1708_05357_b200 as D
-cfg = bench.CONFIGS["c4"]
-A, lab = bench.make_data(cfg, 170805360)
-budget = int(0.25 * cfg["n"] * ((cfg["d"] + 3) // 4) * 16)
+args, cfg = bench.parse_args(["--config", "c4"])
+kw = bench.launch_kwargs(args, cfg)
+A, lab = bench.make_data(cfg, kw["seed"])
+lam = bench.lam_of(cfg, A, lab)
+grid = [tuple(float(x) for x in a.split(":")) for a in sys.argv[1:]] or [(0.05, 2), (0.1, 2)]
 out = []
-for f, passes in [(0.01, 1), (0.02, 1), (0.05, 1), (0.02, 2), (0.05, 2), (0.1, 1)]:
+for f, passes in grid:
+    kw2 = dict(kw, refresh_fraction=f)
+    P = D.create(A, lab, lam, cfg["model"], cert_every=1 << 30, scd_exact=False, **kw2)
     t0 = time.perf_counter()
-    P = D.create(A, lab, 1.0 / cfg["n"], 1, hbm_budget_bytes=budget, m=cfg["m"], refresh_fraction=f,
-                 borrow_host=True, scd_exact=False, cert_every=50)
-    tc = time.perf_counter() - t0
-    r = P.solve(1e-5, 1000, passes=passes)
+    r = P.solve(1e-5, 1000, passes=int(passes))
     t = time.perf_counter() - t0
     c = P.counters()
     P.close()
-    rec = dict(refresh=f, passes=passes, rounds=r["rounds"], status=r["status"], gap=r["gap"], time_s=t,
-               create_s=tc, h2d_GB=c["h2d_bytes"] / 1e9)
+    rec = dict(refresh=f, passes=int(passes), rounds=r["rounds"], status=r["status"], gap=r["gap"], time_s=t,
+               ms_per_round=1e3 * t / max(1, r["rounds"]), h2d_GB=c["h2d_bytes"] / 1e9)
     print(json.dumps(rec), flush=True)
     out.append(rec)
+os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/sweep_c4.json", "w"), indent=1)
