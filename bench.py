@@ -43,8 +43,11 @@ CONFIGS = {
     # with adaptive-only certificates (tools/c3_sweep.py) 6.1 / 5.2 / 4.9 / 5.2 s at 3 / 4 / 5 / 6)
     # with host threads in unit A (--unit-a-host) the refresh no longer hides the epoch: C3 4.3 s at
     # 2 and 3 passes, 5.1 s at 4 (passes_host)
+    # C3 runs the asynchronous TPA-style epoch (scd_async, 128 coordinates in flight): time to 1e-5
+    # 3.16 s vs 3.90 s with the exact k_scd_pipe (profiles/r02_tpa_vs_exact_c3.json); C4 keeps the
+    # exact k_scd_gram (2.62 s vs 3.27 s async at W = 16; W >= 32 stalls on C4's correlated samples)
     "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=5,
-               passes_host=3,
+               passes_host=3, scd_async=True, scd_block=128,
                label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "
                      "(32.1 GB pinned host), HBM budget 25% (8.03 GB), m=50176, lambda=0.07 lambda_max"),
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None, passes=2,
@@ -254,7 +257,8 @@ def swaps_trend(trace):
 def create(D, A, lab, lam, model, **kw):
     """duhl_create (dense) or duhl_create_csc (sparse) with the bench's options."""
     if isinstance(A, Sparse):
-        for k in ("hbm_budget_bytes", "borrow_host", "unit_a_ctas", "unit_a_host_threads", "unit_a_host_share"):
+        for k in ("hbm_budget_bytes", "borrow_host", "unit_a_ctas", "unit_a_host_threads", "unit_a_host_share",
+                  "scd_async", "scd_block"):
             kw.pop(k, None)
         return D.create_csc(A.cp, A.rows, A.vals, A.d, lab, lam, model, **kw)
     return D.create(A, lab, lam, model, **kw)
@@ -661,7 +665,8 @@ def launch_kwargs(args, cfg, rank=0, world=1, local=0):
     return dict(hbm_budget_bytes=budget, m=cfg["m"] // world, device=local, refresh_fraction=args.refresh,
                 seed=170805357 + 3, borrow_host=True, n_global=n, col_offset=rank * n // world,
                 linesearch=world > 1 or args.linesearch, unit_a_ctas=args.unit_a_ctas,
-                unit_a_host_threads=args.unit_a_host, unit_a_host_share=args.host_share)
+                unit_a_host_threads=args.unit_a_host, unit_a_host_share=args.host_share,
+                scd_async=bool(cfg.get("scd_async")) and not args.exact, scd_block=cfg.get("scd_block", 0))
 
 
 def parse_args(argv=None):

@@ -114,6 +114,13 @@ typedef struct {
                                  the device finishes their gaps.  0 = off (the GPU reads them over PCIe) */
     double unit_a_host_share; /* share of the refresh's non-resident columns given to those threads, in
                                  [0, 1]; < 0 = balanced each round from the measured host and PCIe rates */
+    int scd_async;            /* dense problems: 0 = exact sequential Gram-block epoch (k_scd_gram /
+                                 k_scd_pipe, above); 1 = asynchronous TPA-SCD-style epoch (App. D):
+                                 scd_block (default 16) coordinates in flight, each on a cluster of CTAs
+                                 that splits its column by rows, atomic fp32 updates of a shadow of v,
+                                 then the exact fp64 resync v = v0 + A_P (alpha_P - alpha_P0).  Results
+                                 depend on the interleaving (staleness <= scd_block); duhl_round takes
+                                 the exact gamma line search.  scd_exact is ignored in this mode. */
 } duhl_config;
 
 /* One entry per round of duhl_solve (SPEC RoundTrace columns). */
@@ -299,7 +306,8 @@ duhl_status duhl_get_counters(duhl_ctx* ctx, int64_t* launches, int64_t* h2d_byt
 duhl_status duhl_get_unit_a_host(duhl_ctx* ctx, int64_t* cols, double* share);
 
 /* Launch shape of the dense exact SCD epoch chosen at create (cfg.scd_kernel, shared
- * memory): *kernel 1 = k_scd_gram (warp-specialised), 2 = k_scd_pipe (control CTA);
+ * memory): *kernel 1 = k_scd_gram (warp-specialised), 2 = k_scd_pipe (control CTA),
+ * 3 = k_scd_tpa (cfg.scd_async: W coordinates in flight, G = W x cluster CTAs, R rows per CTA);
  * W coordinates per Gram block, G (compute) CTAs of R rows each.  CSC problems report
  * kernel 0 (k_csc_scd).  Any pointer may be NULL. */
 duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R);

@@ -44,7 +44,7 @@ class Config(C.Structure):
                 ("cert_adaptive", C.c_int), ("profile", C.c_int), ("scd_exact", C.c_int),
                 ("n_global", C.c_int64), ("col_offset", C.c_int64), ("linesearch", C.c_int),
                 ("unit_a_ctas", C.c_int), ("scd_kernel", C.c_int), ("eta", C.c_double),
-                ("unit_a_host_threads", C.c_int), ("unit_a_host_share", C.c_double)]
+                ("unit_a_host_threads", C.c_int), ("unit_a_host_share", C.c_double), ("scd_async", C.c_int)]
 
 
 class RoundRecord(C.Structure):
@@ -252,7 +252,7 @@ class Problem:
         """(kernel name, W, G, R) of the exact SCD epoch chosen at create."""
         k, w, g, r = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         self._check(lib().duhl_get_scd_shape(self._h, C.byref(k), C.byref(w), C.byref(g), C.byref(r)))
-        return ["k_csc_scd", "k_scd_gram", "k_scd_pipe"][k.value], w.value, g.value, r.value
+        return ["k_csc_scd", "k_scd_gram", "k_scd_pipe", "k_scd_tpa"][k.value], w.value, g.value, r.value
 
     def counters(self):
         a, b, z, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
@@ -265,7 +265,7 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
            refresh_fraction=0.05, cert_every=10, seed=170805357, borrow_host=False, d=None,
            cert_adaptive=True, profile=False, scd_exact=True, n_global=0, col_offset=0,
            linesearch=False, unit_a_ctas=0, scd_kernel=0, eta=0.0, unit_a_host_threads=0,
-           unit_a_host_share=-1.0):
+           unit_a_host_share=-1.0, scd_async=False):
     """duhl_create.  eta: the elastic-net mix (model ELASTIC_NET only).  A: (n, ld) C-contiguous float32 (row i = column a_i of the d x n matrix)."""
     A = np.asarray(A)
     if A.dtype != np.float32 or A.ndim != 2 or not A.flags.c_contiguous:
@@ -282,7 +282,7 @@ def create(A, b_or_y, lam, model, hbm_budget_bytes=0, m=0, device=0, scd_block=0
                          n_global=n_global, col_offset=col_offset, linesearch=int(bool(linesearch)),
                          unit_a_ctas=unit_a_ctas, scd_kernel=scd_kernel, eta=float(eta),
                          unit_a_host_threads=int(unit_a_host_threads),
-                         unit_a_host_share=float(unit_a_host_share))
+                         unit_a_host_share=float(unit_a_host_share), scd_async=int(bool(scd_async)))
     h = C.c_void_p()
     st = lib().duhl_create(C.byref(mat), _p(lab), lam, model, C.byref(cfg), C.byref(h))
     if st != 0:

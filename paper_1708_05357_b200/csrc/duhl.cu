@@ -105,6 +105,11 @@ struct duhl_ctx {
     std::string err;
     int dev = 0, nsm = 0, unit_a_ctas = 0;
     bool pipe = false;  // SCD epoch runs k_scd_pipe (else k_scd_gram); see choose_scd_shape
+    bool tpa = false;   // cfg.scd_async: asynchronous k_scd_tpa epoch (W clusters of tpa_C CTAs)
+    int tpa_C = 1;
+    int64_t tpa_Rc = 0;
+    float* d_vf = nullptr;          // fp32 shadow of the shared vector (asynchronous epoch)
+    double *d_v0t = nullptr, *d_a0t = nullptr;  // v~ and alpha_P at epoch start (exact resync)
     cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
     cudaEvent_t ev_copy = nullptr, ev_snap = nullptr, ev_ref = nullptr;
     // ---- unit A: pinned host store
@@ -676,7 +681,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
                         ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols,
-                        ctx->d_plan_cols, ctx->d_plan_slots};
+                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -711,6 +716,21 @@ static size_t scd_red_bytes(const duhl_ctx* ctx) {
 static void choose_scd_shape(duhl_ctx* ctx) {
     // the unit-A refresh grid keeps its SMs while the epoch runs
     const int64_t sms = std::max<int64_t>(1, ctx->nsm - std::max(0, ctx->unit_a_ctas));
+    if (ctx->cfg.scd_async && !ctx->csc) {
+        // asynchronous epoch: W coordinates in flight, each on a cluster of C CTAs whose row
+        // slices of the column fit in shared memory (<= 200 KB: C4's 803-KB columns take C = 4)
+        int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 16;
+        int C = 1;
+        while (C < 8 && round4((ctx->d4 + C - 1) / C) * 4 > 200 * 1024) C *= 2;
+        W = (int)std::max<int64_t>(1, std::min<int64_t>(W, sms / C));
+        ctx->tpa = true;
+        ctx->tpa_C = C;
+        ctx->tpa_Rc = round4((ctx->d4 + C - 1) / C);
+        ctx->W = W;
+        ctx->G = W * C;
+        ctx->R = (int)ctx->tpa_Rc;
+        return;
+    }
     // pipelined kernel (scd_pipe.cuh): G compute CTAs + 1 control CTA; W <= 32 with 3 (else 4)
     // TMA stages.  Auto (scd_kernel 0) takes it where shared memory allows W >= 24 (short row
     // slices, e.g. C3: 2x fewer blocks than W = 16, measured 14.7 vs 25 ms per pass); at W <= 16
@@ -847,7 +867,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_ref, cudaEventDisableTiming) != cudaSuccess)
         return bail(DUHL_E_CUDA);
-    if (preload_kernels() != cudaSuccess) return bail(DUHL_E_CUDA);  // no lazy loads mid-epoch
+    if (preload_kernels() != cudaSuccess || preload_tpa_kernels() != cudaSuccess)
+        return bail(DUHL_E_CUDA);  // no lazy loads mid-epoch
     if (ctx->csc) {  // ---- sparse: the CSC arrays go to HBM once
         auto dm = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes > 0 ? bytes : 16) == cudaSuccess; };
         if (!dm((void**)&ctx->d_colptr, (n + 1) * sizeof(int64_t)) || !dm((void**)&ctx->d_rows, ctx->nnz * sizeof(int)) ||
@@ -960,6 +981,13 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     ctx->unit_a_ctas = ctx->cfg.unit_a_ctas > 0 ? std::min(ctx->cfg.unit_a_ctas, ctx->nsm / 2)
                        : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 && !ctx->csc) ? 8 : 0;
     choose_scd_shape(ctx);
+    if (ctx->tpa) {
+        if (ctx->tpa_Rc * 4 > 200 * 1024) { ctx->err = "column too long for the asynchronous epoch"; return bail(DUHL_E_INVALID); }
+        if (!dmal((void**)&ctx->d_vf, d4 * sizeof(float)) || !dmal((void**)&ctx->d_v0t, d4 * sizeof(double)) ||
+            !dmal((void**)&ctx->d_a0t, n * sizeof(double)))
+            return bail(DUHL_E_NOMEM);
+        ctx->cfg.linesearch = 1;  // asynchronous rounds take the exact gamma line search
+    }
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)))
         return bail(DUHL_E_NOMEM);
@@ -1143,7 +1171,7 @@ duhl_status duhl_select(duhl_ctx* ctx, duhl_policy policy, int64_t m, int64_t ro
     if (!ctx) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
     TRY(finalize_staging(ctx));
-    ctx->overlap = ctx->write_value != nullptr;
+    ctx->overlap = ctx->write_value != nullptr && !ctx->tpa;
     TRY(select_impl(ctx, policy, m, round, n_swaps_out));
     if (P_out) {
         TRY(ensure_host_P(ctx));
@@ -1169,6 +1197,34 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
         q.eta = ctx->cfg.eta;
         ProfScope ps(ctx, ctx->st, 0, ctx->csc_pass_bytes);
         CK(launch_csc_scd(q, ctx->cfg.scd_exact ? 1 : ctx->csc_warps, ctx->st, &ctx->launches));
+        ctx->updates += L;
+        return DUHL_OK;
+    }
+    if (ctx->tpa) {
+        TpaParams q{};
+        q.model = ctx->model;
+        q.d = ctx->d;
+        q.d4 = ctx->d4;
+        q.n = ctx->n_glob;
+        q.lambda = ctx->lambda;
+        q.eta = ctx->cfg.eta;
+        q.pool = ctx->pool;
+        q.ld_dev = ctx->ld_dev;
+        q.order_j = ctx->d_order_j;
+        q.order_slot = ctx->d_order_slot;
+        q.order_a = ctx->d_order_a;
+        q.L = L;
+        q.norms = ctx->d_norms;
+        q.y = ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr;
+        q.alpha = ctx->d_alpha;
+        q.vf = ctx->d_vf;
+        q.v0 = ctx->d_v0t;
+        q.C = ctx->tpa_C;
+        q.Rc = ctx->tpa_Rc;
+        q.progress = nullptr;  // the asynchronous epoch starts after its columns landed
+        q.err = ctx->d_flag + 1;
+        ProfScope ps(ctx, ctx->st, waits_on_staging ? 5 : 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
+        CK(launch_scd_tpa(q, ctx->W, ctx->st, &ctx->launches));
         ctx->updates += L;
         return DUHL_OK;
     }
@@ -1250,6 +1306,23 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
     return DUHL_OK;
 }
 
+// Asynchronous epoch (cfg.scd_async): start from v~0, alpha_P0 and a zero fp32 shadow of the
+// epoch's updates; end
+// with the exact resync v~ = v~0 + A_P (alpha_P - alpha_P0) in fp64, so gaps and
+// certificates see the exact shared vector whatever the interleaving was.
+static duhl_status tpa_begin(duhl_ctx* ctx, int64_t m) {
+    CK(cudaMemcpyAsync(ctx->d_v0t, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
+    CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, m, ctx->d_a0t, ctx->st, &ctx->launches));
+    CK(cudaMemsetAsync(ctx->d_vf, 0, ctx->d4 * sizeof(float), ctx->st));
+    return DUHL_OK;
+}
+static duhl_status tpa_end(duhl_ctx* ctx, int64_t m) {
+    ProfScope ps(ctx, ctx->st, 1, (double)m * (4.0 * ctx->d4 + 24.0) + 24.0 * ctx->d4);
+    CK(launch_tpa_resync(ctx->pool, ctx->ld_dev, ctx->d_P_slot, ctx->d_P, ctx->d_alpha, ctx->d_a0t, m, ctx->d_v0t,
+                         ctx->d_vt, ctx->d4, ctx->st, &ctx->launches));
+    return DUHL_OK;
+}
+
 // The epoch on the working set.  Staging copies planned by the last select are
 // enqueued after the pass-0 launch when they overlap it (the kernel waits on the
 // progress counter per block), else before it (the compute stream waits).
@@ -1261,6 +1334,7 @@ static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t 
     // the grid leaves (unit_a_ctas) -- never in the way of the grid it feeds
     if (!ctx->overlap) TRY(issue_staging(ctx));
     const bool staged = ctx->overlap && !ctx->copy_plan.empty();  // pass 0 consumes columns as they land
+    if (ctx->tpa) TRY(tpa_begin(ctx, m));
     for (int pass = 0; pass < passes; ++pass) {
         CK(launch_perm_order(ctx->d_P, ctx->d_P_slot, ctx->d_P_batch, m, seed, round, pass,
                              ctx->d_order_j, ctx->d_order_slot, ctx->d_order_batch, ctx->d_order_a,
@@ -1270,6 +1344,7 @@ static duhl_status scd_passes(duhl_ctx* ctx, int passes, uint64_t seed, int64_t 
         TRY(scd_launch(ctx, m, staged && pass == 0));
         if (pass == 0) TRY(issue_staging(ctx));  // no-op unless overlapping: host enqueue overlaps pass 0
     }
+    if (ctx->tpa) TRY(tpa_end(ctx, m));
     return DUHL_OK;
 }
 
@@ -1307,7 +1382,9 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
                              ctx->d_order_batch, ctx->d_order_a, ctx->d_order_inv, ctx->d_order_y,
                              ctx->d_alpha, ctx->d_norms, ctx->model == DUHL_SVM_DUAL ? ctx->d_y : nullptr,
                              ctx->st, &ctx->launches, ridge_ld(ctx)));
+        if (ctx->tpa) TRY(tpa_begin(ctx, ctx->m_cur));
         TRY(scd_launch(ctx, perm_len));
+        if (ctx->tpa) TRY(tpa_end(ctx, ctx->m_cur));
         TRY(issue_staging(ctx));
         TRY(finalize_staging(ctx));
         return check_flag(ctx, "duhl_scd_epoch");
@@ -1537,7 +1614,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     // restores copies-first.
     static const bool no_host_overlap = std::getenv("DUHL_NO_HOST_OVERLAP") != nullptr;
     const bool host_overlap = ctx->hua && !no_host_overlap;
-    ctx->overlap = ctx->write_value != nullptr && (kref == 0 || host_overlap);
+    ctx->overlap = ctx->write_value != nullptr && (kref == 0 || host_overlap) && !ctx->tpa;
     TRY(select_impl(ctx, policy, ctx->m_cfg, t, &swaps));                  // Alg. 2 l.3-4
     {   // rho_{t,P} (Eq. 6) on the gap memory the selection used
         CK(cudaMemsetAsync(ctx->d_rho, 0, 2 * sizeof(double), ctx->st));
@@ -1862,7 +1939,7 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
 
 duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R) {
     if (!ctx) return DUHL_E_INVALID;
-    if (kernel) *kernel = ctx->csc ? 0 : (ctx->pipe ? 2 : 1);
+    if (kernel) *kernel = ctx->csc ? 0 : (ctx->tpa ? 3 : (ctx->pipe ? 2 : 1));
     if (W) *W = ctx->W;
     if (G) *G = ctx->G;
     if (R) *R = ctx->R;

@@ -91,6 +91,39 @@ struct CscScdParams {
     double eta;              // elastic net only
 };
 
+// Asynchronous (TPA-SCD style) dense epoch, scd_tpa.cu: W clusters of C CTAs, CTA rank r of a
+// cluster owns rows [r Rc, (r + 1) Rc) of every column; v~f = fp32 shadow of the shared vector.
+struct TpaParams {
+    int model;
+    int64_t d, d4, n;
+    double lambda, eta;
+    const float* pool;
+    int64_t ld_dev;
+    const int64_t* order_j;    // [L] coordinate at position t
+    const int* order_slot;     // [L] its HBM slot
+    const double* order_a;     // [L] alpha at pass start
+    int64_t L;
+    const double* norms;       // [n]
+    const double* y;           // [n] SVM labels or nullptr
+    double* alpha;             // [n]
+    float* vf;                 // [d4] fp32 shadow of the epoch's updates of v~ (zero at start), REDed
+    const double* v0;          // [d4] v~ at epoch start (fp64)
+    int C;                     // CTAs per cluster
+    int64_t Rc;                // rows per CTA (multiple of 4)
+    const unsigned* progress;  // staging waits (nullptr: columns resident)
+    int stage_ctas;
+    const unsigned* order_batch;
+    int* err;
+};
+size_t tpa_smem_bytes(int64_t Rc);
+cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* launches);
+// v~ = v~0 + A_P (alpha_P - a0) in fp64 over the working set's HBM slots
+cudaError_t launch_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot, const int64_t* P,
+                              const double* alpha, const double* a0, int64_t m, const double* v0, double* vt,
+                              int64_t d4, cudaStream_t st, int64_t* launches);
+cudaError_t launch_f64_to_f32(const double* x, float* y, int64_t k, cudaStream_t st, int64_t* launches);
+cudaError_t preload_tpa_kernels();
+
 __host__ __device__ int scd_nred(int W);
 size_t scd_red_doubles(int W);  // size of ScdParams::red
 size_t scd_smem_bytes(int W, int R, int NB);

@@ -1,0 +1,212 @@
+// scd_tpa.cu -- asynchronous (TPA-SCD style) SCD epoch on a dense working set, sm_100a.
+//
+// The paper's own GPU design (TPA-SCD; App. D, "the shared vector ... is
+// updated atomically"): many coordinates are processed concurrently, each reads the shared
+// vector as it is (stale by the updates in flight), takes the closed-form step (P:804-815
+// Lasso / ridge / elastic net, P:824-827 SVM) and adds delta_j a_j to the shared vector with
+// atomics.  B200 form ("TPA-style bounded-W async"):
+//   * W = number of thread-block clusters = coordinates in flight (the staleness bound); a
+//     cluster of C CTAs splits one coordinate's column by rows (C chosen so a CTA's slice of
+//     the column fits in shared memory: C4's 803-KB columns take C = 4..8), so all SMs stream
+//     while only W coordinates are concurrent;
+//   * per coordinate: each CTA loads its slice of a_j into shared memory (16-byte streamed
+//     loads) while accumulating its part of a_j^T v~ (fp64 accumulation of fp32 products of
+//     the fp32 shadow v~f, read at L2); the C partial dots meet in the leader's shared memory
+//     (distributed shared memory) behind one cluster barrier; every CTA then takes the same
+//     closed-form step and adds delta_j a_j to its rows of v~f with red.global.add.v4.f32
+//     (one 16-byte RED per 4 rows; App. D's atomic update);
+//   * the shared vector during the epoch is v~0 + dvf: v~0 = the exact fp64 vector at epoch
+//     start (L2-resident), dvf = an fp32 shadow of the epoch's own updates (zero at start,
+//     REDed).  s_j = a_j^T v~0 + a_j^T dvf, fp64 accumulation: the fp32 rounding touches only
+//     the epoch's change, which vanishes near the optimum (an fp32 copy of v~ itself held
+//     C3's Lasso above 1e-5: its gap is sensitive to s through B = ||b||^2/(2 lambda d));
+//   * the epoch ends with the exact resync v~ = v~0 + A_P (alpha_P - alpha_P0) in fp64
+//     (k_tpa_resync, SURVEY 8 a6 "Delta v exact"), so the state the gaps and certificates use
+//     is exact to rounding whatever the interleaving was.
+// Pinned by P7s/P8s (disjoint-support orthogonal designs: any interleaving is the sequential
+// epoch) and by convergence to the oracle's optimum (tests/test_gpu_tpa.py).
+#include <cooperative_groups.h>
+
+#include "device.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace duhl {
+
+constexpr int kTpaThreads = 512;
+constexpr int kTpaMaxCluster = 8;
+
+__device__ __forceinline__ void red_add_v4_f32(float* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constant__ TpaParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4* col = reinterpret_cast<float4*>(smem);  // this CTA's slice of a_j
+    __shared__ double part[2][kTpaMaxCluster];      // partial dots (read through the leader's copy)
+    __shared__ double wsum[kTpaThreads / 32];
+    __shared__ double s_delta;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;
+    const int64_t r0 = (int64_t)rank * p.Rc;
+    const int64_t rows = r0 < p.d4 ? (p.d4 - r0 < p.Rc ? p.d4 - r0 : p.Rc) : 0;  // multiple of 4
+    const int n4 = (int)(rows >> 2);
+    double* lead = cl.map_shared_rank(&part[0][0], 0);
+    const double dd = (double)p.d, nn = (double)p.n;
+    int it = 0;
+    unsigned seen = 0;
+    for (int64_t t = cid; t < p.L; t += ncl, ++it) {
+        const int64_t j = p.order_j[t];
+        const int slot = p.order_slot[t];
+        if (p.progress && tid == 0)
+            wait_staged(p.progress, p.stage_ctas, p.order_batch ? p.order_batch[t] : 0u, seen, p.err, 4000000000ull);
+        __syncthreads();
+        const float4* src = reinterpret_cast<const float4*>(p.pool + (int64_t)slot * p.ld_dev + r0);
+        const float4* vf4 = reinterpret_cast<const float4*>(p.vf + r0);
+        const double2* v02 = reinterpret_cast<const double2*>(p.v0 + r0);
+        double acc0 = 0.0, acc1 = 0.0;
+        for (int q = tid; q < n4; q += kTpaThreads) {
+            const float4 a = ld_stream_f4(src + q);
+            col[q] = a;
+            const float4 dv = __ldcg(vf4 + q);  // dvf is being updated by the other clusters: read at L2
+            const double2 u0 = __ldg(v02 + 2 * q), u1 = __ldg(v02 + 2 * q + 1);
+            acc0 = fma((double)a.x, u0.x + (double)dv.x, acc0);
+            acc1 = fma((double)a.y, u0.y + (double)dv.y, acc1);
+            acc0 = fma((double)a.z, u1.x + (double)dv.z, acc0);
+            acc1 = fma((double)a.w, u1.y + (double)dv.w, acc1);
+        }
+        double s = warp_sum(acc0 + acc1);
+        if (lane == 0) wsum[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kTpaThreads / 32; ++w) tot += wsum[w];
+            lead[(it & 1) * kTpaMaxCluster + rank] = tot;  // distributed shared memory store
+        }
+        cl.sync();  // all C partials of coordinate t are in the leader's part[it & 1]
+        if (tid == 0) {
+            double sj = 0.0;
+            for (int r = 0; r < C; ++r) sj += lead[(it & 1) * kTpaMaxCluster + r];  // rank order: same on every CTA
+            const double a_old = p.order_a[t];
+            const double an = coord_step(p.model, a_old, sj, p.norms[j], p.y ? p.y[j] : 0.0, p.lambda, dd, nn, p.eta);
+            s_delta = an - a_old;
+            if (rank == 0) p.alpha[j] = an;
+        }
+        __syncthreads();
+        const float dl = (float)s_delta;
+        if (s_delta != 0.0) {
+            float* vrow = p.vf + r0;
+            for (int q = tid; q < n4; q += kTpaThreads) {
+                const float4 a = col[q];
+                red_add_v4_f32(vrow + 4 * q, dl * a.x, dl * a.y, dl * a.z, dl * a.w);
+            }
+        }
+        __syncthreads();  // the slice buffer is refilled by the next coordinate
+    }
+    cl.sync();  // no CTA leaves while another may still read the leader's partials
+}
+
+// v~ = v~0 + A_P (alpha_P - alpha_P0), fp64 (the exact resync after an asynchronous epoch).
+// CTA: 128 threads x one 4-row group each (512 rows), all m columns of the working set.
+constexpr int kResyncThreads = 128;
+__global__ void __launch_bounds__(kResyncThreads) k_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot,
+                                                               const int64_t* P, const double* alpha,
+                                                               const double* a0, int64_t m, const double* v0,
+                                                               double* vt, int64_t d4) {
+    __shared__ double sda[1024];
+    __shared__ int sslot[1024];
+    const int64_t r4 = (int64_t)blockIdx.x * kResyncThreads + threadIdx.x;
+    const bool act = 4 * r4 < d4;
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    for (int64_t q0 = 0; q0 < m; q0 += 1024) {
+        const int nq = (int)(m - q0 < 1024 ? m - q0 : 1024);
+        __syncthreads();
+        for (int q = threadIdx.x; q < nq; q += kResyncThreads) {
+            sda[q] = alpha[P[q0 + q]] - a0[q0 + q];
+            sslot[q] = P_slot[q0 + q];
+        }
+        __syncthreads();
+        if (!act) continue;
+        for (int q = 0; q < nq; ++q) {
+            const double da = sda[q];
+            if (da == 0.0) continue;
+            const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(pool + (int64_t)sslot[q] * ld_dev) + r4);
+            x0 = fma(da, (double)a.x, x0);
+            x1 = fma(da, (double)a.y, x1);
+            x2 = fma(da, (double)a.z, x2);
+            x3 = fma(da, (double)a.w, x3);
+        }
+    }
+    if (act) {
+        const int64_t r = 4 * r4;
+        vt[r] = v0[r] + x0;
+        vt[r + 1] = v0[r + 1] + x1;
+        vt[r + 2] = v0[r + 2] + x2;
+        vt[r + 3] = v0[r + 3] + x3;
+    }
+}
+
+__global__ void k_f64_to_f32(const double* x, float* y, int64_t k) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) y[i] = (float)x[i];
+}
+
+size_t tpa_smem_bytes(int64_t Rc) { return (size_t)Rc * sizeof(float); }
+
+cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* launches) {
+    if (p.L <= 0) return cudaSuccess;
+    const size_t smem = tpa_smem_bytes(p.Rc);
+    cudaError_t e = cudaFuncSetAttribute(k_scd_tpa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (p.C > 8) {
+        e = cudaFuncSetAttribute(k_scd_tpa, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(W * p.C));
+    cfg.blockDim = dim3(kTpaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_scd_tpa, p);
+    ++*launches;
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot, const int64_t* P,
+                              const double* alpha, const double* a0, int64_t m, const double* v0, double* vt,
+                              int64_t d4, cudaStream_t st, int64_t* launches) {
+    const int64_t n4 = d4 / 4;
+    k_tpa_resync<<<(unsigned)((n4 + kResyncThreads - 1) / kResyncThreads), kResyncThreads, 0, st>>>(
+        pool, ld_dev, P_slot, P, alpha, a0, m, v0, vt, d4);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f64_to_f32(const double* x, float* y, int64_t k, cudaStream_t st, int64_t* launches) {
+    k_f64_to_f32<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(x, y, k);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t preload_tpa_kernels() {
+    const void* fns[] = {(const void*)k_scd_tpa, (const void*)k_tpa_resync, (const void*)k_f64_to_f32};
+    for (const void* f : fns) {
+        cudaFuncAttributes a;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace duhl

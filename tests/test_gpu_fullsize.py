@@ -47,8 +47,9 @@ def test_full_size_rounds_against_oracle(D, name):
     col_bytes = ((d + 3) // 4) * 16
     budget = int(cfg["budget_frac"] * n * col_bytes)
     m = cfg["m"]
-    with D.create(A, lab, lam, model, hbm_budget_bytes=budget, m=m, refresh_fraction=0.10,
-                  seed=170805357 + 3, borrow_host=True, cert_every=1 << 40, scd_exact=False) as P:
+    args, _ = bench.parse_args(["--config", name])
+    kw = bench.launch_kwargs(args, cfg)   # the bench's launch (C3: the asynchronous epoch)
+    with D.create(A, lab, lam, model, cert_every=1 << 40, scd_exact=False, **kw) as P:
         recs = [P.round(t, passes=cfg["passes"]) for t in range(3)]
         a, v, z = P.get_state()
         rng = np.random.default_rng(5)
@@ -90,8 +91,12 @@ def test_full_size_rounds_against_oracle(D, name):
 
 @pytest.mark.parametrize("name,rounds", [("c4", 3), ("c3", 2)])
 def test_bench_launch_rounds_replay_oracle(D, name, rounds):
+    """C4: the bench's exact launch.  C3's bench launch is the asynchronous epoch, whose order is
+    not reproducible; its exact kernel (k_scd_pipe, W = 32, tensor-core Gram tiles, fast mode) is
+    replayed here and the asynchronous launch is held to the invariants of
+    test_full_size_rounds_against_oracle."""
     args, cfg = bench.parse_args(["--config", name])
-    kw = bench.launch_kwargs(args, cfg)
+    kw = dict(bench.launch_kwargs(args, cfg), scd_async=False)
     d, n, model = cfg["d"], cfg["n"], cfg["model"]
     A, lab = bench.make_data(cfg, kw["seed"])
     lam = bench.lam_of(cfg, A, lab)
