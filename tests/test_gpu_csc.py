@@ -175,3 +175,29 @@ def test_P7s_P8s_async_epoch_with_thousands_of_warps(D, model, warps):
     v_want = A64.T @ want - (lab if model == O.LASSO else 0.0)
     np.testing.assert_allclose(v, v_want, rtol=0, atol=1e-12 * max(1.0, np.abs(v_want).max()))
     assert G < 1e-10
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_csc_gap_pass_long_columns_matches_oracle(D, model):
+    """The CSC gap pass at d = 50,000 rows (w = 400 KB fp64, beyond one SM's L1) and 6,000
+    columns against the oracle's dense gaps (s_i to 1e-9 of the conditioning floor), plus the
+    certificate."""
+    d, n = 50000, 6000
+    csc, A, lab, lam = _problem(model, d, n, 0.01, seed=71 + model)
+    rng = np.random.default_rng(3)
+    alpha = _random_state(model, n, lab, rng)
+    B = O.lasso_B(lab, lam) if model == O.LASSO else 0.0
+    with D.create_csc(*csc, d, lab, lam, model) as P:
+        P.set_state(alpha)
+        g_gpu, s_gpu = P.gaps(want_s=True)
+        G, Ob, Db = P.duality_gap()
+    v = O.matvec(A, alpha)
+    w = O.primal_dual_w(model, v, None if model == O.SVM else lab, n, lam)
+    _, s_or, g_or = O.coord_gaps(model, A, alpha, lab if model == O.SVM else None, w, lam, B)
+    An = np.linalg.norm(A.astype(np.float64), axis=1)
+    floor = KAPPA * An * np.linalg.norm(w)
+    assert np.all(np.abs(s_gpu - s_or) <= 1e-9 * np.maximum(np.abs(s_or), floor) + 1e-300)
+    c = (np.abs(alpha) + B) / d if model == O.LASSO else (np.abs(alpha) + 1) / n
+    assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), KAPPA * c * An * np.linalg.norm(w)) + 1e-300)
+    st, G_ref, O_ref, _ = O.duality_gap(model, A, alpha, lab, lam, B)
+    assert abs(G - G_ref) <= 1e-9 * max(1.0, abs(G_ref)) and abs(Ob - O_ref) <= 1e-9 * max(1.0, abs(O_ref))
