@@ -138,6 +138,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+#ifndef DUHL_STAGE_SLEEP_NS
+#define DUHL_STAGE_SLEEP_NS 128
+#endif
 // staging counter c of the gather lives at progress[c * kProgressStride] (own 128-byte line:
 // the polls of the SCD grid and the releases of the other gather CTAs do not share it)
 constexpr int kProgressStride = 32;
@@ -164,7 +167,7 @@ __device__ __forceinline__ bool wait_staged(const unsigned* progress, int stage_
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     unsigned v;
     while ((v = ld_acquire_u32(c)) < thr) {
-        __nanosleep(128);
+        __nanosleep(DUHL_STAGE_SLEEP_NS);
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         if (t1 - t0 > timeout_ns) { atomicOr(err, 1); return false; }

@@ -121,3 +121,29 @@ def test_bench_launch_rounds_replay_oracle(D, name, rounds):
     assert abs(rec.cert_gap - rr["gap"]) <= 1e-6 * rr["gap"], (rec.cert_gap, rr["gap"])
     del A
     gc.collect()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_c1_c2_bench_launch_replay_to_eps(D, name):
+    """C1 (Lasso 2000 x 1000, lambda = 0.1, m = 25 %) and C2 (SVM dual 500 x 20,000, m = 10 %) at
+    their full shapes in the bench's launch configuration: every round until the certified gap
+    <= 1e-5 is replayed by the oracle on the device's band-verified working set; certificates
+    to 1e-8, the final alpha to 1e-9 of its largest entry (exact SCD kernels, fp64)."""
+    args, cfg = bench.parse_args(["--config", name, "--exact"])
+    kw = bench.launch_kwargs(args, cfg)
+    A, lab = bench.make_data(cfg, kw["seed"])
+    lam = bench.lam_of(cfg, A, lab)
+    n = cfg["n"]
+    R = Alg2(cfg["model"], A, lab, lam, kw["m"], args.passes, int(np.ceil(args.refresh * n - 1e-9)), kw["seed"])
+    with D.create(A, lab, lam, cfg["model"], cert_every=1, scd_exact=True, **kw) as P:
+        for t in range(400):
+            rec = P.round(t, passes=args.passes, certify=True)
+            Pd = P.working_set()
+            R.check_selection([Pd], O.SEL_GAP, t)
+            rr = R.round(t, [Pd])
+            assert abs(rec.cert_gap - rr["gap"]) <= 1e-8 * rr["gap"], (t, rec.cert_gap, rr["gap"])
+            if rec.cert_gap <= 1e-5:
+                break
+        a, _, _ = P.get_state()
+    assert rec.cert_gap <= 1e-5, (t, rec.cert_gap)
+    assert np.abs(a - R.alpha).max() <= 1e-9 * max(1e-300, np.abs(R.alpha).max())
