@@ -438,7 +438,7 @@ def run_duhl(args, cfg, rank, world, local):
     barrier(world)
     torch.cuda.synchronize()
     c0 = P.counters()
-    k0 = {k: P.kernel_stats(k) for k in range(6)}
+    k0 = {k: P.kernel_stats(k) for k in range(7)}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     swaps = refreshed = 0
     with ClockSampler(local) as clk:
@@ -460,7 +460,7 @@ def run_duhl(args, cfg, rank, world, local):
             "zero_copy_bytes_per_step": (c1["zc_bytes"] - c0["zc_bytes"]) / args.steps,
             "achieved_GBps": pcie_bytes / (elapsed / args.steps) / 1e9,
             "peak_GBps": pcie_peak, "frac": pcie_bytes / (elapsed / args.steps) / 1e9 / pcie_peak}
-    k1 = {k: P.kernel_stats(k) for k in range(6)}
+    k1 = {k: P.kernel_stats(k) for k in range(7)}
     # kernel-only SCD roofline: extra passes over the working set now resident in HBM
     # (no staging waits inside the launch), outside the timed region
     P.scd_epoch(passes=3, seed=12345, round=10 ** 6)
@@ -471,9 +471,9 @@ def run_duhl(args, cfg, rank, world, local):
     P.close()
     updates = args.steps * m * args.passes * world
     value = updates / elapsed
-    ms = {k: k1[k][1] - k0[k][1] for k in range(6)}
-    nl = {k: k1[k][0] - k0[k][0] for k in range(6)}
-    by = {k: k1[k][2] - k0[k][2] for k in range(6)}
+    ms = {k: k1[k][1] - k0[k][1] for k in range(7)}
+    nl = {k: k1[k][0] - k0[k][0] for k in range(7)}
+    by = {k: k1[k][2] - k0[k][2] for k in range(7)}
     peak, peak_src = hbm_peak()
     scd_gbs = by[0] / (ms[0] / 1e3) / 1e9 if ms[0] > 0 else None
     gap_gbs = by[1] / (ms[1] / 1e3) / 1e9 if ms[1] > 0 else None
@@ -641,7 +641,7 @@ def run_duhl(args, cfg, rank, world, local):
                                          "note": "3 passes over the HBM-resident working set after the "
                                                  "timed rounds (no staging waits in the launch)"},
             "gap_pass_GBps": gap_gbs, "scd_GBps": scd_gbs,
-            "kernel_ms": {"scd": ms[0], "scd_overlapped_staging": ms[5], "gap_zP": ms[1], "topm": ms[2],
+            "kernel_ms": {"scd": ms[0], "scd_overlapped_staging": ms[5], "tpa_resync": ms[6], "gap_zP": ms[1], "topm": ms[2],
                           "stage_h2d": ms[3],
                           "refresh_unitA": ms[4]},
             "refresh_GBps": (by[4] / (ms[4] / 1e3) / 1e9) if ms[4] > 0 else None,

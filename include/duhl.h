@@ -285,7 +285,8 @@ duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out);
  * stream: copy engine or the k_stage_gather kernel), 4 = unit-A refresh gap pass (its own stream,
  * concurrent with SCD), 5 = SCD epoch launches that consume staged columns as they land (pass 0
  * of a round whose staging overlaps the epoch: bound by the staging, not by HBM; kind 0 then
- * holds only the launches that wait for nothing).  *launches = timed launches, *ms = summed
+ * holds only the launches that wait for nothing), 6 = the exact fp64 resync after an asynchronous
+ * epoch (cfg.scd_async).  *launches = timed launches, *ms = summed
  * CUDA-event milliseconds, *bytes = summed ALGORITHMIC bytes (DESIGN.md
  * "Roofline"): SCD  L (4 d4 + 24) + 16 d4;  gap  k (4 d4 + 24) + 8 d4 tiles;
  * top-m  8 n x passes;  staging  columns x 4 d4. */

@@ -162,8 +162,8 @@ struct duhl_ctx {
     struct Timed { cudaEvent_t a, b; int kind; double bytes; };
     std::vector<Timed> pending;
     std::vector<cudaEvent_t> event_pool;
-    int64_t st_launch[6] = {0, 0, 0, 0, 0, 0};
-    double st_ms[6] = {0, 0, 0, 0, 0, 0}, st_bytes[6] = {0, 0, 0, 0, 0, 0};
+    int64_t st_launch[7] = {0, 0, 0, 0, 0, 0, 0};
+    double st_ms[7] = {0, 0, 0, 0, 0, 0, 0}, st_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
     double* d_s_acc2 = nullptr;  // partial-dot accumulator of the concurrent refresh pass
     // ---- unit A on host threads (cfg.unit_a_host_threads): a_i^T v~ for part of the refresh
     HostUnitA* hua = nullptr;
@@ -1317,7 +1317,7 @@ static duhl_status tpa_begin(duhl_ctx* ctx, int64_t m) {
     return DUHL_OK;
 }
 static duhl_status tpa_end(duhl_ctx* ctx, int64_t m) {
-    ProfScope ps(ctx, ctx->st, 1, (double)m * (4.0 * ctx->d4 + 24.0) + 24.0 * ctx->d4);
+    ProfScope ps(ctx, ctx->st, 6, (double)m * (4.0 * ctx->d4 + 24.0) + 24.0 * ctx->d4);
     CK(launch_tpa_resync(ctx->pool, ctx->ld_dev, ctx->d_P_slot, ctx->d_P, ctx->d_alpha, ctx->d_a0t, m, ctx->d_v0t,
                          ctx->d_vt, ctx->d4, ctx->st, &ctx->launches));
     return DUHL_OK;
@@ -1925,7 +1925,7 @@ duhl_status duhl_get_stream(duhl_ctx* ctx, void** stream_out) {
 
 duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, double* ms,
                                   double* bytes) {
-    if (!ctx || kind < 0 || kind > 5) return DUHL_E_INVALID;
+    if (!ctx || kind < 0 || kind > 6) return DUHL_E_INVALID;
     CK(cudaSetDevice(ctx->dev));
     CK(cudaStreamSynchronize(ctx->st));
     CK(cudaStreamSynchronize(ctx->cst));

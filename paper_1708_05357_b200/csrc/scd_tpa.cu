@@ -110,44 +110,45 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
     cl.sync();  // no CTA leaves while another may still read the leader's partials
 }
 
-// v~ = v~0 + A_P (alpha_P - alpha_P0), fp64 (the exact resync after an asynchronous epoch).
-// CTA: 128 threads x one 4-row group each (512 rows), all m columns of the working set.
+// v~ += A_P (alpha_P - alpha_P0), fp64 (the exact resync after an asynchronous epoch; v~ was
+// reset to v~0 first).  Grid (row groups, column chunks): CTA (x, y) takes 512 rows (one 4-row
+// group per thread) and kResyncChunk columns of P, accumulates in fp64 and adds its partial with
+// fp64 atomics -- enough CTAs to stream A_P at HBM rate (one CTA per 512 rows alone left C3's 40k
+// rows on 79 SMs).
 constexpr int kResyncThreads = 128;
+constexpr int kResyncChunk = 512;
 __global__ void __launch_bounds__(kResyncThreads) k_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot,
                                                                const int64_t* P, const double* alpha,
-                                                               const double* a0, int64_t m, const double* v0,
-                                                               double* vt, int64_t d4) {
-    __shared__ double sda[1024];
-    __shared__ int sslot[1024];
+                                                               const double* a0, int64_t m, double* vt, int64_t d4) {
+    __shared__ double sda[kResyncChunk];
+    __shared__ int sslot[kResyncChunk];
     const int64_t r4 = (int64_t)blockIdx.x * kResyncThreads + threadIdx.x;
-    const bool act = 4 * r4 < d4;
+    const int64_t q0 = (int64_t)blockIdx.y * kResyncChunk;
+    const int nq = (int)(m - q0 < kResyncChunk ? m - q0 : kResyncChunk);
+    int nz = 0;
+    for (int q = threadIdx.x; q < nq; q += kResyncThreads) {
+        sda[q] = alpha[P[q0 + q]] - a0[q0 + q];
+        sslot[q] = P_slot[q0 + q];
+    }
+    __syncthreads();
+    if (4 * r4 >= d4) return;
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-    for (int64_t q0 = 0; q0 < m; q0 += 1024) {
-        const int nq = (int)(m - q0 < 1024 ? m - q0 : 1024);
-        __syncthreads();
-        for (int q = threadIdx.x; q < nq; q += kResyncThreads) {
-            sda[q] = alpha[P[q0 + q]] - a0[q0 + q];
-            sslot[q] = P_slot[q0 + q];
-        }
-        __syncthreads();
-        if (!act) continue;
-        for (int q = 0; q < nq; ++q) {
-            const double da = sda[q];
-            if (da == 0.0) continue;
-            const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(pool + (int64_t)sslot[q] * ld_dev) + r4);
-            x0 = fma(da, (double)a.x, x0);
-            x1 = fma(da, (double)a.y, x1);
-            x2 = fma(da, (double)a.z, x2);
-            x3 = fma(da, (double)a.w, x3);
-        }
+    for (int q = 0; q < nq; ++q) {
+        const double da = sda[q];
+        if (da == 0.0) continue;
+        ++nz;
+        const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(pool + (int64_t)sslot[q] * ld_dev) + r4);
+        x0 = fma(da, (double)a.x, x0);
+        x1 = fma(da, (double)a.y, x1);
+        x2 = fma(da, (double)a.z, x2);
+        x3 = fma(da, (double)a.w, x3);
     }
-    if (act) {
-        const int64_t r = 4 * r4;
-        vt[r] = v0[r] + x0;
-        vt[r + 1] = v0[r + 1] + x1;
-        vt[r + 2] = v0[r + 2] + x2;
-        vt[r + 3] = v0[r + 3] + x3;
-    }
+    if (nz == 0) return;
+    const int64_t r = 4 * r4;
+    atomicAdd(vt + r, x0);
+    atomicAdd(vt + r + 1, x1);
+    atomicAdd(vt + r + 2, x2);
+    atomicAdd(vt + r + 3, x3);
 }
 
 __global__ void k_f64_to_f32(const double* x, float* y, int64_t k) {
@@ -186,9 +187,11 @@ cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* 
 cudaError_t launch_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot, const int64_t* P,
                               const double* alpha, const double* a0, int64_t m, const double* v0, double* vt,
                               int64_t d4, cudaStream_t st, int64_t* launches) {
+    cudaError_t e = cudaMemcpyAsync(vt, v0, d4 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess || m <= 0) return e;
     const int64_t n4 = d4 / 4;
-    k_tpa_resync<<<(unsigned)((n4 + kResyncThreads - 1) / kResyncThreads), kResyncThreads, 0, st>>>(
-        pool, ld_dev, P_slot, P, alpha, a0, m, v0, vt, d4);
+    const dim3 grid((unsigned)((n4 + kResyncThreads - 1) / kResyncThreads), (unsigned)((m + kResyncChunk - 1) / kResyncChunk));
+    k_tpa_resync<<<grid, kResyncThreads, 0, st>>>(pool, ld_dev, P_slot, P, alpha, a0, m, vt, d4);
     ++*launches;
     return cudaGetLastError();
 }

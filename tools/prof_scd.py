@@ -22,6 +22,7 @@ ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--lasso", action="store_true")
 ap.add_argument("--fast", action="store_true")
 ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 warp-specialised, 2 pipelined")
+ap.add_argument("--async_W", type=int, default=0, help="> 0: the asynchronous TPA-style epoch with W in flight")
 a = ap.parse_args()
 if a.lasso:
     A = np.empty((a.n, a.d), dtype=np.float32)
@@ -32,8 +33,9 @@ else:
     A = np.empty((a.n, a.d), dtype=np.float32)
     lab = synth.svm_fill(A, a.d, a.n, 5)
     model, lam = D.SVM_DUAL, 1.0 / 40000
-P = D.create(A, lab, lam, model, profile=True, scd_block=a.W, scd_ctas=a.ctas, borrow_host=True,
-             scd_exact=not a.fast, scd_kernel=a.kernel)
+P = D.create(A, lab, lam, model, profile=True, scd_ctas=a.ctas, borrow_host=True,
+             **({} if a.async_W else {"scd_block": a.W}),
+             scd_exact=not a.fast, scd_kernel=a.kernel, scd_async=a.async_W > 0, **({"scd_block": a.async_W} if a.async_W else {}))
 P.select(D.SEL_GAP, m=a.n)
 t0 = time.perf_counter()
 P.scd_epoch(passes=a.passes, seed=1)
