@@ -203,6 +203,8 @@ duhl_status duhl_scd_epoch(duhl_ctx* ctx, int passes, uint64_t seed, int64_t rou
 /* Certificate (Eq. 2 = sum of Eq. 4 terms) at the current state over all n
  * columns, plus the primal objective O(alpha) and the dual value D so that
  * gap = O - D (D per App. E conjugates).  Any output may be NULL.
+ * The per-coordinate gaps it computes also refresh the whole gap memory z (a full
+ * unit-A pass, Alg. 2 l.7-10; reading R25).
  * Errors: DUHL_E_NUMERIC, DUHL_E_BOUND (Lasso max|alpha_i| > B), DUHL_E_CUDA. */
 duhl_status duhl_duality_gap(duhl_ctx* ctx, double* gap, double* primal, double* dual);
 

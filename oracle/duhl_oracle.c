@@ -504,7 +504,8 @@ int or_solve_scd(int model, const float* A, i64 d, i64 n, i64 ld, const double* 
  *     4. unit B: `passes` randomized SCD passes over P, permutation
  *        key(seed, t, pass, j); alpha and v~ updated in place (gamma = 1)    (l.6, l.11)
  *     5. z_P := gap_P(alpha^(t+1))                                              (R9)
- *     6. every cert_every rounds: certificate; stop at gap <= eps
+ *     6. every cert_every rounds: certificate; its per-coordinate gaps refresh all of z (R25);
+ *        stop at gap <= eps
  * Trace arrays (length >= max_rounds, may be NULL): swaps, certified gap (-1 if
  * not computed that round). */
 /* w from the shared vector: Lasso w = v~ (P:855 with v~ = A alpha - b),
@@ -597,6 +598,11 @@ int or_duhl_solve(const or_duhl_cfg* cfg, const float* A, i64 d, i64 n, i64 ld,
             int s6 = or_duality_gap(model, A, d, n, ld, alpha, b_or_y, lambda, B, &gap, NULL, NULL);
             if (trace_gap) trace_gap[t] = gap;
             if (s6 != OR_OK) { st = s6; break; }
+            /* reading R25: a certificate is a full unit-A pass (Alg. 2 l.7-10 over every j): its
+             * gaps at the current state enter the gap memory */
+            or_shadow_w(model, vt, d, n, lambda, w);
+            int s7 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
+            if (s7 != OR_OK) { st = s7; break; }
             if (gap <= cfg->eps) { st = OR_OK; ++t; break; }
         }
     }
@@ -814,6 +820,11 @@ int or_duhl_solve_cocoa(const or_duhl_cfg* cfg, int K, int linesearch, const flo
             int s6 = or_duality_gap(model, A, d, n, ld, alpha, b_or_y, lambda, B, &gap, NULL, NULL);
             if (trace_gap) trace_gap[t] = gap;
             if (s6 != OR_OK) { st = s6; break; }
+            /* reading R25: a certificate is a full unit-A pass (Alg. 2 l.7-10 over every j): its
+             * gaps at the current state enter the gap memory */
+            or_shadow_w(model, vt, d, n, lambda, w);
+            int s7 = or_coord_gaps(model, A, d, n, ld, alpha, y, w, lambda, B, NULL, n, NULL, z);
+            if (s7 != OR_OK) { st = s7; break; }
             if (gap <= cfg->eps) { st = OR_OK; ++t; break; }
         }
     }

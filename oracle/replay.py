@@ -151,4 +151,7 @@ class Alg2:
         if certify:
             st, gap, _, _ = O.duality_gap(model, A, self.alpha, self.lab, lam, self.B, d=d)
             assert st == O.OK
+            # R25: the certificate's gaps at the current state refresh the whole gap memory
+            st, _, self.z = O.coord_gaps(model, A, self.alpha, self.y, self.w(), lam, self.B, d=d)
+            assert st == O.OK
         return dict(gap=gap, gamma=gamma, swaps=swaps)

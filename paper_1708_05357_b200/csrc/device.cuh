@@ -149,7 +149,8 @@ constexpr int kProgressStride = 32;
 // need = 0: resident.  stage_ctas = 0: copy-engine staging, one monotone sequence
 // counter progress[0] (need = the copy's sequence number; seen caches the last value
 // read).  stage_ctas = G > 0: the gather kernel k_stage_gather, plan entry q = need - 1
-// landed once progress[(q % G) * kProgressStride] > q / G.  After the acquire, a proxy fence orders the
+// landed once progress[(q % G) * kProgressStride] > q / G; a token with the high bit set is a
+// column the copy engine stages beside the gather (sequence number on progress[16 * stride]).  After the acquire, a proxy fence orders the
 // generic-proxy stores of the gather before this thread's async-proxy (TMA) reads.
 // Bounded: after timeout_ns the wait gives up and sets *err (bit 0).
 __device__ __forceinline__ bool wait_staged(const unsigned* progress, int stage_ctas, unsigned need,
@@ -157,7 +158,10 @@ __device__ __forceinline__ bool wait_staged(const unsigned* progress, int stage_
     if (!progress || need == 0) return true;
     const unsigned* c = progress;
     unsigned thr = need;
-    if (stage_ctas > 0) {
+    if (stage_ctas > 0 && (need & 0x80000000u)) {  // a column the copy engine stages (sequence number)
+        c = progress + (size_t)16 * kProgressStride;
+        thr = need & 0x7fffffffu;
+    } else if (stage_ctas > 0) {
         c = progress + (size_t)((need - 1) % (unsigned)stage_ctas) * kProgressStride;
         thr = (need - 1) / (unsigned)stage_ctas + 1;
     } else if (need <= seen) {

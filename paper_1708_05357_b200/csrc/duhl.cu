@@ -31,7 +31,11 @@ using namespace duhl;
 namespace {
 constexpr int kGapTileRows = 4096;
 constexpr int kStageCtas = 16;  // k_stage_gather CTAs (2 per SM the SCD grid leaves): 51.4 GB/s alone (stage2.cu)
-constexpr size_t kProgressBytes = 16 * 128;  // staging counters, one 128-byte line each (kProgressStride)
+constexpr unsigned kCeToken = 0x80000000u;  // wait token of a column the copy engine stages
+constexpr int kCeCounter = 16;              // its progress counter (sequence numbers)
+constexpr double kStageCeShare = 0.3;       // share of a gather round's columns on the copy engine
+constexpr size_t kProgressBytes = 17 * 128;  // staging counters, one 128-byte line each (kProgressStride):
+                                             // 16 gather CTAs + the copy-engine share (kCeCounter)
 inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
 }  // namespace
 
@@ -108,9 +112,12 @@ struct duhl_ctx {
     bool tpa = false;   // cfg.scd_async: asynchronous k_scd_tpa epoch (W clusters of tpa_C CTAs)
     int tpa_C = 1;
     int64_t tpa_Rc = 0;
+    bool tpa_v0s = false;
     float* d_vf = nullptr;          // fp32 shadow of the shared vector (asynchronous epoch)
     double *d_v0t = nullptr, *d_a0t = nullptr;  // v~ and alpha_P at epoch start (exact resync)
     cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
+    cudaStream_t cst2 = nullptr;     // copy-engine share of a gather round's staging
+    cudaEvent_t ev_copy2 = nullptr;
     cudaEvent_t ev_copy = nullptr, ev_snap = nullptr, ev_ref = nullptr;
     // ---- unit A: pinned host store
     float* h_store = nullptr;
@@ -194,7 +201,7 @@ struct duhl_ctx {
     double *d_order_a = nullptr, *d_order_inv = nullptr, *d_order_y = nullptr;
     std::vector<int64_t> pend_cols;      // staged columns not yet in the device table
     std::vector<int> pend_slots;
-    struct Copy { int64_t col; int slot; unsigned seq; };
+    struct Copy { int64_t col; int slot; unsigned seq; };  // gather rounds: seq = wait token
     std::vector<Copy> copy_plan;         // planned, not yet enqueued staging copies
 };
 
@@ -462,19 +469,46 @@ static duhl_status issue_staging(duhl_ctx* ctx) {
         const size_t col_bytes = (size_t)ctx->ld_dev * sizeof(float);
         ProfScope ps(ctx, ctx->cst, 3, (double)(np * col_bytes));
         cudaEventSynchronize(ctx->ev_plan);  // the previous upload has read the pinned plan
+        size_t ng = 0;
+        bool any_ce = false;
         for (size_t q = 0; q < np; ++q) {
-            ctx->h_plan_cols[q] = ctx->copy_plan[q].col;
-            ctx->h_plan_slots[q] = ctx->copy_plan[q].slot;
+            const auto& c = ctx->copy_plan[q];
+            if (c.seq & kCeToken) {  // the copy engine's share, on its own stream: one copy + one
+                                     // progress write per column (the PCIe link takes both paths)
+                any_ce = true;
+                if (cudaMemcpyAsync(ctx->pool + (int64_t)c.slot * ctx->ld_dev, ctx->h_store + c.col * ctx->ld_host,
+                                    col_bytes, cudaMemcpyHostToDevice, ctx->cst2) != cudaSuccess ||
+                    ctx->write_value(ctx->cst2,
+                                     (unsigned long long)(uintptr_t)(ctx->d_progress + (size_t)kCeCounter * kProgressStride),
+                                     c.seq & ~kCeToken, 0) != 0) {
+                    rc = fail(ctx, DUHL_E_CUDA, "staging copy (copy-engine share) failed");
+                    break;
+                }
+                continue;
+            }
+            ctx->h_plan_cols[ng] = c.col;
+            ctx->h_plan_slots[ng] = c.slot;
+            ++ng;
         }
-        if (cudaMemcpyAsync(ctx->d_plan_cols, ctx->h_plan_cols, np * sizeof(int64_t), cudaMemcpyHostToDevice,
-                            ctx->cst) != cudaSuccess ||
-            cudaMemcpyAsync(ctx->d_plan_slots, ctx->h_plan_slots, np * sizeof(int), cudaMemcpyHostToDevice,
-                            ctx->cst) != cudaSuccess ||
-            cudaEventRecord(ctx->ev_plan, ctx->cst) != cudaSuccess ||
-            launch_stage_gather(ctx->h_alias, ctx->ld_host, ctx->pool, ctx->ld_dev, ctx->ld_dev, ctx->d_plan_cols,
-                                ctx->d_plan_slots, (int64_t)np, ctx->d_progress, ctx->stage_ctas, ctx->cst,
-                                &ctx->launches) != cudaSuccess)
+        if (rc == DUHL_OK &&
+            (cudaMemcpyAsync(ctx->d_plan_cols, ctx->h_plan_cols, ng * sizeof(int64_t), cudaMemcpyHostToDevice,
+                             ctx->cst) != cudaSuccess ||
+             cudaMemcpyAsync(ctx->d_plan_slots, ctx->h_plan_slots, ng * sizeof(int), cudaMemcpyHostToDevice,
+                             ctx->cst) != cudaSuccess ||
+             cudaEventRecord(ctx->ev_plan, ctx->cst) != cudaSuccess ||
+             launch_stage_gather(ctx->h_alias, ctx->ld_host, ctx->pool, ctx->ld_dev, ctx->ld_dev, ctx->d_plan_cols,
+                                 ctx->d_plan_slots, (int64_t)ng, ctx->d_progress, ctx->stage_ctas, ctx->cst,
+                                 &ctx->launches) != cudaSuccess))
             rc = fail(ctx, DUHL_E_CUDA, "staging gather launch failed");
+        if (rc != DUHL_OK) {  // let a waiting epoch drain: every token reads as landed
+            std::vector<unsigned> big(kProgressBytes / sizeof(unsigned), 0x7fffffffu);
+            cudaMemcpy(ctx->d_progress, big.data(), kProgressBytes, cudaMemcpyHostToDevice);
+        }
+        if (any_ce) {
+            cudaEventRecord(ctx->ev_copy2, ctx->cst2);
+            cudaStreamWaitEvent(ctx->cst, ctx->ev_copy2, 0);
+        }
+        ps.end();
         ctx->h2d_bytes += (int64_t)(np * col_bytes);
         ctx->copy_plan.clear();
         cudaEventRecord(ctx->ev_copy, ctx->cst);
@@ -609,15 +643,21 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // every earlier copy has landed before this round's epoch (the compute stream waited on
         // ev_copy): kept slots need no wait
         std::fill(ctx->slot_batch.begin(), ctx->slot_batch.end(), 0u);
-        // light rounds that overlap the epoch: zero-copy gather by kStageCtas CTAs on the SMs the
+        // light rounds: zero-copy gather by kStageCtas CTAs on the SMs the
         // SCD grid leaves to unit A (faster than per-column copies); entry q + 1 is the
         // column's wait token.  The counters are zeroed on the compute stream before this round's
         // epoch can poll them.
         static const bool force_ce = std::getenv("DUHL_STAGE_CE") != nullptr;
         static const int nstage = std::getenv("DUHL_STAGE_CTAS") ? std::max(1, std::min(16, std::atoi(std::getenv("DUHL_STAGE_CTAS"))))
                                                                : kStageCtas;  // developer override (<= 16 counters)
-        ctx->stage_ctas = (ctx->overlap && !heavy && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
+        // (also when the copies complete before the epoch: the gather is the faster path either way)
+        ctx->stage_ctas = (!heavy && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
         if (ctx->stage_ctas > 0) CK(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, ctx->st));
+        // share of a gather round's columns copied by the copy engine beside the gather kernel
+        static const double ce_share_cfg = std::getenv("DUHL_STAGE_CE_SHARE") ? std::atof(std::getenv("DUHL_STAGE_CE_SHARE"))
+                                                                              : kStageCeShare;
+        const double ce_share = ctx->write_value ? std::max(0.0, std::min(0.9, ce_share_cfg)) : 0.0;
+        unsigned nce = 0, ngath = 0;
         size_t fi = 0;
         const unsigned heavy_seq = ctx->overlap && heavy ? ctx->batch_seq + 1 : 0u;
         for (size_t q = 0; q < news.size(); ++q) {
@@ -628,7 +668,10 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             ctx->pend_cols.push_back(j);
             ctx->pend_slots.push_back(s);
             unsigned seq = 0;
-            if (ctx->stage_ctas > 0) seq = (unsigned)q + 1;
+            if (ctx->stage_ctas > 0) {  // every k-th column (Bresenham on the share) to the copy engine
+                const bool ce = std::floor((double)(q + 1) * ce_share) > std::floor((double)q * ce_share);
+                seq = ce ? (kCeToken | (unsigned)++nce) : (unsigned)++ngath;
+            }
             else if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
             ctx->slot_batch[s] = seq;
             ctx->copy_plan.push_back({j, s, seq});
@@ -639,6 +682,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
+        CK(cudaStreamWaitEvent(ctx->cst2, ctx->ev_copy, 0));
     } else {  // everything resident: bookkeeping on the device
         CK(cudaMemcpyAsync(ctx->d_P, P.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         TRY(resident_commit(ctx, m, swaps));
@@ -671,6 +715,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
 static void free_all(duhl_ctx* ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->cst) cudaStreamSynchronize(ctx->cst);
+    if (ctx->cst2) cudaStreamSynchronize(ctx->cst2);
     if (ctx->rst) cudaStreamSynchronize(ctx->rst);
     void* dev_ptrs[] = {ctx->pool, ctx->d_col_slot, ctx->d_alpha, ctx->d_vt, ctx->d_b, ctx->d_y,
                         ctx->d_norms, ctx->d_z, ctx->d_P, ctx->d_order_j, ctx->d_cols,
@@ -704,6 +749,8 @@ static void free_all(duhl_ctx* ctx) {
 
     if (ctx->st) cudaStreamDestroy(ctx->st);
     if (ctx->cst) cudaStreamDestroy(ctx->cst);
+    if (ctx->cst2) cudaStreamDestroy(ctx->cst2);
+    if (ctx->ev_copy2) cudaEventDestroy(ctx->ev_copy2);
 }
 
 static size_t scd_red_bytes(const duhl_ctx* ctx) {
@@ -722,6 +769,10 @@ static void choose_scd_shape(duhl_ctx* ctx) {
         int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 16;
         int C = 1;
         while (C < 8 && round4((ctx->d4 + C - 1) / C) * 4 > 200 * 1024) C *= 2;
+        if (const char* e = std::getenv("DUHL_TPA_CLUSTER"))  // developer override (power of 2, <= 8)
+            C = std::max(C, std::min(8, std::atoi(e)));
+        // v~0's slice in shared memory too where it fits (12 bytes per row with the column slice)
+        ctx->tpa_v0s = round4((ctx->d4 + C - 1) / C) * 12 <= 200 * 1024;
         W = (int)std::max<int64_t>(1, std::min<int64_t>(W, sms / C));
         ctx->tpa = true;
         ctx->tpa_C = C;
@@ -862,6 +913,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     ctx->nsm = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->cst2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_copy2, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->rst, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_snap, cudaEventDisableTiming) != cudaSuccess ||
@@ -1219,6 +1272,7 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
         q.alpha = ctx->d_alpha;
         q.vf = ctx->d_vf;
         q.v0 = ctx->d_v0t;
+        q.v0_smem = ctx->tpa_v0s ? 1 : 0;
         q.C = ctx->tpa_C;
         q.Rc = ctx->tpa_Rc;
         q.progress = nullptr;  // the asynchronous epoch starts after its columns landed
@@ -1419,7 +1473,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
         if (kg > 0) {
             CK(cudaMemcpyAsync(ctx->d_cols, gcols.data(), kg * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
             CK(cudaEventRecord(ctx->ev_g0, ctx->st));
-            TRY(run_gaps(ctx, ctx->d_cols, kg, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+            TRY(run_gaps(ctx, ctx->d_cols, kg, nullptr, nullptr, ctx->d_sums, /*write_z=*/true));
             CK(cudaEventRecord(ctx->ev_g1, ctx->st));
         }
         const double host_s = hua_wait(ctx->hua);
@@ -1427,7 +1481,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
         GapParams hp = gap_params(ctx, ctx->d_hcols, kh);
         hp.s_acc = ctx->d_hs;
         hp.sums = ctx->d_sums;
-        hp.z = nullptr;
+        hp.z = ctx->d_z;  // R25: the certificate's gaps refresh the gap memory
         CK(launch_gap_finalize(hp, ctx->st, &ctx->launches));
         CK(cudaStreamSynchronize(ctx->st));  // gcols is pageable and local
         float gms = 0.0f;  // balance the next certificate: both units end together
@@ -1438,7 +1492,7 @@ static duhl_status certificate(duhl_ctx* ctx, double* gap, double* primal, doubl
         }
         ctx->hua_cols += kh;
     } else {
-        TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/false));
+        TRY(run_gaps(ctx, nullptr, ctx->n, nullptr, nullptr, ctx->d_sums, /*write_z=*/true));
     }
     TRY(allreduce(ctx, ctx->d_sums, 3));           // per-column sums over the shards
     TRY(allreduce(ctx, ctx->d_sums + 3, 1, ncclMax));

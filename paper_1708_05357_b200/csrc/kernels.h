@@ -108,6 +108,7 @@ struct TpaParams {
     double* alpha;             // [n]
     float* vf;                 // [d4] fp32 shadow of the epoch's updates of v~ (zero at start), REDed
     const double* v0;          // [d4] v~ at epoch start (fp64)
+    int v0_smem;               // 1: the CTA's slice of v0 is held in shared memory
     int C;                     // CTAs per cluster
     int64_t Rc;                // rows per CTA (multiple of 4)
     const unsigned* progress;  // staging waits (nullptr: columns resident)
@@ -115,7 +116,7 @@ struct TpaParams {
     const unsigned* order_batch;
     int* err;
 };
-size_t tpa_smem_bytes(int64_t Rc);
+size_t tpa_smem_bytes(int64_t Rc, bool v0_smem);
 cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* launches);
 // v~ = v~0 + A_P (alpha_P - a0) in fp64 over the working set's HBM slots
 cudaError_t launch_tpa_resync(const float* pool, int64_t ld_dev, const int* P_slot, const int64_t* P,

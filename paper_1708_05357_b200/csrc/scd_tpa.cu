@@ -45,6 +45,9 @@ __device__ __forceinline__ void red_add_v4_f32(float* addr, float a, float b, fl
 __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constant__ TpaParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4* col = reinterpret_cast<float4*>(smem);  // this CTA's slice of a_j
+    // p.v0_smem: the CTA's slice of v~0 (constant during the epoch) also in shared memory, read
+    // once instead of once per coordinate from L2
+    double2* v0s = reinterpret_cast<double2*>(smem + (size_t)p.Rc * sizeof(float));
     __shared__ double part[2][kTpaMaxCluster];      // partial dots (read through the leader's copy)
     __shared__ double wsum[kTpaThreads / 32];
     __shared__ double s_delta;
@@ -56,6 +59,11 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
     const int64_t rows = r0 < p.d4 ? (p.d4 - r0 < p.Rc ? p.d4 - r0 : p.Rc) : 0;  // multiple of 4
     const int n4 = (int)(rows >> 2);
     double* lead = cl.map_shared_rank(&part[0][0], 0);
+    if (p.v0_smem) {
+        const double2* g = reinterpret_cast<const double2*>(p.v0 + r0);
+        for (int q = tid; q < 2 * n4; q += kTpaThreads) v0s[q] = g[q];
+        __syncthreads();
+    }
     const double dd = (double)p.d, nn = (double)p.n;
     int it = 0;
     unsigned seen = 0;
@@ -67,13 +75,14 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
         __syncthreads();
         const float4* src = reinterpret_cast<const float4*>(p.pool + (int64_t)slot * p.ld_dev + r0);
         const float4* vf4 = reinterpret_cast<const float4*>(p.vf + r0);
-        const double2* v02 = reinterpret_cast<const double2*>(p.v0 + r0);
+        const double2* v02 = p.v0_smem ? v0s : reinterpret_cast<const double2*>(p.v0 + r0);
         double acc0 = 0.0, acc1 = 0.0;
         for (int q = tid; q < n4; q += kTpaThreads) {
             const float4 a = ld_stream_f4(src + q);
             col[q] = a;
             const float4 dv = __ldcg(vf4 + q);  // dvf is being updated by the other clusters: read at L2
-            const double2 u0 = __ldg(v02 + 2 * q), u1 = __ldg(v02 + 2 * q + 1);
+            const double2 u0 = p.v0_smem ? v02[2 * q] : __ldg(v02 + 2 * q);
+            const double2 u1 = p.v0_smem ? v02[2 * q + 1] : __ldg(v02 + 2 * q + 1);
             acc0 = fma((double)a.x, u0.x + (double)dv.x, acc0);
             acc1 = fma((double)a.y, u0.y + (double)dv.y, acc1);
             acc0 = fma((double)a.z, u1.x + (double)dv.z, acc0);
@@ -156,11 +165,11 @@ __global__ void k_f64_to_f32(const double* x, float* y, int64_t k) {
     if (i < k) y[i] = (float)x[i];
 }
 
-size_t tpa_smem_bytes(int64_t Rc) { return (size_t)Rc * sizeof(float); }
+size_t tpa_smem_bytes(int64_t Rc, bool v0_smem) { return (size_t)Rc * (v0_smem ? 12 : 4); }
 
 cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* launches) {
     if (p.L <= 0) return cudaSuccess;
-    const size_t smem = tpa_smem_bytes(p.Rc);
+    const size_t smem = tpa_smem_bytes(p.Rc, p.v0_smem != 0);
     cudaError_t e = cudaFuncSetAttribute(k_scd_tpa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (p.C > 8) {
