@@ -201,3 +201,25 @@ def test_csc_gap_pass_long_columns_matches_oracle(D, model):
     assert np.all(np.abs(g_gpu - g_or) <= TOL * np.maximum(np.abs(g_or), KAPPA * c * An * np.linalg.norm(w)) + 1e-300)
     st, G_ref, O_ref, _ = O.duality_gap(model, A, alpha, lab, lam, B)
     assert abs(G - G_ref) <= 1e-9 * max(1.0, abs(G_ref)) and abs(Ob - O_ref) <= 1e-9 * max(1.0, abs(O_ref))
+
+
+def test_P7_hadamard_csc_async_converges_to_closed_form(D):
+    """Hadamard columns stored as CSC (every entry nonzero) on the asynchronous CSC epoch with
+    1,024 warps in flight: repeated passes reach the unique alpha* = soft(A^T b, lambda d)/d."""
+    d, n = 2048, 1024
+    A = synth.hadamard_columns(d, n)
+    cp = np.arange(n + 1, dtype=np.int64) * d
+    rows = np.tile(np.arange(d, dtype=np.int32), n)
+    vals = A.ravel().astype(np.float32)
+    rng = np.random.default_rng(0)
+    b = rng.integers(-3, 4, size=d).astype(np.float64)
+    lam = 0.1
+    c = A.astype(np.float64) @ b
+    astar = np.sign(c) * np.maximum(np.abs(c) - lam * d, 0) / d
+    with D.create_csc(cp, rows, vals, d, b, lam, D.LASSO, m=n, scd_exact=False, scd_ctas=1024) as P:
+        P.select(D.SEL_GAP, m=n)
+        P.scd_epoch(passes=20, seed=1)
+        a, _, _ = P.get_state()
+        g, _, _ = P.duality_gap()
+    np.testing.assert_allclose(a, astar, rtol=0, atol=1e-9)
+    assert g < 1e-9

@@ -97,3 +97,24 @@ def test_async_duhl_solve_reaches_the_oracle_optimum(D, model, budget_cols):
     ref = O.solve_scd(model, A, lab, lam, 1e-9, 20000)
     _, _, O_ref, _ = O.duality_gap(model, A, ref[1], lab, lam, B)
     assert abs(Ob - O_ref) <= 1e-4 * abs(O_ref)
+
+
+@pytest.mark.parametrize("W", [16, 128])
+def test_P7_hadamard_async_converges_to_closed_form(D, W):
+    """Hadamard design (A^T A = d I: the Lasso optimum alpha* = soft(A^T b, lambda d)/d is unique,
+    P7): the asynchronous epoch is not exact in one pass here (partial column updates are visible
+    to the other coordinates), but repeated passes must reach alpha* (strongly convex problem)."""
+    d, n = 2048, 1024
+    A = synth.hadamard_columns(d, n)
+    rng = np.random.default_rng(0)
+    b = rng.integers(-3, 4, size=d).astype(np.float64)
+    lam = 0.1
+    c = A.astype(np.float64) @ b
+    astar = np.sign(c) * np.maximum(np.abs(c) - lam * d, 0) / d
+    with D.create(A, b, lam, D.LASSO, m=n, scd_async=True, scd_block=W) as P:
+        P.select(D.SEL_GAP, m=n)
+        P.scd_epoch(passes=20, seed=1)
+        a, v, _ = P.get_state()
+        g, _, _ = P.duality_gap()
+    np.testing.assert_allclose(a, astar, rtol=0, atol=1e-9)
+    assert g < 1e-9

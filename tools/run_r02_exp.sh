@@ -12,3 +12,8 @@ done
 timeout 900 python tools/tpa_vs_exact.py c3 128 > gpurun_out/exp_tpa_c1.log 2>&1; tail -1 gpurun_out/exp_tpa_c1.log
 DUHL_TPA_CLUSTER=4 timeout 900 python tools/tpa_vs_exact.py c3 35 > gpurun_out/exp_tpa_c4.log 2>&1; tail -1 gpurun_out/exp_tpa_c4.log
 DUHL_TPA_CLUSTER=2 timeout 900 python tools/tpa_vs_exact.py c3 70 > gpurun_out/exp_tpa_c2.log 2>&1; tail -1 gpurun_out/exp_tpa_c2.log
+export DUHL_NO_HOST_OVERLAP=1
+B3="python bench.py --steps 2 --warmup 6 --no-e2e --no-cpu --no-baselines --no-oracle-tte"
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02_launches_c4.csv $B3 > gpurun_out/r02_ncu_launch_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_gather -c 1 -o gpurun_out/r02_stage_gather_c4 -f $B3 > gpurun_out/r02_ncu_gather.log 2>&1
+tail -n 2 gpurun_out/r02_ncu_launch_c4.log gpurun_out/r02_ncu_gather.log

@@ -1,5 +1,9 @@
-# round-2 ncu evidence: launch lists of the C4 / C3 bench steps, --set full of the dominant kernels
+# round-2 ncu evidence: launch lists of the C4 / C3 bench steps, --set full of the dominant kernels.
+# ncu serialises kernels, so a pass-0 epoch that waits for staged columns could only time out:
+# the profiled runs stage before the epoch (DUHL_NO_HOST_OVERLAP=1; same kernels, including the
+# gather) -- their per-launch times, not the step overlap, are what these lists show.
 set -x
+export DUHL_NO_HOST_OVERLAP=1
 B="python bench.py --steps 3 --warmup 5 --no-e2e --no-cpu --no-baselines --no-oracle-tte"
 for c in c4 c3; do
   timeout 900 $B --config $c > gpurun_out/r02_small_$c.log 2>&1 && \
