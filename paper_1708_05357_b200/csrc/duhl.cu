@@ -652,7 +652,14 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
                                                                : kStageCtas;  // developer override (<= 16 counters)
         // (also when the copies complete before the epoch: the gather is the faster path either way)
         ctx->stage_ctas = (!heavy && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
+        // every round that overlaps (or gathers) starts from zeroed counters: gather CTA 0's counter
+        // is the copy engine's sequence counter progress[0], so a heavy (copy-engine) round after
+        // a gather round would otherwise see the gather's final count as landed copies
+#ifndef DUHL_EXP_OLD_PROGRESS_RESET  // developer: the round-2 bug, kept reproducible for the regression test
+        if (ctx->stage_ctas > 0 || ctx->overlap) CK(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, ctx->st));
+#else
         if (ctx->stage_ctas > 0) CK(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, ctx->st));
+#endif
         // share of a gather round's columns copied by the copy engine beside the gather kernel
         static const double ce_share_cfg = std::getenv("DUHL_STAGE_CE_SHARE") ? std::atof(std::getenv("DUHL_STAGE_CE_SHARE"))
                                                                               : kStageCeShare;

@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(kStageThreads) k_stage_gather(const float* hos
             for (int u = 0; u < kStageUnroll; ++u) dst[i + u * kStageThreads] = x[u];
         }
         for (; i < n4; i += kStageThreads) dst[i] = ld_stream_f4(src + i);
-        __threadfence();  // this thread's stores, device-wide, before the CTA's release below
+        // the consumer reads the slot with the TMA engine (async proxy): order this thread's
+        // generic-proxy stores before the async proxy, then device-wide before the release
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) st_release_gpu_u32(progress + (size_t)blockIdx.x * kProgressStride, ++done);
     }

@@ -728,3 +728,38 @@ def test_select_multi_cta_large_n_with_ties(D, n, m):
     with D.create(A, np.ones(4), 0.1, D.LASSO, m=m, seed=9) as P:
         sel_u, _ = P.select(D.SEL_UNIFORM, m=m, round=3)
     assert sel_u.tolist() == np.sort(O.select_policy(O.SEL_UNIFORM, n, m, 3, 9)).tolist()
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_heavy_round_after_gather_rounds(D, model):
+    """Regression (round 2): a heavy round (more than m/2 new columns: copy-engine staging with one
+    progress write) right after light rounds staged by the gather kernel, with the epoch
+    overlapping the copies (host unit-A threads).  The bug: gather CTA 0's counter is the copy
+    engine's sequence counter, so the heavy round read its columns before they landed (seen in a
+    C4 solve, where a certificate's fresh gaps (R25) swung the selection into a heavy round).
+    Deterministic here: importance-sampling rounds keep 350 high-norm columns and swap ~50
+    others (light, gathered), then a sequential block replaces the whole working set (heavy).
+    Long columns (200,000 rows) keep the copies in flight when the epoch starts.  After every
+    round v = A alpha (- b) to rounding, and the round is the oracle's on the same set."""
+    d, n, m = 200_000, 1600, 400
+    A, lab = _data(model, d, n, seed=808 + model)
+    A[1000:1350] *= 10.0                      # always drawn by the importance sampling (prob ~ ||a||^2)
+    lam = _lam(model, n)
+    pols = [O.SEL_IMPORTANCE] * 5 + [O.SEL_SEQUENTIAL] + [O.SEL_IMPORTANCE] * 3 + [O.SEL_SEQUENTIAL]
+    R = Alg2(model, A, lab, lam, m, 1, 80, 5)
+    swaps = []
+    with D.create(A, lab, lam, model, hbm_budget_bytes=450 * ((d + 3) // 4) * 16, m=m, refresh_fraction=0.05,
+                  cert_every=1 << 30, seed=5, unit_a_host_threads=2, scd_exact=True) as P:
+        for t, pol in enumerate(pols):
+            rec = P.round(t, passes=1, policy=pol)
+            swaps.append(rec.swaps)
+            Pd = P.working_set()
+            R.check_selection([Pd], pol, t)
+            R.round(t, [Pd], certify=False)
+            a, v, _ = P.get_state()
+            nz = np.flatnonzero(a)
+            v_ok = O.matvec(np.ascontiguousarray(A[nz]), a[nz]) - (lab if model != O.SVM else 0.0)
+            assert np.abs(v - v_ok).max() <= 1e-10 * max(1.0, np.abs(v_ok).max()), (t, swaps)
+            assert np.abs(a - R.alpha).max() <= 1e-9 * max(1e-300, np.abs(R.alpha).max()), (t, swaps)
+    # the scenario happened: heavy rounds right after light, gathered ones
+    assert swaps[5] * 2 > m and swaps[9] * 2 > m and 0 < swaps[4] * 2 <= m and 0 < swaps[8] * 2 <= m, swaps
