@@ -241,6 +241,23 @@ def pin_host(A):
     return 0
 
 
+def state_check(P, A, lab, cfg):
+    """Outside the timed region: the solved state's shared vector against A alpha (- b) recomputed
+    in fp64 by torch on the GPU from the host matrix (v is what the certificate used)."""
+    if isinstance(A, Sparse):
+        return None
+    import torch
+    a, v, _ = P.get_state()
+    nz = np.flatnonzero(a)
+    out = torch.zeros(A.shape[1], dtype=torch.float64, device="cuda")
+    At = torch.from_numpy(A)
+    for k in range(0, len(nz), 2048):
+        idx = torch.from_numpy(nz[k:k + 2048])
+        out += At.index_select(0, idx).cuda().double().t() @ torch.from_numpy(a[nz[k:k + 2048]]).cuda()
+    ref = out.cpu().numpy() - (0.0 if cfg["model"] == 1 else lab)
+    return {"max_abs_v_minus_A_alpha": float(np.abs(v - ref).max()), "max_abs_v": float(np.abs(ref).max())}
+
+
 def rho_mean(trace):
     """Mean rho_{t,P} (Eq. 6) over a solve's rounds (on the gap memory, DESIGN R21)."""
     return float(np.mean([t.rho for t in trace])) if trace else None
@@ -532,10 +549,11 @@ def run_duhl(args, cfg, rank, world, local):
             t_solve = time.perf_counter() - t1
             wall = time.perf_counter() - t0
             c2 = P2.counters()
+            state_err = state_check(P2, A, lab, cfg) if rep == 0 else None
             P2.close()
             c2["updates"] = int(max_over_ranks(c2["updates"], world)) * world
             runs.append(dict(r=r, c=c2, t_create=t_c2, t_solve=max_over_ranks(t_solve, world),
-                             wall=max_over_ranks(wall, world)))
+                             wall=max_over_ranks(wall, world), state_err=state_err))
         order = sorted(range(len(runs)), key=lambda q: runs[q]["t_solve"])
         med = runs[order[len(runs) // 2]]
         r, c2, wall = med["r"], med["c"], med["wall"]
@@ -550,6 +568,7 @@ def run_duhl(args, cfg, rank, world, local):
                "rho_mean": rho_mean(r["trace"]),
                "swaps_per_round_first_last": swaps_trend(r["trace"]),
                "create_s": med["t_create"],
+               "state_check": runs[0]["state_err"],
                "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
                        "from the caller's pinned host buffers (used in place; one device pass over A for "
                        "norms + z at alpha=0) + duhl_solve to the certified gap); time_to_eps_s = "

@@ -433,7 +433,7 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols, host):
             R.check_selection([Pd], policy, t)
             rr = R.round(t, [Pd])
             assert rec.swaps == rr["swaps"], t
-            assert abs(rec.cert_gap - rr["gap"]) <= 1e-8 * rr["gap"], (t, rec.cert_gap, rr["gap"])
+            assert abs(rec.cert_gap - rr["gap"]) <= 1e-8 * rr["gap"] + 1e-13, (t, rec.cert_gap, rr["gap"])
         a, v, _ = P.get_state()
     assert np.abs(a - R.alpha).max() <= 1e-9 * max(1e-300, np.abs(R.alpha).max())
 
@@ -584,7 +584,7 @@ def test_aggregation_linesearch_matches_oracle(D, model, with_comm):
             R.check_selection([Pd], O.SEL_GAP, t)
             rr = R.round(t, [Pd])
             assert abs(rec.gamma - rr["gamma"]) <= 1e-8, (t, rec.gamma, rr["gamma"])
-            assert abs(rec.cert_gap - rr["gap"]) <= 1e-7 * rr["gap"], (t, rec.cert_gap, rr["gap"])
+            assert abs(rec.cert_gap - rr["gap"]) <= 1e-7 * rr["gap"] + 1e-13, (t, rec.cert_gap, rr["gap"])
 
 
 def _run_shards(D, parts, body):
@@ -646,7 +646,7 @@ def test_virtual_shards_match_oracle_cocoa(D, model, budget_cols, K):
         for k in range(K):   # replicated scalars: every rank reports the same gamma and certificate
             rec = out[k][0][t]
             assert abs(rec.gamma - rr["gamma"]) <= 1e-8, (t, k, rec.gamma, rr["gamma"])
-            assert abs(rec.cert_gap - rr["gap"]) <= 1e-7 * rr["gap"], (t, k, rec.cert_gap, rr["gap"])
+            assert abs(rec.cert_gap - rr["gap"]) <= 1e-7 * rr["gap"] + 1e-13, (t, k, rec.cert_gap, rr["gap"])
     a = np.concatenate([out[k][2] for k in range(K)])
     assert np.abs(a - R.alpha).max() <= 1e-7 * max(1e-300, np.abs(R.alpha).max())
     for k in range(K):   # v replicated and equal to the oracle's
