@@ -126,7 +126,6 @@ struct duhl_ctx {
     bool csc = false;
     int64_t nnz = 0;
     int64_t* d_colptr = nullptr;
-    int* d_split = nullptr;         // CSC: nonzeros per column in rows < d/2 (two-half gap pass)
     int* d_rows = nullptr;
     float* d_vals = nullptr;
     std::vector<int64_t> h_colptr;  // host copy of col_ptr (algorithmic byte counts)
@@ -404,10 +403,7 @@ static duhl_status run_gaps(duhl_ctx* ctx, const int64_t* d_cols, int64_t k, dou
                       : d_cols == ctx->d_P ? ctx->csc_pass_bytes
                       : (double)p.k * (8.0 * (double)ctx->nnz / (double)ctx->n + 24.0);
     ProfScope ps(ctx, sx, stream ? 4 : 1, by);
-    // CSC: two row halves (each gathering from an L1-sized half of v) where enabled
-    static const bool halves = std::getenv("DUHL_CSC_HALVES") != nullptr;
-    if (ctx->csc) CK(launch_csc_gap(p, cscmat(ctx), max_ctas, sx, &ctx->launches,
-                                    halves && p.k >= 4096 ? ctx->d_split : nullptr));
+    if (ctx->csc) CK(launch_csc_gap(p, cscmat(ctx), max_ctas, sx, &ctx->launches));
     else CK(launch_gap_pass(p, tile_rows, sx, &ctx->launches, max_ctas));
     return DUHL_OK;
 }
@@ -737,7 +733,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
                         ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols,
-                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t, ctx->d_split};
+                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -1121,12 +1117,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     if (!ok2) { cudaGetLastError(); ctx->err = "device setup failed"; return bail(DUHL_E_CUDA); }
     // ---- precompute (a1): B, initial shared vector, then ONE pass over A for ||a_i||^2 and
     // z = the exact gaps at alpha = 0 (SVM: 1/n; regression: from a_i^T (-b))
-    if (ctx->csc) {
-        ck(launch_csc_norms(cscmat(ctx), n, ctx->d_norms, st, &ctx->launches));
-        if (cudaMalloc((void**)&ctx->d_split, n * sizeof(int)) == cudaSuccess)
-            ck(launch_csc_split(cscmat(ctx), n, (int)(d / 2), ctx->d_split, st, &ctx->launches));
-        else { cudaGetLastError(); ctx->d_split = nullptr; }
-    }
+    if (ctx->csc) ck(launch_csc_norms(cscmat(ctx), n, ctx->d_norms, st, &ctx->launches));
     if (model == DUHL_LASSO) {
         double h[2] = {0, 0};
         ck(cudaMemsetAsync(ctx->d_sums, 0, 8 * sizeof(double), st));

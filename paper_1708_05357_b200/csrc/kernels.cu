@@ -1504,20 +1504,14 @@ __global__ void __launch_bounds__(256) k_csc_norms(CscMat A, int64_t n, double* 
 }
 
 // s_i = sum_k a_ki (wscale vt_k) over the column's nonzeros, then the gap (as k_gap_tile).
-// The gathers of vt go through L1 (__ldg).  HALF = 0 / 1 (d > kCscHalfRows... see
-// launch_csc_gap): only the nonzeros with row < / >= d/2 (split[i] = their count below), so the
-// half of vt a launch gathers fits in L1 -- half 0 stores its partial dot in s_acc, half 1 adds
-// and finishes the gap.  HALF = -1: the whole column in one launch.
-template <int HALF>
-__global__ void __launch_bounds__(256) k_csc_gap(GapParams p, CscMat A, const int* split) {
+__global__ void __launch_bounds__(256) k_csc_gap(GapParams p, CscMat A) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     SumAcc acc;
     int flag = 0;
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.k; t += nw) {
         const int64_t i = p.cols ? p.cols[t] : t;
-        const int64_t c0 = A.col_ptr[i], c1 = A.col_ptr[i + 1];
-        const int64_t k0 = HALF == 1 ? c0 + split[i] : c0, k1 = HALF == 0 ? c0 + split[i] : c1;
+        const int64_t k0 = A.col_ptr[i], k1 = A.col_ptr[i + 1];
         double s0 = 0.0, s1 = 0.0;
         int64_t k = k0 + lane;
         for (; k + 32 < k1; k += 64) {  // two independent gathers in flight per lane
@@ -1528,36 +1522,9 @@ __global__ void __launch_bounds__(256) k_csc_gap(GapParams p, CscMat A, const in
         }
         if (k < k1) s0 = fma((double)ld_stream_f32(A.vals + k), __ldg(p.vt + ld_stream_i32(A.rows + k)) * p.wscale, s0);
         const double s = warp_sum(s0 + s1);
-        if (lane == 0) {
-            if (HALF == 0) p.s_acc[t] = s;
-            else if (HALF == 1) {
-                const double tot = p.s_acc[t] + s;
-                p.s_acc[t] = 0.0;
-                gap_finish_one(p, t, i, tot, acc, flag);
-            } else gap_finish_one(p, t, i, s, acc, flag);
-        }
+        if (lane == 0) gap_finish_one(p, t, i, s, acc, flag);
     }
-    if (HALF != 0) block_flush_sums(p, acc, flag);
-}
-
-// split[i] = nonzeros of column i with row < half (rows sorted)
-__global__ void k_csc_split(CscMat A, int64_t n, int half, int* split) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t lo = A.col_ptr[i], hi = A.col_ptr[i + 1];
-    const int64_t c0 = lo;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (A.rows[mid] < half) lo = mid + 1; else hi = mid;
-    }
-    split[i] = (int)(lo - c0);
-}
-
-cudaError_t launch_csc_split(const CscMat& A, int64_t n, int half, int* split, cudaStream_t st, int64_t* launches) {
-    if (n <= 0) return cudaSuccess;
-    k_csc_split<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(A, n, half, split);
-    ++*launches;
-    return cudaGetLastError();
+    block_flush_sums(p, acc, flag);
 }
 
 __global__ void __launch_bounds__(256) k_csc_scd(CscScdParams p) {
@@ -1608,19 +1575,12 @@ cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches,
-                           const int* split) {
+cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches) {
     if (p.k <= 0) return cudaSuccess;
     unsigned g = csc_grid(p.k);
     if (max_ctas > 0 && g > (unsigned)max_ctas) g = (unsigned)max_ctas;
-    if (split) {  // two row halves, each gathering from an L1-sized half of vt
-        k_csc_gap<0><<<g, 256, 0, st>>>(p, A, split);
-        k_csc_gap<1><<<g, 256, 0, st>>>(p, A, split);
-        *launches += 2;
-    } else {
-        k_csc_gap<-1><<<g, 256, 0, st>>>(p, A, nullptr);
-        ++*launches;
-    }
+    k_csc_gap<<<g, 256, 0, st>>>(p, A);
+    ++*launches;
     return cudaGetLastError();
 }
 
@@ -1692,7 +1652,7 @@ cudaError_t preload_kernels() {
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,
-        (const void*)k_csc_norms,   (const void*)k_csc_gap<-1>, (const void*)k_csc_gap<0>, (const void*)k_csc_gap<1>, (const void*)k_csc_split,      (const void*)k_csc_scd,
+        (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
         (const void*)k_csc_matvec,  (const void*)k_topm_hist,    (const void*)k_topm_pick,
         (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write,
         (const void*)k_resident_select, (const void*)k_stage_gather};

@@ -163,10 +163,7 @@ size_t pipe_smem_bytes(int W, int R, int NS);
 cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t preload_kernels();
 cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStream_t st, int64_t* launches);
-// split (nullptr: one pass): launch_csc_split's table for the two-row-half form
-cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches,
-                           const int* split = nullptr);
-cudaError_t launch_csc_split(const CscMat& A, int64_t n, int half, int* split, cudaStream_t st, int64_t* launches);
+cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches);
 cudaError_t launch_csc_scd(const CscScdParams& p, int warps, cudaStream_t st, int64_t* launches);
 // vt += A alpha over the columns with alpha != 0 (fp64 REDs)
 cudaError_t launch_csc_matvec(const CscMat& A, const double* alpha, int64_t n, double* vt, cudaStream_t st,
