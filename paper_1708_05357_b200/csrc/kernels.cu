@@ -702,7 +702,9 @@ struct RedOut {
     double* buf;
     int grp;
     __device__ __forceinline__ void add(int q, double v) const {
+#ifndef DUHL_EXP_NORED  // developer timing experiment only: results are wrong without the REDs
         atomicAdd(&buf[((size_t)q * kRedGroups + grp) * kRedStride], v);
+#endif
     }
 };
 
@@ -745,6 +747,9 @@ __device__ __forceinline__ void tile4(const float* __restrict__ Aj, const float*
         float2 g2[4 * KW];
 #pragma unroll
         for (int e = 0; e < 4 * KW; ++e) g2[e] = make_float2(0.f, 0.f);
+#ifdef DUHL_EXP_NOFMA  // developer timing experiment only: no tile arithmetic
+        hi = lo;
+#endif
         for (int r4 = (lo >> 2) + lane; r4 < (hi >> 2); r4 += 32) {
             float4 x[4], y[KW];
 #pragma unroll
@@ -995,7 +1000,11 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(const __grid_consta
             const double a_in = pf_a, inv_in = pf_inv, y_in = pf_y;
             if (b + 1 < nblk) prefetch_coords(b + 1);
             stamp(0);
+#ifdef DUHL_EXP_ALLPOLL
+            if (true) {
+#else
             if (lane == 0) {
+#endif
                 // A CTA may ARRIVE(b+1) before another has ARRIVEd(b), but never ARRIVE(b+2)
                 // before WAIT(b) completed everywhere: one counter per block parity counts
                 // exactly the arrivals of blocks b, b-2, b-4, ...
@@ -1012,7 +1021,9 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_gram(const __grid_consta
                         break;
                     }
                 }
+#ifndef DUHL_EXP_ALLPOLL
                 __threadfence();
+#endif
             }
             __syncwarp();
             stamp(2);
