@@ -134,6 +134,10 @@ typedef struct {
     double time_s;            /* wall seconds since duhl_solve entry (duhl_round: duration of the round) */
     double rho;               /* rho_{t,P} (Eq. 6) on the gap memory at selection time:
                                  (mean of z over P) / (mean of z over this rank's columns); 1 if z = 0 */
+    double gap_est;           /* estimate of the duality gap after the round from fresh gaps only:
+                                 sum of z over P + (n - m) x the mean z of this round's refreshed
+                                 columns outside P (summed over ranks); -1 when no refresh ran.
+                                 duhl_solve's adaptive certificates use it (else z_sum) */
 } duhl_round_record;
 
 /* Fills *cfg with defaults: budget 0, m 0, device 0, auto SCD shape,

@@ -50,7 +50,7 @@ class Config(C.Structure):
 class RoundRecord(C.Structure):
     _fields_ = [("round", C.c_int64), ("swaps", C.c_int64), ("refreshed", C.c_int64),
                 ("cert_gap", C.c_double), ("z_sum", C.c_double), ("gamma", C.c_double),
-                ("time_s", C.c_double), ("rho", C.c_double)]
+                ("time_s", C.c_double), ("rho", C.c_double), ("gap_est", C.c_double)]
 
 
 TRACE_CB = C.CFUNCTYPE(None, C.POINTER(RoundRecord), C.c_void_p)

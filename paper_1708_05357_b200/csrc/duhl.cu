@@ -137,6 +137,8 @@ struct duhl_ctx {
     int* d_stamp = nullptr;         // [n] id of the select that last took column j
     unsigned long long* d_rsel = nullptr;  // [2] swaps, nnz over P
     double* d_rho = nullptr;               // [2] sum of z over P, over all columns (round record rho)
+    double* d_est = nullptr;               // [4] gap estimate: sum z over P, over the sample, counts
+    int64_t* d_smp = nullptr;              // [n] this round's refreshed columns outside P (the sample)
     int sel_id = 0;
     int64_t m_cur = 0;              // |P|
     bool P_host_valid = true;
@@ -733,7 +735,8 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
                         ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols,
-                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t};
+                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t, ctx->d_est,
+                        ctx->d_smp};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
@@ -1049,7 +1052,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         ctx->cfg.linesearch = 1;  // asynchronous rounds take the exact gamma line search
     }
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
-        !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)))
+        !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)) ||
+        !dmal((void**)&ctx->d_est, 4 * sizeof(double)) || !dmal((void**)&ctx->d_smp, n * sizeof(int64_t)))
         return bail(DUHL_E_NOMEM);
     if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
     if (!ctx->csc && ctx->cfg.unit_a_host_threads > 0) {  // unit A on host threads (duhl.h)
@@ -1685,6 +1689,8 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     }
     auto tstaged = now();
     std::vector<int64_t> idx(kref);
+    static thread_local std::vector<int64_t> smp;
+    smp.clear();
     int64_t kg = kref, kh = 0, nonres = 0;  // refresh columns on the GPU / host threads; non-resident
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
     if (agg) {  // round-start state for the aggregation: v0 and alpha_P
@@ -1700,6 +1706,11 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         for (int64_t q = 0; q < kref; ++q) {
             idx[q] = (ctx->cursor + q) % n;
             host_cols += ctx->col_slot[idx[q]] < 0;
+        }
+        if (ctx->P_host_valid) {  // the refreshed columns outside P: a systematic sample of fresh gaps
+            smp.clear();
+            for (int64_t q = 0; q < kref; ++q)
+                if (!ctx->inP[idx[q]]) smp.push_back(idx[q]);
         }
         ctx->cursor = (ctx->cursor + kref) % n;
         nonres = host_cols;
@@ -1767,6 +1778,27 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     CK(cudaMemsetAsync(ctx->d_sums + 6, 0, sizeof(double), ctx->st));
     CK(launch_sum(ctx->d_z, n, ctx->d_sums + 6, ctx->st, &ctx->launches));
     TRY(allreduce(ctx, ctx->d_sums + 6, 1));
+    // Gap estimate for the adaptive certificates: z_P is fresh (R9) and the refreshed columns
+    // outside P are a systematic sample of fresh gaps of the other n - m columns, so
+    //   est = sum_P z + (n - m) mean_sample z   (every term at most one round old),
+    // where the plain sum of z mixes in gaps up to 1/f rounds stale.
+    double est[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool have_est = !smp.empty();
+    if (have_est) {
+        CK(cudaMemsetAsync(ctx->d_est, 0, 4 * sizeof(double), ctx->st));
+        CK(launch_gather_f64(ctx->d_z, ctx->d_P, m, ctx->d_gap_out, ctx->st, &ctx->launches));
+        CK(launch_sum(ctx->d_gap_out, m, ctx->d_est, ctx->st, &ctx->launches));
+        CK(cudaMemcpyAsync(ctx->d_smp, smp.data(), smp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        CK(launch_gather_f64(ctx->d_z, ctx->d_smp, (int64_t)smp.size(), ctx->d_s_out, ctx->st, &ctx->launches));
+        CK(launch_sum(ctx->d_s_out, (int64_t)smp.size(), ctx->d_est + 1, ctx->st, &ctx->launches));
+        const double cnt[2] = {(double)smp.size(), (double)(n - m)};
+        CK(cudaMemcpyAsync(ctx->d_est + 2, cnt, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+    }
+    if (ctx->group || ctx->comm) {  // every rank takes part (a rank without a sample adds zeros)
+        if (!have_est) CK(cudaMemsetAsync(ctx->d_est, 0, 4 * sizeof(double), ctx->st));
+        TRY(allreduce(ctx, ctx->d_est, 4));
+    }
+    CK(d2h_copy(ctx, est, ctx->d_est, 4 * sizeof(double), ctx->st));
     double zs = 0.0, rs[2] = {0.0, 0.0};
     CK(d2h_copy(ctx, &zs, ctx->d_sums + 6, sizeof(double), ctx->st));
     CK(d2h_copy(ctx, rs, ctx->d_rho, 2 * sizeof(double), ctx->st));
@@ -1789,6 +1821,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->gamma = gamma;
         rec->time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         rec->rho = (rs[1] > 0.0 && m > 0) ? (rs[0] / (double)m) / (rs[1] / (double)n) : 1.0;
+        rec->gap_est = est[2] > 0.0 ? est[0] + est[3] * est[1] / est[2] : -1.0;
     }
     if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0) {
         // balance: the host's columns take as long as what PCIe carries this round (staging
@@ -1841,7 +1874,7 @@ duhl_status duhl_solve(duhl_ctx* ctx, double eps, int64_t max_rounds, int passes
         bool adapt = want(zs);
         duhl_round_record r{};
         TRY(round_impl(ctx, t, passes, policy, (sched || adapt) ? 1 : 0, &r));
-        zs = r.z_sum;
+        zs = r.gap_est >= 0.0 ? r.gap_est : r.z_sum;  // the sampled estimate where a refresh ran
         if (r.cert_gap >= 0.0) {
             gap = r.cert_gap;
             if (adapt && !sched && gap > eps) failed(gap, zs);  // both at the end of round t

@@ -763,3 +763,33 @@ def test_heavy_round_after_gather_rounds(D, model):
             assert np.abs(a - R.alpha).max() <= 1e-9 * max(1e-300, np.abs(R.alpha).max()), (t, swaps)
     # the scenario happened: heavy rounds right after light, gathered ones
     assert swaps[5] * 2 > m and swaps[9] * 2 > m and 0 < swaps[4] * 2 <= m and 0 < swaps[8] * 2 <= m, swaps
+
+
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_round_gap_estimate(D, model):
+    """duhl_round_record.gap_est = sum_P z + (n - m) x mean z over this round's refreshed columns
+    outside P (-1 when the refreshed chunk lies inside P): it tracks the certified gap of the
+    same round (within a factor of 4 here) on a replayed trajectory."""
+    d, n, m = (300, 2000, 400) if model == O.LASSO else (120, 2000, 400)
+    A, lab = _data(model, d, n, seed=95)
+    lam = _lam(model, n)
+    kref = 200
+    R = Alg2(model, A, lab, lam, m, 2, kref, 6)
+    seen = []
+    with D.create(A, lab, lam, model, hbm_budget_bytes=450 * d * 4, m=m, refresh_fraction=kref / n,
+                  cert_every=1 << 30, seed=6) as P:
+        for t in range(10):
+            rec = P.round(t, passes=2, certify=True)
+            Pd = P.working_set()
+            R.check_selection([Pd], O.SEL_GAP, t)
+            rr = R.round(t, [Pd])
+            # the estimate is taken before the certificate refreshes z (R25): recompute it on the
+            # oracle's gap memory as it was after z_P
+            chunk = [(t * kref + q) % n for q in range(kref)]
+            smp = np.array([j for j in chunk if j not in set(Pd.tolist())])
+            if smp.size == 0:       # the refreshed chunk lay inside P: no sample, no estimate
+                assert rec.gap_est == -1.0
+                continue
+            assert 0.25 * rr["gap"] <= rec.gap_est <= 4.0 * rr["gap"] + 1e-12, (t, rec.gap_est, rr["gap"])
+            seen.append(t)
+    assert len(seen) >= 5
