@@ -115,6 +115,7 @@ struct duhl_ctx {
     bool tpa_v0s = false;
     float* d_vf = nullptr;          // fp32 shadow of the shared vector (asynchronous epoch)
     double *d_v0t = nullptr, *d_a0t = nullptr;  // v~ and alpha_P at epoch start (exact resync)
+    double* d_u0 = nullptr;                     // [n] a_j^T v~0 for j in P (asynchronous epoch)
     cudaStream_t st = nullptr, cst = nullptr, rst = nullptr;  // compute, copy (H2D), unit-A refresh
     cudaStream_t cst2 = nullptr;     // copy-engine share of a gather round's staging
     cudaEvent_t ev_copy2 = nullptr;
@@ -735,7 +736,7 @@ static void free_all(duhl_ctx* ctx) {
                         ctx->d_s_acc, ctx->d_gap_out, ctx->d_s_out, ctx->d_sums, ctx->d_flag,
                         ctx->d_red, ctx->d_bar, ctx->d_colptr, ctx->d_rows, ctx->d_vals, ctx->d_topm_work,
                         ctx->d_stamp, ctx->d_rsel, ctx->d_rho, ctx->d_hs, ctx->d_hcols,
-                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t, ctx->d_est,
+                        ctx->d_plan_cols, ctx->d_plan_slots, ctx->d_vf, ctx->d_v0t, ctx->d_a0t, ctx->d_u0, ctx->d_est,
                         ctx->d_smp};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
@@ -777,12 +778,11 @@ static void choose_scd_shape(duhl_ctx* ctx) {
         // asynchronous epoch: W coordinates in flight, each on a cluster of C CTAs whose row
         // slices of the column fit in shared memory (<= 200 KB: C4's 803-KB columns take C = 4)
         int W = ctx->cfg.scd_block > 0 ? ctx->cfg.scd_block : 16;
-        int C = 1;
-        while (C < 8 && round4((ctx->d4 + C - 1) / C) * 4 > 200 * 1024) C *= 2;
+        int C = 1;  // two slices (double buffer) of <= 200 KB together
+        while (C < 8 && round4((ctx->d4 + C - 1) / C) * 8 > 200 * 1024) C *= 2;
         if (const char* e = std::getenv("DUHL_TPA_CLUSTER"))  // developer override (power of 2, <= 8)
             C = std::max(C, std::min(8, std::atoi(e)));
-        // v~0's slice in shared memory too where it fits (12 bytes per row with the column slice)
-        ctx->tpa_v0s = round4((ctx->d4 + C - 1) / C) * 12 <= 200 * 1024;
+        ctx->tpa_v0s = false;
         W = (int)std::max<int64_t>(1, std::min<int64_t>(W, sms / C));
         ctx->tpa = true;
         ctx->tpa_C = C;
@@ -1045,9 +1045,9 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
                        : (ctx->cfg.unit_a_ctas == 0 && ctx->cfg.hbm_budget_bytes != 0 && !ctx->csc) ? 8 : 0;
     choose_scd_shape(ctx);
     if (ctx->tpa) {
-        if (ctx->tpa_Rc * 4 > 200 * 1024) { ctx->err = "column too long for the asynchronous epoch"; return bail(DUHL_E_INVALID); }
+        if (ctx->tpa_Rc * 8 > 200 * 1024) { ctx->err = "column too long for the asynchronous epoch"; return bail(DUHL_E_INVALID); }
         if (!dmal((void**)&ctx->d_vf, d4 * sizeof(float)) || !dmal((void**)&ctx->d_v0t, d4 * sizeof(double)) ||
-            !dmal((void**)&ctx->d_a0t, n * sizeof(double)))
+            !dmal((void**)&ctx->d_a0t, n * sizeof(double)) || !dmal((void**)&ctx->d_u0, n * sizeof(double)))
             return bail(DUHL_E_NOMEM);
         ctx->cfg.linesearch = 1;  // asynchronous rounds take the exact gamma line search
     }
@@ -1283,7 +1283,8 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
         q.alpha = ctx->d_alpha;
         q.vf = ctx->d_vf;
         q.v0 = ctx->d_v0t;
-        q.v0_smem = ctx->tpa_v0s ? 1 : 0;
+        q.v0_smem = 0;
+        q.u0 = ctx->d_u0;
         q.C = ctx->tpa_C;
         q.Rc = ctx->tpa_Rc;
         q.progress = nullptr;  // the asynchronous epoch starts after its columns landed
@@ -1378,6 +1379,20 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
 static duhl_status tpa_begin(duhl_ctx* ctx, int64_t m) {
     CK(cudaMemcpyAsync(ctx->d_v0t, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
     CK(launch_gather_f64(ctx->d_alpha, ctx->d_P, m, ctx->d_a0t, ctx->st, &ctx->launches));
+    // u0_j = a_j^T v~0 for j in P: one gap-kernel pass over the working set (its columns have
+    // landed: the asynchronous epoch runs after its staging; the device table is brought up to
+    // date first), s = a_j^T (wscale v~0) -> u0 = s / wscale
+    TRY(finalize_staging(ctx));
+    {
+        GapParams gp = gap_params(ctx, ctx->d_P, m);
+        gp.vt = ctx->d_v0t;
+        gp.z = nullptr;
+        gp.s_out = ctx->d_s_out;
+        const int64_t tiles = (ctx->d4 + kGapTileRows - 1) / kGapTileRows;
+        ProfScope ps(ctx, ctx->st, 6, (double)m * (4.0 * ctx->d4 + 24.0) + 8.0 * ctx->d4 * tiles);
+        CK(launch_gap_pass(gp, kGapTileRows, ctx->st, &ctx->launches));
+        CK(launch_scatter_scaled(ctx->d_s_out, ctx->d_P, m, 1.0 / gp.wscale, ctx->d_u0, ctx->st, &ctx->launches));
+    }
     CK(cudaMemsetAsync(ctx->d_vf, 0, ctx->d4 * sizeof(float), ctx->st));
     return DUHL_OK;
 }

@@ -108,7 +108,8 @@ struct TpaParams {
     double* alpha;             // [n]
     float* vf;                 // [d4] fp32 shadow of the epoch's updates of v~ (zero at start), REDed
     const double* v0;          // [d4] v~ at epoch start (fp64)
-    int v0_smem;               // 1: the CTA's slice of v0 is held in shared memory
+    int v0_smem;               // unused (kept 0)
+    const double* u0;          // [n] a_j^T v~0 for j in P (taken before the epoch)
     int C;                     // CTAs per cluster
     int64_t Rc;                // rows per CTA (multiple of 4)
     const unsigned* progress;  // staging waits (nullptr: columns resident)
@@ -123,6 +124,8 @@ cudaError_t launch_tpa_resync(const float* pool, int64_t ld_dev, const int* P_sl
                               const double* alpha, const double* a0, int64_t m, const double* v0, double* vt,
                               int64_t d4, cudaStream_t st, int64_t* launches);
 cudaError_t launch_f64_to_f32(const double* x, float* y, int64_t k, cudaStream_t st, int64_t* launches);
+cudaError_t launch_scatter_scaled(const double* s, const int64_t* P, int64_t m, double scale, double* u0,
+                                  cudaStream_t st, int64_t* launches);
 cudaError_t preload_tpa_kernels();
 
 __host__ __device__ int scd_nred(int W);

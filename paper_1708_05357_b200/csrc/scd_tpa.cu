@@ -9,15 +9,17 @@
 //     cluster of C CTAs splits one coordinate's column by rows (C chosen so a CTA's slice of
 //     the column fits in shared memory: C4's 803-KB columns take C = 4..8), so all SMs stream
 //     while only W coordinates are concurrent;
-//   * per coordinate: each CTA loads its slice of a_j into shared memory (16-byte streamed
-//     loads) while accumulating its part of a_j^T v~ (fp64 accumulation of fp32 products of
-//     the fp32 shadow v~f, read at L2); the C partial dots meet in the leader's shared memory
+//   * per coordinate: each CTA's slice of a_j arrives in shared memory by one TMA bulk copy,
+//     double-buffered (the next coordinate's slice streams in while this one is reduced and
+//     REDed); the CTA accumulates its part of a_j^T v~ in fp64; the C partial dots meet in the
+//     leader's shared memory
 //     (distributed shared memory) behind one cluster barrier; every CTA then takes the same
 //     closed-form step and adds delta_j a_j to its rows of v~f with red.global.add.v4.f32
 //     (one 16-byte RED per 4 rows; App. D's atomic update);
 //   * the shared vector during the epoch is v~0 + dvf: v~0 = the exact fp64 vector at epoch
-//     start (L2-resident), dvf = an fp32 shadow of the epoch's own updates (zero at start,
-//     REDed).  s_j = a_j^T v~0 + a_j^T dvf, fp64 accumulation: the fp32 rounding touches only
+//     start, dvf = an fp32 shadow of the epoch's own updates (zero at start, REDed).
+//     s_j = a_j^T v~0 + a_j^T dvf: the first term for every j in P by one gap pass before the
+//     epoch (fp64, u0), the second in fp64 accumulation here: the fp32 rounding touches only
 //     the epoch's change, which vanishes near the optimum (an fp32 copy of v~ itself held
 //     C3's Lasso above 1e-5: its gap is sensitive to s through B = ||b||^2/(2 lambda d));
 //   * the epoch ends with the exact resync v~ = v~0 + A_P (alpha_P - alpha_P0) in fp64
@@ -43,11 +45,9 @@ __device__ __forceinline__ void red_add_v4_f32(float* addr, float a, float b, fl
 }
 
 __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constant__ TpaParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float4* col = reinterpret_cast<float4*>(smem);  // this CTA's slice of a_j
-    // p.v0_smem: the CTA's slice of v~0 (constant during the epoch) also in shared memory, read
-    // once instead of once per coordinate from L2
-    double2* v0s = reinterpret_cast<double2*>(smem + (size_t)p.Rc * sizeof(float));
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* bufs = reinterpret_cast<float*>(smem);   // [2][Rc]: this CTA's slices of two coordinates
+    __shared__ __align__(8) uint64_t mbar[2];        // slice landed (TMA bulk copy, tx bytes)
     __shared__ double part[2][kTpaMaxCluster];      // partial dots (read through the leader's copy)
     __shared__ double wsum[kTpaThreads / 32];
     __shared__ double s_delta;
@@ -59,34 +59,43 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
     const int64_t rows = r0 < p.d4 ? (p.d4 - r0 < p.Rc ? p.d4 - r0 : p.Rc) : 0;  // multiple of 4
     const int n4 = (int)(rows >> 2);
     double* lead = cl.map_shared_rank(&part[0][0], 0);
-    if (p.v0_smem) {
-        const double2* g = reinterpret_cast<const double2*>(p.v0 + r0);
-        for (int q = tid; q < 2 * n4; q += kTpaThreads) v0s[q] = g[q];
-        __syncthreads();
-    }
     const double dd = (double)p.d, nn = (double)p.n;
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // the TMA engine streams the next coordinate's slice into the other buffer while this one's
+    // dot, cluster reduction and REDs run (one thread issues one bulk copy of rows x 4 bytes)
+    auto issue = [&](int64_t it) {
+        const int64_t t = cid + it * ncl;
+        if (t >= p.L || n4 == 0) return;
+        const int b = (int)(it & 1);
+        fence_proxy_async();  // the buffer's last generic reads (two iterations ago) before the async write
+        mbar_arrive_expect_tx(&mbar[b], (unsigned)rows * 4u);
+        bulk_g2s(bufs + (size_t)b * p.Rc, p.pool + (int64_t)p.order_slot[t] * p.ld_dev + r0, (unsigned)rows * 4u,
+                 &mbar[b]);
+    };
+    if (tid == 0) issue(0);
     int it = 0;
-    unsigned seen = 0;
     for (int64_t t = cid; t < p.L; t += ncl, ++it) {
         const int64_t j = p.order_j[t];
-        const int slot = p.order_slot[t];
-        if (p.progress && tid == 0)
-            wait_staged(p.progress, p.stage_ctas, p.order_batch ? p.order_batch[t] : 0u, seen, p.err, 4000000000ull);
-        __syncthreads();
-        const float4* src = reinterpret_cast<const float4*>(p.pool + (int64_t)slot * p.ld_dev + r0);
+        if (tid == 0) issue(it + 1);  // its buffer was released by the __syncthreads closing it - 1
+        const int b = it & 1;
+        if (n4 > 0) mbar_wait(&mbar[b], (unsigned)((it >> 1) & 1));
+        const float4* col = reinterpret_cast<const float4*>(bufs + (size_t)b * p.Rc);
         const float4* vf4 = reinterpret_cast<const float4*>(p.vf + r0);
-        const double2* v02 = p.v0_smem ? v0s : reinterpret_cast<const double2*>(p.v0 + r0);
+        // a_j^T v~0 was taken for every j in P before the epoch (p.u0): only the epoch's own
+        // updates dvf are read here (4 bytes per row from L2, not 12)
         double acc0 = 0.0, acc1 = 0.0;
         for (int q = tid; q < n4; q += kTpaThreads) {
-            const float4 a = ld_stream_f4(src + q);
-            col[q] = a;
+            const float4 a = col[q];
             const float4 dv = __ldcg(vf4 + q);  // dvf is being updated by the other clusters: read at L2
-            const double2 u0 = p.v0_smem ? v02[2 * q] : __ldg(v02 + 2 * q);
-            const double2 u1 = p.v0_smem ? v02[2 * q + 1] : __ldg(v02 + 2 * q + 1);
-            acc0 = fma((double)a.x, u0.x + (double)dv.x, acc0);
-            acc1 = fma((double)a.y, u0.y + (double)dv.y, acc1);
-            acc0 = fma((double)a.z, u1.x + (double)dv.z, acc0);
-            acc1 = fma((double)a.w, u1.y + (double)dv.w, acc1);
+            acc0 = fma((double)a.x, (double)dv.x, acc0);
+            acc1 = fma((double)a.y, (double)dv.y, acc1);
+            acc0 = fma((double)a.z, (double)dv.z, acc0);
+            acc1 = fma((double)a.w, (double)dv.w, acc1);
         }
         double s = warp_sum(acc0 + acc1);
         if (lane == 0) wsum[warp] = s;
@@ -98,7 +107,7 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
         }
         cl.sync();  // all C partials of coordinate t are in the leader's part[it & 1]
         if (tid == 0) {
-            double sj = 0.0;
+            double sj = p.u0[j];
             for (int r = 0; r < C; ++r) sj += lead[(it & 1) * kTpaMaxCluster + r];  // rank order: same on every CTA
             const double a_old = p.order_a[t];
             const double an = coord_step(p.model, a_old, sj, p.norms[j], p.y ? p.y[j] : 0.0, p.lambda, dd, nn, p.eta);
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(kTpaThreads, 1) k_scd_tpa(const __grid_constan
                 red_add_v4_f32(vrow + 4 * q, dl * a.x, dl * a.y, dl * a.z, dl * a.w);
             }
         }
-        __syncthreads();  // the slice buffer is refilled by the next coordinate
+        __syncthreads();  // the slice buffer is refilled two coordinates later
     }
     cl.sync();  // no CTA leaves while another may still read the leader's partials
 }
@@ -160,12 +169,25 @@ __global__ void __launch_bounds__(kResyncThreads) k_tpa_resync(const float* pool
     atomicAdd(vt + r + 3, x3);
 }
 
+// u0[P[q]] = s[q] * scale (a_j^T v~0 of the working set, from a gap pass's s_out)
+__global__ void k_scatter_scaled(const double* s, const int64_t* P, int64_t m, double scale, double* u0) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < m) u0[P[q]] = s[q] * scale;
+}
+cudaError_t launch_scatter_scaled(const double* s, const int64_t* P, int64_t m, double scale, double* u0,
+                                  cudaStream_t st, int64_t* launches) {
+    if (m <= 0) return cudaSuccess;
+    k_scatter_scaled<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(s, P, m, scale, u0);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 __global__ void k_f64_to_f32(const double* x, float* y, int64_t k) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < k) y[i] = (float)x[i];
 }
 
-size_t tpa_smem_bytes(int64_t Rc, bool v0_smem) { return (size_t)Rc * (v0_smem ? 12 : 4); }
+size_t tpa_smem_bytes(int64_t Rc, bool v0_smem) { (void)v0_smem; return (size_t)Rc * 8; }  // 2 slices
 
 cudaError_t launch_scd_tpa(const TpaParams& p, int W, cudaStream_t st, int64_t* launches) {
     if (p.L <= 0) return cudaSuccess;
@@ -212,7 +234,8 @@ cudaError_t launch_f64_to_f32(const double* x, float* y, int64_t k, cudaStream_t
 }
 
 cudaError_t preload_tpa_kernels() {
-    const void* fns[] = {(const void*)k_scd_tpa, (const void*)k_tpa_resync, (const void*)k_f64_to_f32};
+    const void* fns[] = {(const void*)k_scd_tpa, (const void*)k_tpa_resync, (const void*)k_f64_to_f32,
+                         (const void*)k_scatter_scaled};
     for (const void* f : fns) {
         cudaFuncAttributes a;
         cudaError_t e = cudaFuncGetAttributes(&a, f);

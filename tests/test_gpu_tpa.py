@@ -47,8 +47,8 @@ def test_P7s_P8s_async_dense_epoch(D, model, W):
         lam = 1.0 / n
         want = lab * np.clip(lam * n / nrm, 0, 1)
     with D.create(A, lab, lam, model, m=n, scd_async=True, scd_block=W) as P:
-        name, Wd, G, R = P.scd_shape()
-        assert name == "k_scd_tpa" and Wd == W
+        name, Wd, G, R = P.scd_shape()   # W is capped by the SMs: W x cluster size <= the grid
+        assert name == "k_scd_tpa" and 0 < Wd <= W and G == Wd * ((d + R - 1) // R)
         P.select(D.SEL_GAP, m=n)
         P.scd_epoch(passes=1, seed=2)
         a, v, _ = P.get_state()
