@@ -24,7 +24,8 @@ __global__ void gather(const float4* __restrict__ h, const int* cols, int ncol, 
 }
 int main() {
     const size_t col = 200704 * 4;
-    const int ncol = 2400, nsrc = 12000;
+    const int ncol = 2400;
+    const int nsrc = getenv("NSRC") ? atoi(getenv("NSRC")) : 12000;
     const size_t bytes = col * nsrc;
     char* dv; CK(cudaMalloc(&dv, col * ncol));
     std::vector<int> cols(ncol);
