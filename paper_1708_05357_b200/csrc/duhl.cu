@@ -1053,7 +1053,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     }
     if (!dmal((void**)&ctx->d_topm_work, launch_topm_work_bytes()) || !dmal((void**)&ctx->d_stamp, n * sizeof(int)) ||
         !dmal((void**)&ctx->d_rsel, 2 * sizeof(unsigned long long)) || !dmal((void**)&ctx->d_rho, 2 * sizeof(double)) ||
-        !dmal((void**)&ctx->d_est, 4 * sizeof(double)) || !dmal((void**)&ctx->d_smp, n * sizeof(int64_t)))
+        !dmal((void**)&ctx->d_est, 4 * sizeof(double)) || !dmal((void**)&ctx->d_smp, n * sizeof(int64_t)) ||
+        cudaMemset(ctx->d_est, 0, 4 * sizeof(double)) != cudaSuccess)
         return bail(DUHL_E_NOMEM);
     if (cudaMemset(ctx->d_stamp, 0xff, n * sizeof(int)) != cudaSuccess) return bail(DUHL_E_CUDA);  // -1: never
     if (!ctx->csc && ctx->cfg.unit_a_host_threads > 0) {  // unit A on host threads (duhl.h)
@@ -1813,7 +1814,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         if (!have_est) CK(cudaMemsetAsync(ctx->d_est, 0, 4 * sizeof(double), ctx->st));
         TRY(allreduce(ctx, ctx->d_est, 4));
     }
-    CK(d2h_copy(ctx, est, ctx->d_est, 4 * sizeof(double), ctx->st));
+    if (have_est || ctx->group || ctx->comm) CK(d2h_copy(ctx, est, ctx->d_est, 4 * sizeof(double), ctx->st));
     double zs = 0.0, rs[2] = {0.0, 0.0};
     CK(d2h_copy(ctx, &zs, ctx->d_sums + 6, sizeof(double), ctx->st));
     CK(d2h_copy(ctx, rs, ctx->d_rho, 2 * sizeof(double), ctx->st));

@@ -438,17 +438,20 @@ def test_duhl_solve_matches_oracle(D, model, policy, budget_cols, host):
     assert np.abs(a - R.alpha).max() <= 1e-9 * max(1e-300, np.abs(R.alpha).max())
 
 
-@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
-def test_adaptive_certificates_only(D, model):
-    """duhl_solve with no certificate schedule: the gap memory's estimate (calibrated by failed
-    certificates) decides when to certify; the result is still certified <= eps, with few passes."""
+@pytest.mark.parametrize("model,refresh,policy", [(O.LASSO, 0.1, O.SEL_GAP), (O.SVM, 0.1, O.SEL_GAP),
+                                                   (O.SVM, 0.0, O.SEL_UNIFORM), (O.LASSO, 0.0, O.SEL_SEQUENTIAL)])
+def test_adaptive_certificates_only(D, model, refresh, policy):
+    """duhl_solve with no certificate schedule: the gap estimate (sampled from the refresh, else
+    the gap memory's sum; calibrated by failed certificates) decides when to certify; the result
+    is still certified <= eps, with few passes -- also for the batch baselines, which refresh no
+    gaps (a round-2 regression: an unwritten estimate buffer kept them from ever certifying)."""
     d, n = (400, 2000) if model == O.LASSO else (150, 2000)
     A, lab = _data(model, d, n, seed=77)
     lam = _lam(model, n)
     eps = 1e-6
-    with D.create(A, lab, lam, model, hbm_budget_bytes=500 * d * 4, m=400, refresh_fraction=0.1,
+    with D.create(A, lab, lam, model, hbm_budget_bytes=500 * d * 4, m=400, refresh_fraction=refresh,
                   cert_every=1 << 30, seed=3) as P:
-        r = P.solve(eps, 5000, passes=2)
+        r = P.solve(eps, 5000, passes=2, policy=policy)
         g, _, _ = P.duality_gap()
     assert r["status"] == 0 and r["gap"] <= eps and g <= eps
     ncert = sum(1 for t in r["trace"] if t.cert_gap >= 0)
