@@ -526,12 +526,13 @@ __global__ void __launch_bounds__(kStageThreads) k_stage_gather(const float* hos
         int64_t i = threadIdx.x;
         for (; i + (kStageUnroll - 1) * kStageThreads < n4; i += kStageUnroll * kStageThreads) {
             float4 x[kStageUnroll];
+            // plain loads: 45.1 vs 43.2 GB/s with ld.global.nc.L1::no_allocate inside the C4 step
 #pragma unroll
-            for (int u = 0; u < kStageUnroll; ++u) x[u] = ld_stream_f4(src + i + u * kStageThreads);
+            for (int u = 0; u < kStageUnroll; ++u) x[u] = src[i + u * kStageThreads];
 #pragma unroll
             for (int u = 0; u < kStageUnroll; ++u) dst[i + u * kStageThreads] = x[u];
         }
-        for (; i < n4; i += kStageThreads) dst[i] = ld_stream_f4(src + i);
+        for (; i < n4; i += kStageThreads) dst[i] = src[i];
         // the consumer reads the slot with the TMA engine (async proxy): order this thread's
         // generic-proxy stores before the async proxy, then device-wide before the release
         asm volatile("fence.proxy.async.global;" ::: "memory");
