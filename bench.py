@@ -45,7 +45,7 @@ CONFIGS = {
     # 2 and 3 passes, 5.1 s at 4 (passes_host)
     # C3 runs the asynchronous TPA-style epoch (scd_async, 128 coordinates in flight): time to 1e-5
     # 3.16 s vs 3.90 s with the exact k_scd_pipe (profiles/r02_tpa_vs_exact_c3.json); C4 keeps the
-    # exact k_scd_gram (2.62 s vs 3.27 s async at W = 16; W >= 32 stalls on C4's correlated samples)
+    # exact kernel (k_scd_gram then: 2.62 s vs 3.27 s async at W = 16; W >= 32 stalls on C4's correlated samples)
     "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=5,
                passes_host=3, scd_async=True, scd_block=128,
                label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "

@@ -101,11 +101,14 @@ typedef struct {
                                  SCD grid leaves them their SMs.  0 = auto (8 when the data exceeds the
                                  budget and refresh_fraction > 0), -1 = off (the refresh runs on the
                                  whole GPU before the epoch) */
-    int scd_kernel;           /* dense exact SCD kernel: 1 = warp-specialised (a control warp in every CTA,
-                                 W <= 16); 2 = pipelined (one control CTA runs the sequential steps; Gram
-                                 tiles of block b+1 run before delta_{b-1} is known; W <= 32); 0 = auto
-                                 (pipelined where shared memory holds W >= 24).  Both execute the same
-                                 sequential order (App. D), up to summation order. */
+    int scd_kernel;           /* dense exact SCD kernel: 1 = k_scd_gram (warp-specialised: a control warp
+                                 in every CTA, W <= 16; block b+1's partials include the cross Gram
+                                 A_{b+1}^T A_b); 2 = k_scd_pipe (one control CTA runs the sequential
+                                 steps; W <= 32); 3 = k_scd_ser (k_scd_gram's layout without the cross
+                                 Gram: the compute warps assemble u_{b+1} = A_{b+1}^T v_b +
+                                 A_{b+1}^T (A_b delta_b) after each block, W <= 16); 0 = auto
+                                 (k_scd_pipe where shared memory holds W >= 24, else k_scd_ser).  All
+                                 execute the same sequential order (App. D), up to summation order. */
     double eta;               /* DUHL_ELASTIC_NET only: g_i = lambda (eta/2 alpha_i^2 + (1-eta)|alpha_i|)
                                  (P:796-800), 0 < eta < 1; eta = 0 is DUHL_LASSO, eta = 1 DUHL_RIDGE */
     int unit_a_host_threads;  /* unit A on the host (Alg. 2 l.7-10 as the paper's CPU unit):
@@ -314,7 +317,8 @@ duhl_status duhl_get_unit_a_host(duhl_ctx* ctx, int64_t* cols, double* share);
 
 /* Launch shape of the dense exact SCD epoch chosen at create (cfg.scd_kernel, shared
  * memory): *kernel 1 = k_scd_gram (warp-specialised), 2 = k_scd_pipe (control CTA),
- * 3 = k_scd_tpa (cfg.scd_async: W coordinates in flight, G = W x cluster CTAs, R rows per CTA);
+ * 3 = k_scd_tpa (cfg.scd_async: W coordinates in flight, G = W x cluster CTAs, R rows per CTA),
+ * 4 = k_scd_ser (no cross Gram, see cfg.scd_kernel);
  * W coordinates per Gram block, G (compute) CTAs of R rows each.  CSC problems report
  * kernel 0 (k_csc_scd).  Any pointer may be NULL. */
 duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R);

@@ -252,7 +252,7 @@ class Problem:
         """(kernel name, W, G, R) of the exact SCD epoch chosen at create."""
         k, w, g, r = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         self._check(lib().duhl_get_scd_shape(self._h, C.byref(k), C.byref(w), C.byref(g), C.byref(r)))
-        return ["k_csc_scd", "k_scd_gram", "k_scd_pipe", "k_scd_tpa"][k.value], w.value, g.value, r.value
+        return ["k_csc_scd", "k_scd_gram", "k_scd_pipe", "k_scd_tpa", "k_scd_ser"][k.value], w.value, g.value, r.value
 
     def counters(self):
         a, b, z, c, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()

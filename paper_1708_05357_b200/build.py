@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libduhl.so")
 SOURCES = ["duhl.cu", "kernels.cu", "scd_tpa.cu", "unit_a_host.cpp"]
-DEPS = SOURCES + ["device.cuh", "kernels.h", "scd_pipe.cuh", "unit_a_host.h"]
+DEPS = SOURCES + ["device.cuh", "kernels.h", "scd_pipe.cuh", "scd_ser.cuh", "unit_a_host.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

@@ -108,7 +108,8 @@ struct duhl_ctx {
     duhl_config cfg{};
     std::string err;
     int dev = 0, nsm = 0, unit_a_ctas = 0;
-    bool pipe = false;  // SCD epoch runs k_scd_pipe (else k_scd_gram); see choose_scd_shape
+    bool pipe = false;  // SCD epoch runs k_scd_pipe (else k_scd_gram / k_scd_ser); see choose_scd_shape
+    bool ser = false;   // k_scd_ser instead of k_scd_gram (cfg.scd_kernel 0 / 3; 1 = k_scd_gram)
     bool tpa = false;   // cfg.scd_async: asynchronous k_scd_tpa epoch (W clusters of tpa_C CTAs)
     int tpa_C = 1;
     int64_t tpa_Rc = 0;
@@ -796,7 +797,7 @@ static void choose_scd_shape(duhl_ctx* ctx) {
     // TMA stages.  Auto (scd_kernel 0) takes it where shared memory allows W >= 24 (short row
     // slices, e.g. C3: 2x fewer blocks than W = 16, measured 14.7 vs 25 ms per pass); at W <= 16
     // the warp-specialised kernel is as fast or faster (C4, W = 12: 6.6 vs 7.3 ms).
-    if (ctx->cfg.scd_kernel != 1) {
+    if (ctx->cfg.scd_kernel != 1 && ctx->cfg.scd_kernel != 3) {
         const int64_t smax = std::max<int64_t>(1, sms - 1);
         int64_t G = ctx->cfg.scd_ctas > 0 ? std::min<int64_t>(ctx->cfg.scd_ctas, smax)
                                           : std::min<int64_t>(smax, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
@@ -817,6 +818,10 @@ static void choose_scd_shape(duhl_ctx* ctx) {
         }
     }
     ctx->pipe = false;
+    // k_scd_ser (no cross Gram, u assembled by the compute warps) unless k_scd_gram is asked
+    // for: C4 fast mode 4.65 vs 6.87 ms per pass, exact 6.4 vs 7.2
+    ctx->ser = ctx->cfg.scd_kernel != 1;
+    if (const char* e = std::getenv("DUHL_SCD_SER")) ctx->ser = std::atoi(e) != 0;  // developer A/B
     int64_t G = ctx->cfg.scd_ctas > 0 ? std::min<int64_t>(ctx->cfg.scd_ctas, sms)
                                       : std::min<int64_t>(sms, std::max<int64_t>(1, (ctx->d4 + 127) / 128));
     int64_t R = round4((ctx->d4 + G - 1) / G);
@@ -1341,8 +1346,9 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
     p.trace = dtr;
     {
         ProfScope ps(ctx, ctx->st, waits_on_staging ? 5 : 0, (double)L * (4.0 * ctx->d4 + 24.0) + 16.0 * ctx->d4);
-        CK(ctx->pipe ? launch_scd_pipe(p, ctx->st, &ctx->launches)
-                                    : launch_scd_gram(p, ctx->st, &ctx->launches));
+        CK(ctx->pipe  ? launch_scd_pipe(p, ctx->st, &ctx->launches)
+           : ctx->ser ? launch_scd_ser(p, ctx->st, &ctx->launches)
+                      : launch_scd_gram(p, ctx->st, &ctx->launches));
     }
     if (trace) {
         unsigned long long h[16];
@@ -1356,12 +1362,16 @@ static duhl_status scd_launch(duhl_ctx* ctx, int64_t L, bool waits_on_staging = 
         const double cyc_per_us = clk_khz > 0 ? clk_khz / 1e3 : 1965.0;
         std::fprintf(stderr, "scd trace (us/block at %.0f MHz) W=%d G=%d R=%d: ", cyc_per_us, ctx->W, ctx->G,
                      ctx->R);
-        const char* nm0[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
+        const char* nm0a[8] = {"ctl:other", "-", "ctl:WAIT", "ctl:read", "ctl:seq", "cmp:wait-delta",
                               "cmp:vupdate", "cmp:tiles"};
+        const char* const* nm0 = nm0a;
         const char* nm1[8] = {"ctl:poll", "ctl:read", "ctl:steps", "ctl:other", "ctl:publish", "-", "-", "-"};
         const char* nm1c[8] = {"gram:wait-data", "gram:tiles", "gram:sum+arrive", "v:wait-delta", "v:vupd",
                                "v:u+arrive", "v:other", "gram:other"};
+        const char* nms[8] = {"ctl:WAIT", "ctl:read", "ctl:steps", "ctl:other", "cmp:data+G+u'", "cmp:wait-delta",
+                              "cmp:corr", "cmp:RED+arrive+vupd"};
         const bool pipe = ctx->pipe;
+        if (ctx->ser) nm0 = nms;
         for (int c2 = 0; c2 < 2; ++c2) {
             std::fprintf(stderr, "%s", pipe ? (c2 ? " | cta0: " : "control: ") : (c2 ? " | last: " : "cta0: "));
             for (int k = 0; k < 8; ++k)
@@ -2049,7 +2059,7 @@ duhl_status duhl_get_kernel_stats(duhl_ctx* ctx, int kind, int64_t* launches, do
 
 duhl_status duhl_get_scd_shape(duhl_ctx* ctx, int* kernel, int* W, int* G, int* R) {
     if (!ctx) return DUHL_E_INVALID;
-    if (kernel) *kernel = ctx->csc ? 0 : (ctx->tpa ? 3 : (ctx->pipe ? 2 : 1));
+    if (kernel) *kernel = ctx->csc ? 0 : (ctx->tpa ? 3 : (ctx->pipe ? 2 : (ctx->ser ? 4 : 1)));
     if (W) *W = ctx->W;
     if (G) *G = ctx->G;
     if (R) *R = ctx->R;

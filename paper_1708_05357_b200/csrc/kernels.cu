@@ -1287,6 +1287,7 @@ cudaError_t launch_scd_gram(const ScdParams& p, cudaStream_t st, int64_t* launch
 }
 
 #include "scd_pipe.cuh"
+#include "scd_ser.cuh"
 
 // =====================================================================================
 // v = A alpha (- b): exact shared-vector recompute for set_state.  CTA per row
@@ -1661,6 +1662,9 @@ cudaError_t preload_kernels() {
         (const void*)k_scd_pipe<true, kSvm>,   (const void*)k_scd_pipe<false, kSvm>,
         (const void*)k_scd_gram<true, kRidge>, (const void*)k_scd_gram<false, kRidge>,
         (const void*)k_scd_pipe<true, kRidge>, (const void*)k_scd_pipe<false, kRidge>, (const void*)k_ridge_sums,
+        (const void*)k_scd_ser<true, kLasso>, (const void*)k_scd_ser<false, kLasso>,
+        (const void*)k_scd_ser<true, kSvm>,   (const void*)k_scd_ser<false, kSvm>,
+        (const void*)k_scd_ser<true, kRidge>, (const void*)k_scd_ser<false, kRidge>,
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,

@@ -164,6 +164,8 @@ cudaError_t launch_stage_gather(const float* host, int64_t ld_host, float* pool,
 size_t pipe_red_doubles(int W);   // size of ScdParams::red (reduction + delta buffers)
 size_t pipe_smem_bytes(int W, int R, int NS);
 cudaError_t launch_scd_pipe(const ScdParams& p, cudaStream_t st, int64_t* launches);
+// k_scd_ser (scd_ser.cuh): k_scd_gram's layout without the cross Gram, u taken after each update
+cudaError_t launch_scd_ser(const ScdParams& p, cudaStream_t st, int64_t* launches);
 cudaError_t preload_kernels();
 cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches);

@@ -1,7 +1,7 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
 test_bench_launch_rounds_replay_oracle: the bench's own options (bench.parse_args +
-bench.launch_kwargs: fast-mode SCD, k_scd_gram W = 12 on 140 CTAs at C4 / k_scd_pipe W = 32
+bench.launch_kwargs: fast-mode SCD, k_scd_ser W = 12 on 140 CTAs at C4 / k_scd_pipe W = 32
 with tensor-core Gram tiles at C3, 8 unit-A refresh CTAs, host unit-A threads, passes per
 round) for the first rounds from alpha = 0, each round replayed by the oracle on the device's
 (band-verified) working set (oracle/replay.py): alpha and v element-wise, the certificate.
@@ -104,7 +104,7 @@ def test_bench_launch_rounds_replay_oracle(D, name, rounds):
     R = Alg2(model, A, lab, lam, m, passes, int(np.ceil(args.refresh * n - 1e-9)), kw["seed"])
     with D.create(A, lab, lam, model, cert_every=1 << 40, scd_exact=args.exact, **kw) as P:
         shape = P.scd_shape()
-        assert shape[0] == ("k_scd_gram" if name == "c4" else "k_scd_pipe")
+        assert shape[0] == ("k_scd_ser" if name == "c4" else "k_scd_pipe")
         for t in range(rounds):
             rec = P.round(t, passes=passes, certify=(t == rounds - 1))
             Pd = P.working_set()

@@ -210,7 +210,7 @@ def test_select_importance_matches_oracle(D, n, m):
 
 
 # ------------------------------------------------------------------------- SCD epoch (a5)
-@pytest.mark.parametrize("kernel", [1, 2])   # warp-specialised / pipelined (control CTA)
+@pytest.mark.parametrize("kernel", [1, 2, 3])   # warp-specialised / pipelined (control CTA) / serial
 @pytest.mark.parametrize("model,d,n,m,W", [
     (O.LASSO, 2000, 1000, 250, 0),      # C1 shape, 25% working set
     (O.SVM, 500, 4000, 400, 0),         # C2 aspect, 10% working set
@@ -245,7 +245,7 @@ def test_scd_epoch_explicit_order_matches_oracle(D, model, d, n, m, W, kernel):
     assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("m", [1, 3, 33])
 def test_scd_epoch_tiny_working_sets(D, kernel, m):
     """Edge cases of the block pipeline: one coordinate, one partial block, W + 1."""
@@ -264,12 +264,13 @@ def test_scd_epoch_tiny_working_sets(D, kernel, m):
     assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("model,d,n,m", [(O.LASSO, 40000, 400, 390), (O.SVM, 200704 // 8, 300, 290),
                                          (O.RIDGE, 40000, 400, 390)])
 def test_scd_epoch_fast_mode_matches_oracle(D, model, d, n, m, kernel):
     """Fast mode (scd_exact=0, the bench's): fp32 Gram partials inside a CTA (k_scd_pipe) or a
-    warp (k_scd_gram), fp64 across CTAs and everywhere else.  The Gram entries only correct s_j
+    warp (k_scd_gram; k_scd_ser: G and the fp32 correction A_{b+1}^T (A_b delta_b)), fp64 across
+    CTAs and everywhere else.  The Gram entries only correct s_j
     for the updates of the current / previous block, so the epoch stays within ~1e-6 of the
     oracle's sequential epoch (relative to max |alpha|); a wrong index or sign is O(1)."""
     A, lab = _data(model, d, n, seed=300 + d)
@@ -327,7 +328,7 @@ def test_scd_internal_permutation_generator_matches_oracle(D):
     assert np.abs(a_gpu - alpha).max() <= 1e-11 * np.abs(alpha).max()
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_P7_hadamard_one_epoch_on_gpu(D, kernel):
     d, n = 2048, 1024
     A = synth.hadamard_columns(d, n)
@@ -345,7 +346,7 @@ def test_P7_hadamard_one_epoch_on_gpu(D, kernel):
     assert g < 1e-10
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_P8_orthogonal_svm_one_epoch_on_gpu(D, kernel):
     d, n = 256, 128
     rng = np.random.default_rng(1)
@@ -362,7 +363,7 @@ def test_P8_orthogonal_svm_one_epoch_on_gpu(D, kernel):
     assert g < 1e-12
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_zero_columns(D, kernel):
     d, n = 64, 40
     A, y = synth.svm_dense(d, n, seed=8)
