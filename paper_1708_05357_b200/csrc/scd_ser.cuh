@@ -44,12 +44,24 @@
 
 static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction buffers");
 
+// Warps: control = 3, producer = the last, compute = the others (k_scd_gram's layout at 8).
+// Measured (C4, 140 CTAs, fast / exact ms per pass): 8 warps 4.69 / 6.46, 12 warps 4.96 / 6.67,
+// 16 warps 5.30 / 8.94 (register spills) -- the compute warps' per-block work (~540 KB of
+// shared-memory reads: G tiles 230, u' 81, correction 138, v update 92) does not shrink with
+// more warps.
+#ifndef DUHL_SER_WARPS
+#define DUHL_SER_WARPS 8
+#endif
+constexpr int kSerThreads = DUHL_SER_WARPS * 32;
+constexpr int kSerCompute = DUHL_SER_WARPS - 2;
+constexpr int kSerProd = DUHL_SER_WARPS - 1;
+
 
 // u'_j = a_j^T v over the thread's 4-row groups (fp64), NW = W columns unrolled.
 template <int NW>
 __device__ __forceinline__ void ser_uprime(const float* __restrict__ An, int R, const double2* v2, int r4_0,
                                            int nr4, double (&u)[16]) {
-    for (int r4 = r4_0; r4 < nr4; r4 += kCompute * 32) {
+    for (int r4 = r4_0; r4 < nr4; r4 += kSerCompute * 32) {
         const double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
         float4 y[NW];
 #pragma unroll
@@ -78,7 +90,7 @@ __device__ __forceinline__ void ser_corr(const float* __restrict__ A, const floa
         double d[NW];
 #pragma unroll
         for (int j = 0; j < NW; ++j) d[j] = dcur[j];
-        for (int r4 = r4_0; r4 < nr4; r4 += kCompute * 32) {
+        for (int r4 = r4_0; r4 < nr4; r4 += kSerCompute * 32) {
             float4 x[NW];
 #pragma unroll
             for (int j = 0; j < NW; ++j) x[j] = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
@@ -120,7 +132,7 @@ __device__ __forceinline__ void ser_corr(const float* __restrict__ A, const floa
         float2 c[NW];
 #pragma unroll
         for (int j = 0; j < NW; ++j) c[j] = make_float2(0.f, 0.f);
-        for (int r4 = r4_0; r4 < nr4; r4 += kCompute * 32) {
+        for (int r4 = r4_0; r4 < nr4; r4 += kSerCompute * 32) {
             float4 x[NW];
 #pragma unroll
             for (int j = 0; j < NW; ++j) x[j] = reinterpret_cast<const float4*>(A + (size_t)j * R)[r4];
@@ -151,7 +163,7 @@ __device__ __forceinline__ void ser_vupdate(const float* __restrict__ A, int R, 
     double d[NW];
 #pragma unroll
     for (int j = 0; j < NW; ++j) d[j] = dcur[j];
-    for (int r4 = r4_0; r4 < nr4; r4 += kCompute * 32) {
+    for (int r4 = r4_0; r4 < nr4; r4 += kSerCompute * 32) {
         double2 v01 = v2[2 * r4], v23 = v2[2 * r4 + 1];
         float4 x[NW];
 #pragma unroll
@@ -177,7 +189,7 @@ __device__ __forceinline__ void ser_vupdate(const float* __restrict__ A, int R, 
     }
 
 template <bool EXACT, int MODEL>
-__global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constant__ ScdParams p) {
+__global__ void __launch_bounds__(kSerThreads, 1) k_scd_ser(const __grid_constant__ ScdParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int W = p.W, R = p.R, T = W / 4;
     const int NQ = scd_off_C(W);  // reduced entries per block: u [0, W), G lower after
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
     double* delta = reinterpret_cast<double*>(smem + off);  // [2][16]
     __shared__ double sT[16], sP[16], sA[16], sS[16], sC[16 * 16];
     __shared__ int sZ[16];
-    __shared__ double su[kCompute * 16];  // per-compute-warp u partials
+    __shared__ double su[kSerCompute * 16];  // per-compute-warp u partials
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
@@ -204,12 +216,12 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
     const size_t bufsz = (size_t)scd_nred(W) * kRedGroups * kRedStride;
     const int grp = c % kRedGroups;
 
-    for (int q = tid; q < kScdStages * W * R; q += kScdThreads) Abuf[q] = 0.0f;
-    for (int r = tid; r < R; r += kScdThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
+    for (int q = tid; q < kScdStages * W * R; q += kSerThreads) Abuf[q] = 0.0f;
+    for (int r = tid; r < R; r += kSerThreads) vs[r] = r < rows ? p.vt[r0 + r] : 0.0;
     if (tid == 0) {
         for (int q = 0; q < kScdStages; ++q) {
             mbar_init(&full[q], 1);
-            mbar_init(&empty[q], kCompute);
+            mbar_init(&empty[q], kSerCompute);
         }
         mbar_init(&dfull[0], 1);
         mbar_init(&dfull[1], 1);
@@ -237,15 +249,15 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
     };
     const int64_t nblk = (p.L + W - 1) / W;
     auto stage = [&](int64_t blk) { return Abuf + (size_t)(blk % kScdStages) * W * R; };
-    const bool ctrl = warp == kCtrlWarp, prod = warp == kProdWarp;
-    const int cw = warp < kCtrlWarp ? warp : (warp > kCtrlWarp && warp < kProdWarp ? warp - 1 : -1);
+    const bool ctrl = warp == kCtrlWarp, prod = warp == kSerProd;
+    const int cw = warp < kCtrlWarp ? warp : (warp > kCtrlWarp && warp < kSerProd ? warp - 1 : -1);
 
     // per-compute-warp G tile lists, built once: item = jt | k0 << 4 | kw << 9 | part << 13
     // (4 x 8 tiles split by rows into two items, so W = 12's four tiles are six equal items)
-    __shared__ int witems[kCompute][12];
-    __shared__ int wcount[kCompute];
+    __shared__ int witems[kSerCompute][12];
+    __shared__ int wcount[kSerCompute];
     if (tid == 0) {
-        for (int w = 0; w < kCompute; ++w) wcount[w] = 0;
+        for (int w = 0; w < kSerCompute; ++w) wcount[w] = 0;
         int item = 0;
         for (int cost = 2; cost >= 1; --cost)
             for (int jt = 0; jt < T; ++jt)
@@ -253,8 +265,8 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
                     const int kw = 4 * jt + 4 - k0 >= 8 ? 8 : 4;
                     if ((kw == 8) != (cost == 2)) continue;
                     for (int part = 0; part < (kw == 8 ? 2 : 1); ++part) {
-                        const int rnd = item / kCompute, pos = item % kCompute;
-                        const int owner = (rnd & 1) ? kCompute - 1 - pos : pos;
+                        const int rnd = item / kSerCompute, pos = item % kSerCompute;
+                        const int owner = (rnd & 1) ? kSerCompute - 1 - pos : pos;
                         ++item;
                         if (wcount[owner] < 12) witems[owner][wcount[owner]++] = jt | k0 << 4 | kw << 9 | part << 13;
                     }
@@ -439,12 +451,12 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
             const int Wn = (int)imin64(W, p.L - blk * W);
             const double s = reduce_scatter<double, 16>(u, lane);
             if (lane < 16) su[cw * 16 + lane] = s;
-            named_sync(kBarCompute, kCompute * 32);
+            named_sync(kBarCompute, kSerCompute * 32);
             if (cw == 0) {
                 if (lane < Wn) {
                     double t = 0.0;
 #pragma unroll
-                    for (int w = 0; w < kCompute; ++w) t += su[w * 16 + lane];
+                    for (int w = 0; w < kSerCompute; ++w) t += su[w * 16 + lane];
                     const RedOut out{p.red + (size_t)(blk % kRedBufs) * bufsz, grp};
                     out.add(lane, t);
                 }
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(kScdThreads, 1) k_scd_ser(const __grid_constan
         stamp(7);
     }
     __syncthreads();
-    for (int r = tid; r < rows; r += kScdThreads) p.vt[r0 + r] = vs[r];
+    for (int r = tid; r < rows; r += kSerThreads) p.vt[r0 + r] = vs[r];
     if (tr)
         for (int q = 0; q < 8; ++q)
             if (trc[q]) atomicAdd(&p.trace[(c == 0 ? 0 : 8) + q], trc[q]);
@@ -522,7 +534,7 @@ cudaError_t launch_scd_ser(const ScdParams& p, cudaStream_t st, int64_t* launche
     if (e != cudaSuccess) return e;
     ScdParams q = p;
     void* args[] = {&q};
-    e = cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(kScdThreads), args, smem, st);
+    e = cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(kSerThreads), args, smem, st);
     ++*launches;
     return e;
 }

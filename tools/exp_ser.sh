@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "kernel or 3" -p no:cacheprovider 2>&1 | tail -2
-DUHL_SCD_TRACE=1 timeout 300 python tools/prof_scd.py --fast --passes 3 --ctas 140 --kernel 3 2>&1 | grep -v "^gap\|^topm" | tail -3 | head -1
-for rep in 1 2; do
-  timeout 300 python tools/prof_scd.py --fast --passes 3 --ctas 140 --kernel 3 2>&1 | grep "^scd"
+for v in "" tools/variants/libduhl_w12.so tools/variants/libduhl_w16.so; do
+  echo "lib=$v"
+  DUHL_LIB=$v timeout 300 python tools/prof_scd.py --fast --passes 3 --ctas 140 --kernel 3 2>&1 | grep "^scd"
+  DUHL_LIB=$v timeout 300 python tools/prof_scd.py --passes 3 --ctas 140 --kernel 3 2>&1 | grep "^scd"
 done
-timeout 300 python tools/prof_scd.py --passes 3 --ctas 140 --kernel 3 2>&1 | grep "^scd"
+DUHL_LIB=tools/variants/libduhl_w12.so timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "kernel or 3" -p no:cacheprovider 2>&1 | tail -2
