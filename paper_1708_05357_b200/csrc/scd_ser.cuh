@@ -48,7 +48,9 @@ static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction 
 // Measured (C4, 140 CTAs, fast / exact ms per pass): 8 warps 4.69 / 6.46, 12 warps 4.96 / 6.67,
 // 16 warps 5.30 / 8.94 (register spills) -- the compute warps' per-block work (~540 KB of
 // shared-memory reads: G tiles 230, u' 81, correction 138, v update 92) does not shrink with
-// more warps.
+// more warps.  Taking u' inside the k0 = 0 Gram tiles (x slices already in registers, no u'
+// sweep) and sharing the x loads of diagonal tiles: 7.49 ms -- the fp64 u' work then sits on
+// the five tile warps unevenly and the kernel needs a 168-byte local frame.
 #ifndef DUHL_SER_WARPS
 #define DUHL_SER_WARPS 8
 #endif
