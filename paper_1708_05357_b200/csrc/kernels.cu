@@ -11,6 +11,8 @@
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "device.cuh"
@@ -60,8 +62,9 @@ __device__ __forceinline__ void gap_finish_one(const GapParams& p, int64_t t, in
     acc.amax = fmax(acc.amax, fabs(a));
 }
 
+template <int NT = kGapThreads>
 __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
-    __shared__ double sh[4][kGapThreads / 32];
+    __shared__ double sh[4][NT / 32];
     __shared__ int shf;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) shf = 0;
@@ -85,7 +88,7 @@ __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
         if (shf) atomicOr(p.flag, shf);
         if (p.sums) {
             double g = 0, x = 0, a = 0, mx = 0;
-            for (int w = 0; w < kGapThreads / 32; ++w) {
+            for (int w = 0; w < NT / 32; ++w) {
                 g += sh[0][w];
                 x += sh[1][w];
                 a += sh[2][w];
@@ -1588,8 +1591,69 @@ cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStre
     return cudaGetLastError();
 }
 
+// The same pass with the head of the shared vector in shared memory: one 1024-thread CTA per
+// SM stages w_r = wscale vt_r for rows r < Rs (fp64, up to DUHL_CSC_SMEM_KB, default 160 KB)
+// and gathers those rows from shared memory, the rest through L1 / L2 as above.  A warp's 32
+// row indices of one column are ~100 rows apart (uniform rows, 1 % density), so a global
+// gather touches ~32 L1 lines -- the L1 tag rate, ~1 line per clock per SM, bounds
+// k_csc_gap at ~1 nonzero per clock per SM; a shared-memory gather costs a few bank
+// wavefronts instead.  Same products (vt_r wscale rounded once); four partial sums per lane
+// (fp64; k_csc_gap keeps two).  Measured (C5s, gap pass GB/s): k_csc_gap 2274; this kernel
+// with 64 / 96 / 128 / 160 / 192 KB of rows in shared memory 2443 / 2548 / 2607 / 2624 /
+// 2568; two partial sums at 200 KB 1737; eight (predicated tails, next column's extent
+// prefetched) 2024-2189 -- register-limited at 1024 threads.
+constexpr int kCscSmemThreads = 1024;
+__global__ void __launch_bounds__(kCscSmemThreads, 1) k_csc_gap_smem(GapParams p, CscMat A, int Rs) {
+    extern __shared__ double sw[];
+    for (int r = threadIdx.x; r < Rs; r += kCscSmemThreads) sw[r] = p.vt[r] * p.wscale;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    SumAcc acc;
+    int flag = 0;
+    auto wget = [&](int r) { return r < Rs ? sw[r] : __ldg(p.vt + r) * p.wscale; };
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.k; t += nw) {
+        const int64_t i = p.cols ? p.cols[t] : t;
+        const int64_t k0 = A.col_ptr[i], k1 = A.col_ptr[i + 1];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t k = k0 + lane;
+        for (; k + 96 < k1; k += 128) {  // four independent gathers in flight per lane
+            const int r0 = ld_stream_i32(A.rows + k), r1 = ld_stream_i32(A.rows + k + 32);
+            const int r2 = ld_stream_i32(A.rows + k + 64), r3 = ld_stream_i32(A.rows + k + 96);
+            const float x0 = ld_stream_f32(A.vals + k), x1 = ld_stream_f32(A.vals + k + 32);
+            const float x2 = ld_stream_f32(A.vals + k + 64), x3 = ld_stream_f32(A.vals + k + 96);
+            s0 = fma((double)x0, wget(r0), s0);
+            s1 = fma((double)x1, wget(r1), s1);
+            s2 = fma((double)x2, wget(r2), s2);
+            s3 = fma((double)x3, wget(r3), s3);
+        }
+        for (; k < k1; k += 32) s0 = fma((double)ld_stream_f32(A.vals + k), wget(ld_stream_i32(A.rows + k)), s0);
+        const double s = warp_sum((s0 + s1) + (s2 + s3));
+        if (lane == 0) gap_finish_one(p, t, i, s, acc, flag);
+    }
+    block_flush_sums<kCscSmemThreads>(p, acc, flag);
+}
+
 cudaError_t launch_csc_gap(const GapParams& p, const CscMat& A, int max_ctas, cudaStream_t st, int64_t* launches) {
     if (p.k <= 0) return cudaSuccess;
+    static const int smem_kb = [] {
+        const char* e = std::getenv("DUHL_CSC_SMEM_KB");  // developer A/B; 0 = k_csc_gap
+        return e ? std::atoi(e) : 160;
+    }();
+    if (smem_kb > 0 && p.k >= 4096) {
+        const int Rs = (int)std::min<int64_t>(p.d, (int64_t)smem_kb * 1024 / 8);
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        int g = nsm;
+        if (max_ctas > 0 && g > max_ctas) g = max_ctas;
+        const size_t smem = (size_t)Rs * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_csc_gap_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_csc_gap_smem<<<g, kCscSmemThreads, smem, st>>>(p, A, Rs);
+        ++*launches;
+        return cudaGetLastError();
+    }
     unsigned g = csc_grid(p.k);
     if (max_ctas > 0 && g > (unsigned)max_ctas) g = (unsigned)max_ctas;
     k_csc_gap<<<g, 256, 0, st>>>(p, A);
@@ -1668,7 +1732,7 @@ cudaError_t preload_kernels() {
         (const void*)k_matvec,      (const void*)k_set_slots,    (const void*)k_sum,
         (const void*)k_gather_f64,  (const void*)k_delta_v,      (const void*)k_ydalpha,
         (const void*)k_lasso_dgrid, (const void*)k_apply_gamma,  (const void*)k_vec_sums,
-        (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_scd,
+        (const void*)k_csc_norms,   (const void*)k_csc_gap,      (const void*)k_csc_gap_smem,      (const void*)k_csc_scd,
         (const void*)k_csc_matvec,  (const void*)k_topm_hist,    (const void*)k_topm_pick,
         (const void*)k_topm_count,  (const void*)k_topm_offsets, (const void*)k_topm_write,
         (const void*)k_resident_select, (const void*)k_stage_gather};

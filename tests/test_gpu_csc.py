@@ -181,7 +181,8 @@ def test_P7s_P8s_async_epoch_with_thousands_of_warps(D, model, warps):
 def test_csc_gap_pass_long_columns_matches_oracle(D, model):
     """The CSC gap pass at d = 50,000 rows (w = 400 KB fp64, beyond one SM's L1) and 6,000
     columns against the oracle's dense gaps (s_i to 1e-9 of the conditioning floor), plus the
-    certificate."""
+    certificate.  6,000 columns take k_csc_gap_smem: rows below 20,480 gathered from shared
+    memory, the rest through L1 / L2 -- both branches."""
     d, n = 50000, 6000
     csc, A, lab, lam = _problem(model, d, n, 0.01, seed=71 + model)
     rng = np.random.default_rng(3)
