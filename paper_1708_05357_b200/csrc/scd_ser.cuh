@@ -50,7 +50,9 @@ static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction 
 // shared-memory reads: G tiles 230, u' 81, correction 138, v update 92) does not shrink with
 // more warps.  Taking u' inside the k0 = 0 Gram tiles (x slices already in registers, no u'
 // sweep) and sharing the x loads of diagonal tiles: 7.49 ms -- the fp64 u' work then sits on
-// the five tile warps unevenly and the kernel needs a 168-byte local frame.
+// the five tile warps unevenly and the kernel needs a 168-byte local frame.  Sharing the x
+// loads of diagonal tiles alone (12 of 40 loads per row group): fast 4.79 vs 4.68 ms, exact
+// 6.25 vs 6.47 -- not kept.
 #ifndef DUHL_SER_WARPS
 #define DUHL_SER_WARPS 8
 #endif
