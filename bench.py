@@ -571,9 +571,10 @@ def run_duhl(args, cfg, rank, world, local):
                "state_check": runs[0]["state_err"],
                "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
                        "from the caller's pinned host buffers (used in place; one device pass over A for "
-                       "norms + z at alpha=0) + duhl_solve to the certified gap); time_to_eps_s = "
-                       "duhl_solve alone (cold HBM fill included); h2d = cold fill + swaps (copy engine and "
-                       "staging gather); zero-copy = refresh + certificate reads of non-resident columns; "
+                       "norms + z at alpha=0, which also leaves columns 0..S-1 in the S HBM slots) + "
+                       "duhl_solve to the certified gap); time_to_eps_s = duhl_solve alone (the rest of the "
+                       "cold HBM fill included); h2d = fill + swaps (copy engine and staging gather); "
+                       "zero-copy = create's pass + refresh + certificate reads of non-resident columns; "
                        "d2h = the library's read-backs (counted)"}
 
     # ---------------- baselines: same library, budget and kernels, batch selection

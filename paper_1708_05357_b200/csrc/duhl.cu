@@ -686,8 +686,10 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             else if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
             ctx->slot_batch[s] = seq;
             ctx->copy_plan.push_back({j, s, seq});
-            ++nsw;
         }
+        // swaps = |P_t \ P_{t-1}| (Fig. 4b's count; P_{-1} = {}): the columns copied, except that
+        // round 0 may find some of them left in the pool by duhl_create's ingest pass
+        for (int64_t j : P) nsw += ctx->inP[j] ? 0 : 1;
         if (ctx->overlap && ctx->stage_ctas == 0 && !news.empty())
             ctx->batch_seq = heavy ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
         // the compute stream may still read evicted slots (previous epoch): order copies after it
@@ -1144,9 +1146,21 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         ck(cudaMemsetAsync(ctx->d_norms, 0, n * sizeof(double), st));
         GapParams p = gap_params(ctx, nullptr, n);
         p.norms_out = ctx->d_norms;
+        // budgeted: the pass also leaves columns 0..S-1 in slots 0..S-1 (it reads them anyway);
+        // the first selection keeps those of them it picks and evicts the rest (stage_working_set)
+        const bool prefill = ctx->cfg.hbm_budget_bytes != 0 && !std::getenv("DUHL_NO_PREFILL");
+        if (prefill) {
+            p.fill_pool = ctx->pool;
+            p.fill_ld = ctx->ld_dev;
+            p.fill_cols = std::min<int64_t>(ctx->S, n);
+        }
         ProfScope ps(ctx, st, 1, (double)n * (4.0 * ctx->d4 + 24.0));
         ck(launch_gap_pass(p, kGapTileRows, st, &ctx->launches));
         ps.end();
+        if (prefill) {
+            for (int64_t i = 0; i < p.fill_cols; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
+            ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+        }
         double h = 0.0;
         ck(cudaMemsetAsync(ctx->d_sums + 7, 0, sizeof(double), st));
         ck(launch_sum(ctx->d_norms, n, ctx->d_sums + 7, st, &ctx->launches));

@@ -107,7 +107,8 @@ __device__ void block_flush_sums(const GapParams& p, SumAcc acc, int flag) {
 // smaller than the item count loops (a persistent unit-A grid beside the SCD epoch).
 // INGEST (duhl_create's one pass over A): also ||a_i||^2 into
 // p.norms_out (fp64; added atomically across row tiles, zero on entry) -- a non-finite
-// element makes it non-finite, which is how create detects invalid data.
+// element makes it non-finite, which is how create detects invalid data -- and, for
+// columns i < p.fill_cols, the column itself into HBM slot i (the pass reads it anyway).
 template <bool INGEST>
 __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int tile_rows, int ntiles, int64_t ngroups) {
     extern __shared__ double ws[];
@@ -139,11 +140,18 @@ __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int ti
                 n0 = fma((double)f.z, (double)f.z, n0); n1 = fma((double)f.w, (double)f.w, n1);
             }
         };
+        // INGEST: the first fill_cols columns also land in their HBM slots (slot i = column i)
+        float4* fill = (INGEST && i < p.fill_cols)
+                           ? reinterpret_cast<float4*>(p.fill_pool + i * p.fill_ld + r0) : nullptr;
         int q = lane;
         for (; q + 96 < nv; q += 128) {  // 4 independent 16-B loads in flight per lane
             float4 f0 = ld_stream_f4(a + q), f1 = ld_stream_f4(a + q + 32);
             float4 f2 = ld_stream_f4(a + q + 64), f3 = ld_stream_f4(a + q + 96);
             sq(f0); sq(f1); sq(f2); sq(f3);
+            if (INGEST && fill) {
+                __stcs(fill + q, f0); __stcs(fill + q + 32, f1);
+                __stcs(fill + q + 64, f2); __stcs(fill + q + 96, f3);
+            }
             double2 u, v;
             u = w2[2 * q]; v = w2[2 * q + 1];
             s0 = fma((double)f0.x, u.x, s0); s1 = fma((double)f0.y, u.y, s1);
@@ -161,6 +169,7 @@ __global__ void __launch_bounds__(kGapThreads, 4) k_gap_tile(GapParams p, int ti
         for (; q < nv; q += 32) {
             float4 f = ld_stream_f4(a + q);
             sq(f);
+            if (INGEST && fill) __stcs(fill + q, f);
             double2 u = w2[2 * q], v = w2[2 * q + 1];
             s0 = fma((double)f.x, u.x, s0); s1 = fma((double)f.y, u.y, s1);
             s0 = fma((double)f.z, v.x, s0); s1 = fma((double)f.w, v.y, s1);

@@ -34,6 +34,8 @@ struct GapParams {
     double* sums;              // [4] certificate sums or nullptr: sum gap, sum aux, sum |a| / sum y a, max |a| (bits)
     int* flag;                 // bit0 negative gap, bit1 non-finite
     double* norms_out;         // create's ingest pass: ||a_i||^2 by column index (zero on entry) or nullptr
+    float* fill_pool;          // create's ingest pass: columns i < fill_cols also stored to slot i
+    int64_t fill_ld, fill_cols;  //   of the HBM pool (stride fill_ld floats); nullptr / 0 = off
 };
 
 struct ScdParams {

@@ -471,7 +471,35 @@ def test_budget_smaller_than_data_swaps(D):
     assert r["status"] == 0
     sw = np.array([t.swaps for t in r["trace"]])
     assert sw[0] == m and sw[-len(sw) // 4:].mean() <= sw[:len(sw) // 4].mean()
-    assert c["h2d_bytes"] >= sw.sum() * d * 4
+    # every swap is one column copy, except round 0's picks among the m columns create's ingest
+    # pass left in the pool
+    assert (sw.sum() - m) * d * 4 <= c["h2d_bytes"] <= sw.sum() * d * 4
+
+
+@pytest.mark.parametrize("kernel", [1, 3])
+def test_create_leaves_the_first_columns_in_the_pool(D, kernel):
+    """duhl_create's ingest pass stores columns 0..S-1 in HBM slots 0..S-1 (it reads them
+    anyway).  SVM gaps at alpha = 0 are all 1/n, so the first gap selection is
+    0..m-1 (ties to the lowest index) and needs no copy; the epoch on those slots equals the
+    oracle's sequential epoch (P12, 1e-11)."""
+    d, n, m = 3001, 1200, 300
+    A, y = synth.svm_dense(d, n, seed=77)
+    lam = 1.0 / n
+    order = synth.permutation(np.arange(m), 3)
+    with D.create(A, y, lam, D.SVM_DUAL, hbm_budget_bytes=m * ((d + 3) // 4 * 4) * 4, m=m,
+                  scd_kernel=kernel) as P:
+        sel, sw = P.select(D.SEL_GAP, m=m, round=0)
+        assert sel.tolist() == list(range(m)) and sw == m   # swaps count P minus P_prev (Fig. 4b)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+        assert P.counters()["h2d_bytes"] == 0
+        sel2, sw2 = P.select(D.SEL_SEQUENTIAL, m=m, round=1)   # columns m..2m-1: copied now
+        P.scd_epoch(passes=1, seed=1, round=1)
+        assert sw2 == m and P.counters()["h2d_bytes"] == m * ((d + 3) // 4 * 4) * 4
+    alpha, vt = np.zeros(n), np.zeros(d)
+    O.scd_pass(O.SVM, A, O.col_norms(A), y, lam, alpha, vt, order)
+    assert np.abs(a_gpu - alpha).max() <= 1e-11 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
 
 
 
