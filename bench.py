@@ -42,12 +42,15 @@ CONFIGS = {
     # C4 time-to-eps 5.5 / 4.8 / 6.2 s at 1 / 2 / 4 passes; C3 14.2 / 8.1 / 6.6 s at 1 / 2 / 3, and
     # with adaptive-only certificates (tools/c3_sweep.py) 6.1 / 5.2 / 4.9 / 5.2 s at 3 / 4 / 5 / 6)
     # with host threads in unit A (--unit-a-host) the refresh no longer hides the epoch: C3 4.3 s at
-    # 2 and 3 passes, 5.1 s at 4 (passes_host)
+    # 2 and 3 passes, 5.1 s at 4 (passes_host); re-swept with the asynchronous epoch and the pool
+    # prefill (tools/sweep_c4.py --config c3, profiles/r02_sweep_c3.json): refresh 0.1 at 2 / 3 / 4 /
+    # 5 / 6 passes 3.23 / 2.71 / 2.57-2.60 / 2.65 / 2.70 s; 0.05 / 0.07 / 0.15 at 3 passes 2.98 /
+    # 2.74 / 3.07 s
     # C3 runs the asynchronous TPA-style epoch (scd_async, 128 coordinates in flight): time to 1e-5
     # 3.16 s vs 3.90 s with the exact k_scd_pipe (profiles/r02_tpa_vs_exact_c3.json); C4 keeps the
     # exact kernel (k_scd_gram then: 2.62 s vs 3.27 s async at W = 16; W >= 32 stalls on C4's correlated samples)
     "c3": dict(model=0, d=40000, n=200704, budget_frac=0.25, m=50176, lam=None, lam_rel=0.07, passes=5,
-               passes_host=3, scd_async=True, scd_block=128,
+               passes_host=4, scd_async=True, scd_block=128,
                label="C3: Lasso, ImageNet-shaped dense synthetic 40000 samples x 200704 features fp32 "
                      "(32.1 GB pinned host), HBM budget 25% (8.03 GB), m=50176, lambda=0.07 lambda_max"),
     "c4": dict(model=1, d=200704, n=40000, budget_frac=0.25, m=10000, lam=None, passes=2,
