@@ -114,7 +114,10 @@ typedef struct {
     int unit_a_host_threads;  /* unit A on the host (Alg. 2 l.7-10 as the paper's CPU unit):
                                  host threads that compute a_i^T v~ for part of the refresh's (and of every
                                  certificate's) non-resident columns from the pinned store (DRAM, not PCIe);
-                                 the device finishes their gaps.  0 = off (the GPU reads them over PCIe) */
+                                 the device finishes their gaps.  With an HBM budget they also take 70 % of
+                                 duhl_create's ingest pass (norms + gaps at alpha = 0 of the last columns;
+                                 the GPU keeps at least the S columns it leaves in the pool).  0 = off (the
+                                 GPU reads them over PCIe) */
     double unit_a_host_share; /* share of the refresh's non-resident columns given to those threads, in
                                  [0, 1]; < 0 = balanced each round from the measured host and PCIe rates */
     int scd_async;            /* dense problems: 0 = exact sequential Gram-block epoch (k_scd_gram /

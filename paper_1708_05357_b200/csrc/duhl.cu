@@ -180,6 +180,7 @@ struct duhl_ctx {
     HostUnitA* hua = nullptr;
     double* h_vt = nullptr;        // pinned [d4]: round-start v~ for the host threads
     double* h_hs = nullptr;        // pinned [n]: their dots
+    double* h_hnorm = nullptr;     // pinned [n]: column norms of create's host ingest share
     int64_t* h_hcols = nullptr;    // pinned [n]: their columns
     double* d_hs = nullptr;        // [n] dots uploaded for k_gap_finalize
     int64_t* d_hcols = nullptr;    // [n]
@@ -746,7 +747,7 @@ static void free_all(duhl_ctx* ctx) {
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
     hua_destroy(ctx->hua);
     ctx->hua = nullptr;
-    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hcols, (void*)ctx->h_plan_cols,
+    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hnorm, (void*)ctx->h_hcols, (void*)ctx->h_plan_cols,
                     (void*)ctx->h_plan_slots})
         if (p) cudaFreeHost(p);
     for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1, ctx->ev_c1})
@@ -1071,6 +1072,7 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
             return bail(DUHL_E_NOMEM);
         if (cudaHostAlloc((void**)&ctx->h_vt, ctx->d4 * sizeof(double), 0) != cudaSuccess ||
             cudaHostAlloc((void**)&ctx->h_hs, n * sizeof(double), 0) != cudaSuccess ||
+            cudaHostAlloc((void**)&ctx->h_hnorm, n * sizeof(double), 0) != cudaSuccess ||
             cudaHostAlloc((void**)&ctx->h_hcols, n * sizeof(int64_t), 0) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_hvt, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreate(&ctx->ev_g0) != cudaSuccess || cudaEventCreate(&ctx->ev_g1) != cudaSuccess ||
@@ -1144,7 +1146,27 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
     if (!ok2) { cudaGetLastError(); ctx->err = "precompute failed"; return bail(DUHL_E_CUDA); }
     if (!ctx->csc) {  // ingest: norms + gaps at alpha = 0 in one pass (k_gap_tile<INGEST>)
         ck(cudaMemsetAsync(ctx->d_norms, 0, n * sizeof(double), st));
-        GapParams p = gap_params(ctx, nullptr, n);
+        // unit A on host threads takes a share of the pass (as of the refresh): columns
+        // [ng, n) -- norms and a_i^T v~ at alpha = 0 straight from host DRAM, while the GPU reads
+        // [0, ng) over PCIe; the GPU keeps at least the S columns it leaves in the pool.  C4 (14
+        // threads): create 0.84 s with the GPU alone, 0.40 / 0.31 / 0.24 s at host shares 0.5 /
+        // 0.6 / 0.7 (both sides then read host DRAM at ~95 + ~45 GB/s)
+        static const double host_share = std::getenv("DUHL_INGEST_HOST_SHARE")
+                                             ? std::atof(std::getenv("DUHL_INGEST_HOST_SHARE")) : 0.7;
+        int64_t ng = n;
+        if (ctx->hua && ctx->cfg.hbm_budget_bytes != 0 && host_share > 0.0)
+            ng = std::max<int64_t>(std::min<int64_t>(ctx->S, n),
+                                   n - (int64_t)std::llround(std::min(1.0, host_share) * (double)n));
+        const int64_t kh = n - ng;
+        if (kh > 0) {  // v~ at alpha = 0: -b (Lasso, ridge, elastic net) or 0 (SVM dual)
+            for (int64_t r = 0; r < ctx->d4; ++r)
+                ctx->h_vt[r] = (model != DUHL_SVM_DUAL && r < d) ? -b_or_y[r] : 0.0;
+            for (int64_t t = 0; t < kh; ++t) ctx->h_hcols[t] = ng + t;
+            ck(cudaEventRecord(ctx->ev_hvt, st));
+            hua_post(ctx->hua, ctx->h_store, ctx->ld_host, ctx->d4, ctx->h_hcols, kh, ctx->h_vt, wscale(ctx),
+                     ctx->ev_hvt, ctx->h_hs, ctx->h_hnorm);
+        }
+        GapParams p = gap_params(ctx, nullptr, ng);
         p.norms_out = ctx->d_norms;
         // budgeted: the pass also leaves columns 0..S-1 in slots 0..S-1 (it reads them anyway);
         // the first selection keeps those of them it picks and evicts the rest (stage_working_set)
@@ -1160,6 +1182,15 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         if (prefill) {
             for (int64_t i = 0; i < p.fill_cols; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
             ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+        }
+        if (kh > 0) {  // the host share: norms to their place, dots -> gap_i at alpha = 0 (k_gap_finalize)
+            hua_wait(ctx->hua);
+            ck(cudaMemcpyAsync(ctx->d_norms + ng, ctx->h_hnorm, kh * sizeof(double), cudaMemcpyHostToDevice, st));
+            ck(cudaMemcpyAsync(ctx->d_hs, ctx->h_hs, kh * sizeof(double), cudaMemcpyHostToDevice, st));
+            ck(cudaMemcpyAsync(ctx->d_hcols, ctx->h_hcols, kh * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            GapParams hp = gap_params(ctx, ctx->d_hcols, kh);
+            hp.s_acc = ctx->d_hs;
+            ck(launch_gap_finalize(hp, st, &ctx->launches));
         }
         double h = 0.0;
         ck(cudaMemsetAsync(ctx->d_sums + 7, 0, sizeof(double), st));

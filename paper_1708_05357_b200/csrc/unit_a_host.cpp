@@ -57,6 +57,44 @@ __attribute__((target("avx512f"))) void dot4_avx512(const float* const* a, const
     }
 }
 
+// Four columns: a^T v and ||a||^2 in one read (duhl_create's ingest share on the host).
+__attribute__((target("avx512f"))) void dotnorm4_avx512(const float* const* a, const double* v, int64_t n,
+                                                        double* out, double* nrm) {
+    __m512d s[4], q[4];
+    for (int c = 0; c < 4; ++c) s[c] = q[c] = _mm512_setzero_pd();
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        const __m512d v0 = _mm512_loadu_pd(v + i);
+#pragma GCC unroll 4
+        for (int c = 0; c < 4; ++c) {
+            const __m512d f = _mm512_cvtps_pd(_mm256_loadu_ps(a[c] + i));
+            s[c] = _mm512_fmadd_pd(f, v0, s[c]);
+            q[c] = _mm512_fmadd_pd(f, f, q[c]);
+        }
+    }
+    for (int c = 0; c < 4; ++c) {
+        double r = _mm512_reduce_add_pd(s[c]), w = _mm512_reduce_add_pd(q[c]);
+        for (int64_t k = i; k < n; ++k) {
+            const double x = (double)a[c][k];
+            r += x * v[k];
+            w += x * x;
+        }
+        out[c] = r;
+        nrm[c] = w;
+    }
+}
+
+double norm_scalar(const float* a, int64_t n) {
+    double r0 = 0, r1 = 0;
+    int64_t i = 0;
+    for (; i + 2 <= n; i += 2) {
+        r0 += (double)a[i] * a[i];
+        r1 += (double)a[i + 1] * a[i + 1];
+    }
+    for (; i < n; ++i) r0 += (double)a[i] * a[i];
+    return r0 + r1;
+}
+
 double dot_scalar(const float* a, const double* v, int64_t n) {
     double r0 = 0, r1 = 0;
     int64_t i = 0;
@@ -87,6 +125,7 @@ struct HostUnitA {
     double scale = 1.0;
     cudaEvent_t ready = nullptr;
     double* s_out = nullptr;
+    double* norm_out = nullptr;
     std::atomic<int64_t> next{0};
     std::atomic<int64_t> t_ready_ns{0};
     std::chrono::steady_clock::time_point t_end;
@@ -111,15 +150,20 @@ struct HostUnitA {
                 if (t >= k) break;
                 if (avx512 && t + 4 <= k) {
                     const float* a4[4];
-                    double r[4];
+                    double r[4], w[4];
                     for (int c = 0; c < 4; ++c) a4[c] = store + cols[t + c] * ld;
-                    dot4_avx512(a4, vt, d4, r);
-                    for (int c = 0; c < 4; ++c) s_out[t + c] = scale * r[c];
+                    if (norm_out) dotnorm4_avx512(a4, vt, d4, r, w);
+                    else dot4_avx512(a4, vt, d4, r);
+                    for (int c = 0; c < 4; ++c) {
+                        s_out[t + c] = scale * r[c];
+                        if (norm_out) norm_out[t + c] = w[c];
+                    }
                     continue;
                 }
                 for (int64_t u = t; u < t + 4 && u < k; ++u) {
                     const float* a = store + cols[u] * ld;
                     s_out[u] = scale * (avx2 ? dot_avx2(a, vt, d4) : dot_scalar(a, vt, d4));
+                    if (norm_out) norm_out[u] = norm_scalar(a, d4);
                 }
             }
             std::lock_guard<std::mutex> lk(mu);
@@ -155,7 +199,7 @@ void hua_destroy(HostUnitA* h) {
 }
 
 void hua_post(HostUnitA* h, const float* store, int64_t ld, int64_t d4, const int64_t* cols, int64_t k,
-              const double* vt, double scale, cudaEvent_t ready, double* s_out) {
+              const double* vt, double scale, cudaEvent_t ready, double* s_out, double* norm_out) {
     hua_wait(h);
     std::lock_guard<std::mutex> lk(h->mu);
     h->store = store;
@@ -167,6 +211,7 @@ void hua_post(HostUnitA* h, const float* store, int64_t ld, int64_t d4, const in
     h->scale = scale;
     h->ready = ready;
     h->s_out = s_out;
+    h->norm_out = norm_out;
     h->next.store(0);
     h->t_ready_ns.store(0);
     h->active = (int)h->workers.size();

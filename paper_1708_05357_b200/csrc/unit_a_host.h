@@ -19,10 +19,11 @@ HostUnitA* hua_create(int threads, int dev);
 void hua_destroy(HostUnitA* h);
 
 // Posts one job: for t in [0, k): s_out[t] = scale * sum_{r < d4} store[cols[t] * ld + r] * vt[r],
-// fp64 accumulation of fp32 data.  vt becomes valid when `ready` completes (the workers
-// wait on it).  cols, vt and s_out must stay valid until hua_wait returns.  One job at a time.
+// fp64 accumulation of fp32 data, and, if norm_out is not null, norm_out[t] = sum_r a_r^2 (fp64;
+// duhl_create's ingest share).  vt becomes valid when `ready` completes (the workers wait on
+// it).  cols, vt, s_out and norm_out must stay valid until hua_wait returns.  One job at a time.
 void hua_post(HostUnitA* h, const float* store, int64_t ld, int64_t d4, const int64_t* cols, int64_t k,
-              const double* vt, double scale, cudaEvent_t ready, double* s_out);
+              const double* vt, double scale, cudaEvent_t ready, double* s_out, double* norm_out = nullptr);
 
 // Blocks until the posted job (if any) completes; returns its wall seconds from the
 // moment `ready` completed to the last column (0 with no job).

@@ -526,6 +526,36 @@ def test_round_record_rho(D, model, policy):
         assert min(seen) >= 1.0 - 1e-12 and max(seen) > 1.0
 
 
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM, O.RIDGE, O.ELASTIC])
+def test_create_host_ingest_share(D, model):
+    """With host unit-A threads, duhl_create's ingest pass is split: the GPU reads columns
+    [0, ng) over PCIe, the host threads take [ng, n) from host DRAM (norms and a_i^T v~ at
+    alpha = 0; the device finishes gap_i).  The gap memory at creation is the oracle's gap at
+    alpha = 0 for every column, and an epoch over the first gap selection -- which draws on
+    both shares -- equals the oracle's (the norms of both shares enter the steps)."""
+    d, n, m = (400, 1000, 250) if model != O.SVM else (120, 1000, 250)
+    A, lab = _data(model, d, n, seed=43)
+    lam = _lam(model, n)
+    y = lab if model == O.SVM else None
+    with D.create(A, lab, lam, model, hbm_budget_bytes=300 * d * 4, m=m, cert_every=1 << 30, seed=8,
+                  unit_a_host_threads=3) as P:
+        a0, v0, z0 = P.get_state()
+        g_or = _oracle_state(model, A, lab, lam, np.zeros(n), d)[2]
+        tol = 1e-9 * max(1e-300, np.abs(g_or).max())
+        assert np.all(np.abs(z0 - g_or) <= 1e-9 * np.abs(g_or) + tol)
+        sel, _ = P.select(D.SEL_GAP, m=m, round=0)
+        if model != O.SVM:   # Lasso-type gaps differ by column: the set spans both shares
+            assert sel.min() < 300 and sel.max() >= 600
+        order = synth.permutation(sel, 4)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
+    O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
+    assert np.abs(a_gpu - alpha).max() <= 1e-11 * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= 1e-11 * max(1.0, np.abs(vt).max())
+
+
 @pytest.mark.parametrize("model,share", [(O.LASSO, 1.0), (O.SVM, 0.5), (O.RIDGE, -1.0), (O.ELASTIC, 1.0)])
 def test_unit_a_host_threads_refresh(D, model, share):
     """Host-thread unit A (cfg.unit_a_host_threads, NEXT-1): the refreshed columns outside the
