@@ -1177,14 +1177,23 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
             p.fill_cols = std::min<int64_t>(ctx->S, n);
         }
         ProfScope ps(ctx, st, 1, (double)n * (4.0 * ctx->d4 + 24.0));
+        if (kh > 0) ck(cudaEventRecord(ctx->ev_g0, st));
         ck(launch_gap_pass(p, kGapTileRows, st, &ctx->launches));
+        if (kh > 0) ck(cudaEventRecord(ctx->ev_g1, st));
         ps.end();
         if (prefill) {
             for (int64_t i = 0; i < p.fill_cols; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
             ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
         }
         if (kh > 0) {  // the host share: norms to their place, dots -> gap_i at alpha = 0 (k_gap_finalize)
-            hua_wait(ctx->hua);
+            const double host_s = hua_wait(ctx->hua);
+            float gms = 0.0f;  // both units' column rates seed the certificates' split (same regime:
+                               // host threads and PCIe reads drawing on host DRAM together)
+            if (cudaEventSynchronize(ctx->ev_g1) == cudaSuccess && host_s > 0.0 &&
+                cudaEventElapsedTime(&gms, ctx->ev_g0, ctx->ev_g1) == cudaSuccess && gms > 0.0f) {
+                const double rh = (double)kh / host_s, rg = (double)ng / (1e-3 * gms);
+                ctx->cert_share = std::min(0.95, std::max(0.05, rh / (rh + rg)));
+            }
             ck(cudaMemcpyAsync(ctx->d_norms + ng, ctx->h_hnorm, kh * sizeof(double), cudaMemcpyHostToDevice, st));
             ck(cudaMemcpyAsync(ctx->d_hs, ctx->h_hs, kh * sizeof(double), cudaMemcpyHostToDevice, st));
             ck(cudaMemcpyAsync(ctx->d_hcols, ctx->h_hcols, kh * sizeof(int64_t), cudaMemcpyHostToDevice, st));
