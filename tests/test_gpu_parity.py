@@ -311,6 +311,31 @@ def test_scd_epoch_fast_mode_block_sizes(D, model, W):
     assert np.abs(v_gpu - vt).max() <= 1e-6 * max(1.0, np.abs(vt).max())
 
 
+@pytest.mark.parametrize("W", [4, 8, 12, 16])
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("model", [O.LASSO, O.SVM])
+def test_scd_ser_block_sizes(D, model, W, exact):
+    """k_scd_ser at every block width it unrolls (W = 4, 8, 12, 16), ragged rows (d = 20,001 over
+    many CTAs) and a ragged last block (m = 190): exact mode = the oracle's sequential epoch to
+    1e-11, fast mode (fp32 Gram entries and block corrections) to 1e-6."""
+    d, n, m = 20001, 200, 190
+    A, lab = _data(model, d, n, seed=600 + W)
+    lam = _lam(model, n)
+    y = lab if model == O.SVM else None
+    order = synth.permutation(np.arange(m), 10 + W)
+    with D.create(A, lab, lam, model, m=m, scd_kernel=3, scd_block=W, scd_exact=exact) as P:
+        assert P.scd_shape()[:2] == ("k_scd_ser", W)
+        P.select(D.SEL_SEQUENTIAL, m=m, round=0)
+        P.scd_epoch(perm=order)
+        a_gpu, v_gpu, _ = P.get_state()
+    alpha = np.zeros(n)
+    vt = -lab.copy() if model != O.SVM else np.zeros(d)
+    O.scd_pass(model, A, O.col_norms(A), y, lam, alpha, vt, order)
+    tol = 1e-11 if exact else 1e-6
+    assert np.abs(a_gpu - alpha).max() <= tol * max(1e-300, np.abs(alpha).max())
+    assert np.abs(v_gpu - vt).max() <= tol * max(1.0, np.abs(vt).max())
+
+
 def test_scd_internal_permutation_generator_matches_oracle(D):
     """The device counter-based permutation equals the oracle's."""
     A, b = synth.lasso_dense(1000, 800, seed=3)
