@@ -696,14 +696,16 @@ def _run_shards(D, parts, body):
     return out
 
 
-@pytest.mark.parametrize("model,budget_cols,K", [(O.SVM, 150, 2), (O.LASSO, 0, 2), (O.LASSO, 160, 3),
-                                                 (O.RIDGE, 0, 2)])
-def test_virtual_shards_match_oracle_cocoa(D, model, budget_cols, K):
+@pytest.mark.parametrize("model,budget_cols,K,host", [(O.SVM, 150, 2, 0), (O.LASSO, 0, 2, 0), (O.LASSO, 160, 3, 0),
+                                                      (O.RIDGE, 0, 2, 0), (O.LASSO, 160, 2, 2), (O.SVM, 150, 3, 2)])
+def test_virtual_shards_match_oracle_cocoa(D, model, budget_cols, K, host):
     """K column shards on one GPU: K contexts with (col_offset, n_global), each on
     its own host thread, joined by an in-process group (the library's collectives: dv sum,
     line-search sums, certificate sums and max).  Round by round: every shard's working set is a
     valid top-m of the oracle's shard gap memory, and gamma and the certified gap equal the
-    oracle's CoCoA round (or_duhl_solve_cocoa's arithmetic) on those sets."""
+    oracle's CoCoA round (or_duhl_solve_cocoa's arithmetic) on those sets.  host > 0: each shard
+    also runs host unit-A threads (its share of the ingest pass, the refresh and the
+    certificates) and, with a budget, starts from its pool prefill."""
     d, n = (300, 1200) if model != O.SVM else (80, 1200)
     A, lab = _data(model, d, n, seed=700 + model + K)
     lam = _lam(model, n)
@@ -717,7 +719,7 @@ def test_virtual_shards_match_oracle_cocoa(D, model, budget_cols, K):
             recs, sets = [], []
             with D.create(Ak, labk, lam, model, hbm_budget_bytes=budget_cols * d * 4, m=m,
                           refresh_fraction=rc / (hi - lo), cert_every=1, seed=11, n_global=n,
-                          col_offset=lo) as P:
+                          col_offset=lo, unit_a_host_threads=host) as P:
                 P.comm_init_group(G, k)
                 for t in range(rounds):
                     recs.append(P.round(t, passes=passes, certify=True))
