@@ -1181,6 +1181,8 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         ck(launch_gap_pass(p, kGapTileRows, st, &ctx->launches));
         if (kh > 0) ck(cudaEventRecord(ctx->ev_g1, st));
         ps.end();
+        if (ctx->cfg.hbm_budget_bytes != 0)  // the GPU's share read the pinned store over PCIe
+            ctx->zc_bytes += ng * ctx->ld_dev * (int64_t)sizeof(float);
         if (prefill) {
             for (int64_t i = 0; i < p.fill_cols; ++i) { ctx->col_slot[i] = (int)i; ctx->slot_col[i] = (int)i; }
             ck(cudaMemcpyAsync(ctx->d_col_slot, ctx->col_slot.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
