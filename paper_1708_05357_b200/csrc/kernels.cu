@@ -1610,7 +1610,9 @@ cudaError_t launch_csc_norms(const CscMat& A, int64_t n, double* norms, cudaStre
 // (fp64; k_csc_gap keeps two).  Measured (C5s, gap pass GB/s): k_csc_gap 2274; this kernel
 // with 64 / 96 / 128 / 160 / 192 KB of rows in shared memory 2443 / 2548 / 2607 / 2624 /
 // 2568; two partial sums at 200 KB 1737; eight (predicated tails, next column's extent
-// prefetched) 2024-2189 -- register-limited at 1024 threads.
+// prefetched) 2024-2189 -- register-limited at 1024 threads; the index / value loads of the
+// next 128-nonzero window software-pipelined across the warp's column stream 2313 (1024
+// threads, spills) / 2235 (768) / 1618 (512), against 2629 for this loop in the same run.
 constexpr int kCscSmemThreads = 1024;
 __global__ void __launch_bounds__(kCscSmemThreads, 1) k_csc_gap_smem(GapParams p, CscMat A, int Rs) {
     extern __shared__ double sw[];
