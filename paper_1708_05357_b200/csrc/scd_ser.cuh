@@ -25,10 +25,6 @@
 //   wait delta_b; correction sweep; warp reduce-scatter -> shared memory -> warp 0
 //     REDs u_{b+1} (one RED per entry per CTA) and ARRIVEs(b+1)
 //   off the chain: fast mode v += A_b delta_b (fp64); free stage b (mbarrier empty)
-// Measured variants (C4 fast mode, 140 CTAs, 4.65 ms per pass as built): fusing the v update
-// with u'_{b+2} in one sweep 4.91 ms (u' then waits on the update's 12-deep DFMA chains);
-// warp 7 taking a double share of the sweeps (TMA issue moved into it) 4.65 ms -- the
-// compute warps are bound by their per-lane latency chains, not by sub-partition issue.
 // control warp: WAIT(b) -> zero red[(b+5) % 6] (CTA 0) -> read red[b % 6] ->
 //     the W steps -> publish delta_b (mbarrier dfull[b & 1]).
 // producer warp: block q into stage q % 3 once block q-3's stage is free.
@@ -40,6 +36,10 @@
 // Arrival counters: bar[b & 1] counts the arrivals of blocks b, b-2, ...; a CTA
 // ARRIVEs(b+1) only after its own WAIT(b) completed, so no CTA can ARRIVE(b+2)
 // before every WAIT(b) saw its target.
+// Measured variants (C4 fast mode, 140 CTAs, 4.65 ms per pass as built): fusing the v update
+// with u'_{b+2} in one sweep 4.91 ms (u' then waits on the update's 12-deep DFMA chains);
+// warp 7 taking a double share of the sweeps (TMA issue moved into it) 4.65 ms -- the
+// compute warps are bound by their per-lane latency chains, not by sub-partition issue.
 #pragma once
 
 static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction buffers");
