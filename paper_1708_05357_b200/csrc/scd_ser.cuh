@@ -52,7 +52,8 @@ static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction 
 // sweep) and sharing the x loads of diagonal tiles: 7.49 ms -- the fp64 u' work then sits on
 // the five tile warps unevenly and the kernel needs a 168-byte local frame.  Sharing the x
 // loads of diagonal tiles alone (12 of 40 loads per row group): fast 4.79 vs 4.68 ms, exact
-// 6.25 vs 6.47 -- not kept.
+// 6.25 vs 6.47 -- not kept.  The fast-mode v update with two half-depth chains per component
+// 4.58 ms, or with the thread's two row groups interleaved 4.61, against 4.59-4.63: noise.
 #ifndef DUHL_SER_WARPS
 #define DUHL_SER_WARPS 8
 #endif
