@@ -45,7 +45,8 @@ CONFIGS = {
     # 2 and 3 passes, 5.1 s at 4 (passes_host); re-swept with the asynchronous epoch and the pool
     # prefill (tools/sweep_c4.py --config c3, profiles/r02_sweep_c3.json): refresh 0.1 at 2 / 3 / 4 /
     # 5 / 6 passes 3.23 / 2.71 / 2.57-2.60 / 2.65 / 2.70 s; 0.05 / 0.07 / 0.15 at 3 passes 2.98 /
-    # 2.74 / 3.07 s
+    # 2.74 / 3.07 s; with the gather staging C3's heavy rounds (profiles/r02_sweep_c3_gather.json)
+    # 3 / 4 / 5 passes 2.03 / 1.91 / 1.93 s, refresh 0.08 / 0.12 at 4 passes 1.99 / 1.99 s
     # C3 runs the asynchronous TPA-style epoch (scd_async, 128 coordinates in flight): time to 1e-5
     # 3.16 s vs 3.90 s with the exact k_scd_pipe (profiles/r02_tpa_vs_exact_c3.json); C4 keeps the
     # exact kernel (k_scd_gram then: 2.62 s vs 3.27 s async at W = 16; W >= 32 stalls on C4's correlated samples)

@@ -596,6 +596,9 @@ static duhl_status ensure_host_P(duhl_ctx* ctx) {
     return DUHL_OK;
 }
 
+constexpr int64_t kHeavyRunCols = 16;  // mean index-run length that sends a heavy round to the copy engine
+constexpr size_t kStageCeMinBytes = 512 * 1024;  // shorter columns: no copy-engine share in gather rounds
+
 static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& P, int64_t round,
                                      int64_t* swaps) {
     TRY(finalize_staging(ctx));
@@ -644,7 +647,19 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // new): columns in index order with consecutive slots, so runs coalesce into
         // large copies at full PCIe rate, and one progress write at the end.
         const bool heavy = (int64_t)news.size() * 2 > m;
-        if (heavy) std::sort(news.begin(), news.end());
+        // A heavy round goes to the copy engine in coalesced runs only when its new columns form
+        // long index runs (C4's first rounds: whole index blocks, ~51 GB/s).  Scattered columns
+        // (C3's Lasso selections: one 160-KB copy each, ~22 GB/s) take the gather kernel like a
+        // light round.
+        bool heavy_ce = false;
+        if (heavy) {
+            std::vector<int64_t> srt(news);
+            std::sort(srt.begin(), srt.end());
+            int64_t runs = srt.empty() ? 0 : 1;
+            for (size_t q = 1; q < srt.size(); ++q) runs += srt[q] != srt[q - 1] + 1;
+            heavy_ce = runs == 0 || (int64_t)srt.size() >= kHeavyRunCols * runs || ctx->unit_a_ctas <= 0;
+            if (heavy_ce) news.swap(srt);
+        }
         // every earlier copy has landed before this round's epoch (the compute stream waited on
         // ev_copy): kept slots need no wait
         std::fill(ctx->slot_batch.begin(), ctx->slot_batch.end(), 0u);
@@ -656,7 +671,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         static const int nstage = std::getenv("DUHL_STAGE_CTAS") ? std::max(1, std::min(16, std::atoi(std::getenv("DUHL_STAGE_CTAS"))))
                                                                : kStageCtas;  // developer override (<= 16 counters)
         // (also when the copies complete before the epoch: the gather is the faster path either way)
-        ctx->stage_ctas = (!heavy && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
+        ctx->stage_ctas = (!heavy_ce && ctx->unit_a_ctas > 0 && !force_ce) ? nstage : 0;
         // every round that overlaps (or gathers) starts from zeroed counters: gather CTA 0's counter
         // is the copy engine's sequence counter progress[0], so a heavy (copy-engine) round after
         // a gather round would otherwise see the gather's final count as landed copies
@@ -665,13 +680,17 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
 #else
         if (ctx->stage_ctas > 0) CK(cudaMemsetAsync(ctx->d_progress, 0, kProgressBytes, ctx->st));
 #endif
-        // share of a gather round's columns copied by the copy engine beside the gather kernel
-        static const double ce_share_cfg = std::getenv("DUHL_STAGE_CE_SHARE") ? std::atof(std::getenv("DUHL_STAGE_CE_SHARE"))
-                                                                              : kStageCeShare;
+        // share of a gather round's columns copied by the copy engine beside the gather kernel:
+        // only for long columns -- a per-column copy costs a fixed setup, so 160-KB columns (C3)
+        // move at ~22 GB/s on the copy engine against ~50 for the gather (C3 time to 1e-5 2.30 s
+        // with a 0.3 share, 1.88 s without)
+        static const char* ce_env = std::getenv("DUHL_STAGE_CE_SHARE");
+        const double ce_share_cfg = ce_env ? std::atof(ce_env)
+                                           : ((size_t)ctx->ld_dev * sizeof(float) >= kStageCeMinBytes ? kStageCeShare : 0.0);
         const double ce_share = ctx->write_value ? std::max(0.0, std::min(0.9, ce_share_cfg)) : 0.0;
         unsigned nce = 0, ngath = 0;
         size_t fi = 0;
-        const unsigned heavy_seq = ctx->overlap && heavy ? ctx->batch_seq + 1 : 0u;
+        const unsigned heavy_seq = ctx->overlap && heavy_ce ? ctx->batch_seq + 1 : 0u;
         for (size_t q = 0; q < news.size(); ++q) {
             const int64_t j = news[q];
             const int s = free_slots[fi++];
@@ -684,7 +703,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
                 const bool ce = std::floor((double)(q + 1) * ce_share) > std::floor((double)q * ce_share);
                 seq = ce ? (kCeToken | (unsigned)++nce) : (unsigned)++ngath;
             }
-            else if (ctx->overlap) seq = heavy ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
+            else if (ctx->overlap) seq = heavy_ce ? heavy_seq : ctx->batch_seq + 1 + (unsigned)(q / 4);
             ctx->slot_batch[s] = seq;
             ctx->copy_plan.push_back({j, s, seq});
         }
@@ -692,7 +711,7 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
         // round 0 may find some of them left in the pool by duhl_create's ingest pass
         for (int64_t j : P) nsw += ctx->inP[j] ? 0 : 1;
         if (ctx->overlap && ctx->stage_ctas == 0 && !news.empty())
-            ctx->batch_seq = heavy ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
+            ctx->batch_seq = heavy_ce ? heavy_seq : ctx->batch_seq + (unsigned)((news.size() + 3) / 4);
         // the compute stream may still read evicted slots (previous epoch): order copies after it
         CK(cudaEventRecord(ctx->ev_copy, ctx->st));
         CK(cudaStreamWaitEvent(ctx->cst, ctx->ev_copy, 0));
