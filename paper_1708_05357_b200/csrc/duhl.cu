@@ -657,7 +657,9 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
             std::sort(srt.begin(), srt.end());
             int64_t runs = srt.empty() ? 0 : 1;
             for (size_t q = 1; q < srt.size(); ++q) runs += srt[q] != srt[q - 1] + 1;
-            heavy_ce = runs == 0 || (int64_t)srt.size() >= kHeavyRunCols * runs || ctx->unit_a_ctas <= 0;
+            static const int64_t run_cols = std::getenv("DUHL_HEAVY_RUN_COLS")  // developer A/B
+                                                ? std::atoll(std::getenv("DUHL_HEAVY_RUN_COLS")) : kHeavyRunCols;
+            heavy_ce = runs == 0 || (int64_t)srt.size() >= run_cols * runs || ctx->unit_a_ctas <= 0;
             if (heavy_ce) news.swap(srt);
         }
         // every earlier copy has landed before this round's epoch (the compute stream waited on
