@@ -747,6 +747,10 @@ static duhl_status stage_working_set(duhl_ctx* ctx, const std::vector<int64_t>& 
     return DUHL_OK;
 }
 
+// (Device memory comes from plain cudaMalloc: the stream-ordered pool allocator would avoid the
+// driver's occasional 0.1-1 s cudaFree / cudaMalloc stalls seen in repeated create / close loops
+// (tools/create_timing.py), but cuStreamWriteValue32 -- the staging progress counters -- rejects
+// pool memory, and creates still stalled now and then with it.)
 static void free_all(duhl_ctx* ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->cst) cudaStreamSynchronize(ctx->cst);

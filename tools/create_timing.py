@@ -10,9 +10,14 @@ kw = bench.launch_kwargs(args, cfg)
 A, lab = bench.make_data(cfg, kw["seed"])
 lam = bench.lam_of(cfg, A, lab)
 bench.pin_host(A)
+solve = len(sys.argv) > 3 and sys.argv[3] == "solve"
 for r in range(reps):
     t0 = time.perf_counter()
     P = D.create(A, lab, lam, cfg["model"], scd_exact=args.exact, **kw)
     t1 = time.perf_counter()
+    if solve:
+        P.solve(1e-5, 1000, passes=args.passes)
+    t2 = time.perf_counter()
     P.close()
-    print(name, "create", round(t1 - t0, 4), "close", round(time.perf_counter() - t1, 4), flush=True)
+    print(name, "create", round(t1 - t0, 4), "solve", round(t2 - t1, 4), "close", round(time.perf_counter() - t2, 4),
+          flush=True)
