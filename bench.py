@@ -558,25 +558,29 @@ def run_duhl(args, cfg, rank, world, local):
             c2["updates"] = int(max_over_ranks(c2["updates"], world)) * world
             runs.append(dict(r=r, c=c2, t_create=t_c2, t_solve=max_over_ranks(t_solve, world),
                              wall=max_over_ranks(wall, world), state_err=state_err))
-        order = sorted(range(len(runs)), key=lambda q: runs[q]["t_solve"])
+        # the median run by create + solve wall time (value, bytes, create_s); time_to_eps_s is the
+        # median duhl_solve time on its own (the two medians may come from different runs)
+        order = sorted(range(len(runs)), key=lambda q: runs[q]["wall"])
         med = runs[order[len(runs) // 2]]
         r, c2, wall = med["r"], med["c"], med["wall"]
+        t_solve_med = sorted(q["t_solve"] for q in runs)[len(runs) // 2]
         rounds = max(1, r["rounds"])
         e2e = {"value": c2["updates"] / wall, "unit": "coord updates/s",
                "h2d_bytes_per_step": int(c2["h2d_bytes"] / rounds),
                "zero_copy_bytes_per_step": int(c2["zc_bytes"] / rounds),
                "d2h_bytes_per_step": int(c2["d2h_bytes"] / rounds),
-               "time_to_eps_s": med["t_solve"], "time_to_eps_runs_s": [q["t_solve"] for q in runs],
+               "time_to_eps_s": t_solve_med, "time_to_eps_runs_s": [q["t_solve"] for q in runs],
+               "create_plus_solve_runs_s": [q["wall"] for q in runs],
                "eps": args.eps, "certified_gap": r["gap"], "create_plus_solve_s": wall,
                "converged": all(q["r"]["status"] == 0 for q in runs), "rounds": r["rounds"],
                "rho_mean": rho_mean(r["trace"]),
                "swaps_per_round_first_last": swaps_trend(r["trace"]),
                "create_s": med["t_create"],
                "state_check": runs[0]["state_err"],
-               "note": "median run of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
+               "note": "median (by create + solve wall) of --e2e-runs fresh (create, solve) pairs; value = updates / (duhl_create "
                        "from the caller's pinned host buffers (used in place; one device pass over A for "
                        "norms + z at alpha=0, which also leaves columns 0..S-1 in the S HBM slots) + "
-                       "duhl_solve to the certified gap); time_to_eps_s = duhl_solve alone (the rest of the "
+                       "duhl_solve to the certified gap); time_to_eps_s = the median duhl_solve alone (the rest of the "
                        "cold HBM fill included); h2d = fill + swaps (copy engine and staging gather); "
                        "zero-copy = create's pass + refresh + certificate reads of non-resident columns; "
                        "d2h = the library's read-backs (counted)"}
