@@ -54,6 +54,8 @@ static_assert(kRedBufs == 6, "the zeroing rule of k_scd_ser assumes 6 reduction 
 // loads of diagonal tiles alone (12 of 40 loads per row group): fast 4.79 vs 4.68 ms, exact
 // 6.25 vs 6.47 -- not kept.  The fast-mode v update with two half-depth chains per component
 // 4.58 ms, or with the thread's two row groups interleaved 4.61, against 4.59-4.63: noise.
+// Warps 1-5 only arriving at the u-publish barrier (bar.arrive) and going on to their v update
+// while warp 0 sums and releases: 4.74-4.78 vs 4.66-4.69 -- slower.
 #ifndef DUHL_SER_WARPS
 #define DUHL_SER_WARPS 8
 #endif
