@@ -1799,6 +1799,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     static thread_local std::vector<int64_t> smp;
     smp.clear();
     int64_t kg = kref, kh = 0, nonres = 0;  // refresh columns on the GPU / host threads; non-resident
+    bool heavy_round = false;             // the threads took every non-resident column (see below)
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
     if (agg) {  // round-start state for the aggregation: v0 and alpha_P
         CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
@@ -1822,7 +1823,12 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         ctx->cursor = (ctx->cursor + kref) % n;
         nonres = host_cols;
         // the host threads take the last kh of the non-resident columns; the GPU the rest
-        kh = ctx->hua ? (ctx->overlap ? host_cols : (int64_t)std::llround(ctx->hua_share * (double)host_cols)) : 0;
+        // (a round that stages more than m/2 columns leaves PCIe to the staging: the threads take all)
+        static const bool heavy_host = std::getenv("DUHL_NO_HEAVY_HOST_REFRESH") == nullptr;
+        heavy_round = heavy_host && swaps * 2 > ctx->m_cur;
+        kh = ctx->hua ? ((ctx->overlap || heavy_round) ? host_cols
+                                                       : (int64_t)std::llround(ctx->hua_share * (double)host_cols))
+                      : 0;
         if (kh > 0) {
             int64_t g = 0, hcount = 0, seen = 0;
             for (int64_t q = 0; q < kref; ++q) {
@@ -1930,7 +1936,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         rec->rho = (rs[1] > 0.0 && m > 0) ? (rs[0] / (double)m) / (rs[1] / (double)n) : 1.0;
         rec->gap_est = est[2] > 0.0 ? est[0] + est[3] * est[1] / est[2] : -1.0;
     }
-    if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0) {
+    if (kh > 0 && ctx->cfg.unit_a_host_share < 0.0 && !heavy_round) {  // (a forced share measures no balance)
         // balance: the host's columns take as long as what PCIe carries this round (staging
         // copies + the GPU's zero-copy columns): kh = (swaps + nonres) r_h / (r_h + r_p)
         float gms = 0.0f, cms = 0.0f;
