@@ -1406,23 +1406,47 @@ cudaError_t launch_ridge_sums(const double* alpha, const int64_t* P, const doubl
     ++*launches;
     return cudaGetLastError();
 }
-// Lasso: out[g] += sum_q da_q sgn+(aold_q + gam[g] da_q), da_q = alpha_j - aold_q  (g < ng)
+// Lasso: out[g] += sum_q da_q sgn+(aold_q + gam[g] da_q), da_q = alpha_j - aold_q  (g < ng,
+// gam ascending), sgn+(x) = sign(x), and sign(da) at x = 0 (the right derivative).  Along the
+// grid x_q(g) = fma(g, da, aold) is monotone, so coordinate q contributes -|da_q| below its
+// switch index j*_q (the first grid point where x_q has reached da's side of 0, by the same
+// fma predicate the direct evaluation uses) and +|da_q| from j*_q on:
+//   out[g] = sum_q |da_q| - 2 sum_{q: j*_q > g} |da_q|.
+// One binary search and one shared-memory atomic per coordinate instead of ng.
 __global__ void k_lasso_dgrid(const double* alpha, const int64_t* P, const double* aold, int64_t k,
                               const double* gam, int ng, double* out) {
-    __shared__ double sh[64];
-    for (int g = threadIdx.x; g < ng; g += blockDim.x) sh[g] = 0.0;
+    __shared__ double sg[64], cnt[65], sbase[8];
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) sg[g] = gam[g];
+    for (int g = threadIdx.x; g <= ng; g += blockDim.x) cnt[g] = 0.0;
     __syncthreads();
+    double base = 0.0;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += (int64_t)gridDim.x * blockDim.x) {
         const double a0 = aold[q], da = alpha[P[q]] - a0;
         if (da == 0.0) continue;
-        for (int g = 0; g < ng; ++g) {
-            const double x = fma(gam[g], da, a0);
-            const double sg = x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (da > 0.0 ? 1.0 : -1.0));
-            atomicAdd(&sh[g], da * sg);
+        const double w = fabs(da);
+        base += w;
+        int lo = 0, hi = ng;  // first j in [0, ng] with the predicate true (ng: never)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const double x = fma(sg[mid], da, a0);
+            const bool reached = da > 0.0 ? x >= 0.0 : x <= 0.0;
+            if (reached) hi = mid;
+            else lo = mid + 1;
+        }
+        if (lo > 0) atomicAdd(&cnt[lo], w);  // j* = lo: grid points 0..lo-1 lie below the switch
+    }
+    base = warp_sum(base);
+    if ((threadIdx.x & 31) == 0) sbase[threadIdx.x >> 5] = base;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += sbase[w];
+        double suffix = 0.0;  // sum of cnt[j'] for j' > g, walking g downwards
+        for (int g = ng - 1; g >= 0; --g) {
+            suffix += cnt[g + 1];
+            atomicAdd(&out[g], b - 2.0 * suffix);
         }
     }
-    __syncthreads();
-    for (int g = threadIdx.x; g < ng; g += blockDim.x) atomicAdd(&out[g], sh[g]);
 }
 // v = v0 + gamma dv ; alpha_P = aold + gamma (alpha_P - aold)
 __global__ void k_apply_gamma(double* v, const double* v0, const double* dv, int64_t d4, double* alpha,
