@@ -181,6 +181,8 @@ struct duhl_ctx {
     double* h_vt = nullptr;        // pinned [d4]: round-start v~ for the host threads
     double* h_hs = nullptr;        // pinned [n]: their dots
     double* h_hnorm = nullptr;     // pinned [n]: column norms of create's host ingest share
+    int64_t* h_ref_idx = nullptr;  // pinned [n]: a round's refresh columns (async upload, no realloc)
+    int64_t* h_ref_smp = nullptr;  // pinned [n]: the refreshed columns outside P (gap-estimate sample)
     int64_t* h_hcols = nullptr;    // pinned [n]: their columns
     double* d_hs = nullptr;        // [n] dots uploaded for k_gap_finalize
     int64_t* d_hcols = nullptr;    // [n]
@@ -772,7 +774,8 @@ static void free_all(duhl_ctx* ctx) {
     if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
     hua_destroy(ctx->hua);
     ctx->hua = nullptr;
-    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hnorm, (void*)ctx->h_hcols, (void*)ctx->h_plan_cols,
+    for (void* p : {(void*)ctx->h_vt, (void*)ctx->h_hs, (void*)ctx->h_hnorm, (void*)ctx->h_hcols,
+                    (void*)ctx->h_ref_idx, (void*)ctx->h_ref_smp, (void*)ctx->h_plan_cols,
                     (void*)ctx->h_plan_slots})
         if (p) cudaFreeHost(p);
     for (cudaEvent_t e : {ctx->ev_hvt, ctx->ev_g0, ctx->ev_g1, ctx->ev_c1})
@@ -1113,6 +1116,9 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         (cudaHostAlloc((void**)&ctx->h_plan_cols, n * sizeof(int64_t), 0) != cudaSuccess ||
          cudaHostAlloc((void**)&ctx->h_plan_slots, n * sizeof(int), 0) != cudaSuccess ||
          cudaEventCreateWithFlags(&ctx->ev_plan, cudaEventDisableTiming) != cudaSuccess))
+        return bail(DUHL_E_NOMEM);
+    if (cudaHostAlloc((void**)&ctx->h_ref_idx, std::max<int64_t>(1, n) * sizeof(int64_t), 0) != cudaSuccess ||
+        cudaHostAlloc((void**)&ctx->h_ref_smp, std::max<int64_t>(1, n) * sizeof(int64_t), 0) != cudaSuccess)
         return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
     ctx->slot_col.assign(ctx->S, -1);
@@ -1795,9 +1801,12 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         CK(launch_sum(ctx->d_z, n, ctx->d_rho + 1, ctx->st, &ctx->launches));
     }
     auto tstaged = now();
-    std::vector<int64_t> idx(kref);
-    static thread_local std::vector<int64_t> smp;
-    smp.clear();
+    // pinned per-context buffers: no per-round allocation, and the uploads are truly asynchronous
+    // (C5 refreshes 1 M columns a round: two 8-MB pageable copies and a zero-filled vector cost
+    // ~6 ms of host time per 17-ms round before)
+    int64_t* idx = ctx->h_ref_idx;
+    int64_t* smp = ctx->h_ref_smp;
+    int64_t nsmp = 0;
     int64_t kg = kref, kh = 0, nonres = 0;  // refresh columns on the GPU / host threads; non-resident
     bool heavy_round = false;             // the threads took every non-resident column (see below)
     const bool agg = ctx->nranks > 1 || ctx->cfg.linesearch;
@@ -1811,14 +1820,19 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
                      // otherwise the epoch waits for it (it would hold the SMs the
                      // cooperative launch needs)
         int64_t host_cols = 0;
-        for (int64_t q = 0; q < kref; ++q) {
-            idx[q] = (ctx->cursor + q) % n;
-            host_cols += ctx->col_slot[idx[q]] < 0;
+        {   // the cursor's range (no modulo per entry); non-resident count only with a budget
+            int64_t c = ctx->cursor;
+            for (int64_t q = 0; q < kref; ++q) {
+                idx[q] = c;
+                if (++c == n) c = 0;
+            }
+            if (ctx->cfg.hbm_budget_bytes != 0)
+                for (int64_t q = 0; q < kref; ++q) host_cols += ctx->col_slot[idx[q]] < 0;
         }
         if (ctx->P_host_valid) {  // the refreshed columns outside P: a systematic sample of fresh gaps
-            smp.clear();
+            nsmp = 0;
             for (int64_t q = 0; q < kref; ++q)
-                if (!ctx->inP[idx[q]]) smp.push_back(idx[q]);
+                if (!ctx->inP[idx[q]]) smp[nsmp++] = idx[q];
         }
         ctx->cursor = (ctx->cursor + kref) % n;
         nonres = host_cols;
@@ -1840,7 +1854,7 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
         }
         ctx->zc_bytes += (host_cols - kh) * ctx->ld_dev * (int64_t)sizeof(float);
         if (kg > 0)
-            CK(cudaMemcpyAsync(ctx->d_cols, idx.data(), kg * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+            CK(cudaMemcpyAsync(ctx->d_cols, idx, kg * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
         if (!agg)
             CK(cudaMemcpyAsync(ctx->d_vsnap, ctx->d_vt, ctx->d4 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->st));
         CK(cudaEventRecord(ctx->ev_snap, ctx->st));
@@ -1896,15 +1910,15 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     //   est = sum_P z + (n - m) mean_sample z   (every term at most one round old),
     // where the plain sum of z mixes in gaps up to 1/f rounds stale.
     double est[4] = {0.0, 0.0, 0.0, 0.0};
-    const bool have_est = !smp.empty();
+    const bool have_est = nsmp > 0;
     if (have_est) {
         CK(cudaMemsetAsync(ctx->d_est, 0, 4 * sizeof(double), ctx->st));
         CK(launch_gather_f64(ctx->d_z, ctx->d_P, m, ctx->d_gap_out, ctx->st, &ctx->launches));
         CK(launch_sum(ctx->d_gap_out, m, ctx->d_est, ctx->st, &ctx->launches));
-        CK(cudaMemcpyAsync(ctx->d_smp, smp.data(), smp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
-        CK(launch_gather_f64(ctx->d_z, ctx->d_smp, (int64_t)smp.size(), ctx->d_s_out, ctx->st, &ctx->launches));
-        CK(launch_sum(ctx->d_s_out, (int64_t)smp.size(), ctx->d_est + 1, ctx->st, &ctx->launches));
-        const double cnt[2] = {(double)smp.size(), (double)(n - m)};
+        CK(cudaMemcpyAsync(ctx->d_smp, smp, nsmp * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+        CK(launch_gather_f64(ctx->d_z, ctx->d_smp, nsmp, ctx->d_s_out, ctx->st, &ctx->launches));
+        CK(launch_sum(ctx->d_s_out, nsmp, ctx->d_est + 1, ctx->st, &ctx->launches));
+        const double cnt[2] = {(double)nsmp, (double)(n - m)};
         CK(cudaMemcpyAsync(ctx->d_est + 2, cnt, 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
     }
     if (ctx->group || ctx->comm) {  // every rank takes part (a rank without a sample adds zeros)

@@ -1,17 +1,16 @@
-"""Developer timing of C4 DuHL rounds (DUHL_ROUND_TRACE / DUHL_SCD_TRACE)."""
-import os, sys, time
-import numpy as np
+"""Developer: DUHL_ROUND_TRACE phase timing of a few rounds in the bench's launch configuration.
+python tools/round_trace.py [c5s] [rounds]"""
+import os, sys
+os.environ["DUHL_ROUND_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench, paper_1708_05357_b200 as D
-cfg = bench.CONFIGS["c4"]
-A, lab = bench.make_data(cfg, 170805360)
-f = float(os.environ.get("REFRESH", "0.01"))
-P = D.create(A, lab, 1.0 / cfg["n"], 1, hbm_budget_bytes=int(0.25 * cfg["n"] * cfg["d"] * 4), m=10000,
-             refresh_fraction=f, borrow_host=True, profile=True, scd_exact=False)
-for t in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
-    r = P.round(t)
-    print(t, "swaps", r.swaps, "time_ms", round(1e3 * r.time_s, 2), file=sys.stderr)
-
-for k, nm in enumerate(["scd", "gap", "topm", "stage", "refresh"]):
-    n_, ms, by = P.kernel_stats(k)
-    if n_: print(nm, n_, round(ms / n_, 3), "ms/launch", round(by / ms / 1e6, 1), "GB/s", file=sys.stderr)
+name = sys.argv[1] if len(sys.argv) > 1 else "c5s"
+rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+args, cfg = bench.parse_args(["--config", name])
+kw = bench.launch_kwargs(args, cfg)
+A, lab = bench.make_data(cfg, kw["seed"])
+lam = bench.lam_of(cfg, A, lab)
+P = bench.create(D, A, lab, lam, cfg["model"], cert_every=1 << 30, scd_exact=args.exact, **kw)
+for t in range(rounds):
+    P.round(t, passes=args.passes)
+P.close()

@@ -1,5 +1,5 @@
 """Round-by-round trace of a duhl_solve in the bench's launch configuration (time, swaps,
-certificates, gamma) plus per-kind kernel time.   python tools/solve_trace.py [c4|c3]"""
+certificates, gamma) plus per-kind kernel time.   python tools/solve_trace.py [c4|c3|c5|c5s]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench, paper_1708_05357_b200 as D
@@ -8,9 +8,10 @@ args, cfg = bench.parse_args(["--config", name] + sys.argv[2:])
 kw = bench.launch_kwargs(args, cfg)
 A, lab = bench.make_data(cfg, kw["seed"])
 lam = bench.lam_of(cfg, A, lab)
-bench.pin_host(A)
+if not cfg.get("sparse"):
+    bench.pin_host(A)
 t0 = time.perf_counter()
-P = D.create(A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact, profile=True, **kw)
+P = bench.create(D, A, lab, lam, cfg["model"], cert_every=args.cert_every, scd_exact=args.exact, profile=True, **kw)
 print("create", round(time.perf_counter() - t0, 2), "shape", P.scd_shape(), file=sys.stderr)
 t0 = time.perf_counter()
 r = P.solve(1e-5, 1000, passes=args.passes)
