@@ -181,8 +181,9 @@ struct duhl_ctx {
     double* h_vt = nullptr;        // pinned [d4]: round-start v~ for the host threads
     double* h_hs = nullptr;        // pinned [n]: their dots
     double* h_hnorm = nullptr;     // pinned [n]: column norms of create's host ingest share
-    int64_t* h_ref_idx = nullptr;  // pinned [n]: a round's refresh columns (async upload, no realloc)
-    int64_t* h_ref_smp = nullptr;  // pinned [n]: the refreshed columns outside P (gap-estimate sample)
+    int64_t* h_ref_idx = nullptr;  // a round's refresh columns (async upload, no realloc): pinned [n],
+    int64_t* h_ref_smp = nullptr;  // and the gap-estimate sample, allocated at the first large refresh
+    std::vector<int64_t> ref_idx_v, ref_smp_v;  // small refreshes: plain heap buffers
     int64_t* h_hcols = nullptr;    // pinned [n]: their columns
     double* d_hs = nullptr;        // [n] dots uploaded for k_gap_finalize
     int64_t* d_hcols = nullptr;    // [n]
@@ -598,6 +599,7 @@ static duhl_status ensure_host_P(duhl_ctx* ctx) {
     return DUHL_OK;
 }
 
+constexpr int64_t kPinnedRefreshCols = 65536;  // refresh lists at least this long live in pinned memory
 constexpr int64_t kHeavyRunCols = 16;  // mean index-run length that sends a heavy round to the copy engine
 constexpr size_t kStageCeMinBytes = 512 * 1024;  // shorter columns: no copy-engine share in gather rounds
 
@@ -1116,9 +1118,6 @@ static duhl_status create_impl(const duhl_matrix* A, const duhl_csc* C, const do
         (cudaHostAlloc((void**)&ctx->h_plan_cols, n * sizeof(int64_t), 0) != cudaSuccess ||
          cudaHostAlloc((void**)&ctx->h_plan_slots, n * sizeof(int), 0) != cudaSuccess ||
          cudaEventCreateWithFlags(&ctx->ev_plan, cudaEventDisableTiming) != cudaSuccess))
-        return bail(DUHL_E_NOMEM);
-    if (cudaHostAlloc((void**)&ctx->h_ref_idx, std::max<int64_t>(1, n) * sizeof(int64_t), 0) != cudaSuccess ||
-        cudaHostAlloc((void**)&ctx->h_ref_smp, std::max<int64_t>(1, n) * sizeof(int64_t), 0) != cudaSuccess)
         return bail(DUHL_E_NOMEM);
     ctx->col_slot.assign(n, -1);
     ctx->slot_col.assign(ctx->S, -1);
@@ -1804,8 +1803,16 @@ static duhl_status round_impl(duhl_ctx* ctx, int64_t t, int passes, duhl_policy 
     // pinned per-context buffers: no per-round allocation, and the uploads are truly asynchronous
     // (C5 refreshes 1 M columns a round: two 8-MB pageable copies and a zero-filled vector cost
     // ~6 ms of host time per 17-ms round before)
-    int64_t* idx = ctx->h_ref_idx;
-    int64_t* smp = ctx->h_ref_smp;
+    if (kref >= kPinnedRefreshCols && !ctx->h_ref_idx &&
+        (cudaHostAlloc((void**)&ctx->h_ref_idx, n * sizeof(int64_t), 0) != cudaSuccess ||
+         cudaHostAlloc((void**)&ctx->h_ref_smp, n * sizeof(int64_t), 0) != cudaSuccess))
+        return fail(ctx, DUHL_E_NOMEM, "pinned refresh buffers");
+    if (kref < kPinnedRefreshCols && (int64_t)ctx->ref_idx_v.size() < kref) {
+        ctx->ref_idx_v.resize(kref);
+        ctx->ref_smp_v.resize(kref);
+    }
+    int64_t* idx = kref >= kPinnedRefreshCols ? ctx->h_ref_idx : ctx->ref_idx_v.data();
+    int64_t* smp = kref >= kPinnedRefreshCols ? ctx->h_ref_smp : ctx->ref_smp_v.data();
     int64_t nsmp = 0;
     int64_t kg = kref, kh = 0, nonres = 0;  // refresh columns on the GPU / host threads; non-resident
     bool heavy_round = false;             // the threads took every non-resident column (see below)
